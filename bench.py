@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Bench of the SpecPrefill hot path on B200: prompt tokens scored+selected/s.
+
+One step = sp_score -> sp_select -> sp_gather over one batch of synthetic
+input already resident in HBM (the whole hot path, SURVEY.md §8(a) rows
+a1-a11).  Default workload: BASELINE.json configs[3] (8B-shaped speculator,
+32K prompt, keep 10%) -- the configuration the north_star's >=70%-of-HBM
+target is quoted on.  K (2 GiB) is far larger than L2 (126 MB), so no L2
+flush is needed between steps.
+
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--algo fused|simt]
+  python bench.py --impl reference ...     # the float64 oracle on host cores (the reference arm)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "prompt tokens scored+selected/sec"
+UNIT = "tokens/s"
+HBM_FALLBACK_GBS = 6650.0           # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
+SPEC_HBM_GBS = 8000.0               # BASELINE.json "~8 TB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3", choices=["C0", "C1", "C2", "C3", "C4"])
+    ap.add_argument("--algo", default="fused", choices=["fused", "simt", "auto"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-layers", type=int, default=4)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        busy = [s for s in sm if s > 0.5 * max(sm)]
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def workload(name):
+    from spgen import gen
+    return gen.CONFIGS[name]
+
+
+# ---------------------------------------------------------------- cpu baseline (oracle)
+def cpu_baseline(w, n_layers: int):
+    """The float64 oracle as it stands, on this host's cores, on a bounded
+    sample: request 0, the first n_layers layers over all N tokens, plus the
+    full selection.  Scaled to tokens/s of the whole workload geometry."""
+    import numpy as np
+    from threadpoolctl import threadpool_info
+
+    from oracle import ref
+    from spgen import gen
+    Ls = min(n_layers, w.L)
+    Q = ref.bf16_to_f64(np.stack([gen.gen_Q(w, 0, l) for l in range(Ls)]))
+    Ks = [ref.bf16_to_f64(np.stack([gen.gen_K(w, 0, l, g) for g in range(w.Hkv)])) for l in range(Ls)]
+    t0 = time.perf_counter()
+    imp = ref.token_importance(Q, lambda l: Ks[l], w.scale, w.Rv)
+    t1 = time.perf_counter()
+    ref.select(imp, w.keep, w.pool_k, w.chunk)
+    t2 = time.perf_counter()
+    t_req = (t1 - t0) * (w.L / Ls) + (t2 - t1)          # one whole request
+    threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    return {"value": w.N / t_req, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"request 0 of {w.name}: layers 0..{Ls - 1} of {w.L} over all {w.N} tokens "
+                      f"(scaled x{w.L / Ls:g}) + full selection; {t2 - t0:.1f} s of CPU work",
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    """--impl reference: the oracle is the reference arm (no reference code
+    exists for this paper).  Rank 0 only; other ranks exit without work."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = workload(args.config)
+    layers = max(1, min(w.L, 2))
+    times = []
+    cb = None
+    for s in range(args.warmup + args.steps):
+        cb = cpu_baseline(w, layers)
+        if s >= args.warmup:
+            times.append(w.N / cb["value"])
+    ms = 1000.0 * statistics.mean(times)
+    val = w.N / (ms / 1000.0)
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} {w.name}", "B": w.B, "N": w.N, "L": w.L, "H": w.H,
+                       "Hkv": w.Hkv, "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cb["cores"], "kind": "oracle",
+                             "sample": cb["sample"]},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+
+    import paper_2502_02789_b200 as sp
+    from spgen import cuda as spgen_cuda
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = workload(args.config)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    # ---- inputs resident in HBM (device-side generator, bit-identical to spgen.gen)
+    Q, K, T = spgen_cuda.make_inputs(w, device=dev)
+    torch.cuda.synchronize()
+    imp = torch.empty((w.B, w.N), dtype=torch.float32, device=dev)
+    ids = torch.empty((w.B, w.N), dtype=torch.int32, device=dev)
+    pos = torch.empty_like(ids)
+    nk = torch.empty((w.B,), dtype=torch.int32, device=dev)
+    out = torch.empty_like(ids)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        sp.score(Q, K, R_valid=w.Rv, scale=w.scale, out=imp, algo=args.algo)
+        if ev is not None:
+            ev[1].record(stream)
+        sp.select(imp, w.keep, w.pool_k, w.chunk, w.pos0, ids=ids, pos=pos, n_kept=nk)
+        sp.gather(T, ids, nk, out=out)
+
+    for _ in range(args.warmup):
+        step()
+    sp.check_device_error()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    score_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for s in range(args.steps):
+        step(score_ev[s])
+    t_end.record(stream)
+    barrier()
+    clk = clocks.stop()
+    sp.check_device_error()
+    ms_total = t_start.elapsed_time(t_end)
+    score_ms = statistics.mean(a.elapsed_time(b) for a, b in score_ev)
+    if dist is not None:
+        tt = torch.tensor([ms_total, score_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total, score_ms = tt.tolist()
+    ms_step = ms_total / args.steps
+    tokens_per_step = w.B * w.N * world
+    value = tokens_per_step / (ms_step / 1000.0)
+
+    # ---- roofline of the dominant kernel (sp_score): algorithmic bytes / duration
+    peak, peak_src = peaks()
+    q_bytes = w.B * w.L * w.Rv * w.H * w.d * 2
+    alg_bytes = w.k_bytes + q_bytes + w.B * w.N * 4
+    achieved = alg_bytes / (score_ms / 1000.0) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"{args.config}/{args.algo}")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "sp_score", "kernel_ms": score_ms,
+                "algorithmic_bytes": alg_bytes, "peak_source": peak_src,
+                "frac_of_8TBs": achieved / SPEC_HBM_GBS, "score_share_of_step": score_ms / ms_step}
+
+    # ---- end to end through the C ABI with host (pinned) buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, w, Q, K, T, dev, stream, dist, world)
+
+    launches_per_step = {"fused": 1, "simt": 4, "auto": 1}[args.algo] + 2
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{args.config} {w.name}", "B": w.B, "N": w.N, "L": w.L, "H": w.H, "Hkv": w.Hkv,
+                       "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk,
+                       "algo": args.algo, "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": f"inputs larger than L2 (K = {w.k_bytes / 2**30:.2f} GiB per GPU), no flush"},
+            "roofline": roofline, "clocks": clk, "e2e": e2e, "gpu_launches": launches_per_step * args.steps}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w, args.cpu_sample_layers)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, w, Q, K, T, dev, stream, dist, world):
+    """Same metric through sp_run_host: H2D of the step's inputs from pinned
+    host memory, score/select/gather, D2H of ids/pos/n_kept/tokens."""
+    import torch
+
+    import paper_2502_02789_b200 as sp
+    Qh = Q.cpu().pin_memory()
+    Kh = K.cpu().pin_memory()
+    Th = T.cpu().pin_memory()
+    ho = {k: torch.empty((w.B, w.N), dtype=torch.int32).pin_memory() for k in ("ids", "pos", "out_tokens")}
+    ho["n_kept"] = torch.empty((w.B,), dtype=torch.int32).pin_memory()
+    nbytes = sp.run_workspace_bytes(Q, K, w.keep, w.pool_k, w.chunk, w.Rv, w.scale, w.pos0)
+    dv = {"Q": torch.empty_like(Q), "K": torch.empty_like(K), "tokens": torch.empty_like(T),
+          "importance": torch.empty((w.B, w.N), dtype=torch.float32, device=dev),
+          "ids": torch.empty_like(T), "pos": torch.empty_like(T), "n_kept": torch.empty((w.B,), dtype=torch.int32,
+                                                                                      device=dev),
+          "out_tokens": torch.empty_like(T), "ws": torch.zeros(nbytes, dtype=torch.uint8, device=dev)}
+    steps = max(2, min(args.steps, 5))
+    for _ in range(2):
+        sp.run_host(Qh, Kh, Th, dv, w.keep, w.pool_k, w.chunk, w.Rv, w.scale, w.pos0, host_out=ho)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        sp.run_host(Qh, Kh, Th, dv, w.keep, w.pool_k, w.chunk, w.Rv, w.scale, w.pos0, host_out=ho)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    h2d = Qh.numel() * 2 + Kh.numel() * 2 + Th.numel() * 4
+    d2h = 3 * w.B * w.N * 4 + w.B * 4
+    return {"value": w.B * w.N * world / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

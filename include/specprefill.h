@@ -1,0 +1,215 @@
+/*
+ * specprefill.h -- C ABI of the B200 (sm_100a) SpecPrefill hot path.
+ *
+ * SpecPrefill (arXiv 2502.02789) speculator-side token importance estimation
+ * and selection: score -> aggregate -> pool -> chunked top-k -> gather.
+ * Citations: P:n = line n of the paper's LaTeX with its section
+ * label; Zk = reading k of the ambiguity register in DESIGN.md.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * Ownership   The caller owns every buffer.  Device pointers are plain
+ *             cudaMalloc / PyTorch CUDA memory; the library never allocates
+ *             or frees device memory on the hot path.  Scratch comes from a
+ *             caller-provided workspace of at least *_workspace_bytes() bytes,
+ *             which must be zero-filled once before its first use (the kernels
+ *             leave their counters at zero when they finish).
+ * Streams     Every call is enqueued on `stream` (a cudaStream_t / CUstream;
+ *             NULL = legacy default stream) and returns without synchronising.
+ *             Outputs are valid in stream order.
+ * Errors      Arguments are validated on the host before anything is
+ *             launched; an invalid call returns a non-zero sp_status and
+ *             touches nothing.  Device-side failures (non-finite softmax
+ *             statistics, a stats exchange that never completes) set a
+ *             device flag read by sp_check_device_error().  No C++ exception
+ *             crosses this boundary.  There is no CPU fallback: a missing
+ *             device or kernel is an error.
+ * Determinism Same inputs, geometry and device give bit-identical outputs:
+ *             every floating-point reduction has a fixed order.
+ * Device      sm_100a (B200) only.
+ */
+#ifndef SPECPREFILL_H
+#define SPECPREFILL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_ABI_VERSION 1
+
+typedef enum sp_status {
+  SP_OK = 0,
+  SP_EINVAL = 1,        /* invalid argument (shape, stride, alignment, keep rate, pool window, ...) */
+  SP_EUNSUPPORTED = 2,  /* valid but no kernel for this geometry / device */
+  SP_ECUDA = 3,         /* a CUDA runtime call failed */
+  SP_ENONFINITE = 5,    /* device flag: a softmax statistic was not finite (Z15) */
+  SP_EEMPTY = 6,        /* zero valid look-ahead rows */
+  SP_EWORKSPACE = 7,    /* workspace too small or misaligned */
+  SP_ETIMEOUT = 8       /* device flag: an in-kernel stats exchange timed out */
+} sp_status;
+
+/* A cudaStream_t / CUstream handle. */
+typedef void* sp_stream;
+
+/*
+ * Geometry of one uniform batch (Alg.1 P:142-171 retrieve_qk: Q of the
+ * look-ahead rows and K of the speculator KV cache C_s).
+ *   B        requests in the batch (each is scored and selected independently)
+ *   L        speculator layers
+ *   H, Hkv   query / kv heads; H % Hkv == 0; query head h reads kv head h / (H/Hkv) (Z4)
+ *   d        head dim; 16 <= d <= 256, d % 16 == 0
+ *   R        captured query rows per request (look-ahead rows; Z1)
+ *   R_valid  valid prefix of the rows (EOS check, Alg.1); 1 <= R_valid <= R
+ *   N        prompt tokens per request (M in the paper's eq.)
+ *   scale    softmax scale applied to q.k (Z3; 1/sqrt(d) for Llama)
+ */
+typedef struct sp_geom {
+  int32_t B, L, H, Hkv, d;
+  int32_t R, R_valid;
+  int64_t N;
+  float scale;
+} sp_geom;
+
+/*
+ * Element strides (bf16 elements, not bytes) of the two inputs.  The head
+ * dimension is always contiguous (stride 1).
+ *   K[b][l][g][i][:]  at  K + b*k_b + l*k_l + g*k_g + i*k_i     (bf16)
+ *   Q[b][l][r][h][:]  at  Q + b*q_b + l*q_l + r*q_r + h*q_h     (bf16)
+ * Alignment: K, Q and every stride*2 bytes must be multiples of 16 bytes
+ * (TMA tensor maps), strides must be non-negative.
+ */
+typedef struct sp_layout {
+  int64_t k_b, k_l, k_g, k_i;
+  int64_t q_b, q_l, q_r, q_h;
+} sp_layout;
+
+/*
+ * Selection parameters (sec:chunk_select P:121-123, sec:position_ids P:125-133).
+ *   keep_rate  ratio of chunks kept, (0, 1]; K_c = sp_kept_chunks(n_c, keep_rate)
+ *   pool_k     odd 1-D average-pool window >= 1, centred, shrinking at the edges (Z6)
+ *   chunk      contiguous chunk size >= 1; the last chunk may be partial (Z8)
+ *   pos0       position id of prompt token 0 (kept positions are ids + pos0)
+ */
+typedef struct sp_select_params {
+  double keep_rate;
+  int32_t pool_k;
+  int32_t chunk;
+  int32_t pos0;
+} sp_select_params;
+
+/* Score kernel choice. */
+typedef enum sp_score_algo {
+  SP_SCORE_AUTO = 0,   /* fused when supported, else SIMT */
+  SP_SCORE_FUSED = 1,  /* tcgen05/TMA persistent kernel, logits TMEM-resident, one K read */
+  SP_SCORE_SIMT = 2    /* two-pass FP32-FMA kernels (baseline; reads K twice) */
+} sp_score_algo;
+
+/* ------------------------------------------------------------------ utilities */
+int sp_abi_version(void);
+const char* sp_status_string(sp_status s);
+
+/* K_c = clamp(ceil(keep_rate * n_chunks), 1, n_chunks), evaluated exactly on
+ * keep_rate snapped to parts per million (Z9).  Returns -1 for an
+ * invalid keep_rate or n_chunks < 1. */
+int64_t sp_kept_chunks(int64_t n_chunks, double keep_rate);
+
+/* Synchronises `stream`, then reads and clears the device error flag.
+ * Returns SP_OK, SP_ENONFINITE, SP_ETIMEOUT or SP_ECUDA. */
+sp_status sp_check_device_error(sp_stream stream);
+
+/* Number of SMs the persistent kernels size their grid for (current device). */
+int sp_device_sm_count(void);
+
+/* ------------------------------------------------------------------ score
+ * Token importance (O1-O4 in DESIGN.md):
+ *   s[l,h,r,i]   = scale * <Q[b][l][r][h], K[b][l][h/G][i]>
+ *   lse[l,h,r]   = log sum_i exp(s[l,h,r,i])   over the N prompt keys     (Z2)
+ *   acc[r,i]     = max_{l,h} (s[l,h,r,i] - lse[l,h,r])                    (max over H and L)
+ *   importance[b][i] = (1/R_valid) sum_{r<R_valid} exp(acc[r,i])          (mean over rows)
+ * importance: device fp32 [B][N] (contiguous), written completely.
+ * Q rows r >= R_valid are never read. */
+size_t sp_score_workspace_bytes(const sp_geom* g, int algo);
+sp_status sp_score(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay,
+                   float* importance, void* ws, size_t ws_bytes, sp_stream stream);
+sp_status sp_score_ex(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay,
+                      float* importance, void* ws, size_t ws_bytes, int algo, sp_stream stream);
+
+/* ------------------------------------------------------------------ score, sequence-sharded split
+ * For a prompt split along tokens over P ranks.  Each
+ * rank passes its own K shard (N = local tokens).  Statistics are in the log2
+ * domain: x = s*log2(e);  m2 = max_i x;  l = sum_i 2^(x - m2).
+ *   stats [B][L][H][R_valid][2] fp32 (m2, l) over the local tokens.
+ * sp_stats_combine merges P gathered stats blocks [P][n_rows][2] in rank order
+ * (deterministic) into lse2[n_rows] = m2 + log2(l), n_rows = B*L*H*R_valid.
+ * sp_score_finish computes importance over the local tokens given the global
+ * lse2 (same formula as sp_score). */
+size_t sp_score_split_workspace_bytes(const sp_geom* g);
+sp_status sp_score_stats(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay,
+                         float* stats, void* ws, size_t ws_bytes, sp_stream stream);
+sp_status sp_stats_combine(const float* parts, int32_t P, int64_t n_rows, float* lse2, sp_stream stream);
+sp_status sp_score_finish(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay,
+                          const float* lse2, float* importance, void* ws, size_t ws_bytes, sp_stream stream);
+
+/* ------------------------------------------------------------------ select
+ * Pool, chunk means, top-K_c chunks, positions (O5-O9, Alg.1):
+ *   pooled[i] = mean(importance[j] : |j-i| <= (pool_k-1)/2, 0 <= j < N)      (Z6)
+ *   cs[c]     = mean(pooled[c*chunk .. min(N,(c+1)*chunk)-1])                 (Z8)
+ *   keep the K_c chunks first in (cs desc, c asc) order                       (Z10)
+ *   ids  = ascending union of the kept chunks' token indices                  (Z11)
+ *   pos  = ids + pos0;  the first decode position is N + pos0
+ * importance: device fp32 [B][N].  ids, pos: device int32 [B][N] (capacity N per
+ * request; entries >= n_kept[b] are left untouched).  n_kept: device int32 [B]. */
+size_t sp_select_workspace_bytes(int32_t B, int64_t N, const sp_select_params* p);
+sp_status sp_select(const float* importance, int32_t B, int64_t N, const sp_select_params* p,
+                    int32_t* ids, int32_t* pos, int32_t* n_kept, void* ws, size_t ws_bytes,
+                    sp_stream stream);
+
+/* ------------------------------------------------------------------ gather
+ * out[b][j] = tokens[b][ids[b][j]] for j < n_kept[b] (merge_requests input,
+ * Alg.1).  tokens, ids, out: device int32 [B][N]; n_kept device int32 [B].
+ * Bit-exact. */
+sp_status sp_gather(const int32_t* tokens, const int32_t* ids, const int32_t* n_kept, int32_t B,
+                    int64_t N, int32_t* out, sp_stream stream);
+
+/* ------------------------------------------------------------------ end to end from host buffers
+ * The whole path with host inputs/outputs: copies Q, K and tokens host->device,
+ * runs sp_score -> sp_select -> sp_gather, copies ids, pos, n_kept and the
+ * gathered tokens device->host, all enqueued on `stream` (host buffers should
+ * be pinned for the copies to be asynchronous).  Host Q/K use the same element
+ * strides `lay` as the device copies; host outputs are [B][N] / [B]. */
+typedef struct sp_host_io {
+  const void* Q;
+  const void* K;
+  const int32_t* tokens;
+  int32_t* ids;
+  int32_t* pos;
+  int32_t* n_kept;
+  int32_t* out_tokens;
+  size_t q_bytes;   /* bytes of Q / K to copy (span of the strided layout) */
+  size_t k_bytes;
+} sp_host_io;
+
+typedef struct sp_device_bufs {
+  void* Q;
+  void* K;
+  int32_t* tokens;
+  float* importance;
+  int32_t* ids;
+  int32_t* pos;
+  int32_t* n_kept;
+  int32_t* out_tokens;
+  void* ws;
+  size_t ws_bytes;
+} sp_device_bufs;
+
+size_t sp_run_workspace_bytes(const sp_geom* g, const sp_select_params* p);
+sp_status sp_run_host(const sp_host_io* host, const sp_device_bufs* dev, const sp_geom* g,
+                      const sp_layout* lay, const sp_select_params* p, sp_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECPREFILL_H */

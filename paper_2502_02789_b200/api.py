@@ -1,0 +1,152 @@
+"""Thin PyTorch-facing wrappers over the C ABI (argument marshalling only).
+
+PyTorch provides device memory and streams; every step of the path runs in the
+CUDA kernels of libspecprefill.so.  Names follow the paper's Alg.1:
+``score`` = compute_attention_score + aggregate_attention_score, ``select`` =
+chunk_select_from_smoothed_attention + restore_pos_ids, ``gather`` = the
+token gather of merge_requests.
+
+Tensor layouts (strides are passed through, the head dim must be contiguous):
+  Q  bf16 [B][L][R][H][d]     look-ahead query rows (post-RoPE)
+  K  bf16 [B][L][Hkv][N][d]   speculator key cache
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+
+from . import _lib
+from ._lib import check, lib
+
+ALGOS = {"auto": _lib.SP_SCORE_AUTO, "fused": _lib.SP_SCORE_FUSED, "simt": _lib.SP_SCORE_SIMT}
+
+_ws_cache: dict = {}
+
+
+def _stream_ptr(stream) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def workspace(tag: str, nbytes: int, device) -> torch.Tensor:
+    """Zero-initialised, cached device workspace (the fused kernel leaves its
+    counters at zero, so a workspace is zeroed only when first allocated)."""
+    key = (tag, torch.device(device).index)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def make_geom(Q: torch.Tensor, K: torch.Tensor, R_valid: int | None = None, scale: float | None = None):
+    if Q.dtype != torch.bfloat16 or K.dtype != torch.bfloat16:
+        raise TypeError("Q and K must be bfloat16")
+    if Q.dim() != 5 or K.dim() != 5:
+        raise ValueError("Q must be [B][L][R][H][d] and K [B][L][Hkv][N][d]")
+    B, L, R, H, d = Q.shape
+    Bk, Lk, Hkv, N, dk = K.shape
+    if (B, L, d) != (Bk, Lk, dk):
+        raise ValueError(f"Q {tuple(Q.shape)} and K {tuple(K.shape)} disagree")
+    if Q.stride(-1) != 1 or K.stride(-1) != 1:
+        raise ValueError("head dim must be contiguous")
+    g = _lib.sp_geom(B=B, L=L, H=H, Hkv=Hkv, d=d, R=R, R_valid=R if R_valid is None else R_valid, N=N,
+                     scale=float(1.0 / math.sqrt(d)) if scale is None else float(scale))
+    lay = _lib.sp_layout(k_b=K.stride(0), k_l=K.stride(1), k_g=K.stride(2), k_i=K.stride(3),
+                         q_b=Q.stride(0), q_l=Q.stride(1), q_r=Q.stride(2), q_h=Q.stride(3))
+    return g, lay
+
+
+def score(Q, K, R_valid=None, scale=None, out=None, algo: str = "auto", stream=None) -> torch.Tensor:
+    """Token importance [B][N] fp32 (O1-O4)."""
+    g, lay = make_geom(Q, K, R_valid, scale)
+    if out is None:
+        out = torch.empty((g.B, g.N), dtype=torch.float32, device=K.device)
+    a = ALGOS[algo]
+    nbytes = lib().sp_score_workspace_bytes(C.byref(g), a)
+    ws = workspace("score-" + algo, nbytes, K.device)
+    check(lib().sp_score_ex(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), out.data_ptr(), ws.data_ptr(),
+                            ws.numel(), a, _stream_ptr(stream)), "sp_score")
+    return out
+
+
+def select(importance: torch.Tensor, keep: float, pool_k: int, chunk: int, pos0: int = 0, ids=None, pos=None,
+           n_kept=None, stream=None):
+    """(ids [B][N] int32, pos [B][N] int32, n_kept [B] int32); only the first
+    n_kept[b] entries of row b are meaningful (O5-O9)."""
+    if importance.dtype != torch.float32 or importance.dim() != 2 or not importance.is_contiguous():
+        raise ValueError("importance must be contiguous fp32 [B][N]")
+    B, N = importance.shape
+    dev = importance.device
+    p = _lib.sp_select_params(keep_rate=float(keep), pool_k=int(pool_k), chunk=int(chunk), pos0=int(pos0))
+    ids = torch.empty((B, N), dtype=torch.int32, device=dev) if ids is None else ids
+    pos = torch.empty((B, N), dtype=torch.int32, device=dev) if pos is None else pos
+    n_kept = torch.empty((B,), dtype=torch.int32, device=dev) if n_kept is None else n_kept
+    nbytes = lib().sp_select_workspace_bytes(B, N, C.byref(p))
+    if nbytes == 0:
+        check(_lib.SP_EINVAL, "sp_select")
+    ws = workspace("select", nbytes, dev)
+    check(lib().sp_select(importance.data_ptr(), B, N, C.byref(p), ids.data_ptr(), pos.data_ptr(), n_kept.data_ptr(),
+                          ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_select")
+    return ids, pos, n_kept
+
+
+def gather(tokens: torch.Tensor, ids: torch.Tensor, n_kept: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    """out[b][j] = tokens[b][ids[b][j]] for j < n_kept[b] (bit-exact)."""
+    if tokens.dtype != torch.int32 or not tokens.is_contiguous():
+        raise ValueError("tokens must be contiguous int32 [B][N]")
+    B, N = tokens.shape
+    out = torch.empty_like(tokens) if out is None else out
+    check(lib().sp_gather(tokens.data_ptr(), ids.data_ptr(), n_kept.data_ptr(), B, N, out.data_ptr(),
+                          _stream_ptr(stream)), "sp_gather")
+    return out
+
+
+def kept_chunks(n_chunks: int, keep: float) -> int:
+    k = lib().sp_kept_chunks(int(n_chunks), float(keep))
+    if k < 0:
+        raise ValueError("invalid keep rate / chunk count")
+    return k
+
+
+def check_device_error(stream=None):
+    check(lib().sp_check_device_error(_stream_ptr(stream)), "device")
+
+
+def specprefill(Q, K, tokens, keep, pool_k, chunk, R_valid=None, scale=None, pos0=0, algo="auto", stream=None):
+    """The whole hot path (Alg.1): importance, kept ids, positions,
+    gathered tokens, and the first decode position N + pos0."""
+    imp = score(Q, K, R_valid, scale, algo=algo, stream=stream)
+    ids, pos, n_kept = select(imp, keep, pool_k, chunk, pos0, stream=stream)
+    out = gather(tokens, ids, n_kept, stream=stream)
+    return dict(importance=imp, ids=ids, pos=pos, n_kept=n_kept, out_tokens=out, first_decode=K.shape[3] + pos0)
+
+
+def run_host(Qh, Kh, tokens_h, dev: dict, keep, pool_k, chunk, R_valid=None, scale=None, pos0=0, host_out=None,
+             stream=None):
+    """End to end from host (pinned) buffers through sp_run_host: H2D copies,
+    score, select, gather and D2H copies, all enqueued on one stream.
+    ``dev`` holds preallocated device tensors Q, K, tokens, importance, ids,
+    pos, n_kept, out_tokens, ws (see bench.py)."""
+    g, lay = make_geom(dev["Q"], dev["K"], R_valid, scale)
+    p = _lib.sp_select_params(keep_rate=float(keep), pool_k=int(pool_k), chunk=int(chunk), pos0=int(pos0))
+    ho = host_out
+    io = _lib.sp_host_io(Q=Qh.data_ptr(), K=Kh.data_ptr(), tokens=tokens_h.data_ptr(), ids=ho["ids"].data_ptr(),
+                         pos=ho["pos"].data_ptr(), n_kept=ho["n_kept"].data_ptr(),
+                         out_tokens=ho["out_tokens"].data_ptr(),
+                         q_bytes=Qh.numel() * 2, k_bytes=Kh.numel() * 2)
+    db = _lib.sp_device_bufs(Q=dev["Q"].data_ptr(), K=dev["K"].data_ptr(), tokens=dev["tokens"].data_ptr(),
+                             importance=dev["importance"].data_ptr(), ids=dev["ids"].data_ptr(),
+                             pos=dev["pos"].data_ptr(), n_kept=dev["n_kept"].data_ptr(),
+                             out_tokens=dev["out_tokens"].data_ptr(), ws=dev["ws"].data_ptr(),
+                             ws_bytes=dev["ws"].numel())
+    check(lib().sp_run_host(C.byref(io), C.byref(db), C.byref(g), C.byref(lay), C.byref(p), _stream_ptr(stream)),
+          "sp_run_host")
+
+
+def run_workspace_bytes(Q, K, keep, pool_k, chunk, R_valid=None, scale=None, pos0=0) -> int:
+    g, _ = make_geom(Q, K, R_valid, scale)
+    p = _lib.sp_select_params(keep_rate=float(keep), pool_k=int(pool_k), chunk=int(chunk), pos0=int(pos0))
+    return lib().sp_run_workspace_bytes(C.byref(g), C.byref(p))

@@ -1,0 +1,292 @@
+// C ABI of libspecprefill.so (declared in include/specprefill.h).
+//
+// Host-side argument validation, workspace carving and kernel dispatch.  No
+// exception crosses this boundary; every entry point returns an sp_status.
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "sp_internal.h"
+
+namespace sp {
+
+__device__ int g_sp_err;      // device error flag (DevErr), one per device
+
+int* device_error_flag() {
+  static int* ptrs[64] = {nullptr};
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (ptrs[dev] == nullptr) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_sp_err) != cudaSuccess) return nullptr;
+    ptrs[dev] = reinterpret_cast<int*>(p);
+  }
+  return ptrs[dev];
+}
+
+namespace {
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// sm_100 device present and current?
+sp_status check_device() {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return SP_ECUDA; }
+  int major = 0, minor = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return SP_ECUDA;
+  }
+  if (major != 10 || minor != 0) return SP_EUNSUPPORTED;   // sm_100a only
+  return SP_OK;
+}
+
+sp_status check_geom(const sp_geom* g) {
+  if (g == nullptr) return SP_EINVAL;
+  if (g->B < 1 || g->L < 1 || g->H < 1 || g->Hkv < 1 || g->R < 1 || g->N < 1) return SP_EINVAL;
+  if (g->H % g->Hkv != 0) return SP_EINVAL;
+  if (g->d < 16 || g->d > 256 || g->d % 16 != 0) return SP_EINVAL;
+  if (g->R_valid < 0 || g->R_valid > g->R) return SP_EINVAL;
+  if (g->R_valid == 0) return SP_EEMPTY;
+  if (!(std::isfinite(g->scale) && g->scale > 0.f)) return SP_EINVAL;
+  if (g->N >= (1LL << 31)) return SP_EINVAL;
+  return SP_OK;
+}
+
+sp_status check_layout(const sp_geom* g, const sp_layout* l, const void* Q, const void* K) {
+  if (l == nullptr || Q == nullptr || K == nullptr) return SP_EINVAL;
+  const long long ks[4] = {l->k_b, l->k_l, l->k_g, l->k_i};
+  const long long kn[4] = {g->B, g->L, g->Hkv, g->N};
+  const long long qs[4] = {l->q_b, l->q_l, l->q_r, l->q_h};
+  const long long qn[4] = {g->B, g->L, g->R, g->H};
+  for (int i = 0; i < 4; ++i) {
+    if (ks[i] < 0 || qs[i] < 0) return SP_EINVAL;
+    if (kn[i] > 1 && (ks[i] * 2) % 16 != 0) return SP_EINVAL;   // TMA: strides multiple of 16 B
+    if (qn[i] > 1 && (qs[i] * 2) % 16 != 0) return SP_EINVAL;
+  }
+  if (l->k_i < g->d && g->N > 1) return SP_EINVAL;               // rows of one head may not overlap
+  if (!aligned16(Q) || !aligned16(K)) return SP_EINVAL;
+  return SP_OK;
+}
+
+sp_status check_select(int32_t B, int64_t N, const sp_select_params* p) {
+  if (p == nullptr || B < 1 || N < 1 || N >= (1LL << 31)) return SP_EINVAL;
+  if (!(p->keep_rate > 0.0 && p->keep_rate <= 1.0)) return SP_EINVAL;
+  if (p->pool_k < 1 || p->pool_k % 2 == 0) return SP_EINVAL;
+  if (p->chunk < 1) return SP_EINVAL;
+  if (p->pos0 < 0 || (long long)p->pos0 + N >= (1LL << 31)) return SP_EINVAL;
+  return SP_OK;
+}
+
+sp_status from_cuda(cudaError_t e) {
+  if (e == cudaSuccess) return SP_OK;
+  cudaGetLastError();
+  return SP_ECUDA;
+}
+
+int resolve_algo(const Geom& g, int algo) {
+  if (algo == SP_SCORE_AUTO) return fused_supported(g, Layout{}, nullptr, nullptr) ? SP_SCORE_FUSED : SP_SCORE_SIMT;
+  return algo;
+}
+
+size_t score_ws(const Geom& g, int algo) {
+  algo = resolve_algo(g, algo);
+  return algo == SP_SCORE_FUSED ? fused_score_ws_bytes(g) : simt_score_ws_bytes(g);
+}
+
+}  // namespace
+}  // namespace sp
+
+using namespace sp;
+
+extern "C" {
+
+int sp_abi_version(void) { return SP_ABI_VERSION; }
+
+const char* sp_status_string(sp_status s) {
+  switch (s) {
+    case SP_OK: return "SP_OK";
+    case SP_EINVAL: return "SP_EINVAL: invalid argument";
+    case SP_EUNSUPPORTED: return "SP_EUNSUPPORTED: no kernel for this geometry/device (sm_100a required)";
+    case SP_ECUDA: return "SP_ECUDA: CUDA runtime error";
+    case SP_ENONFINITE: return "SP_ENONFINITE: non-finite softmax statistic";
+    case SP_EEMPTY: return "SP_EEMPTY: zero valid look-ahead rows";
+    case SP_EWORKSPACE: return "SP_EWORKSPACE: workspace too small or misaligned";
+    case SP_ETIMEOUT: return "SP_ETIMEOUT: in-kernel statistics exchange timed out";
+  }
+  return "SP_?: unknown status";
+}
+
+int64_t sp_kept_chunks(int64_t n_chunks, double keep_rate) {
+  if (n_chunks < 1 || !(keep_rate > 0.0 && keep_rate <= 1.0)) return -1;
+  const long long ppm = (long long)std::floor(keep_rate * 1000000.0 + 0.5);
+  long long k = (ppm * n_chunks + 999999) / 1000000;
+  if (k < 1) k = 1;
+  if (k > n_chunks) k = n_chunks;
+  return k;
+}
+
+int sp_device_sm_count(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return 0; }
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) { cudaGetLastError(); return 0; }
+  return n;
+}
+
+sp_status sp_check_device_error(sp_stream stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaStreamSynchronize(st) != cudaSuccess) { cudaGetLastError(); return SP_ECUDA; }
+  int v = 0, zero = 0;
+  if (cudaMemcpyFromSymbol(&v, g_sp_err, sizeof(int)) != cudaSuccess) { cudaGetLastError(); return SP_ECUDA; }
+  if (v != 0 && cudaMemcpyToSymbol(g_sp_err, &zero, sizeof(int)) != cudaSuccess) { cudaGetLastError(); return SP_ECUDA; }
+  if (v == kDevNonFinite) return SP_ENONFINITE;
+  if (v == kDevTimeout) return SP_ETIMEOUT;
+  return SP_OK;
+}
+
+size_t sp_score_workspace_bytes(const sp_geom* g, int algo) {
+  if (check_geom(g) != SP_OK) return 0;
+  return score_ws(to_geom(*g), algo);
+}
+
+sp_status sp_score_ex(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, float* importance,
+                      void* ws, size_t ws_bytes, int algo, sp_stream stream) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if ((s = check_layout(g, lay, Q, K)) != SP_OK) return s;
+  if (importance == nullptr) return SP_EINVAL;
+  if (algo != SP_SCORE_AUTO && algo != SP_SCORE_FUSED && algo != SP_SCORE_SIMT) return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
+  Geom G = to_geom(*g);
+  Layout Lay = to_layout(*lay);
+  algo = resolve_algo(G, algo);
+  if (algo == SP_SCORE_FUSED && !fused_supported(G, Lay, Q, K)) return SP_EUNSUPPORTED;
+  const size_t need = score_ws(G, algo);
+  if (ws == nullptr || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return SP_EWORKSPACE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const __nv_bfloat16* q = reinterpret_cast<const __nv_bfloat16*>(Q);
+  const __nv_bfloat16* k = reinterpret_cast<const __nv_bfloat16*>(K);
+  if (algo == SP_SCORE_FUSED) return from_cuda(fused_score(q, k, G, Lay, importance, ws, ws_bytes, st));
+  return from_cuda(simt_score(q, k, G, Lay, importance, ws, st));
+}
+
+sp_status sp_score(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, float* importance, void* ws,
+                   size_t ws_bytes, sp_stream stream) {
+  return sp_score_ex(Q, K, g, lay, importance, ws, ws_bytes, SP_SCORE_AUTO, stream);
+}
+
+size_t sp_score_split_workspace_bytes(const sp_geom* g) {
+  if (check_geom(g) != SP_OK) return 0;
+  Geom G = to_geom(*g);
+  size_t a = simt_split_ws_bytes(G);
+  size_t b = align256((size_t)G.B * G.Rv * G.N * sizeof(unsigned));
+  return a > b ? a : b;
+}
+
+sp_status sp_score_stats(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, float* stats, void* ws,
+                         size_t ws_bytes, sp_stream stream) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if ((s = check_layout(g, lay, Q, K)) != SP_OK) return s;
+  if (stats == nullptr) return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
+  if (ws == nullptr || ws_bytes < sp_score_split_workspace_bytes(g)) return SP_EWORKSPACE;
+  return from_cuda(simt_score_stats(reinterpret_cast<const __nv_bfloat16*>(Q), reinterpret_cast<const __nv_bfloat16*>(K),
+                                    to_geom(*g), to_layout(*lay), stats, ws, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sp_status sp_stats_combine(const float* parts, int32_t P, int64_t n_rows, float* lse2, sp_stream stream) {
+  if (parts == nullptr || lse2 == nullptr || P < 1 || n_rows < 1) return SP_EINVAL;
+  sp_status s = check_device();
+  if (s != SP_OK) return s;
+  return from_cuda(stats_combine(parts, P, n_rows, lse2, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sp_status sp_score_finish(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, const float* lse2,
+                          float* importance, void* ws, size_t ws_bytes, sp_stream stream) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if ((s = check_layout(g, lay, Q, K)) != SP_OK) return s;
+  if (lse2 == nullptr || importance == nullptr) return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
+  if (ws == nullptr || ws_bytes < sp_score_split_workspace_bytes(g)) return SP_EWORKSPACE;
+  return from_cuda(simt_score_finish(reinterpret_cast<const __nv_bfloat16*>(Q),
+                                     reinterpret_cast<const __nv_bfloat16*>(K), to_geom(*g), to_layout(*lay), lse2,
+                                     importance, ws, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+size_t sp_select_workspace_bytes(int32_t B, int64_t N, const sp_select_params* p) {
+  if (check_select(B, N, p) != SP_OK) return 0;
+  return select_ws_bytes(B, N, p->chunk);
+}
+
+sp_status sp_select(const float* importance, int32_t B, int64_t N, const sp_select_params* p, int32_t* ids,
+                    int32_t* pos, int32_t* n_kept, void* ws, size_t ws_bytes, sp_stream stream) {
+  sp_status s = check_select(B, N, p);
+  if (s != SP_OK) return s;
+  if (importance == nullptr || ids == nullptr || pos == nullptr || n_kept == nullptr) return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
+  if (ws == nullptr || ws_bytes < select_ws_bytes(B, N, p->chunk)) return SP_EWORKSPACE;
+  const long long n_c = (N + p->chunk - 1) / p->chunk;
+  const long long K_c = sp_kept_chunks(n_c, p->keep_rate);
+  return from_cuda(select_launch(importance, B, N, p->pool_k, p->chunk, p->pos0, K_c, ids, pos, n_kept, ws,
+                                 reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sp_status sp_gather(const int32_t* tokens, const int32_t* ids, const int32_t* n_kept, int32_t B, int64_t N,
+                    int32_t* out, sp_stream stream) {
+  if (tokens == nullptr || ids == nullptr || n_kept == nullptr || out == nullptr || B < 1 || N < 1 ||
+      N >= (1LL << 31))
+    return SP_EINVAL;
+  sp_status s = check_device();
+  if (s != SP_OK) return s;
+  return from_cuda(gather_launch(tokens, ids, n_kept, B, N, out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+size_t sp_run_workspace_bytes(const sp_geom* g, const sp_select_params* p) {
+  if (check_geom(g) != SP_OK || check_select(g->B, g->N, p) != SP_OK) return 0;
+  // score and select get disjoint regions: the fused score kernel's counters
+  // must stay zero between calls
+  return align256(score_ws(to_geom(*g), SP_SCORE_AUTO)) + select_ws_bytes(g->B, g->N, p->chunk);
+}
+
+sp_status sp_run_host(const sp_host_io* host, const sp_device_bufs* dev, const sp_geom* g, const sp_layout* lay,
+                      const sp_select_params* p, sp_stream stream) {
+  if (host == nullptr || dev == nullptr) return SP_EINVAL;
+  if (host->Q == nullptr || host->K == nullptr || host->tokens == nullptr || host->ids == nullptr ||
+      host->pos == nullptr || host->n_kept == nullptr || host->out_tokens == nullptr)
+    return SP_EINVAL;
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if ((s = check_layout(g, lay, dev->Q, dev->K)) != SP_OK) return s;
+  if ((s = check_select(g->B, g->N, p)) != SP_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t tok_bytes = (size_t)g->B * g->N * sizeof(int32_t);
+  if (cudaMemcpyAsync(dev->Q, host->Q, host->q_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(dev->K, host->K, host->k_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(dev->tokens, host->tokens, tok_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    cudaGetLastError();
+    return SP_ECUDA;
+  }
+  if ((s = sp_score(dev->Q, dev->K, g, lay, dev->importance, dev->ws, dev->ws_bytes, stream)) != SP_OK) return s;
+  const size_t score_bytes = align256(score_ws(to_geom(*g), SP_SCORE_AUTO));
+  if (dev->ws_bytes < score_bytes) return SP_EWORKSPACE;
+  if ((s = sp_select(dev->importance, g->B, g->N, p, dev->ids, dev->pos, dev->n_kept,
+                     reinterpret_cast<char*>(dev->ws) + score_bytes, dev->ws_bytes - score_bytes, stream)) != SP_OK)
+    return s;
+  if ((s = sp_gather(dev->tokens, dev->ids, dev->n_kept, g->B, g->N, dev->out_tokens, stream)) != SP_OK) return s;
+  if (cudaMemcpyAsync(host->n_kept, dev->n_kept, (size_t)g->B * sizeof(int32_t), cudaMemcpyDeviceToHost, st) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(host->ids, dev->ids, tok_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(host->pos, dev->pos, tok_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(host->out_tokens, dev->out_tokens, tok_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) {
+    cudaGetLastError();
+    return SP_ECUDA;
+  }
+  return SP_OK;
+}
+
+}  // extern "C"

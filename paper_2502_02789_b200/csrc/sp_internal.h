@@ -1,0 +1,76 @@
+// Internal declarations shared by the translation units of libspecprefill.so.
+// Not part of the ABI (include/specprefill.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/specprefill.h"
+
+namespace sp {
+
+// log2(e): the kernels work in the log2 domain, x = s * log2(e), so that
+// exp(s - lse) == exp2(x - lse2) with one ex2 per probability.
+constexpr float kLog2e = 1.4426950408889634f;
+
+// Device error codes written into the device flag (first error wins).
+enum DevErr : int { kDevOk = 0, kDevNonFinite = 1, kDevTimeout = 2 };
+
+// Pointer to this device's error flag (int), resolved once per device.
+int* device_error_flag();
+
+struct Geom {
+  int B, L, H, Hkv, d, R, Rv, G;
+  long long N;
+  float scale;
+};
+
+struct Layout {
+  long long k_b, k_l, k_g, k_i;
+  long long q_b, q_l, q_r, q_h;
+};
+
+inline Geom to_geom(const sp_geom& g) {
+  Geom o;
+  o.B = g.B; o.L = g.L; o.H = g.H; o.Hkv = g.Hkv; o.d = g.d; o.R = g.R; o.Rv = g.R_valid;
+  o.G = g.H / g.Hkv; o.N = g.N; o.scale = g.scale;
+  return o;
+}
+inline Layout to_layout(const sp_layout& l) {
+  Layout o;
+  o.k_b = l.k_b; o.k_l = l.k_l; o.k_g = l.k_g; o.k_i = l.k_i;
+  o.q_b = l.q_b; o.q_l = l.q_l; o.q_r = l.q_r; o.q_h = l.q_h;
+  return o;
+}
+
+// Round up to a multiple of 256 bytes (workspace carving).
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ---------------------------------------------------------------- SIMT score (score_simt.cu)
+size_t simt_score_ws_bytes(const Geom& g);
+size_t simt_split_ws_bytes(const Geom& g);
+// full single-device score: stats -> combine -> finish -> importance
+cudaError_t simt_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                       float* importance, void* ws, cudaStream_t st);
+// split API pieces
+cudaError_t simt_score_stats(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                             float* stats, void* ws, cudaStream_t st);
+cudaError_t stats_combine(const float* parts, int P, long long n_rows, float* lse2, cudaStream_t st);
+cudaError_t simt_score_finish(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                              const float* lse2, float* importance, void* ws, cudaStream_t st);
+
+// ---------------------------------------------------------------- fused tcgen05 score (score_fused.cu)
+bool fused_supported(const Geom& g, const Layout& lay, const void* Q, const void* K);
+size_t fused_score_ws_bytes(const Geom& g);
+cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                        float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
+
+// ---------------------------------------------------------------- select / gather (select.cu, gather.cu)
+size_t select_ws_bytes(int B, long long N, int chunk);
+cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int chunk, int pos0,
+                          long long K_c, int* ids, int* pos, int* n_kept, void* ws, cudaStream_t st);
+cudaError_t gather_launch(const int* tokens, const int* ids, const int* n_kept, int B, long long N, int* out,
+                          cudaStream_t st);
+
+}  // namespace sp

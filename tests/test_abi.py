@@ -1,0 +1,128 @@
+"""CPU checks of the C ABI boundary: the library loads, exports every symbol
+include/specprefill.h declares, and validates arguments on the host (no
+compute is launched without a GPU)."""
+import ctypes as C
+import math
+import os
+import re
+
+import pytest
+
+import paper_2502_02789_b200 as sp
+from paper_2502_02789_b200 import _lib
+from oracle import ref
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "specprefill.h")
+
+
+def _declared():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(sp_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_header_symbols_exported_and_bound():
+    names = _declared()
+    assert len(names) >= 15
+    h = C.CDLL(_lib.LIB_PATH)
+    for n in names:
+        assert hasattr(h, n), f"{n} declared in specprefill.h but not exported"
+        assert n in _lib.SIGNATURES, f"{n} has no Python binding"
+    assert set(_lib.SIGNATURES) == set(names)
+    assert sp.lib().sp_abi_version() == 1
+
+
+def test_spgen_library_exports():
+    h = C.CDLL(os.path.join(ROOT, "spgen", "libspgen.so"))
+    for n in ("spgen_fill_K", "spgen_fill_Q", "spgen_fill_tokens"):
+        assert hasattr(h, n)
+
+
+def test_status_strings():
+    for code in (0, 1, 2, 3, 5, 6, 7, 8):
+        assert sp.lib().sp_status_string(code).startswith(b"SP_")
+
+
+def test_kept_chunks_matches_oracle_rule():
+    L = sp.lib()
+    for keep in [0.001, 0.1, 0.2, 0.25, 0.3, 0.5, 0.6, 0.7, 0.9, 1.0] + [i / 10.0 for i in range(1, 11)]:
+        for n in [1, 2, 3, 7, 16, 25, 50, 128, 1024, 4096, 131072]:
+            assert L.sp_kept_chunks(n, keep) == ref.kept_chunk_count(n, keep)
+    assert L.sp_kept_chunks(10, 0.0) == -1 and L.sp_kept_chunks(10, 1.5) == -1 and L.sp_kept_chunks(0, 0.5) == -1
+
+
+def _geom(**kw):
+    d = dict(B=1, L=2, H=4, Hkv=2, d=16, R=2, R_valid=2, N=64, scale=0.25)
+    d.update(kw)
+    return _lib.sp_geom(**d)
+
+
+def _layout(g):
+    N, d = g.N, g.d
+    return _lib.sp_layout(k_b=g.L * g.Hkv * N * d, k_l=g.Hkv * N * d, k_g=N * d, k_i=d,
+                          q_b=g.L * g.R * g.H * d, q_l=g.R * g.H * d, q_r=g.H * d, q_h=d)
+
+
+FAKE = 1 << 20          # aligned fake device pointers: validation fails before any use
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(d=15), _lib.SP_EINVAL), (dict(d=8), _lib.SP_EINVAL), (dict(d=272), _lib.SP_EINVAL),
+    (dict(H=5), _lib.SP_EINVAL), (dict(N=0), _lib.SP_EINVAL), (dict(R_valid=3), _lib.SP_EINVAL),
+    (dict(R_valid=0), _lib.SP_EEMPTY), (dict(scale=float("nan")), _lib.SP_EINVAL), (dict(scale=0.0), _lib.SP_EINVAL),
+    (dict(B=0), _lib.SP_EINVAL),
+])
+def test_score_validation(kw, code):
+    g = _geom(**kw)
+    lay = _layout(_geom())
+    rc = sp.lib().sp_score(FAKE, FAKE, C.byref(g), C.byref(lay), FAKE, FAKE, 1 << 20, None)
+    assert rc == code
+
+
+def test_score_layout_validation():
+    g = _geom()
+    lay = _layout(g)
+    lay.k_i = 12                                         # 24 B: not a multiple of 16 B
+    assert sp.lib().sp_score(FAKE, FAKE, C.byref(g), C.byref(lay), FAKE, FAKE, 1 << 20, None) == _lib.SP_EINVAL
+    lay = _layout(g)
+    assert sp.lib().sp_score(FAKE + 2, FAKE, C.byref(g), C.byref(lay), FAKE, FAKE, 1 << 20, None) == _lib.SP_EINVAL
+    lay.k_g = -16
+    assert sp.lib().sp_score(FAKE, FAKE, C.byref(g), C.byref(lay), FAKE, FAKE, 1 << 20, None) == _lib.SP_EINVAL
+    assert sp.lib().sp_score(FAKE, FAKE, None, C.byref(lay), FAKE, FAKE, 1 << 20, None) == _lib.SP_EINVAL
+
+
+@pytest.mark.parametrize("keep,pool,chunk,code", [
+    (0.0, 3, 4, _lib.SP_EINVAL), (1.01, 3, 4, _lib.SP_EINVAL), (float("nan"), 3, 4, _lib.SP_EINVAL),
+    (0.5, 2, 4, _lib.SP_EINVAL), (0.5, 0, 4, _lib.SP_EINVAL), (0.5, 3, 0, _lib.SP_EINVAL),
+])
+def test_select_validation(keep, pool, chunk, code):
+    p = _lib.sp_select_params(keep_rate=keep, pool_k=pool, chunk=chunk, pos0=0)
+    rc = sp.lib().sp_select(FAKE, 1, 64, C.byref(p), FAKE, FAKE, FAKE, FAKE, 1 << 20, None)
+    assert rc == code
+    assert sp.lib().sp_select_workspace_bytes(1, 64, C.byref(p)) == 0
+
+
+def test_gather_validation():
+    assert sp.lib().sp_gather(None, FAKE, FAKE, 1, 10, FAKE, None) == _lib.SP_EINVAL
+    assert sp.lib().sp_gather(FAKE, FAKE, FAKE, 0, 10, FAKE, None) == _lib.SP_EINVAL
+
+
+def test_workspace_sizes_positive():
+    g = _geom()
+    assert sp.lib().sp_score_workspace_bytes(C.byref(g), _lib.SP_SCORE_SIMT) > 0
+    assert sp.lib().sp_score_split_workspace_bytes(C.byref(g)) > 0
+    p = _lib.sp_select_params(keep_rate=0.5, pool_k=3, chunk=4, pos0=0)
+    assert sp.lib().sp_select_workspace_bytes(1, 64, C.byref(p)) >= 16 * 4
+
+
+def test_no_cpu_fallback_without_device():
+    """With valid arguments and no usable sm_100 device the call fails (it
+    never computes on the CPU)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    g = _geom()
+    lay = _layout(g)
+    rc = sp.lib().sp_score(FAKE, FAKE, C.byref(g), C.byref(lay), FAKE, FAKE, 1 << 30, None)
+    assert rc in (_lib.SP_ECUDA, _lib.SP_EUNSUPPORTED)

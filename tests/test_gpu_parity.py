@@ -1,0 +1,227 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the float64 oracle.
+
+Element-by-element importance within 1e-3 relative; selected ids/positions
+bit-exact wherever the K_c-th chunk-score margin exceeds 1e-3 (else a valid
+top-K_c set); gathers always bit-exact.  Inputs are seeded and synthetic
+(spgen); the oracle regenerates them independently on the host.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2502_02789_b200 as sp
+from oracle import ref
+from spgen import cuda as spgen_cuda
+from spgen import gen
+from tests import _util
+
+pytestmark = pytest.mark.gpu
+
+ALGOS = ("fused", "simt")
+
+
+def _dev(bits: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).cuda()
+
+
+def _score(Q, K, w, algo, **kw):
+    try:
+        imp = sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo=algo, **kw)
+    except sp.SpError as e:
+        if algo == "fused" and e.code == 2:
+            pytest.skip("fused kernel unsupported for this geometry")
+        raise
+    sp.check_device_error()
+    return imp
+
+
+def _small_case(w: gen.Workload, algo: str, k_pad: int = 0):
+    """Host-generated inputs (numpy generator) for every request of w."""
+    Qb, Kb, tok = gen.gen_batch(w)
+    Q = _dev(Qb)
+    if k_pad:
+        Kfull = torch.zeros((w.B, w.L, w.Hkv, w.N + k_pad, w.d), dtype=torch.bfloat16, device="cuda")
+        Kfull[:, :, :, :w.N] = _dev(Kb)
+        K = Kfull[:, :, :, :w.N]
+    else:
+        K = _dev(Kb)
+    imp = _score(Q, K, w, algo).double().cpu().numpy()
+    for b in range(w.B):
+        exact = ref.token_importance(ref.bf16_to_f64(Qb[b]), ref.bf16_to_f64(Kb[b]), w.scale, w.Rv)
+        err = _util.rel_err(imp[b], exact)
+        assert err <= _util.REL_TOL, f"{w} b={b}: importance rel err {err:.3e}"
+    return Qb, Kb, tok, imp
+
+
+# ---------------------------------------------------------------- generator
+def test_device_generator_bitexact():
+    w = gen.CONFIGS["C1"].with_(N=1000, B=2, seed=3)
+    Q, K, tok = spgen_cuda.make_inputs(w, i0=0, k_pad=24)
+    Kh = K.view(torch.int16).cpu().numpy().view(np.uint16)
+    for (b, l, g) in [(0, 0, 0), (1, 31, 7), (0, 17, 3), (1, 5, 0)]:
+        np.testing.assert_array_equal(Kh[b, l, g], gen.gen_K(w, b, l, g))
+    Qh = Q.view(torch.int16).cpu().numpy().view(np.uint16)
+    for (b, l) in [(0, 0), (1, 31), (0, 9)]:
+        np.testing.assert_array_equal(Qh[b, l], gen.gen_Q(w, b, l))
+    np.testing.assert_array_equal(tok.cpu().numpy()[1], gen.gen_tokens(w, 1))
+    # a sequence shard: global tokens [400, 700)
+    _, Ks, _ = spgen_cuda.make_inputs(w, i0=400, n_local=300)
+    np.testing.assert_array_equal(Ks.view(torch.int16).cpu().numpy().view(np.uint16)[1, 2, 3],
+                                  gen.gen_K(w, 1, 2, 3, 400, 700))
+
+
+# ---------------------------------------------------------------- score, small geometries
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("seed", range(6))
+def test_c0_tiny(algo, seed):
+    w = gen.CONFIGS["C0"].with_(seed=seed)
+    Qb, Kb, tok, imp = _small_case(w, algo)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("variant", [
+    dict(N=1), dict(N=5), dict(N=127), dict(N=129), dict(N=1000),        # ragged tails, < one tile
+    dict(R=4, R_valid=2), dict(R=1), dict(R=9, N=300),                    # look-ahead rows
+    dict(d=32), dict(d=48), dict(d=64), dict(d=96), dict(d=128), dict(d=256),
+    dict(H=4, Hkv=4), dict(H=16, Hkv=2, R=4), dict(B=3, N=200), dict(L=5, N=333),
+])
+def test_geometries(algo, variant):
+    w = gen.CONFIGS["C0"].with_(**variant)
+    _small_case(w, algo)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_strided_cache(algo):
+    w = gen.CONFIGS["C0"].with_(N=300, B=2, d=64)
+    _small_case(w, algo, k_pad=40)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_8b_geometry_short(algo):
+    """Full 8B head geometry (L32 H32 Hkv8 d128 R8) at a short prompt."""
+    w = gen.CONFIGS["C1"].with_(N=700, seed=5)
+    _small_case(w, algo)
+
+
+# ---------------------------------------------------------------- select / gather
+def test_select_exact_ties_dyadic():
+    """Dyadic importances make every fp32 sum exact, so the GPU must reproduce
+    the oracle's tie-break (lowest chunk index) bit for bit."""
+    rng = np.random.default_rng(0)
+    for trial in range(20):
+        N = int(rng.integers(1, 3000))
+        chunk = int(rng.choice([1, 2, 4, 8, 32]))
+        imp = rng.integers(0, 4, size=(3, N)).astype(np.float64) / 64.0
+        keep = float(rng.choice([0.1, 0.3, 0.5, 0.9, 1.0]))
+        ids, pos, nk = sp.select(torch.tensor(imp, dtype=torch.float32, device="cuda"), keep, 1, chunk, pos0=7)
+        for b in range(3):
+            o = ref.select(imp[b], keep, 1, chunk, 7)
+            n = int(nk[b])
+            assert n == o["n_kept"]
+            np.testing.assert_array_equal(ids[b, :n].cpu().numpy(), o["ids"])
+            np.testing.assert_array_equal(pos[b, :n].cpu().numpy(), o["pos"])
+
+
+@pytest.mark.parametrize("pool_k,chunk", [(1, 1), (3, 4), (5, 32), (7, 5), (9, 1), (5, 2048)])
+def test_select_parity_random(pool_k, chunk):
+    rng = np.random.default_rng(pool_k * 100 + chunk)
+    B, N = 4, 5000
+    imp = rng.random((B, N)) ** 4 + 1e-6
+    imp32 = imp.astype(np.float32)
+    ids, pos, nk = sp.select(torch.tensor(imp32, device="cuda"), 0.2, pool_k, chunk)
+    for b in range(B):
+        o = ref.select(imp32[b].astype(np.float64), 0.2, pool_k, chunk)
+        _util.check_selection(ids[b].cpu().numpy(), pos[b].cpu().numpy(), int(nk[b]), o, chunk, N, 0)
+
+
+def test_select_keep_all_and_single_chunk():
+    imp = torch.rand((2, 77), device="cuda") + 0.01
+    ids, pos, nk = sp.select(imp, 1.0, 3, 8, pos0=5)
+    assert nk.tolist() == [77, 77]
+    assert ids[0].tolist() == list(range(77)) and pos[1].tolist() == list(range(5, 82))
+    ids, pos, nk = sp.select(imp[:, :3].contiguous(), 0.1, 5, 32)
+    assert nk.tolist() == [3, 3] and ids[0, :3].tolist() == [0, 1, 2]
+
+
+def test_gather_bitexact():
+    rng = np.random.default_rng(1)
+    B, N = 3, 4000
+    tok = torch.tensor(rng.integers(0, 2**31 - 1, size=(B, N)), dtype=torch.int32, device="cuda")
+    nk = torch.tensor([0, 1234, 4000], dtype=torch.int32, device="cuda")
+    ids = torch.zeros((B, N), dtype=torch.int32, device="cuda")
+    for b, n in enumerate(nk.tolist()):
+        ids[b, :n] = torch.tensor(np.sort(rng.choice(N, n, replace=False)), dtype=torch.int32)
+    out = torch.full((B, N), -1, dtype=torch.int32, device="cuda")
+    sp.gather(tok, ids, nk, out=out)
+    for b, n in enumerate(nk.tolist()):
+        assert torch.equal(out[b, :n], tok[b][ids[b, :n].long()])
+        assert (out[b, n:] == -1).all()
+
+
+# ---------------------------------------------------------------- errors, determinism
+def test_nonfinite_flag():
+    w = gen.CONFIGS["C0"]
+    Qb, Kb, _ = gen.gen_batch(w)
+    K = _dev(Kb)
+    K[0, 1, 0, 5, 0] = float("inf")
+    with pytest.raises(sp.SpError) as e:
+        sp.score(_dev(Qb), K, scale=w.scale, algo="simt")
+        sp.check_device_error()
+    assert e.value.code == 5
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_deterministic(algo):
+    w = gen.CONFIGS["C1"].with_(N=2048)
+    Q, K, T = spgen_cuda.make_inputs(w)
+    a = _score(Q, K, w, algo).clone()
+    b = _score(Q, K, w, algo)
+    assert torch.equal(a, b)
+
+
+# ---------------------------------------------------------------- full configs
+def _full_config(w: gen.Workload, algo: str, requests, keeps=None):
+    Q, K, T = spgen_cuda.make_inputs(w)
+    imp = _score(Q, K, w, algo)
+    regimes = []
+    exact = {b: _util.oracle_importance(w, b) for b in requests}
+    for keep in (keeps or [w.keep]):
+        ids, pos, nk = sp.select(imp, keep, w.pool_k, w.chunk, w.pos0)
+        out = sp.gather(T, ids, nk)
+        sp.check_device_error()
+        for b in requests:
+            o = ref.select(exact[b], keep, w.pool_k, w.chunk, w.pos0)
+            o["imp"] = exact[b]
+            err = _util.rel_err(imp[b].double().cpu().numpy(), o["imp"])
+            assert err <= _util.REL_TOL, f"b={b}: importance rel err {err:.3e}"
+            n = int(nk[b])
+            regimes.append(_util.check_selection(ids[b].cpu().numpy(), pos[b].cpu().numpy(), n, o, w.chunk, w.N,
+                                                 w.pos0))
+            idb = ids[b, :n].long()
+            assert torch.equal(out[b, :n], T[b][idb])
+    return regimes
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_c1_full(algo):
+    _full_config(gen.CONFIGS["C1"], algo, [0])
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_c2_sampled_requests(algo):
+    """64 x 1K batch at full size; the oracle checks a sample of requests."""
+    _full_config(gen.CONFIGS["C2"], algo, [0, 21, 63])
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_c3_full(algo):
+    _full_config(gen.CONFIGS["C3"], algo, [0])
+
+
+@pytest.mark.slow
+def test_c4_keep_sweep():
+    w = gen.CONFIGS["C4"]
+    regimes = _full_config(w, "fused" if "fused" in ALGOS else "simt", [0], keeps=[i / 10.0 for i in range(1, 10)])
+    assert len(regimes) == 9
