@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--algo", default="fused", choices=["fused", "simt", "auto"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-layers", type=int, default=4)
+    ap.add_argument("--cpu-sample-layers", type=int, default=32)
     return ap.parse_args()
 
 

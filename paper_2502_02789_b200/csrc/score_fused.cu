@@ -1,11 +1,744 @@
-// Fused tcgen05 score kernel (placeholder until the kernel lands).
+// Fused token-importance kernel for sm_100a: one HBM read of K.
+//
+// Computes, for every request b and prompt token i (O1-O4;
+// PAPER.md sec:token_importance eq. P:105-107 and sec:attn_agg P:119):
+//   x[l,h,r,i]  = scale*log2(e) * <Q[b][l][r][h], K[b][l][h/G][i]>   (log2-domain logit)
+//   lse2[l,h,r] = log2 sum_i 2^x[l,h,r,i]            (softmax over the N prompt keys, Z2)
+//   acc[r,i]    = max_{l,h} (x - lse2)               (max over H and L, log domain)
+//   imp[b][i]   = (1/Rv) sum_{r<Rv} 2^acc[r,i]       (mean over the valid look-ahead rows)
+//
+// Design:
+// * Persistent cooperative grid, one CTA per SM.  A request's N tokens are cut
+//   into 128-token tiles and its L*Hkv (layer, kv-head) "units" into groups; a
+//   job = (request, token group, unit group).  All jobs of one request run in
+//   the same wave of CTAs, so every CTA that shares a unit is co-resident.
+// * Warp roles (384 threads): warp 0 TMA producer, warp 1 tcgen05.mma issuer
+//   (+TMEM owner), warps 4-7 softmax statistics, warps 8-11 max-aggregation.
+// * K tiles [128 tokens x d] bf16 stream HBM -> SMEM by TMA (SWIZZLE_128B);
+//   the unit's query block [G*Rv x d] is the MMA B operand; the logits
+//   D[128 x G*Rv] fp32 accumulate in TMEM and STAY there: every tile of the
+//   unit is resident (tiles_per_cta * Ncols <= 256 columns, two unit slots).
+// * Statistics warps reduce each unit's columns over the CTA's tokens (online
+//   (m, l) in the log2 domain), publish the CTA partial to global memory and
+//   bump the unit's counter.  Aggregation warps wait for all token groups of
+//   the unit, combine the partials in fixed order (deterministic lse), re-read
+//   the logits from TMEM and fold max_h (x - lse2) into a per-token running
+//   max kept in SMEM.  K is read from HBM exactly once; logits never leave
+//   the chip.
+// * Cross-unit-group max: partial acc maps go to the workspace and the CTAs of
+//   a token group split the final mean-of-exp2 among themselves.
 #include "sp_internal.h"
 
+#include <cuda.h>
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
 namespace sp {
-bool fused_supported(const Geom&, const Layout&, const void*, const void*) { return false; }
-size_t fused_score_ws_bytes(const Geom&) { return 0; }
-cudaError_t fused_score(const __nv_bfloat16*, const __nv_bfloat16*, const Geom&, const Layout&, float*, void*, size_t,
-                        cudaStream_t) {
-  return cudaErrorNotSupported;
+namespace {
+
+constexpr int kThreads = 384;
+constexpr int kTileM = 128;
+constexpr int kStatsWarp0 = 4;
+constexpr int kFinalWarp0 = 8;
+constexpr int kMaxStages = 8;
+constexpr int kMaxChunks = 8;          // NCP <= 128 columns (16-column chunks)
+constexpr int kTmemCols = 512;
+constexpr int kSmemLimit = 232448;     // sm_100 max dynamic shared memory per block
+
+// ------------------------------------------------------------------ parameters
+struct FusedParams {
+  CUtensorMap tmK;                     // 5-D: {d, N, Hkv, L, B}
+  CUtensorMap tmQ;                     // 5-D: {d, H, R, L, B}
+  int B, L, Hkv, G, Rv, d, N;
+  int T, U;                            // tiles / units per request
+  int n_tg, n_ug, J;                   // token groups, unit groups, jobs per request
+  long long total_jobs;
+  int NC, NCP, W, nkb, stages, nbuf, slot_cols, tpc;
+  float xs;                            // scale * log2(e)
+  uint32_t idesc;                      // tcgen05 instruction descriptor
+  uint32_t layout_type;                // UMMA smem descriptor swizzle code
+  // smem carve (byte offsets from the 1024-aligned base)
+  uint32_t off_k, off_q, off_acc, off_red, off_lse, off_bar;
+  uint32_t k_stage_bytes, q_slot_bytes;
+  // workspace
+  float2* part;                        // [B][U][NC][n_tg] (m2, l)
+  unsigned* cnt;                       // [B][U]       exchange counters (self-cleaning)
+  float* accpart;                      // [B][n_ug][Rv][N]
+  unsigned* fin_cnt;                   // [B][n_tg]    finalize counters (self-cleaning)
+  float* imp;                          // [B][N]
+  int* err;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait for an mbarrier phase.  Bounded: a pipeline that never completes
+// (which would be a bug) traps after ~4 s instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (!mbar_try_wait(bar, parity)) {
+    if (globaltimer_ns() - t0 > 4000000000ull) asm volatile("trap;");
+  }
+}
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2,
+                                            int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t sbo_bytes, uint32_t layout_type) {
+  uint64_t desc = 0;
+  desc |= (uint64_t)((saddr >> 4) & 0x3FFFu);               // [0,14)  start address >> 4
+  desc |= (uint64_t)1u << 16;                                // [16,30) LBO (unused for swizzled K-major)
+  desc |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;     // [32,46) SBO: 8-row group stride
+  desc |= (uint64_t)1u << 46;                                // [46,48) version = 1 (sm_100)
+  desc |= (uint64_t)(layout_type & 7u) << 61;                // [61,64) swizzle mode
+  return desc;
+}
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void set_err(int* err, int code) { atomicCAS(err, 0, code); }
+
+// Spin (one thread) until *p >= target; bounded so a broken exchange can never hang the GPU.
+__device__ __forceinline__ void spin_geq(const unsigned* p, unsigned target, int* err) {
+  long long it = 0;
+  while (ld_acquire(p) < target) {
+    if (++it > (1LL << 25)) {
+      set_err(err, kDevTimeout);
+      return;
+    }
+    if (it > 64) __nanosleep(64);
+  }
+}
+
+// Transposed butterfly over 16 columns x 32 lanes: returns, in every lane,
+// the reduction over all 32 lanes of column (lane >> 1).  15 + 1 shuffles.
+template <bool kMax>
+__device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
+  auto op = [](float a, float b) { return kMax ? fmaxf(a, b) : a + b; };
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool up = lane & 16;
+    float send = up ? v[i] : v[i + 8], keep = up ? v[i + 8] : v[i];
+    v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool up = lane & 8;
+    float send = up ? v[i] : v[i + 4], keep = up ? v[i + 4] : v[i];
+    v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool up = lane & 4;
+    float send = up ? v[i] : v[i + 2], keep = up ? v[i + 2] : v[i];
+    v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+  }
+  {
+    const bool up = lane & 2;
+    float send = up ? v[0] : v[1], keep = up ? v[1] : v[0];
+    v[0] = op(keep, __shfl_xor_sync(0xffffffffu, send, 2));
+  }
+  return op(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
+}
+
+struct Job {
+  int b, tg, ug, t_lo, t_hi, u_lo, u_hi;
+};
+__device__ __forceinline__ Job decode_job(const FusedParams& p, long long job) {
+  Job j;
+  j.b = (int)(job / p.J);
+  const int r = (int)(job % p.J);
+  j.tg = r / p.n_ug;
+  j.ug = r % p.n_ug;
+  j.t_lo = (int)((long long)j.tg * p.T / p.n_tg);
+  j.t_hi = (int)((long long)(j.tg + 1) * p.T / p.n_tg);
+  j.u_lo = (int)((long long)j.ug * p.U / p.n_ug);
+  j.u_hi = (int)((long long)(j.ug + 1) * p.U / p.n_ug);
+  return j;
+}
+
+// ------------------------------------------------------------------ the kernel
+__global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ FusedParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+  // barrier map: full[S] empty[S] qfull[2] qempty[2] tfull[2] tempty[2]; then tmem base
+  const uint32_t bar_full = smem_u32(bars), bar_empty = bar_full + 8 * p.stages;
+  const uint32_t bar_qfull = bar_empty + 8 * p.stages, bar_qempty = bar_qfull + 16;
+  const uint32_t bar_tfull = bar_qempty + 16, bar_tempty = bar_tfull + 16;
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 2 * p.stages + 8);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(bar_qfull + 8 * s, 1);
+      mbar_init(bar_qempty + 8 * s, 1);
+      mbar_init(bar_tfull + 8 * s, 1);
+      mbar_init(bar_tempty + 8 * s, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_tmap(&p.tmK);
+    prefetch_tmap(&p.tmQ);
+  }
+  // zero both Q slots once: rows >= NC (MMA padding columns) are never written by TMA
+  for (uint32_t o = threadIdx.x * 16; o < 2 * p.q_slot_bytes; o += kThreads * 16)
+    *reinterpret_cast<uint4*>(smem + p.off_q + o) = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_s)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_s;
+
+  if (warp == 0) {
+    // ================================================================ TMA producer
+    if (lane == 0) {
+      uint32_t stage = 0, sphase = 0, ui = 0;
+      for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
+        const Job jb = decode_job(p, job);
+        for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
+          const int l = u / p.Hkv, g = u % p.Hkv;
+          const uint32_t qs = ui & 1, qpar = (ui >> 1) & 1;
+          mbar_wait(bar_qempty + 8 * qs, qpar ^ 1);
+          mbar_expect_tx(bar_qfull + 8 * qs, (uint32_t)(p.NC * p.d * 2));
+          const uint32_t qdst = smem_u32(smem + p.off_q + qs * p.q_slot_bytes);
+          for (int kb = 0; kb < p.nkb; ++kb)
+            tma_load_5d(qdst + kb * (p.NCP * p.W * 2), &p.tmQ, bar_qfull + 8 * qs, kb * p.W, g * p.G, 0, l, jb.b);
+          for (int t = jb.t_lo; t < jb.t_hi; ++t) {
+            mbar_wait(bar_empty + 8 * stage, sphase ^ 1);
+            mbar_expect_tx(bar_full + 8 * stage, p.k_stage_bytes);
+            const uint32_t kdst = smem_u32(smem + p.off_k + stage * p.k_stage_bytes);
+            for (int kb = 0; kb < p.nkb; ++kb)
+              tma_load_5d(kdst + kb * (kTileM * p.W * 2), &p.tmK, bar_full + 8 * stage, kb * p.W, t * kTileM, g, l,
+                          jb.b);
+            if (++stage == (uint32_t)p.stages) { stage = 0; sphase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================================ MMA issuer
+    if (lane == 0) {
+      uint32_t stage = 0, sphase = 0, ui = 0;
+      const uint32_t sbo = 8 * p.W * 2;
+      for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
+        const Job jb = decode_job(p, job);
+        for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
+          const uint32_t slot = ui % p.nbuf, tpar = (ui / p.nbuf) & 1;
+          const uint32_t qs = ui & 1, qpar = (ui >> 1) & 1;
+          mbar_wait(bar_tempty + 8 * slot, tpar ^ 1);
+          mbar_wait(bar_qfull + 8 * qs, qpar);
+          tc_fence_after();
+          const uint32_t qbase = smem_u32(smem + p.off_q + qs * p.q_slot_bytes);
+          for (int t = jb.t_lo; t < jb.t_hi; ++t) {
+            mbar_wait(bar_full + 8 * stage, sphase);
+            tc_fence_after();
+            const uint32_t kbase = smem_u32(smem + p.off_k + stage * p.k_stage_bytes);
+            const uint32_t dcol = tmem + slot * p.slot_cols + (uint32_t)(t - jb.t_lo) * p.NCP;
+            for (int kb = 0; kb < p.nkb; ++kb) {
+              for (int ks = 0; ks < p.W / 16; ++ks) {
+                const uint64_t a = make_sdesc(kbase + kb * (kTileM * p.W * 2) + ks * 32, sbo, p.layout_type);
+                const uint64_t b = make_sdesc(qbase + kb * (p.NCP * p.W * 2) + ks * 32, sbo, p.layout_type);
+                umma_bf16(dcol, a, b, p.idesc, (kb | ks) != 0);
+              }
+            }
+            umma_commit(bar_empty + 8 * stage);
+            if (++stage == (uint32_t)p.stages) { stage = 0; sphase ^= 1; }
+          }
+          umma_commit(bar_qempty + 8 * qs);
+          umma_commit(bar_tfull + 8 * slot);
+        }
+      }
+    }
+  } else if (warp >= kStatsWarp0 && warp < kFinalWarp0) {
+    // ================================================================ softmax statistics
+    const int q = warp & 3;                       // TMEM lane quarter
+    const int nch = p.NCP / 16;
+    float2* red = reinterpret_cast<float2*>(smem + p.off_red);   // [2][4][NCP]
+    uint32_t ui = 0;
+    for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
+      const Job jb = decode_job(p, job);
+      for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
+        const uint32_t slot = ui % p.nbuf, tpar = (ui / p.nbuf) & 1;
+        mbar_wait(bar_tfull + 8 * slot, tpar);
+        tc_fence_after();
+        float M[kMaxChunks], Ls[kMaxChunks];
+#pragma unroll
+        for (int k = 0; k < kMaxChunks; ++k) { M[k] = -CUDART_INF_F; Ls[k] = 0.f; }
+        for (int t = jb.t_lo; t < jb.t_hi; ++t) {
+          const bool valid = (long long)t * kTileM + q * 32 + lane < p.N;
+          const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + slot * p.slot_cols + (uint32_t)(t - jb.t_lo) * p.NCP;
+#pragma unroll
+          for (int k = 0; k < kMaxChunks; ++k) {
+            if (k < nch) {
+              float x[16], e[16];
+              tmem_ld16(tbase + k * 16, x);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) { x[i] = valid ? x[i] * p.xs : -CUDART_INF_F; e[i] = x[i]; }
+              const float mt = transpose_reduce16<true>(e, lane);            // column (lane>>1) max
+              const float ms = (mt == -CUDART_INF_F) ? 0.f : mt;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float mi = __shfl_sync(0xffffffffu, ms, 2 * i);
+                e[i] = valid ? exp2f(x[i] - mi) : 0.f;
+              }
+              const float st = transpose_reduce16<false>(e, lane);
+              // merge (mt, st) into the running (M, L) of column 16k + (lane>>1)
+              const float Mn = fmaxf(M[k], mt);
+              if (Mn != -CUDART_INF_F) {
+                const float a = (M[k] == -CUDART_INF_F) ? 0.f : Ls[k] * exp2f(M[k] - Mn);
+                const float c = (mt == -CUDART_INF_F) ? 0.f : st * exp2f(mt - Mn);
+                Ls[k] = a + c;
+                M[k] = Mn;
+              }
+            }
+          }
+        }
+        // CTA partial: combine the 4 statistics warps in fixed order, publish, count
+        float2* rb = red + (ui & 1) * 4 * p.NCP;
+        if ((lane & 1) == 0) {
+#pragma unroll
+          for (int k = 0; k < kMaxChunks; ++k)
+            if (k < nch) rb[q * p.NCP + 16 * k + (lane >> 1)] = make_float2(M[k], Ls[k]);
+        }
+        named_bar(1, 128);
+        if (q == 0) {
+          const long long ubase = (long long)jb.b * p.U + u;
+          for (int c = lane; c < p.NC; c += 32) {
+            float mm = -CUDART_INF_F;
+            for (int w = 0; w < 4; ++w) mm = fmaxf(mm, rb[w * p.NCP + c].x);
+            float ss = 0.f;
+            for (int w = 0; w < 4; ++w) {
+              const float2 v = rb[w * p.NCP + c];
+              if (v.y > 0.f) ss += v.y * exp2f(v.x - mm);
+            }
+            p.part[(ubase * p.NC + c) * p.n_tg + jb.tg] = make_float2(mm, ss);
+          }
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) atomicAdd(p.cnt + ubase, 1u);
+        }
+      }
+    }
+  } else if (warp >= kFinalWarp0) {
+    // ================================================================ (l,h)-max aggregation
+    const int q = warp & 3;
+    const int nch = p.NCP / 16;
+    float* acc = reinterpret_cast<float*>(smem + p.off_acc);      // [tpc][Rv][128]
+    float* lse_s = reinterpret_cast<float*>(smem + p.off_lse);    // [2][NCP]
+    const int tok = q * 32 + lane;
+    uint32_t ui = 0;
+    for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
+      const Job jb = decode_job(p, job);
+      const int ntile = jb.t_hi - jb.t_lo;
+      for (int t = 0; t < ntile; ++t)
+        for (int r = 0; r < p.Rv; ++r) acc[(t * p.Rv + r) * kTileM + tok] = -CUDART_INF_F;
+      for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
+        const uint32_t slot = ui % p.nbuf, tpar = (ui / p.nbuf) & 1;
+        const long long ubase = (long long)jb.b * p.U + u;
+        float* ls = lse_s + (ui & 1) * p.NCP;
+        if (q == 0) {
+          if (lane == 0) spin_geq(p.cnt + ubase, (unsigned)p.n_tg, p.err);
+          __syncwarp();
+          __threadfence();
+          for (int c = lane; c < p.NC; c += 32) {
+            const float2* src = p.part + (ubase * p.NC + c) * p.n_tg;
+            float mm = -CUDART_INF_F;
+            for (int s = 0; s < p.n_tg; ++s) mm = fmaxf(mm, __ldcg(&src[s].x));
+            float ss = 0.f;
+            for (int s = 0; s < p.n_tg; ++s) {
+              const float2 v = __ldcg(&src[s]);
+              if (v.y > 0.f) ss += v.y * exp2f(v.x - mm);
+            }
+            const float l2 = mm + log2f(ss);
+            if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
+            ls[c] = l2;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            // self-cleaning counter: the last of the 2*n_tg arrivals resets it to zero
+            if (atomicAdd(p.cnt + ubase, 1u) == 2u * p.n_tg - 1u) atomicExch(p.cnt + ubase, 0u);
+          }
+        }
+        named_bar(2, 128);
+        mbar_wait(bar_tfull + 8 * slot, tpar);
+        tc_fence_after();
+        for (int t = 0; t < ntile; ++t) {
+          const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + slot * p.slot_cols + (uint32_t)t * p.NCP;
+          int r = 0, hh = 0;
+          float best = -CUDART_INF_F;
+          float* arow = acc + (t * p.Rv) * kTileM + tok;
+#pragma unroll
+          for (int k = 0; k < kMaxChunks; ++k) {
+            if (k < nch) {
+              float x[16];
+              tmem_ld16(tbase + k * 16, x);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const int c = 16 * k + i;
+                if (c < p.NC) {
+                  best = fmaxf(best, x[i] * p.xs - ls[c]);
+                  if (++hh == p.G) {
+                    float* a = arow + r * kTileM;
+                    *a = fmaxf(*a, best);
+                    best = -CUDART_INF_F;
+                    hh = 0;
+                    ++r;
+                  }
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_tempty + 8 * slot);
+      }
+      // ---- job epilogue: importance = mean_r 2^acc (possibly across unit groups)
+      const float inv = 1.f / (float)p.Rv;
+      if (p.n_ug == 1) {
+        for (int t = 0; t < ntile; ++t) {
+          const long long i = (long long)(jb.t_lo + t) * kTileM + tok;
+          if (i < p.N) {
+            float s = 0.f;
+            for (int r = 0; r < p.Rv; ++r) s += exp2f(acc[(t * p.Rv + r) * kTileM + tok]);
+            p.imp[(long long)jb.b * p.N + i] = s * inv;
+          }
+        }
+      } else {
+        for (int t = 0; t < ntile; ++t) {
+          const long long i = (long long)(jb.t_lo + t) * kTileM + tok;
+          if (i < p.N)
+            for (int r = 0; r < p.Rv; ++r)
+              p.accpart[(((long long)jb.b * p.n_ug + jb.ug) * p.Rv + r) * p.N + i] = acc[(t * p.Rv + r) * kTileM + tok];
+        }
+        __threadfence();
+        named_bar(2, 128);
+        unsigned* fc = p.fin_cnt + (long long)jb.b * p.n_tg + jb.tg;
+        if (threadIdx.x == kFinalWarp0 * 32) {
+          atomicAdd(fc, 1u);
+          spin_geq(fc, (unsigned)p.n_ug, p.err);
+          __threadfence();
+        }
+        named_bar(2, 128);
+        // this CTA finalises slice ug of the token group's tokens
+        const long long g_lo = (long long)jb.t_lo * kTileM;
+        const long long g_hi = min((long long)jb.t_hi * kTileM, (long long)p.N);
+        const long long n = g_hi - g_lo;
+        const long long s_lo = g_lo + n * jb.ug / p.n_ug, s_hi = g_lo + n * (jb.ug + 1) / p.n_ug;
+        for (long long i = s_lo + tok; i < s_hi; i += kTileM) {
+          float s = 0.f;
+          for (int r = 0; r < p.Rv; ++r) {
+            float m = -CUDART_INF_F;
+            for (int g = 0; g < p.n_ug; ++g)
+              m = fmaxf(m, __ldcg(&p.accpart[(((long long)jb.b * p.n_ug + g) * p.Rv + r) * p.N + i]));
+            s += exp2f(m);
+          }
+          p.imp[(long long)jb.b * p.N + i] = s * inv;
+        }
+        named_bar(2, 128);
+        if (threadIdx.x == kFinalWarp0 * 32) {
+          if (atomicAdd(fc, 1u) == 2u * p.n_ug - 1u) atomicExch(fc, 0u);
+        }
+      }
+    }
+  }
+
+  // ---- teardown
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+struct Plan {
+  int P = 0, n_tg = 0, n_ug = 0, J = 0, T = 0, U = 0, tpc = 0, upc = 0;
+  int NC = 0, NCP = 0, W = 0, nkb = 0, stages = 0, nbuf = 0, slot_cols = 0;
+  long long total_jobs = 0;
+  uint32_t off_k = 0, off_q = 0, off_acc = 0, off_red = 0, off_lse = 0, off_bar = 0, smem = 0;
+  uint32_t k_stage_bytes = 0, q_slot_bytes = 0;
+  size_t ws_part = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0;
+  bool ok = false;
+};
+
+int sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 148;
+  }
+  return n;
+}
+
+// Layout of shared memory for a given (tpc, stage count); returns total bytes.
+uint32_t carve(Plan& pl, int Rv, int stages) {
+  uint32_t o = 0;
+  pl.off_k = o;
+  o += (uint32_t)stages * pl.k_stage_bytes;
+  pl.off_q = o;
+  o += 2 * pl.q_slot_bytes;
+  pl.off_acc = o;
+  o += (uint32_t)pl.tpc * Rv * kTileM * 4;
+  pl.off_red = o;
+  o += 2 * 4 * pl.NCP * 8;
+  pl.off_lse = o;
+  o += 2 * pl.NCP * 4;
+  o = (o + 15) & ~15u;
+  pl.off_bar = o;
+  o += (2 * stages + 8) * 8 + 16;
+  return o + 1024;                                   // slack for the manual 1024-byte alignment
+}
+
+Plan make_plan(const Geom& g) {
+  Plan pl;
+  pl.NC = g.G * g.Rv;
+  pl.NCP = ((pl.NC + 15) / 16) * 16;
+  if (pl.NCP > 16 * kMaxChunks) return pl;
+  pl.W = (g.d % 64 == 0) ? 64 : (g.d % 32 == 0 ? 32 : 16);
+  pl.nkb = g.d / pl.W;
+  pl.k_stage_bytes = (uint32_t)kTileM * g.d * 2;
+  pl.q_slot_bytes = (uint32_t)pl.NCP * g.d * 2;
+  if (pl.q_slot_bytes * 2 > 64 * 1024) return pl;
+  pl.P = sm_count();
+  pl.T = (int)((g.N + kTileM - 1) / kTileM);
+  pl.U = g.L * g.Hkv;
+  // choose (n_tg, n_ug): J = n_tg*n_ug divides the grid so a request never
+  // straddles two waves; minimise waves * (tiles x units per job)
+  double best = 1e300;
+  for (int J = 1; J <= pl.P; ++J) {
+    if (pl.P % J) continue;
+    for (int n_tg = 1; n_tg <= J; ++n_tg) {
+      if (J % n_tg) continue;
+      const int n_ug = J / n_tg;
+      if (n_tg > pl.T || n_ug > pl.U) continue;
+      const int tpc = (pl.T + n_tg - 1) / n_tg, upc = (pl.U + n_ug - 1) / n_ug;
+      if (tpc * pl.NCP > kTmemCols) continue;
+      const int nbuf = (tpc * pl.NCP <= kTmemCols / 2) ? 2 : 1;
+      const long long jobs = (long long)g.B * J;
+      const int grid = (int)std::min<long long>(pl.P, jobs);
+      const long long waves = (jobs + grid - 1) / grid;
+      double cost = (double)waves * tpc * upc * pl.k_stage_bytes;
+      cost *= (nbuf == 1) ? 1.5 : 1.0;                                   // no TMEM double buffering
+      cost += (double)waves * upc * (n_tg * pl.NC * 8.0) * 0.25;         // partial-stats reads (L2)
+      cost += (double)waves * (n_ug > 1 ? n_ug * g.Rv * tpc * kTileM * 4.0 : 0.0);
+      if (cost < best) {
+        best = cost;
+        pl.J = J; pl.n_tg = n_tg; pl.n_ug = n_ug; pl.tpc = tpc; pl.upc = upc; pl.nbuf = nbuf;
+      }
+    }
+  }
+  if (pl.J == 0) return pl;
+  pl.slot_cols = (pl.nbuf == 2) ? kTmemCols / 2 : kTmemCols;
+  pl.total_jobs = (long long)g.B * pl.J;
+  int stages = kMaxStages;
+  while (stages >= 2 && carve(pl, g.Rv, stages) > (uint32_t)kSmemLimit) --stages;
+  if (stages < 2) return pl;
+  pl.stages = stages;
+  pl.smem = carve(pl, g.Rv, stages);
+  pl.ws_part = align256((size_t)g.B * pl.U * pl.NC * pl.n_tg * sizeof(float2));
+  pl.ws_cnt = align256((size_t)g.B * pl.U * sizeof(unsigned));
+  pl.ws_acc = pl.n_ug > 1 ? align256((size_t)g.B * pl.n_ug * g.Rv * g.N * sizeof(float)) : 0;
+  pl.ws_fin = align256((size_t)g.B * pl.n_tg * sizeof(unsigned));
+  pl.ok = true;
+  return pl;
+}
+
+bool encode_maps(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay, const Plan& pl,
+                 CUtensorMap* tmK, CUtensorMap* tmQ) {
+  PFN_encodeTiled_t enc = encode_fn();
+  if (enc == nullptr) return false;
+  const CUtensorMapSwizzle sw = pl.W == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                           : (pl.W == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  // strides of size-1 dims are irrelevant; give them a harmless contiguous value
+  auto fix = [](long long stride, long long prev_extent_bytes, long long size) -> cuuint64_t {
+    return (size == 1 || stride == 0) ? (cuuint64_t)prev_extent_bytes : (cuuint64_t)(stride * 2);
+  };
+  {
+    cuuint64_t dims[5] = {(cuuint64_t)g.d, (cuuint64_t)g.N, (cuuint64_t)g.Hkv, (cuuint64_t)g.L, (cuuint64_t)g.B};
+    cuuint64_t s1 = fix(lay.k_i, (long long)g.d * 2, g.N);
+    cuuint64_t s2 = fix(lay.k_g, (long long)s1 * g.N, g.Hkv);
+    cuuint64_t s3 = fix(lay.k_l, (long long)s2 * g.Hkv, g.L);
+    cuuint64_t s4 = fix(lay.k_b, (long long)s3 * g.L, g.B);
+    cuuint64_t strides[4] = {s1, s2, s3, s4};
+    cuuint32_t box[5] = {(cuuint32_t)pl.W, (cuuint32_t)kTileM, 1, 1, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    if (enc(tmK, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<__nv_bfloat16*>(K), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  {
+    cuuint64_t dims[5] = {(cuuint64_t)g.d, (cuuint64_t)g.H, (cuuint64_t)g.R, (cuuint64_t)g.L, (cuuint64_t)g.B};
+    cuuint64_t s1 = fix(lay.q_h, (long long)g.d * 2, g.H);
+    cuuint64_t s2 = fix(lay.q_r, (long long)s1 * g.H, g.R);
+    cuuint64_t s3 = fix(lay.q_l, (long long)s2 * g.R, g.L);
+    cuuint64_t s4 = fix(lay.q_b, (long long)s3 * g.L, g.B);
+    cuuint64_t strides[4] = {s1, s2, s3, s4};
+    cuuint32_t box[5] = {(cuuint32_t)pl.W, (cuuint32_t)g.G, (cuuint32_t)g.Rv, 1, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    if (enc(tmQ, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<__nv_bfloat16*>(Q), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
+}
+
+}  // namespace
+
+bool fused_supported(const Geom& g, const Layout&, const void*, const void*) {
+  if (g.G > 256 || g.Rv > 256) return false;         // TMA box dims
+  return make_plan(g).ok;
+}
+
+size_t fused_score_ws_bytes(const Geom& g) {
+  Plan pl = make_plan(g);
+  if (!pl.ok) return 0;
+  return pl.ws_part + pl.ws_cnt + pl.ws_acc + pl.ws_fin;
+}
+
+cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                        float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
+  Plan pl = make_plan(g);
+  if (!pl.ok || ws_bytes < pl.ws_part + pl.ws_cnt + pl.ws_acc + pl.ws_fin) return cudaErrorInvalidValue;
+  static FusedParams p;                               // large (two tensor maps); host-side scratch
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  std::memset(&p, 0, sizeof(p));
+  if (!encode_maps(Q, K, g, lay, pl, &p.tmK, &p.tmQ)) return cudaErrorInvalidValue;
+  p.B = g.B; p.L = g.L; p.Hkv = g.Hkv; p.G = g.G; p.Rv = g.Rv; p.d = g.d; p.N = (int)g.N;
+  p.T = pl.T; p.U = pl.U; p.n_tg = pl.n_tg; p.n_ug = pl.n_ug; p.J = pl.J; p.total_jobs = pl.total_jobs;
+  p.NC = pl.NC; p.NCP = pl.NCP; p.W = pl.W; p.nkb = pl.nkb; p.stages = pl.stages; p.nbuf = pl.nbuf;
+  p.slot_cols = pl.slot_cols; p.tpc = pl.tpc;
+  p.xs = g.scale * kLog2e;
+  p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(pl.NCP >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
+  p.layout_type = pl.W == 64 ? 2u : (pl.W == 32 ? 4u : 6u);
+  p.off_k = pl.off_k; p.off_q = pl.off_q; p.off_acc = pl.off_acc; p.off_red = pl.off_red; p.off_lse = pl.off_lse;
+  p.off_bar = pl.off_bar; p.k_stage_bytes = pl.k_stage_bytes; p.q_slot_bytes = pl.q_slot_bytes;
+  char* w = reinterpret_cast<char*>(ws);
+  p.part = reinterpret_cast<float2*>(w);
+  p.cnt = reinterpret_cast<unsigned*>(w + pl.ws_part);
+  p.accpart = pl.ws_acc ? reinterpret_cast<float*>(w + pl.ws_part + pl.ws_cnt) : nullptr;
+  p.fin_cnt = reinterpret_cast<unsigned*>(w + pl.ws_part + pl.ws_cnt + pl.ws_acc);
+  p.imp = importance;
+  p.err = device_error_flag();
+
+  static int configured_smem = -1;
+  if (configured_smem < (int)pl.smem) {
+    cudaError_t e = cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+    if (e != cudaSuccess) return e;
+    configured_smem = kSmemLimit;
+  }
+  const int grid = (int)std::min<long long>(pl.P, pl.total_jobs);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;       // all CTAs co-resident (in-kernel exchange)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_fused, p);
+}
+
 }  // namespace sp

@@ -164,12 +164,15 @@ def test_gather_bitexact():
 def test_nonfinite_flag():
     w = gen.CONFIGS["C0"]
     Qb, Kb, _ = gen.gen_batch(w)
-    K = _dev(Kb)
-    K[0, 1, 0, 5, 0] = float("inf")
-    with pytest.raises(sp.SpError) as e:
-        sp.score(_dev(Qb), K, scale=w.scale, algo="simt")
-        sp.check_device_error()
-    assert e.value.code == 5
+    for algo in ALGOS:
+        K = _dev(Kb)
+        Q = _dev(Qb)
+        K[0, 1, 0, 5, 0] = float("inf")           # +inf logit for the (l=1, kv=0) heads with q[0] > 0
+        Q[0, 1, :, 0:w.G, 0] = 1.0
+        with pytest.raises(sp.SpError) as e:
+            sp.score(Q, K, scale=w.scale, algo=algo)
+            sp.check_device_error()
+        assert e.value.code == 5, algo
 
 
 @pytest.mark.parametrize("algo", ALGOS)
