@@ -11,9 +11,12 @@
  * Ownership   The caller owns every buffer.  Device pointers are plain
  *             cudaMalloc / PyTorch CUDA memory; the library never allocates
  *             or frees device memory on the hot path.  Scratch comes from a
- *             caller-provided workspace of at least *_workspace_bytes() bytes,
- *             which must be zero-filled once before its first use (the kernels
- *             leave their counters at zero when they finish).
+ *             caller-provided workspace of at least *_workspace_bytes() bytes.
+ *             A score workspace must be zero-filled before its first use with a
+ *             given geometry (sp_geom) and may then be reused for that geometry
+ *             indefinitely: the fused kernel's exchange counters are left at zero
+ *             at the end of every successful call.  Reusing it for another
+ *             geometry, or after SP_ETIMEOUT, requires zero-filling it again.
  * Streams     Every call is enqueued on `stream` (a cudaStream_t / CUstream;
  *             NULL = legacy default stream) and returns without synchronising.
  *             Outputs are valid in stream order.

@@ -30,15 +30,23 @@ def _stream_ptr(stream) -> int:
     return s.cuda_stream
 
 
-def workspace(tag: str, nbytes: int, device) -> torch.Tensor:
-    """Zero-initialised, cached device workspace (the fused kernel leaves its
-    counters at zero, so a workspace is zeroed only when first allocated)."""
+def workspace(tag, nbytes: int, device) -> torch.Tensor:
+    """Zero-initialised, cached device workspace.  The fused kernel leaves its
+    counters at zero after every call, but their position depends on the
+    geometry, so a workspace is only ever reused for the same ``tag`` (which
+    includes the geometry): see include/specprefill.h, "Ownership"."""
     key = (tag, torch.device(device).index)
     buf = _ws_cache.get(key)
     if buf is None or buf.numel() < nbytes:
+        if len(_ws_cache) > 64:
+            _ws_cache.clear()
         buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
         _ws_cache[key] = buf
     return buf
+
+
+def _geom_key(g) -> tuple:
+    return (g.B, g.L, g.H, g.Hkv, g.d, g.R, g.R_valid, g.N)
 
 
 def make_geom(Q: torch.Tensor, K: torch.Tensor, R_valid: int | None = None, scale: float | None = None):
@@ -66,7 +74,7 @@ def score(Q, K, R_valid=None, scale=None, out=None, algo: str = "auto", stream=N
         out = torch.empty((g.B, g.N), dtype=torch.float32, device=K.device)
     a = ALGOS[algo]
     nbytes = lib().sp_score_workspace_bytes(C.byref(g), a)
-    ws = workspace("score-" + algo, nbytes, K.device)
+    ws = workspace(("score", algo, _geom_key(g)), nbytes, K.device)
     check(lib().sp_score_ex(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), out.data_ptr(), ws.data_ptr(),
                             ws.numel(), a, _stream_ptr(stream)), "sp_score")
     return out
