@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3", choices=["C0", "C1", "C2", "C3", "C4"])
     ap.add_argument("--algo", default="fused", choices=["fused", "simt", "auto"])
+    ap.add_argument("--plan", default=None, help="fused-kernel decomposition override 'n_tg,n_ug'")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=32)
@@ -262,12 +263,13 @@ def run_ours(args):
         e2e = run_e2e(args, w, Q, K, T, dev, stream, dist, world)
 
     launches_per_step = {"fused": 1, "simt": 4, "auto": 1}[args.algo] + 2
+    plan = sp.score_plan(Q, K, w.Rv) if args.algo != "simt" else None
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{args.config} {w.name}", "B": w.B, "N": w.N, "L": w.L, "H": w.H, "Hkv": w.Hkv,
                        "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk,
-                       "algo": args.algo, "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "algo": args.algo, "plan": plan, "parallelism": f"replicas{world}" if world > 1 else "single",
                        "l2": f"inputs larger than L2 (K = {w.k_bytes / 2**30:.2f} GiB per GPU), no flush"},
             "roofline": roofline, "clocks": clk, "e2e": e2e, "gpu_launches": launches_per_step * args.steps}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -320,6 +322,8 @@ def run_e2e(args, w, Q, K, T, dev, stream, dist, world):
 
 def main():
     args = parse()
+    if args.plan:
+        os.environ["SP_FUSED_PLAN"] = args.plan
     if args.impl == "reference":
         run_reference(args)
     else:

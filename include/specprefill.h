@@ -140,6 +140,12 @@ sp_status sp_score(const void* Q, const void* K, const sp_geom* g, const sp_layo
 sp_status sp_score_ex(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay,
                       float* importance, void* ws, size_t ws_bytes, int algo, sp_stream stream);
 
+/* Launch plan of the fused kernel for g on the current device (for reports
+ * and tests): out[0..8] = grid, jobs per request, token groups, unit groups,
+ * tiles per job, units per job, TMEM unit slots, SMEM pipeline stages,
+ * dynamic SMEM bytes.  Returns SP_EUNSUPPORTED if the fused kernel cannot run g. */
+sp_status sp_score_plan(const sp_geom* g, int64_t out[9]);
+
 /* ------------------------------------------------------------------ score, sequence-sharded split
  * For a prompt split along tokens over P ranks.  Each
  * rank passes its own K shard (N = local tokens).  Statistics are in the log2

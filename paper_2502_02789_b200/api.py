@@ -46,7 +46,8 @@ def workspace(tag, nbytes: int, device) -> torch.Tensor:
 
 
 def _geom_key(g) -> tuple:
-    return (g.B, g.L, g.H, g.Hkv, g.d, g.R, g.R_valid, g.N)
+    import os
+    return (g.B, g.L, g.H, g.Hkv, g.d, g.R, g.R_valid, g.N, os.environ.get("SP_FUSED_PLAN"))
 
 
 def make_geom(Q: torch.Tensor, K: torch.Tensor, R_valid: int | None = None, scale: float | None = None):
@@ -110,6 +111,16 @@ def gather(tokens: torch.Tensor, ids: torch.Tensor, n_kept: torch.Tensor, out=No
     check(lib().sp_gather(tokens.data_ptr(), ids.data_ptr(), n_kept.data_ptr(), B, N, out.data_ptr(),
                           _stream_ptr(stream)), "sp_gather")
     return out
+
+
+def score_plan(Q, K, R_valid=None) -> dict:
+    """The fused kernel's launch plan for this geometry on the current device."""
+    g, _ = make_geom(Q, K, R_valid)
+    out = (C.c_int64 * 9)()
+    check(lib().sp_score_plan(C.byref(g), out), "sp_score_plan")
+    keys = ("grid", "jobs_per_request", "token_groups", "unit_groups", "tiles_per_job", "units_per_job",
+            "tmem_slots", "stages", "smem_bytes")
+    return dict(zip(keys, list(out)))
 
 
 def kept_chunks(n_chunks: int, keep: float) -> int:

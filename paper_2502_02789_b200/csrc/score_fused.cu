@@ -33,6 +33,8 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -45,6 +47,7 @@ constexpr int kStatsWarp0 = 4;
 constexpr int kFinalWarp0 = 8;
 constexpr int kMaxStages = 8;
 constexpr int kMaxChunks = 8;          // NCP <= 128 columns (16-column chunks)
+constexpr int kMaxBuf = 8;             // TMEM unit slots
 constexpr int kTmemCols = 512;
 constexpr int kSmemLimit = 232448;     // sm_100 max dynamic shared memory per block
 
@@ -64,8 +67,9 @@ struct FusedParams {
   uint32_t off_k, off_q, off_acc, off_red, off_lse, off_bar;
   uint32_t k_stage_bytes, q_slot_bytes;
   // workspace
-  float2* part;                        // [B][U][NC][n_tg] (m2, l)
-  unsigned* cnt;                       // [B][U]       exchange counters (self-cleaning)
+  float2* part;                        // [B][U][n_tg][NC] CTA partials (m, s), m in raw-logit units
+  float* lse_g;                        // [B][U][NC]       combined lse2 per (l, h, r) column
+  unsigned* cnt;                       // [B][U]           exchange counters (self-cleaning)
   float* accpart;                      // [B][n_ug][Rv][N]
   unsigned* fin_cnt;                   // [B][n_tg]    finalize counters (self-cleaning)
   float* imp;                          // [B][N]
@@ -231,11 +235,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
-  // barrier map: full[S] empty[S] qfull[2] qempty[2] tfull[2] tempty[2]; then tmem base
+  // barrier map: full[S] empty[S] qfull[2] qempty[2] tfull[kMaxBuf] tempty[kMaxBuf]; then tmem base
   const uint32_t bar_full = smem_u32(bars), bar_empty = bar_full + 8 * p.stages;
   const uint32_t bar_qfull = bar_empty + 8 * p.stages, bar_qempty = bar_qfull + 16;
-  const uint32_t bar_tfull = bar_qempty + 16, bar_tempty = bar_tfull + 16;
-  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 2 * p.stages + 8);
+  const uint32_t bar_tfull = bar_qempty + 16, bar_tempty = bar_tfull + 8 * kMaxBuf;
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 2 * p.stages + 4 + 2 * kMaxBuf);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -245,6 +249,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar_qfull + 8 * s, 1);
       mbar_init(bar_qempty + 8 * s, 1);
+    }
+    for (int s = 0; s < kMaxBuf; ++s) {
       mbar_init(bar_tfull + 8 * s, 1);
       mbar_init(bar_tempty + 8 * s, 4);
     }
@@ -329,71 +335,103 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     }
   } else if (warp >= kStatsWarp0 && warp < kFinalWarp0) {
     // ================================================================ softmax statistics
+    // Two passes over the unit's logits, both from TMEM (no HBM traffic):
+    //   A: per-column max over this warp's token rows of every tile (thread-local, one
+    //      transposed butterfly per 16 columns);
+    //   B: per-column sum of 2^((x - max) * xs) (thread-local, one exp2 per logit).
+    // The 4 warps' (max, sum) pairs merge in SMEM; warp 4 publishes the CTA partial and
+    // the last CTA of the token groups combines them into lse2 for every CTA.
     const int q = warp & 3;                       // TMEM lane quarter
     const int nch = p.NCP / 16;
     float2* red = reinterpret_cast<float2*>(smem + p.off_red);   // [2][4][NCP]
     uint32_t ui = 0;
     for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
       const Job jb = decode_job(p, job);
+      const int ntile = jb.t_hi - jb.t_lo;
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
         const uint32_t slot = ui % p.nbuf, tpar = (ui / p.nbuf) & 1;
         mbar_wait(bar_tfull + 8 * slot, tpar);
         tc_fence_after();
-        float M[kMaxChunks], Ls[kMaxChunks];
+        const uint32_t sbase = tmem + ((uint32_t)(q * 32) << 16) + slot * p.slot_cols;
+        float2* rb = red + (ui & 1) * 4 * p.NCP;
+#pragma unroll 1
+        for (int k = 0; k < nch; ++k) {
+          // ---- pass A: column max (raw logits; xs > 0 so scaling commutes with max)
+          float m[16];
 #pragma unroll
-        for (int k = 0; k < kMaxChunks; ++k) { M[k] = -CUDART_INF_F; Ls[k] = 0.f; }
-        for (int t = jb.t_lo; t < jb.t_hi; ++t) {
-          const bool valid = (long long)t * kTileM + q * 32 + lane < p.N;
-          const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + slot * p.slot_cols + (uint32_t)(t - jb.t_lo) * p.NCP;
+          for (int i = 0; i < 16; ++i) m[i] = -CUDART_INF_F;
+          for (int t = 0; t < ntile; ++t) {
+            const bool valid = (long long)(jb.t_lo + t) * kTileM + q * 32 + lane < p.N;
+            float x[16];
+            tmem_ld16(sbase + (uint32_t)t * p.NCP + k * 16, x);
+            if (valid) {
 #pragma unroll
-          for (int k = 0; k < kMaxChunks; ++k) {
-            if (k < nch) {
-              float x[16], e[16];
-              tmem_ld16(tbase + k * 16, x);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) { x[i] = valid ? x[i] * p.xs : -CUDART_INF_F; e[i] = x[i]; }
-              const float mt = transpose_reduce16<true>(e, lane);            // column (lane>>1) max
-              const float ms = (mt == -CUDART_INF_F) ? 0.f : mt;
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const float mi = __shfl_sync(0xffffffffu, ms, 2 * i);
-                e[i] = valid ? exp2f(x[i] - mi) : 0.f;
-              }
-              const float st = transpose_reduce16<false>(e, lane);
-              // merge (mt, st) into the running (M, L) of column 16k + (lane>>1)
-              const float Mn = fmaxf(M[k], mt);
-              if (Mn != -CUDART_INF_F) {
-                const float a = (M[k] == -CUDART_INF_F) ? 0.f : Ls[k] * exp2f(M[k] - Mn);
-                const float c = (mt == -CUDART_INF_F) ? 0.f : st * exp2f(mt - Mn);
-                Ls[k] = a + c;
-                M[k] = Mn;
-              }
+              for (int i = 0; i < 16; ++i) m[i] = fmaxf(m[i], x[i]);
             }
           }
-        }
-        // CTA partial: combine the 4 statistics warps in fixed order, publish, count
-        float2* rb = red + (ui & 1) * 4 * p.NCP;
-        if ((lane & 1) == 0) {
+          const float mcol = transpose_reduce16<true>(m, lane);        // column 16k + (lane >> 1)
+          const float mref = (mcol == -CUDART_INF_F) ? 0.f : mcol * p.xs;
+          float nref[16];
 #pragma unroll
-          for (int k = 0; k < kMaxChunks; ++k)
-            if (k < nch) rb[q * p.NCP + 16 * k + (lane >> 1)] = make_float2(M[k], Ls[k]);
+          for (int i = 0; i < 16; ++i) nref[i] = -__shfl_sync(0xffffffffu, mref, 2 * i);
+          // ---- pass B: sum of exp2(x*xs - max*xs)
+          float e[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) e[i] = 0.f;
+          for (int t = 0; t < ntile; ++t) {
+            const bool valid = (long long)(jb.t_lo + t) * kTileM + q * 32 + lane < p.N;
+            float x[16];
+            tmem_ld16(sbase + (uint32_t)t * p.NCP + k * 16, x);
+            if (valid) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) e[i] += exp2f(fmaf(x[i], p.xs, nref[i]));
+            }
+          }
+          const float scol = transpose_reduce16<false>(e, lane);
+          if ((lane & 1) == 0) rb[q * p.NCP + 16 * k + (lane >> 1)] = make_float2(mcol, scol);
         }
         named_bar(1, 128);
         if (q == 0) {
+          // CTA partial: merge the 4 warps in fixed order (m in raw-logit units)
           const long long ubase = (long long)jb.b * p.U + u;
+          float2* mypart = p.part + (ubase * p.n_tg + jb.tg) * p.NC;
           for (int c = lane; c < p.NC; c += 32) {
             float mm = -CUDART_INF_F;
+#pragma unroll
             for (int w = 0; w < 4; ++w) mm = fmaxf(mm, rb[w * p.NCP + c].x);
             float ss = 0.f;
+#pragma unroll
             for (int w = 0; w < 4; ++w) {
               const float2 v = rb[w * p.NCP + c];
-              if (v.y > 0.f) ss += v.y * exp2f(v.x - mm);
+              if (v.y > 0.f) ss += v.y * exp2f((v.x - mm) * p.xs);
             }
-            p.part[(ubase * p.NC + c) * p.n_tg + jb.tg] = make_float2(mm, ss);
+            mypart[c] = make_float2(mm, ss);
           }
           __threadfence();
           __syncwarp();
-          if (lane == 0) atomicAdd(p.cnt + ubase, 1u);
+          unsigned old = 0;
+          if (lane == 0) old = atomicAdd(p.cnt + ubase, 1u);
+          old = __shfl_sync(0xffffffffu, old, 0);
+          if (old == (unsigned)p.n_tg - 1) {
+            // last arrival: combine the n_tg partials (fixed tg order -> deterministic lse2)
+            __threadfence();
+            const float2* src = p.part + ubase * p.n_tg * p.NC;
+            for (int c = lane; c < p.NC; c += 32) {
+              float mm = -CUDART_INF_F;
+              for (int s2 = 0; s2 < p.n_tg; ++s2) mm = fmaxf(mm, __ldcg(&src[s2 * p.NC + c].x));
+              float ss = 0.f;
+              for (int s2 = 0; s2 < p.n_tg; ++s2) {
+                const float2 v = __ldcg(&src[s2 * p.NC + c]);
+                if (v.y > 0.f) ss += v.y * exp2f((v.x - mm) * p.xs);
+              }
+              const float l2 = mm * p.xs + log2f(ss);
+              if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
+              p.lse_g[ubase * p.NC + c] = l2;
+            }
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(p.cnt + ubase, 1u);               // n_tg + 1: lse2 ready
+          }
         }
       }
     }
@@ -415,46 +453,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const long long ubase = (long long)jb.b * p.U + u;
         float* ls = lse_s + (ui & 1) * p.NCP;
         if (q == 0) {
-          if (lane == 0) spin_geq(p.cnt + ubase, (unsigned)p.n_tg, p.err);
+          if (lane == 0) spin_geq(p.cnt + ubase, (unsigned)p.n_tg + 1u, p.err);
           __syncwarp();
           __threadfence();
-          for (int c = lane; c < p.NC; c += 32) {
-            const float2* src = p.part + (ubase * p.NC + c) * p.n_tg;
-            float mm = -CUDART_INF_F;
-            for (int s = 0; s < p.n_tg; ++s) mm = fmaxf(mm, __ldcg(&src[s].x));
-            float ss = 0.f;
-            for (int s = 0; s < p.n_tg; ++s) {
-              const float2 v = __ldcg(&src[s]);
-              if (v.y > 0.f) ss += v.y * exp2f(v.x - mm);
-            }
-            const float l2 = mm + log2f(ss);
-            if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
-            ls[c] = l2;
-          }
+          for (int c = lane; c < p.NCP; c += 32) ls[c] = (c < p.NC) ? __ldcg(p.lse_g + ubase * p.NC + c) : 0.f;
           __syncwarp();
           if (lane == 0) {
-            // self-cleaning counter: the last of the 2*n_tg arrivals resets it to zero
-            if (atomicAdd(p.cnt + ubase, 1u) == 2u * p.n_tg - 1u) atomicExch(p.cnt + ubase, 0u);
+            // self-cleaning counter: n_tg arrivals + 1 combine + n_tg readers; the last resets it
+            if (atomicAdd(p.cnt + ubase, 1u) == 2u * p.n_tg) atomicExch(p.cnt + ubase, 0u);
           }
         }
         named_bar(2, 128);
         mbar_wait(bar_tfull + 8 * slot, tpar);
         tc_fence_after();
+        const uint32_t sbase = tmem + ((uint32_t)(q * 32) << 16) + slot * p.slot_cols;
         for (int t = 0; t < ntile; ++t) {
-          const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + slot * p.slot_cols + (uint32_t)t * p.NCP;
           int r = 0, hh = 0;
           float best = -CUDART_INF_F;
           float* arow = acc + (t * p.Rv) * kTileM + tok;
 #pragma unroll
           for (int k = 0; k < kMaxChunks; ++k) {
             if (k < nch) {
-              float x[16];
-              tmem_ld16(tbase + k * 16, x);
+              float x[16], lv[16];
+              tmem_ld16(sbase + (uint32_t)t * p.NCP + k * 16, x);
+#pragma unroll
+              for (int i4 = 0; i4 < 4; ++i4) {
+                const float4 v4 = *reinterpret_cast<const float4*>(ls + 16 * k + 4 * i4);
+                lv[4 * i4] = v4.x; lv[4 * i4 + 1] = v4.y; lv[4 * i4 + 2] = v4.z; lv[4 * i4 + 3] = v4.w;
+              }
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                const int c = 16 * k + i;
-                if (c < p.NC) {
-                  best = fmaxf(best, x[i] * p.xs - ls[c]);
+                if (16 * k + i < p.NC) {
+                  best = fmaxf(best, fmaf(x[i], p.xs, -lv[i]));
                   if (++hh == p.G) {
                     float* a = arow + r * kTileM;
                     *a = fmaxf(*a, best);
@@ -555,7 +585,8 @@ struct Plan {
   long long total_jobs = 0;
   uint32_t off_k = 0, off_q = 0, off_acc = 0, off_red = 0, off_lse = 0, off_bar = 0, smem = 0;
   uint32_t k_stage_bytes = 0, q_slot_bytes = 0;
-  size_t ws_part = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0;
+  size_t ws_part = 0, ws_lse = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0;
+  size_t ws_total() const { return ws_part + ws_lse + ws_cnt + ws_acc + ws_fin; }
   bool ok = false;
 };
 
@@ -583,11 +614,11 @@ uint32_t carve(Plan& pl, int Rv, int stages) {
   o += 2 * pl.NCP * 4;
   o = (o + 15) & ~15u;
   pl.off_bar = o;
-  o += (2 * stages + 8) * 8 + 16;
+  o += (2 * stages + 4 + 2 * kMaxBuf) * 8 + 16;
   return o + 1024;                                   // slack for the manual 1024-byte alignment
 }
 
-Plan make_plan(const Geom& g) {
+Plan make_plan(const Geom& g, bool allow_override = true) {
   Plan pl;
   pl.NC = g.G * g.Rv;
   pl.NCP = ((pl.NC + 15) / 16) * 16;
@@ -601,8 +632,17 @@ Plan make_plan(const Geom& g) {
   pl.T = (int)((g.N + kTileM - 1) / kTileM);
   pl.U = g.L * g.Hkv;
   // choose (n_tg, n_ug): J = n_tg*n_ug divides the grid so a request never
-  // straddles two waves; minimise waves * (tiles x units per job)
+  // straddles two waves of CTAs.  Time model in units of one K-tile load at an
+  // SM's share of HBM bandwidth: a unit costs max(tpc, chain/(nbuf-1)) where
+  // `chain` is the stats -> exchange -> aggregation latency that the nbuf TMEM
+  // slots must hide.
+  const double kChain = 6.0;
   double best = 1e300;
+  // test/tuning override: SP_FUSED_PLAN="n_tg,n_ug" (ignored unless valid for g)
+  int force_tg = 0, force_ug = 0;
+  if (const char* env = allow_override ? std::getenv("SP_FUSED_PLAN") : nullptr) {
+    if (std::sscanf(env, "%d,%d", &force_tg, &force_ug) != 2) force_tg = force_ug = 0;
+  }
   for (int J = 1; J <= pl.P; ++J) {
     if (pl.P % J) continue;
     for (int n_tg = 1; n_tg <= J; ++n_tg) {
@@ -611,22 +651,27 @@ Plan make_plan(const Geom& g) {
       if (n_tg > pl.T || n_ug > pl.U) continue;
       const int tpc = (pl.T + n_tg - 1) / n_tg, upc = (pl.U + n_ug - 1) / n_ug;
       if (tpc * pl.NCP > kTmemCols) continue;
-      const int nbuf = (tpc * pl.NCP <= kTmemCols / 2) ? 2 : 1;
+      if (force_tg > 0 && (n_tg != force_tg || n_ug != force_ug)) continue;
+      const int nbuf = std::min(kMaxBuf, kTmemCols / (tpc * pl.NCP));
       const long long jobs = (long long)g.B * J;
       const int grid = (int)std::min<long long>(pl.P, jobs);
       const long long waves = (jobs + grid - 1) / grid;
-      double cost = (double)waves * tpc * upc * pl.k_stage_bytes;
-      cost *= (nbuf == 1) ? 1.5 : 1.0;                                   // no TMEM double buffering
-      cost += (double)waves * upc * (n_tg * pl.NC * 8.0) * 0.25;         // partial-stats reads (L2)
-      cost += (double)waves * (n_ug > 1 ? n_ug * g.Rv * tpc * kTileM * 4.0 : 0.0);
-      if (cost < best) {
+      const double tile_scale = (double)pl.k_stage_bytes / 32768.0;
+      const double t_unit = nbuf >= 2 ? std::max((double)tpc * tile_scale, kChain / (nbuf - 1))
+                                      : tpc * tile_scale + kChain;
+      double cost = (double)upc * t_unit;
+      cost += upc * (n_tg * pl.NC * 8.0) / 32768.0 / 8.0;                  // combiner reads (L2)
+      cost += (n_ug > 1 ? 2.0 * g.Rv * tpc * kTileM * 4.0 / 32768.0 + kChain : 0.0);  // cross-group max
+      cost *= (double)waves;
+      if (cost < best * 0.999) {
         best = cost;
         pl.J = J; pl.n_tg = n_tg; pl.n_ug = n_ug; pl.tpc = tpc; pl.upc = upc; pl.nbuf = nbuf;
       }
     }
   }
+  if (pl.J == 0 && force_tg > 0) return make_plan(g, false);   // invalid override: plan normally
   if (pl.J == 0) return pl;
-  pl.slot_cols = (pl.nbuf == 2) ? kTmemCols / 2 : kTmemCols;
+  pl.slot_cols = pl.tpc * pl.NCP;
   pl.total_jobs = (long long)g.B * pl.J;
   int stages = kMaxStages;
   while (stages >= 2 && carve(pl, g.Rv, stages) > (uint32_t)kSmemLimit) --stages;
@@ -634,6 +679,7 @@ Plan make_plan(const Geom& g) {
   pl.stages = stages;
   pl.smem = carve(pl, g.Rv, stages);
   pl.ws_part = align256((size_t)g.B * pl.U * pl.NC * pl.n_tg * sizeof(float2));
+  pl.ws_lse = align256((size_t)g.B * pl.U * pl.NC * sizeof(float));
   pl.ws_cnt = align256((size_t)g.B * pl.U * sizeof(unsigned));
   pl.ws_acc = pl.n_ug > 1 ? align256((size_t)g.B * pl.n_ug * g.Rv * g.N * sizeof(float)) : 0;
   pl.ws_fin = align256((size_t)g.B * pl.n_tg * sizeof(unsigned));
@@ -689,16 +735,24 @@ bool fused_supported(const Geom& g, const Layout&, const void*, const void*) {
   return make_plan(g).ok;
 }
 
+bool fused_plan_info(const Geom& g, long long out[9]) {
+  Plan pl = make_plan(g);
+  if (!pl.ok) return false;
+  out[0] = std::min<long long>(pl.P, pl.total_jobs); out[1] = pl.J; out[2] = pl.n_tg; out[3] = pl.n_ug;
+  out[4] = pl.tpc; out[5] = pl.upc; out[6] = pl.nbuf; out[7] = pl.stages; out[8] = pl.smem;
+  return true;
+}
+
 size_t fused_score_ws_bytes(const Geom& g) {
   Plan pl = make_plan(g);
   if (!pl.ok) return 0;
-  return pl.ws_part + pl.ws_cnt + pl.ws_acc + pl.ws_fin;
+  return pl.ws_total();
 }
 
 cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                         float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
   Plan pl = make_plan(g);
-  if (!pl.ok || ws_bytes < pl.ws_part + pl.ws_cnt + pl.ws_acc + pl.ws_fin) return cudaErrorInvalidValue;
+  if (!pl.ok || ws_bytes < pl.ws_total()) return cudaErrorInvalidValue;
   static FusedParams p;                               // large (two tensor maps); host-side scratch
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
@@ -714,10 +768,16 @@ cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Ge
   p.off_k = pl.off_k; p.off_q = pl.off_q; p.off_acc = pl.off_acc; p.off_red = pl.off_red; p.off_lse = pl.off_lse;
   p.off_bar = pl.off_bar; p.k_stage_bytes = pl.k_stage_bytes; p.q_slot_bytes = pl.q_slot_bytes;
   char* w = reinterpret_cast<char*>(ws);
+  // counters first: their offsets depend only on (B, U), not on the plan
+  p.cnt = reinterpret_cast<unsigned*>(w);
+  w += pl.ws_cnt;
+  p.fin_cnt = reinterpret_cast<unsigned*>(w);
+  w += pl.ws_fin;
   p.part = reinterpret_cast<float2*>(w);
-  p.cnt = reinterpret_cast<unsigned*>(w + pl.ws_part);
-  p.accpart = pl.ws_acc ? reinterpret_cast<float*>(w + pl.ws_part + pl.ws_cnt) : nullptr;
-  p.fin_cnt = reinterpret_cast<unsigned*>(w + pl.ws_part + pl.ws_cnt + pl.ws_acc);
+  w += pl.ws_part;
+  p.lse_g = reinterpret_cast<float*>(w);
+  w += pl.ws_lse;
+  p.accpart = pl.ws_acc ? reinterpret_cast<float*>(w) : nullptr;
   p.imp = importance;
   p.err = device_error_flag();
 

@@ -178,6 +178,16 @@ sp_status sp_score(const void* Q, const void* K, const sp_geom* g, const sp_layo
   return sp_score_ex(Q, K, g, lay, importance, ws, ws_bytes, SP_SCORE_AUTO, stream);
 }
 
+sp_status sp_score_plan(const sp_geom* g, int64_t out[9]) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if (out == nullptr) return SP_EINVAL;
+  long long o[9];
+  if (!fused_plan_info(to_geom(*g), o)) return SP_EUNSUPPORTED;
+  for (int i = 0; i < 9; ++i) out[i] = o[i];
+  return SP_OK;
+}
+
 size_t sp_score_split_workspace_bytes(const sp_geom* g) {
   if (check_geom(g) != SP_OK) return 0;
   Geom G = to_geom(*g);
