@@ -146,6 +146,16 @@ sp_status sp_score_ex(const void* Q, const void* K, const sp_geom* g, const sp_l
  * dynamic SMEM bytes.  Returns SP_EUNSUPPORTED if the fused kernel cannot run g. */
 sp_status sp_score_plan(const sp_geom* g, int64_t out[9]);
 
+/* Debug tracing of the fused kernel (not for production runs): while enabled,
+ * every sp_score launch writes globaltimer stamps (ns) into device_buffer laid
+ * out as [grid CTA][unit index within the CTA][8] uint64:
+ *   0 producer starts the unit, 1 MMA starts it (TMEM slot free), 2 statistics
+ *   start (logits in TMEM), 3 CTA partial published, 4 lse2 combined (last CTA
+ *   only), 5 aggregation sees lse2, 6 aggregation done (TMEM slot released).
+ * records = capacity in uint64; units beyond capacity are not traced.
+ * device_buffer = NULL disables tracing. */
+sp_status sp_trace_enable(uint64_t* device_buffer, int64_t records);
+
 /* ------------------------------------------------------------------ score, sequence-sharded split
  * For a prompt split along tokens over P ranks.  Each
  * rank passes its own K shard (N = local tokens).  Statistics are in the log2

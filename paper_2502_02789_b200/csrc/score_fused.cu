@@ -64,7 +64,7 @@ struct FusedParams {
   uint32_t idesc;                      // tcgen05 instruction descriptor
   uint32_t layout_type;                // UMMA smem descriptor swizzle code
   // smem carve (byte offsets from the 1024-aligned base)
-  uint32_t off_k, off_q, off_acc, off_red, off_lse, off_bar;
+  uint32_t off_k, off_q, off_acc, off_red, off_lse, off_comb, off_bar;
   uint32_t k_stage_bytes, q_slot_bytes;
   // workspace
   float2* part;                        // [B][U][n_tg][NC] CTA partials (m, s), m in raw-logit units
@@ -74,6 +74,8 @@ struct FusedParams {
   unsigned* fin_cnt;                   // [B][n_tg]    finalize counters (self-cleaning)
   float* imp;                          // [B][N]
   int* err;
+  unsigned long long* trace;           // optional [grid][trace_units][8] globaltimer stamps (debug)
+  int trace_units;
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -148,17 +150,84 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t 
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
+// tcgen05.ld of 32 consecutive fp32 columns of this warp's 32 TMEM lanes, WITHOUT
+// waiting: the registers are undefined until tmem_wait() + tie32().
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, float (&v)[32]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Re-define the registers after tmem_wait() so no use of them can be scheduled
+// before the wait (the compiler does not know tcgen05.ld is asynchronous).
+__device__ __forceinline__ void tie32(float (&v)[32]) {
+  asm volatile(""
+               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]),
+                 "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]), "+f"(v[14]),
+                 "+f"(v[15]), "+f"(v[16]), "+f"(v[17]), "+f"(v[18]), "+f"(v[19]), "+f"(v[20]), "+f"(v[21]),
+                 "+f"(v[22]), "+f"(v[23]), "+f"(v[24]), "+f"(v[25]), "+f"(v[26]), "+f"(v[27]), "+f"(v[28]),
+                 "+f"(v[29]), "+f"(v[30]), "+f"(v[31]));
+}
+// f(x[32], t) for every tile t < ntile of a TMEM column group; the load of tile
+// t+1 is in flight while tile t is processed.
+template <class F>
+__device__ __forceinline__ void for_tiles(uint32_t base, uint32_t stride, int ntile, F&& f) {
+  float a[32], b[32];
+  if (ntile <= 0) return;
+  tmem_ld32_issue(base, a);
+  for (int t = 0; t < ntile; t += 2) {
+    tmem_wait();
+    tie32(a);
+    if (t + 1 < ntile) tmem_ld32_issue(base + (uint32_t)(t + 1) * stride, b);
+    f(a, t);
+    if (t + 1 < ntile) {
+      tmem_wait();
+      tie32(b);
+      if (t + 2 < ntile) tmem_ld32_issue(base + (uint32_t)(t + 2) * stride, a);
+      f(b, t + 1);
+    }
+  }
+}
+
+__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, float (&v)[16]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tie16(float (&v)[16]) {
+  asm volatile(""
+               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]),
+                 "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]), "+f"(v[14]),
+                 "+f"(v[15]));
+}
+template <class F>
+__device__ __forceinline__ void for_tiles16(uint32_t base, uint32_t stride, int ntile, F&& f) {
+  float a[16], b[16];
+  if (ntile <= 0) return;
+  tmem_ld16_issue(base, a);
+  for (int t = 0; t < ntile; t += 2) {
+    tmem_wait();
+    tie16(a);
+    if (t + 1 < ntile) tmem_ld16_issue(base + (uint32_t)(t + 1) * stride, b);
+    f(a, t);
+    if (t + 1 < ntile) {
+      tmem_wait();
+      tie16(b);
+      if (t + 2 < ntile) tmem_ld16_issue(base + (uint32_t)(t + 2) * stride, a);
+      f(b, t + 1);
+    }
+  }
+}
+
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -212,6 +281,87 @@ __device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
   return op(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
 }
 
+// Merge a partial (m, s) -- s = sum 2^((x - m) * xs) over a token subset, m the
+// subset's max raw logit -- into the running pair (M, S).  Empty partials (s == 0)
+// are skipped, so an all-masked subset (m = -inf) is harmless.
+__device__ __forceinline__ void lse_merge(float& M, float& S, float2 v, float xs) {
+  if (!(v.y > 0.f)) return;
+  if (v.x > M) {
+    S = S * exp2f((M - v.x) * xs) + v.y;
+    M = v.x;
+  } else {
+    S += v.y * exp2f((v.x - M) * xs);
+  }
+}
+
+// Debug trace: stamp event e of the CTA's ui-th unit (no-op unless enabled).
+__device__ __forceinline__ void trace_stamp(const FusedParams& p, uint32_t ui, int e) {
+  if (p.trace != nullptr && ui < (uint32_t)p.trace_units)
+    p.trace[((size_t)blockIdx.x * p.trace_units + ui) * 8 + e] = globaltimer_ns();
+}
+
+// Transposed butterfly over 32 columns x 32 lanes: lane l returns the reduction
+// over all 32 lanes of column l.  16 + 8 + 4 + 2 + 1 = 31 shuffles.
+template <bool kMax>
+__device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
+  auto op = [](float a, float b) { return kMax ? fmaxf(a, b) : a + b; };
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool up = lane & w;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? v[i] : v[i + w], keep = up ? v[i + w] : v[i];
+      v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, w));
+    }
+  }
+  return v[0];
+}
+
+// Fold one tile's 32 logit columns (group grp) into the running (l,h)-max of
+// this thread's token: acc[(t*Rv + r)*128 + tok] = max(acc, max_h (x*xs - lse2)).
+// Columns are r-major (c = r*G + h).  kG > 0: compile-time group size dividing 32.
+template <int kG>
+__device__ __forceinline__ void fold_tile(const float (&x)[32], const float (&lv)[32], float xs, int grp, int NC,
+                                          int G, int Rv, float* arow) {
+  if constexpr (kG > 0) {
+#pragma unroll
+    for (int rr = 0; rr < 32 / kG; ++rr) {
+      const int r = grp * (32 / kG) + rr;
+      if (r < Rv) {
+        float best = fmaf(x[rr * kG], xs, -lv[rr * kG]);
+#pragma unroll
+        for (int h = 1; h < kG; ++h) best = fmaxf(best, fmaf(x[rr * kG + h], xs, -lv[rr * kG + h]));
+        float* a = arow + r * kTileM;
+        *a = fmaxf(*a, best);
+      }
+    }
+  } else {
+    // generic G: rows may straddle column groups; the row index is recomputed
+    float best = -CUDART_INF_F;
+    int cur = -1;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int c = grp * 32 + i;
+      if (c < NC) {
+        const int r = c / G;
+        if (r != cur) {
+          if (cur >= 0) {
+            float* a = arow + cur * kTileM;
+            *a = fmaxf(*a, best);
+          }
+          best = -CUDART_INF_F;
+          cur = r;
+        }
+        best = fmaxf(best, fmaf(x[i], xs, -lv[i]));
+      }
+    }
+    if (cur >= 0) {
+      float* a = arow + cur * kTileM;
+      *a = fmaxf(*a, best);
+    }
+  }
+}
+
 struct Job {
   int b, tg, ug, t_lo, t_hi, u_lo, u_hi;
 };
@@ -235,11 +385,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
-  // barrier map: full[S] empty[S] qfull[2] qempty[2] tfull[kMaxBuf] tempty[kMaxBuf]; then tmem base
+  // barrier map: full[S] empty[S] qfull[2] qempty[2] tfull[kMaxBuf] tempty[kMaxBuf]
+  //              rfull[2] rempty[2] lfull[kMaxBuf]; then the TMEM base address
   const uint32_t bar_full = smem_u32(bars), bar_empty = bar_full + 8 * p.stages;
   const uint32_t bar_qfull = bar_empty + 8 * p.stages, bar_qempty = bar_qfull + 16;
   const uint32_t bar_tfull = bar_qempty + 16, bar_tempty = bar_tfull + 8 * kMaxBuf;
-  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 2 * p.stages + 4 + 2 * kMaxBuf);
+  const uint32_t bar_rfull = bar_tempty + 8 * kMaxBuf, bar_rempty = bar_rfull + 16;
+  const uint32_t bar_lfull = bar_rempty + 16;
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 2 * p.stages + 8 + 3 * kMaxBuf);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -253,6 +406,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     for (int s = 0; s < kMaxBuf; ++s) {
       mbar_init(bar_tfull + 8 * s, 1);
       mbar_init(bar_tempty + 8 * s, 4);
+      mbar_init(bar_lfull + 8 * s, 32);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(bar_rfull + 8 * s, 128);
+      mbar_init(bar_rempty + 8 * s, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&p.tmK);
@@ -283,6 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           const int l = u / p.Hkv, g = u % p.Hkv;
           const uint32_t qs = ui & 1, qpar = (ui >> 1) & 1;
           mbar_wait(bar_qempty + 8 * qs, qpar ^ 1);
+          trace_stamp(p, ui, 0);
           mbar_expect_tx(bar_qfull + 8 * qs, (uint32_t)(p.NC * p.d * 2));
           const uint32_t qdst = smem_u32(smem + p.off_q + qs * p.q_slot_bytes);
           for (int kb = 0; kb < p.nkb; ++kb)
@@ -310,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           const uint32_t slot = ui % p.nbuf, tpar = (ui / p.nbuf) & 1;
           const uint32_t qs = ui & 1, qpar = (ui >> 1) & 1;
           mbar_wait(bar_tempty + 8 * slot, tpar ^ 1);
+          trace_stamp(p, ui, 1);
           mbar_wait(bar_qfull + 8 * qs, qpar);
           tc_fence_after();
           const uint32_t qbase = smem_u32(smem + p.off_q + qs * p.q_slot_bytes);
@@ -342,7 +502,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     // The 4 warps' (max, sum) pairs merge in SMEM; warp 4 publishes the CTA partial and
     // the last CTA of the token groups combines them into lse2 for every CTA.
     const int q = warp & 3;                       // TMEM lane quarter
-    const int nch = p.NCP / 16;
     float2* red = reinterpret_cast<float2*>(smem + p.off_red);   // [2][4][NCP]
     uint32_t ui = 0;
     for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
@@ -351,24 +510,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
         const uint32_t slot = ui % p.nbuf, tpar = (ui / p.nbuf) & 1;
         mbar_wait(bar_tfull + 8 * slot, tpar);
+        if (q == 0 && lane == 0) trace_stamp(p, ui, 2);
         tc_fence_after();
+        mbar_wait(bar_rempty + 8 * (ui & 1), ((ui >> 1) & 1) ^ 1);   // exchange warp done with this buffer
         const uint32_t sbase = tmem + ((uint32_t)(q * 32) << 16) + slot * p.slot_cols;
         float2* rb = red + (ui & 1) * 4 * p.NCP;
+        const long long tok0 = (long long)jb.t_lo * kTileM + q * 32 + lane;
 #pragma unroll 1
-        for (int k = 0; k < nch; ++k) {
+        for (int k = 0; k < p.NCP / 16; ++k) {
           // ---- pass A: column max (raw logits; xs > 0 so scaling commutes with max)
           float m[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) m[i] = -CUDART_INF_F;
-          for (int t = 0; t < ntile; ++t) {
-            const bool valid = (long long)(jb.t_lo + t) * kTileM + q * 32 + lane < p.N;
-            float x[16];
-            tmem_ld16(sbase + (uint32_t)t * p.NCP + k * 16, x);
-            if (valid) {
+          for_tiles16(sbase + k * 16, p.NCP, ntile, [&](const float(&x)[16], int t) {
+            if (tok0 + (long long)t * kTileM < p.N) {
 #pragma unroll
               for (int i = 0; i < 16; ++i) m[i] = fmaxf(m[i], x[i]);
             }
-          }
+          });
           const float mcol = transpose_reduce16<true>(m, lane);        // column 16k + (lane >> 1)
           const float mref = (mcol == -CUDART_INF_F) ? 0.f : mcol * p.xs;
           float nref[16];
@@ -378,69 +537,107 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           float e[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) e[i] = 0.f;
-          for (int t = 0; t < ntile; ++t) {
-            const bool valid = (long long)(jb.t_lo + t) * kTileM + q * 32 + lane < p.N;
-            float x[16];
-            tmem_ld16(sbase + (uint32_t)t * p.NCP + k * 16, x);
-            if (valid) {
+          for_tiles16(sbase + k * 16, p.NCP, ntile, [&](const float(&x)[16], int t) {
+            if (tok0 + (long long)t * kTileM < p.N) {
 #pragma unroll
               for (int i = 0; i < 16; ++i) e[i] += exp2f(fmaf(x[i], p.xs, nref[i]));
             }
-          }
+          });
           const float scol = transpose_reduce16<false>(e, lane);
           if ((lane & 1) == 0) rb[q * p.NCP + 16 * k + (lane >> 1)] = make_float2(mcol, scol);
         }
-        named_bar(1, 128);
-        if (q == 0) {
-          // CTA partial: merge the 4 warps in fixed order (m in raw-logit units)
-          const long long ubase = (long long)jb.b * p.U + u;
-          float2* mypart = p.part + (ubase * p.n_tg + jb.tg) * p.NC;
+        mbar_arrive(bar_rfull + 8 * (ui & 1));                       // 128 arrivals: all columns written
+      }
+    }
+  } else if (warp == 2) {
+    // ================================================================ statistics exchange
+    // Merge the 4 statistics warps into the CTA partial, publish it, and -- if
+    // this CTA is the last of the unit's token groups -- combine all partials
+    // into lse2 (fixed token-group order: deterministic) and mark it ready.
+    const float2* red = reinterpret_cast<const float2*>(smem + p.off_red);   // [2][4][NCP]
+    uint32_t ui = 0;
+    for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
+      const Job jb = decode_job(p, job);
+      for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
+        const long long ubase = (long long)jb.b * p.U + u;
+        mbar_wait(bar_rfull + 8 * (ui & 1), (ui >> 1) & 1);
+        const float2* rb = red + (ui & 1) * 4 * p.NCP;
+        float2* mypart = p.part + (ubase * p.n_tg + jb.tg) * p.NC;
+        for (int c = lane; c < p.NC; c += 32) {
+          float mm = -CUDART_INF_F, ss = 0.f;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) lse_merge(mm, ss, rb[w * p.NCP + c], p.xs);
+          mypart[c] = make_float2(mm, ss);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_rempty + 8 * (ui & 1));
+        __threadfence();
+        __syncwarp();
+        unsigned old = 0;
+        if (lane == 0) {
+          old = atomicAdd(p.cnt + ubase, 1u);
+          trace_stamp(p, ui, 3);
+        }
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old == (unsigned)p.n_tg - 1) {
+          __threadfence();
+          const float2* src = p.part + ubase * p.n_tg * p.NC;
           for (int c = lane; c < p.NC; c += 32) {
-            float mm = -CUDART_INF_F;
+            float mm = -CUDART_INF_F, ss = 0.f;
+            for (int s0 = 0; s0 < p.n_tg; s0 += 16) {
+              float2 v[16];
 #pragma unroll
-            for (int w = 0; w < 4; ++w) mm = fmaxf(mm, rb[w * p.NCP + c].x);
-            float ss = 0.f;
+              for (int j = 0; j < 16; ++j)
+                v[j] = s0 + j < p.n_tg ? __ldcg(&src[(s0 + j) * p.NC + c]) : make_float2(-CUDART_INF_F, 0.f);
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              const float2 v = rb[w * p.NCP + c];
-              if (v.y > 0.f) ss += v.y * exp2f((v.x - mm) * p.xs);
+              for (int j = 0; j < 16; ++j) lse_merge(mm, ss, v[j], p.xs);
             }
-            mypart[c] = make_float2(mm, ss);
+            const float l2 = mm * p.xs + log2f(ss);
+            if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
+            p.lse_g[ubase * p.NC + c] = l2;
           }
           __threadfence();
           __syncwarp();
-          unsigned old = 0;
-          if (lane == 0) old = atomicAdd(p.cnt + ubase, 1u);
-          old = __shfl_sync(0xffffffffu, old, 0);
-          if (old == (unsigned)p.n_tg - 1) {
-            // last arrival: combine the n_tg partials (fixed tg order -> deterministic lse2)
-            __threadfence();
-            const float2* src = p.part + ubase * p.n_tg * p.NC;
-            for (int c = lane; c < p.NC; c += 32) {
-              float mm = -CUDART_INF_F;
-              for (int s2 = 0; s2 < p.n_tg; ++s2) mm = fmaxf(mm, __ldcg(&src[s2 * p.NC + c].x));
-              float ss = 0.f;
-              for (int s2 = 0; s2 < p.n_tg; ++s2) {
-                const float2 v = __ldcg(&src[s2 * p.NC + c]);
-                if (v.y > 0.f) ss += v.y * exp2f((v.x - mm) * p.xs);
-              }
-              const float l2 = mm * p.xs + log2f(ss);
-              if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
-              p.lse_g[ubase * p.NC + c] = l2;
-            }
-            __threadfence();
-            __syncwarp();
-            if (lane == 0) atomicAdd(p.cnt + ubase, 1u);               // n_tg + 1: lse2 ready
+          if (lane == 0) {
+            atomicAdd(p.cnt + ubase, 1u);                               // n_tg + 1: lse2 ready
+            trace_stamp(p, ui, 4);
           }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // ================================================================ lse2 fetch
+    // Waits for the unit's combined lse2 and stages it in SMEM for the
+    // aggregation warps (slot of the unit's TMEM buffer).
+    float* lse_s = reinterpret_cast<float*>(smem + p.off_lse);    // [kMaxBuf][NCP]
+    uint32_t ui = 0;
+    for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
+      const Job jb = decode_job(p, job);
+      for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
+        const uint32_t slot = ui % p.nbuf, tpar = (ui / p.nbuf) & 1;
+        const long long ubase = (long long)jb.b * p.U + u;
+        mbar_wait(bar_tempty + 8 * slot, tpar ^ 1);                   // previous user of ls[slot] done
+        if (lane == 0) {
+          spin_geq(p.cnt + ubase, (unsigned)p.n_tg + 1u, p.err);
+          trace_stamp(p, ui, 5);
+        }
+        __syncwarp();
+        __threadfence();
+        float* ls = lse_s + slot * p.NCP;
+        for (int c = lane; c < p.NCP; c += 32) ls[c] = (c < p.NC) ? __ldcg(p.lse_g + ubase * p.NC + c) : 0.f;
+        mbar_arrive(bar_lfull + 8 * slot);
+        __syncwarp();
+        if (lane == 0) {
+          // self-cleaning counter: n_tg arrivals + 1 combine + n_tg readers; the last resets it
+          if (atomicAdd(p.cnt + ubase, 1u) == 2u * p.n_tg) atomicExch(p.cnt + ubase, 0u);
         }
       }
     }
   } else if (warp >= kFinalWarp0) {
     // ================================================================ (l,h)-max aggregation
     const int q = warp & 3;
-    const int nch = p.NCP / 16;
     float* acc = reinterpret_cast<float*>(smem + p.off_acc);      // [tpc][Rv][128]
-    float* lse_s = reinterpret_cast<float*>(smem + p.off_lse);    // [2][NCP]
+    float* lse_s = reinterpret_cast<float*>(smem + p.off_lse);    // [kMaxBuf][NCP]
     const int tok = q * 32 + lane;
     uint32_t ui = 0;
     for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
@@ -450,56 +647,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         for (int r = 0; r < p.Rv; ++r) acc[(t * p.Rv + r) * kTileM + tok] = -CUDART_INF_F;
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
         const uint32_t slot = ui % p.nbuf, tpar = (ui / p.nbuf) & 1;
-        const long long ubase = (long long)jb.b * p.U + u;
-        float* ls = lse_s + (ui & 1) * p.NCP;
-        if (q == 0) {
-          if (lane == 0) spin_geq(p.cnt + ubase, (unsigned)p.n_tg + 1u, p.err);
-          __syncwarp();
-          __threadfence();
-          for (int c = lane; c < p.NCP; c += 32) ls[c] = (c < p.NC) ? __ldcg(p.lse_g + ubase * p.NC + c) : 0.f;
-          __syncwarp();
-          if (lane == 0) {
-            // self-cleaning counter: n_tg arrivals + 1 combine + n_tg readers; the last resets it
-            if (atomicAdd(p.cnt + ubase, 1u) == 2u * p.n_tg) atomicExch(p.cnt + ubase, 0u);
-          }
-        }
-        named_bar(2, 128);
+        float* ls = lse_s + slot * p.NCP;
+        mbar_wait(bar_lfull + 8 * slot, tpar);
         mbar_wait(bar_tfull + 8 * slot, tpar);
         tc_fence_after();
         const uint32_t sbase = tmem + ((uint32_t)(q * 32) << 16) + slot * p.slot_cols;
-        for (int t = 0; t < ntile; ++t) {
-          int r = 0, hh = 0;
-          float best = -CUDART_INF_F;
-          float* arow = acc + (t * p.Rv) * kTileM + tok;
+#pragma unroll 1
+        for (int grp = 0; grp < p.NCP / 32; ++grp) {
+          float lv[32];
 #pragma unroll
-          for (int k = 0; k < kMaxChunks; ++k) {
-            if (k < nch) {
-              float x[16], lv[16];
-              tmem_ld16(sbase + (uint32_t)t * p.NCP + k * 16, x);
-#pragma unroll
-              for (int i4 = 0; i4 < 4; ++i4) {
-                const float4 v4 = *reinterpret_cast<const float4*>(ls + 16 * k + 4 * i4);
-                lv[4 * i4] = v4.x; lv[4 * i4 + 1] = v4.y; lv[4 * i4 + 2] = v4.z; lv[4 * i4 + 3] = v4.w;
-              }
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                if (16 * k + i < p.NC) {
-                  best = fmaxf(best, fmaf(x[i], p.xs, -lv[i]));
-                  if (++hh == p.G) {
-                    float* a = arow + r * kTileM;
-                    *a = fmaxf(*a, best);
-                    best = -CUDART_INF_F;
-                    hh = 0;
-                    ++r;
-                  }
-                }
-              }
-            }
+          for (int i4 = 0; i4 < 8; ++i4) {
+            const float4 v4 = *reinterpret_cast<const float4*>(ls + grp * 32 + 4 * i4);
+            lv[4 * i4] = v4.x; lv[4 * i4 + 1] = v4.y; lv[4 * i4 + 2] = v4.z; lv[4 * i4 + 3] = v4.w;
           }
+          auto fold = [&](const float(&x)[32], int t) {
+            float* arow = acc + (t * p.Rv) * kTileM + tok;
+            switch (p.G) {
+              case 1: fold_tile<1>(x, lv, p.xs, grp, p.NC, p.G, p.Rv, arow); break;
+              case 2: fold_tile<2>(x, lv, p.xs, grp, p.NC, p.G, p.Rv, arow); break;
+              case 4: fold_tile<4>(x, lv, p.xs, grp, p.NC, p.G, p.Rv, arow); break;
+              case 8: fold_tile<8>(x, lv, p.xs, grp, p.NC, p.G, p.Rv, arow); break;
+              default: fold_tile<0>(x, lv, p.xs, grp, p.NC, p.G, p.Rv, arow); break;
+            }
+          };
+          for_tiles(sbase + grp * 32, p.NCP, ntile, fold);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_tempty + 8 * slot);
+        if (q == 0 && lane == 0) trace_stamp(p, ui, 6);
       }
       // ---- job epilogue: importance = mean_r 2^acc (possibly across unit groups)
       const float inv = 1.f / (float)p.Rv;
@@ -583,7 +759,7 @@ struct Plan {
   int P = 0, n_tg = 0, n_ug = 0, J = 0, T = 0, U = 0, tpc = 0, upc = 0;
   int NC = 0, NCP = 0, W = 0, nkb = 0, stages = 0, nbuf = 0, slot_cols = 0;
   long long total_jobs = 0;
-  uint32_t off_k = 0, off_q = 0, off_acc = 0, off_red = 0, off_lse = 0, off_bar = 0, smem = 0;
+  uint32_t off_k = 0, off_q = 0, off_acc = 0, off_red = 0, off_lse = 0, off_comb = 0, off_bar = 0, smem = 0;
   uint32_t k_stage_bytes = 0, q_slot_bytes = 0;
   size_t ws_part = 0, ws_lse = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0;
   size_t ws_total() const { return ws_part + ws_lse + ws_cnt + ws_acc + ws_fin; }
@@ -611,17 +787,20 @@ uint32_t carve(Plan& pl, int Rv, int stages) {
   pl.off_red = o;
   o += 2 * 4 * pl.NCP * 8;
   pl.off_lse = o;
-  o += 2 * pl.NCP * 4;
+  o += kMaxBuf * pl.NCP * 4;
+  o = (o + 15) & ~15u;
+  pl.off_comb = o;
+  o += 16 + 4 * pl.NCP * 8;
   o = (o + 15) & ~15u;
   pl.off_bar = o;
-  o += (2 * stages + 4 + 2 * kMaxBuf) * 8 + 16;
+  o += (2 * stages + 8 + 3 * kMaxBuf) * 8 + 16;
   return o + 1024;                                   // slack for the manual 1024-byte alignment
 }
 
 Plan make_plan(const Geom& g, bool allow_override = true) {
   Plan pl;
   pl.NC = g.G * g.Rv;
-  pl.NCP = ((pl.NC + 15) / 16) * 16;
+  pl.NCP = ((pl.NC + 31) / 32) * 32;                  // TMEM column groups of 32 (one tcgen05.ld.x32)
   if (pl.NCP > 16 * kMaxChunks) return pl;
   pl.W = (g.d % 64 == 0) ? 64 : (g.d % 32 == 0 ? 32 : 16);
   pl.nkb = g.d / pl.W;
@@ -730,6 +909,14 @@ bool encode_maps(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, 
 
 }  // namespace
 
+static unsigned long long* g_trace = nullptr;
+static long long g_trace_records = 0;
+
+void fused_set_trace(unsigned long long* buf, long long records) {
+  g_trace = buf;
+  g_trace_records = records;
+}
+
 bool fused_supported(const Geom& g, const Layout&, const void*, const void*) {
   if (g.G > 256 || g.Rv > 256) return false;         // TMA box dims
   return make_plan(g).ok;
@@ -765,7 +952,7 @@ cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Ge
   p.xs = g.scale * kLog2e;
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(pl.NCP >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
   p.layout_type = pl.W == 64 ? 2u : (pl.W == 32 ? 4u : 6u);
-  p.off_k = pl.off_k; p.off_q = pl.off_q; p.off_acc = pl.off_acc; p.off_red = pl.off_red; p.off_lse = pl.off_lse;
+  p.off_k = pl.off_k; p.off_q = pl.off_q; p.off_acc = pl.off_acc; p.off_red = pl.off_red; p.off_lse = pl.off_lse; p.off_comb = pl.off_comb;
   p.off_bar = pl.off_bar; p.k_stage_bytes = pl.k_stage_bytes; p.q_slot_bytes = pl.q_slot_bytes;
   char* w = reinterpret_cast<char*>(ws);
   // counters first: their offsets depend only on (B, U), not on the plan
@@ -780,6 +967,16 @@ cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Ge
   p.accpart = pl.ws_acc ? reinterpret_cast<float*>(w) : nullptr;
   p.imp = importance;
   p.err = device_error_flag();
+  p.trace = nullptr;
+  p.trace_units = 0;
+  if (g_trace != nullptr) {
+    const long long grid = std::min<long long>(pl.P, pl.total_jobs);
+    const long long units = (g_trace_records / 8) / grid;
+    if (units > 0) {
+      p.trace = g_trace;
+      p.trace_units = (int)std::min<long long>(units, 1 << 30);
+    }
+  }
 
   static int configured_smem = -1;
   if (configured_smem < (int)pl.smem) {

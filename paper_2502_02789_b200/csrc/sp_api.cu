@@ -188,6 +188,15 @@ sp_status sp_score_plan(const sp_geom* g, int64_t out[9]) {
   return SP_OK;
 }
 
+sp_status sp_trace_enable(uint64_t* device_buffer, int64_t records) {
+  if (device_buffer == nullptr || records < 8) {
+    fused_set_trace(nullptr, 0);
+    return SP_OK;
+  }
+  fused_set_trace(reinterpret_cast<unsigned long long*>(device_buffer), records);
+  return SP_OK;
+}
+
 size_t sp_score_split_workspace_bytes(const sp_geom* g) {
   if (check_geom(g) != SP_OK) return 0;
   Geom G = to_geom(*g);

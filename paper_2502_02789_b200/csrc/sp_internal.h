@@ -64,6 +64,7 @@ cudaError_t simt_score_finish(const __nv_bfloat16* Q, const __nv_bfloat16* K, co
 bool fused_supported(const Geom& g, const Layout& lay, const void* Q, const void* K);
 size_t fused_score_ws_bytes(const Geom& g);
 bool fused_plan_info(const Geom& g, long long out[9]);
+void fused_set_trace(unsigned long long* buf, long long records);
 cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                         float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
 

@@ -92,19 +92,19 @@ def test_geometries(algo, variant):
     _small_case(w, algo)
 
 
-@pytest.mark.parametrize("plan", ["1,1", "2,1", "1,2", "2,2", "4,1", "1,4", "37,1", "37,2", "37,4"])
-def test_fused_forced_plans(plan, monkeypatch):
+@pytest.mark.parametrize("plan,N", [("1,1", 2000), ("1,2", 2000), ("1,4", 2000), ("2,1", 5000), ("2,2", 5000),
+                                    ("4,1", 5000), ("37,1", 5000), ("37,2", 5000), ("37,4", 5000)])
+def test_fused_forced_plans(plan, N, monkeypatch):
     """Every decomposition of the fused kernel (token groups x unit groups) gives
     the oracle's importance: single-CTA, multi-CTA statistics exchange, and the
     cross-unit-group max."""
     monkeypatch.setenv("SP_FUSED_PLAN", plan)
-    w = gen.CONFIGS["C0"].with_(L=4, H=8, Hkv=2, d=64, N=5000, R=3, B=2)
-    Q = torch.empty(0)
-    _small_case(w, "fused")
-    Qd = _dev(gen.gen_batch(w)[0])
+    w = gen.CONFIGS["C0"].with_(L=4, H=8, Hkv=2, d=64, N=N, R=3, B=2)
+    Qb = gen.gen_batch(w)[0]
     K = torch.empty((w.B, w.L, w.Hkv, w.N, w.d), dtype=torch.bfloat16, device="cuda")
-    pl = sp.score_plan(Qd, K)
+    pl = sp.score_plan(_dev(Qb), K)
     assert (pl["token_groups"], pl["unit_groups"]) == tuple(int(x) for x in plan.split(","))
+    _small_case(w, "fused")
 
 
 @pytest.mark.parametrize("algo", ALGOS)

@@ -1,0 +1,70 @@
+"""Timeline of the fused score kernel from its globaltimer trace (debug tool).
+
+  python tools/trace_fused.py [--config C3] [--plan n_tg,n_ug]
+
+Event ids per (CTA, unit): 0 producer starts unit, 1 MMA starts (slot free),
+2 stats start, 3 CTA partial published, 4 lse combined (last CTA), 5 aggregation
+sees lse, 6 aggregation done.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2502_02789_b200 as sp  # noqa: E402
+from spgen import cuda as spgen_cuda  # noqa: E402
+from spgen import gen  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--plan", default=None)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    if a.plan:
+        os.environ["SP_FUSED_PLAN"] = a.plan
+    w = gen.CONFIGS[a.config]
+    Q, K, T = spgen_cuda.make_inputs(w)
+    plan = sp.score_plan(Q, K, w.Rv)
+    grid, upj = plan["grid"], plan["units_per_job"]
+    units = upj * ((w.B * plan["jobs_per_request"] + grid - 1) // grid)
+    buf = torch.zeros(grid * units * 8, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")
+    sp.lib().sp_trace_enable(buf.data_ptr(), buf.numel())
+    sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")
+    torch.cuda.synchronize()
+    sp.lib().sp_trace_enable(None, 0)
+    tr = buf.view(grid, units, 8).cpu().numpy().astype(np.float64)
+    t0 = tr[tr > 0].min()
+    tr = np.where(tr > 0, (tr - t0) / 1000.0, np.nan)            # microseconds from the first stamp
+    if a.out:
+        np.save(a.out, tr)
+    print("plan", plan, "units/CTA", units)
+    print("kernel span (us) %.1f" % np.nanmax(tr))
+    names = ["prod", "mma", "stats", "publ", "comb", "lseseen", "aggdone"]
+    for (x, y) in [(1, 2), (2, 3), (3, 5), (5, 6), (1, 6), (0, 1)]:
+        d = tr[:, :, y] - tr[:, :, x]
+        print(f"{names[x]:>8} -> {names[y]:<8} mean {np.nanmean(d):8.2f} us  p50 {np.nanmedian(d):8.2f}  max {np.nanmax(d):8.2f}")
+    # per-unit period: successive MMA starts
+    per = np.diff(tr[:, :, 1], axis=1)
+    print("MMA start period per unit: mean %.2f us  p50 %.2f" % (np.nanmean(per), np.nanmedian(per)))
+    per = np.diff(tr[:, :, 6], axis=1)
+    print("agg done period per unit:  mean %.2f us  p50 %.2f" % (np.nanmean(per), np.nanmedian(per)))
+    # skew: for each unit index, spread of publish times across CTAs
+    pub = tr[:, :, 3]
+    print("publish skew across CTAs per unit (max-min): mean %.2f us" % np.nanmean(np.nanmax(pub, 0) - np.nanmin(pub, 0)))
+    for c in [0, grid // 2, grid - 1]:
+        print(f"CTA {c}: first units (us):")
+        for u in range(min(4, units)):
+            print("   ", " ".join(f"{x:8.1f}" for x in tr[c, u, :7]))
+
+
+if __name__ == "__main__":
+    main()
