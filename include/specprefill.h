@@ -150,8 +150,9 @@ sp_status sp_score_plan(const sp_geom* g, int64_t out[9]);
  * every sp_score launch writes globaltimer stamps (ns) into device_buffer laid
  * out as [grid CTA][unit index within the CTA][8] uint64:
  *   0 producer starts the unit, 1 MMA starts it (TMEM slot free), 2 statistics
- *   start (logits in TMEM), 3 CTA partial published, 4 lse2 combined (last CTA
- *   only), 5 aggregation sees lse2, 6 aggregation done (TMEM slot released).
+ *   start (logits in TMEM), 3 CTA partial published, 4 partials read (cleanup
+ *   done), 5 lse2 combined from all partials, 6 aggregation done (TMEM slot
+ *   released), 7 statistics compute done.
  * records = capacity in uint64; units beyond capacity are not traced.
  * device_buffer = NULL disables tracing. */
 sp_status sp_trace_enable(uint64_t* device_buffer, int64_t records);

@@ -47,7 +47,8 @@ constexpr int kStatsWarp0 = 4;
 constexpr int kFinalWarp0 = 8;
 constexpr int kMaxStages = 8;
 constexpr int kMaxChunks = 8;          // NCP <= 128 columns (16-column chunks)
-constexpr int kMaxBuf = 8;             // TMEM unit slots
+constexpr int kMaxSlots = 16;          // TMEM tile slots (512 columns / 32)
+constexpr int kMaxLseBatch = 20;       // float4 partial loads in flight per lane (40 token groups)
 constexpr int kTmemCols = 512;
 constexpr int kSmemLimit = 232448;     // sm_100 max dynamic shared memory per block
 
@@ -59,7 +60,7 @@ struct FusedParams {
   int T, U;                            // tiles / units per request
   int n_tg, n_ug, J;                   // token groups, unit groups, jobs per request
   long long total_jobs;
-  int NC, NCP, W, nkb, stages, nbuf, slot_cols, tpc;
+  int NC, NCP, W, nkb, stages, nslots, tpc;
   float xs;                            // scale * log2(e)
   uint32_t idesc;                      // tcgen05 instruction descriptor
   uint32_t layout_type;                // UMMA smem descriptor swizzle code
@@ -67,9 +68,9 @@ struct FusedParams {
   uint32_t off_k, off_q, off_acc, off_red, off_lse, off_comb, off_bar;
   uint32_t k_stage_bytes, q_slot_bytes;
   // workspace
-  float2* part;                        // [B][U][n_tg][NC] CTA partials (m, s), m in raw-logit units
-  float* lse_g;                        // [B][U][NC]       combined lse2 per (l, h, r) column
-  unsigned* cnt;                       // [B][U]           exchange counters (self-cleaning)
+  unsigned long long* part;            // [B][U][n_tg][NCP] CTA partials: (m, s) packed in one 64-bit word,
+                                       // m = max raw logit, s = sum 2^((x-m)*xs); 0 = "not yet written"
+  unsigned* cnt;                       // [B][U]           readers done (the last one re-zeroes the partials)
   float* accpart;                      // [B][n_ug][Rv][N]
   unsigned* fin_cnt;                   // [B][n_tg]    finalize counters (self-cleaning)
   float* imp;                          // [B][N]
@@ -107,13 +108,21 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// Wait for an mbarrier phase.  Bounded: a pipeline that never completes
-// (which would be a bug) traps after ~4 s instead of hanging the GPU.
+// Wait for an mbarrier phase.  After a few immediate retries the waiting warp
+// backs off with __nanosleep so that idle waiters (up to half the CTA's warps at
+// any time) do not steal issue slots from the epilogue warps on their SMSP.
+// Bounded: a pipeline that never completes (a bug) traps after ~4 s.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
-  const uint64_t t0 = globaltimer_ns();
-  while (!mbar_try_wait(bar, parity)) {
-    if (globaltimer_ns() - t0 > 4000000000ull) asm volatile("trap;");
+  uint64_t t0 = 0;
+  for (uint32_t i = 1;; ++i) {
+    if (mbar_try_wait(bar, parity)) return;
+    if (i > 4) __nanosleep(i < 32 ? 20 : 80);
+    if ((i & 1023) == 0) {
+      const uint64_t now = globaltimer_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 4000000000ull) asm volatile("trap;");
+    }
   }
 }
 __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2,
@@ -228,6 +237,56 @@ __device__ __forceinline__ void for_tiles16(uint32_t base, uint32_t stride, int 
   }
 }
 
+// f(x, t) for every tile t < ntile, loading NB tiles per tcgen05.wait::ld so
+// that NB TMEM round trips overlap (tcgen05.ld latency is ~hundreds of cycles).
+template <int NB, class F>
+__device__ __forceinline__ void for_tiles16_batched(uint32_t base, uint32_t stride, int ntile, F&& f) {
+  for (int t0 = 0; t0 < ntile; t0 += NB) {
+    float x[NB][16];
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (t0 + j < ntile) tmem_ld16_issue(base + (uint32_t)(t0 + j) * stride, x[j]);
+    tmem_wait();
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      tie16(x[j]);
+      if (t0 + j < ntile) f(x[j], t0 + j);
+    }
+  }
+}
+template <int NB, class F>
+__device__ __forceinline__ void for_tiles32_batched(uint32_t base, uint32_t stride, int ntile, F&& f) {
+  for (int t0 = 0; t0 < ntile; t0 += NB) {
+    float x[NB][32];
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (t0 + j < ntile) tmem_ld32_issue(base + (uint32_t)(t0 + j) * stride, x[j]);
+    tmem_wait();
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      tie32(x[j]);
+      if (t0 + j < ntile) f(x[j], t0 + j);
+    }
+  }
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long pack_ms(float m, float s) {
+  return (unsigned long long)__float_as_uint(m) | ((unsigned long long)__float_as_uint(s) << 32);
+}
+__device__ __forceinline__ float2 unpack_ms(unsigned long long w) {
+  return make_float2(__uint_as_float((unsigned)w), __uint_as_float((unsigned)(w >> 32)));
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -246,7 +305,7 @@ __device__ __forceinline__ void spin_geq(const unsigned* p, unsigned target, int
       set_err(err, kDevTimeout);
       return;
     }
-    if (it > 64) __nanosleep(64);
+    if (it > 8) __nanosleep(it < 64 ? 32 : 100);
   }
 }
 
@@ -281,16 +340,24 @@ __device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
   return op(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
 }
 
+// 2^x with one MUFU op (flush-to-zero: results below 2^-126 contribute nothing
+// measurable to a softmax denominator or a probability > 1e-30).
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Merge a partial (m, s) -- s = sum 2^((x - m) * xs) over a token subset, m the
 // subset's max raw logit -- into the running pair (M, S).  Empty partials (s == 0)
 // are skipped, so an all-masked subset (m = -inf) is harmless.
 __device__ __forceinline__ void lse_merge(float& M, float& S, float2 v, float xs) {
   if (!(v.y > 0.f)) return;
   if (v.x > M) {
-    S = S * exp2f((M - v.x) * xs) + v.y;
+    S = S * ex2((M - v.x) * xs) + v.y;
     M = v.x;
   } else {
-    S += v.y * exp2f((v.x - M) * xs);
+    S += v.y * ex2((v.x - M) * xs);
   }
 }
 
@@ -320,13 +387,13 @@ __device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
 // Fold one tile's 32 logit columns (group grp) into the running (l,h)-max of
 // this thread's token: acc[(t*Rv + r)*128 + tok] = max(acc, max_h (x*xs - lse2)).
 // Columns are r-major (c = r*G + h).  kG > 0: compile-time group size dividing 32.
-template <int kG>
-__device__ __forceinline__ void fold_tile(const float (&x)[32], const float (&lv)[32], float xs, int grp, int NC,
+template <int kG, int kW>
+__device__ __forceinline__ void fold_tile(const float (&x)[kW], const float (&lv)[kW], float xs, int grp, int NC,
                                           int G, int Rv, float* arow) {
   if constexpr (kG > 0) {
 #pragma unroll
-    for (int rr = 0; rr < 32 / kG; ++rr) {
-      const int r = grp * (32 / kG) + rr;
+    for (int rr = 0; rr < kW / kG; ++rr) {
+      const int r = grp * (kW / kG) + rr;
       if (r < Rv) {
         float best = fmaf(x[rr * kG], xs, -lv[rr * kG]);
 #pragma unroll
@@ -340,8 +407,8 @@ __device__ __forceinline__ void fold_tile(const float (&x)[32], const float (&lv
     float best = -CUDART_INF_F;
     int cur = -1;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int c = grp * 32 + i;
+    for (int i = 0; i < kW; ++i) {
+      const int c = grp * kW + i;
       if (c < NC) {
         const int r = c / G;
         if (r != cur) {
@@ -379,38 +446,70 @@ __device__ __forceinline__ Job decode_job(const FusedParams& p, long long job) {
 }
 
 // ------------------------------------------------------------------ the kernel
+// Online (max, sum) merge in the log2 domain: (m, s) <- (m, s) (+) (m2, s2),
+// s = sum 2^(x - m).  Empty partials are (-inf, 0); two empties stay empty.
+__device__ __forceinline__ void merge2(float& m, float& s, float m2, float s2) {
+  const float M = fmaxf(m, m2);
+  const float Ms = (M == -CUDART_INF_F) ? 0.f : M;
+  s = s * ex2(m - Ms) + s2 * ex2(m2 - Ms);
+  m = M;
+}
+
+// Transposed butterfly merge of 32 columns x 32 lanes of (m, s) pairs: lane l
+// returns column l merged over all 32 lanes.  31 merges per lane.
+__device__ __forceinline__ void transpose_merge32(float (&m)[32], float (&s)[32], int lane, float& mo, float& so) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool up = lane & w;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float sm = up ? m[i] : m[i + w], ss = up ? s[i] : s[i + w];
+      float km = up ? m[i + w] : m[i], ks = up ? s[i + w] : s[i];
+      merge2(km, ks, __shfl_xor_sync(0xffffffffu, sm, w), __shfl_xor_sync(0xffffffffu, ss, w));
+      m[i] = km;
+      s[i] = ks;
+    }
+  }
+  mo = m[0];
+  so = s[0];
+}
+
+// kG: compile-time GQA group size (1, 2, 4, 8) or 0 for any G.  One
+// instantiation per group size keeps the kernel's hot code small: the warp
+// roles run different code concurrently on each SMSP and share the
+// instruction cache.
+template <int kG>
 __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ FusedParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
-  // barrier map: full[S] empty[S] qfull[2] qempty[2] tfull[kMaxBuf] tempty[kMaxBuf]
-  //              rfull[2] rempty[2] lfull[kMaxBuf]; then the TMEM base address
+  // barrier map: full[S] empty[S] qfull[2] qempty[2] tfull[kMaxSlots] tempty[kMaxSlots]
+  //              rfull[2] rempty[2] lfull[2] lempty[2]; then the TMEM base address
   const uint32_t bar_full = smem_u32(bars), bar_empty = bar_full + 8 * p.stages;
   const uint32_t bar_qfull = bar_empty + 8 * p.stages, bar_qempty = bar_qfull + 16;
-  const uint32_t bar_tfull = bar_qempty + 16, bar_tempty = bar_tfull + 8 * kMaxBuf;
-  const uint32_t bar_rfull = bar_tempty + 8 * kMaxBuf, bar_rempty = bar_rfull + 16;
-  const uint32_t bar_lfull = bar_rempty + 16;
-  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 2 * p.stages + 8 + 3 * kMaxBuf);
+  const uint32_t bar_tfull = bar_qempty + 16, bar_tempty = bar_tfull + 8 * kMaxSlots;
+  const uint32_t bar_rfull = bar_tempty + 8 * kMaxSlots, bar_rempty = bar_rfull + 16;
+  const uint32_t bar_lfull = bar_rempty + 16, bar_lempty = bar_lfull + 16;
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 2 * p.stages + 12 + 2 * kMaxSlots);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(bar_full + 8 * s, 1);
       mbar_init(bar_empty + 8 * s, 1);
     }
+    for (int s = 0; s < kMaxSlots; ++s) {
+      mbar_init(bar_tfull + 8 * s, 1);
+      mbar_init(bar_tempty + 8 * s, 4);
+    }
     for (int s = 0; s < 2; ++s) {
       mbar_init(bar_qfull + 8 * s, 1);
       mbar_init(bar_qempty + 8 * s, 1);
-    }
-    for (int s = 0; s < kMaxBuf; ++s) {
-      mbar_init(bar_tfull + 8 * s, 1);
-      mbar_init(bar_tempty + 8 * s, 4);
-      mbar_init(bar_lfull + 8 * s, 32);
-    }
-    for (int s = 0; s < 2; ++s) {
       mbar_init(bar_rfull + 8 * s, 128);
       mbar_init(bar_rempty + 8 * s, 1);
+      mbar_init(bar_lfull + 8 * s, 32);
+      mbar_init(bar_lempty + 8 * s, 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&p.tmK);
@@ -430,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_base_s;
+  const uint32_t nslots = (uint32_t)p.nslots;
 
   if (warp == 0) {
     // ================================================================ TMA producer
@@ -460,24 +560,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     }
   } else if (warp == 1) {
     // ================================================================ MMA issuer
+    // Each tile's logits D[128 x NCP] go to the next slot of a ring of nslots
+    // TMEM tile slots; a slot is released by the aggregation warps once they
+    // have folded that tile (tile-granular reuse hides the exchange latency).
     if (lane == 0) {
-      uint32_t stage = 0, sphase = 0, ui = 0;
+      uint32_t stage = 0, sphase = 0, ui = 0, gt = 0;
       const uint32_t sbo = 8 * p.W * 2;
       for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
         const Job jb = decode_job(p, job);
         for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
-          const uint32_t slot = ui % p.nbuf, tpar = (ui / p.nbuf) & 1;
           const uint32_t qs = ui & 1, qpar = (ui >> 1) & 1;
-          mbar_wait(bar_tempty + 8 * slot, tpar ^ 1);
-          trace_stamp(p, ui, 1);
           mbar_wait(bar_qfull + 8 * qs, qpar);
-          tc_fence_after();
           const uint32_t qbase = smem_u32(smem + p.off_q + qs * p.q_slot_bytes);
-          for (int t = jb.t_lo; t < jb.t_hi; ++t) {
+          for (int t = jb.t_lo; t < jb.t_hi; ++t, ++gt) {
+            const uint32_t slot = gt % nslots;
+            mbar_wait(bar_tempty + 8 * slot, ((gt / nslots) & 1) ^ 1);
+            if (t == jb.t_lo) trace_stamp(p, ui, 1);
             mbar_wait(bar_full + 8 * stage, sphase);
             tc_fence_after();
             const uint32_t kbase = smem_u32(smem + p.off_k + stage * p.k_stage_bytes);
-            const uint32_t dcol = tmem + slot * p.slot_cols + (uint32_t)(t - jb.t_lo) * p.NCP;
+            const uint32_t dcol = tmem + slot * p.NCP;
             for (int kb = 0; kb < p.nkb; ++kb) {
               for (int ks = 0; ks < p.W / 16; ++ks) {
                 const uint64_t a = make_sdesc(kbase + kb * (kTileM * p.W * 2) + ks * 32, sbo, p.layout_type);
@@ -486,74 +588,77 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
               }
             }
             umma_commit(bar_empty + 8 * stage);
+            umma_commit(bar_tfull + 8 * slot);
             if (++stage == (uint32_t)p.stages) { stage = 0; sphase ^= 1; }
           }
           umma_commit(bar_qempty + 8 * qs);
-          umma_commit(bar_tfull + 8 * slot);
         }
       }
     }
   } else if (warp >= kStatsWarp0 && warp < kFinalWarp0) {
     // ================================================================ softmax statistics
-    // Two passes over the unit's logits, both from TMEM (no HBM traffic):
-    //   A: per-column max over this warp's token rows of every tile (thread-local, one
-    //      transposed butterfly per 16 columns);
-    //   B: per-column sum of 2^((x - max) * xs) (thread-local, one exp2 per logit).
-    // The 4 warps' (max, sum) pairs merge in SMEM; warp 4 publishes the CTA partial and
-    // the last CTA of the token groups combines them into lse2 for every CTA.
+    // Progressive: each tile is folded as soon as its MMA completes into a
+    // per-thread running (ref, sum) per column, sum = sum 2^(x*xs - ref) with
+    // ref the first value seen (re-based only if a value exceeds it by > 2^64,
+    // which keeps fp32 finite): one exp2 per logit, no per-tile shuffles.  At
+    // the end of the unit one transposed merge gives the warp's (max, sum) per
+    // column; the exchange warp merges the 4 warps and publishes.
     const int q = warp & 3;                       // TMEM lane quarter
     float2* red = reinterpret_cast<float2*>(smem + p.off_red);   // [2][4][NCP]
-    uint32_t ui = 0;
+    uint32_t ui = 0, gt = 0;
     for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
       const Job jb = decode_job(p, job);
-      const int ntile = jb.t_hi - jb.t_lo;
+      const long long tok0 = (long long)jb.t_lo * kTileM + q * 32 + lane;
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
-        const uint32_t slot = ui % p.nbuf, tpar = (ui / p.nbuf) & 1;
-        mbar_wait(bar_tfull + 8 * slot, tpar);
-        if (q == 0 && lane == 0) trace_stamp(p, ui, 2);
-        tc_fence_after();
-        mbar_wait(bar_rempty + 8 * (ui & 1), ((ui >> 1) & 1) ^ 1);   // exchange warp done with this buffer
-        const uint32_t sbase = tmem + ((uint32_t)(q * 32) << 16) + slot * p.slot_cols;
+        const uint32_t gt0 = gt;
         float2* rb = red + (ui & 1) * 4 * p.NCP;
-        const long long tok0 = (long long)jb.t_lo * kTileM + q * 32 + lane;
+        mbar_wait(bar_rempty + 8 * (ui & 1), ((ui >> 1) & 1) ^ 1);   // exchange warp done with rb
 #pragma unroll 1
-        for (int k = 0; k < p.NCP / 16; ++k) {
-          // ---- pass A: column max (raw logits; xs > 0 so scaling commutes with max)
-          float m[16];
+        for (int grp = 0; grp < p.NCP / 32; ++grp) {
+          float ref[32], sum[32];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) m[i] = -CUDART_INF_F;
-          for_tiles16(sbase + k * 16, p.NCP, ntile, [&](const float(&x)[16], int t) {
-            if (tok0 + (long long)t * kTileM < p.N) {
+          for (int i = 0; i < 32; ++i) { ref[i] = -CUDART_INF_F; sum[i] = 0.f; }
+          gt = gt0;
+          for (int t = jb.t_lo; t < jb.t_hi; ++t, ++gt) {
+            const uint32_t slot = gt % nslots;
+            mbar_wait(bar_tfull + 8 * slot, (gt / nslots) & 1);
+            if (grp == 0 && t == jb.t_lo && q == 0 && lane == 0) trace_stamp(p, ui, 2);
+            tc_fence_after();
+            float x[32];
+            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + slot * p.NCP + grp * 32;
+            float* x0 = x;
+            tmem_ld16_issue(ta, *reinterpret_cast<float(*)[16]>(x0));
+            tmem_ld16_issue(ta + 16, *reinterpret_cast<float(*)[16]>(x0 + 16));
+            tmem_wait();
+            tie16(*reinterpret_cast<float(*)[16]>(x0));
+            tie16(*reinterpret_cast<float(*)[16]>(x0 + 16));
+            if (tok0 + (long long)(t - jb.t_lo) * kTileM < p.N) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) m[i] = fmaxf(m[i], x[i]);
+              for (int i = 0; i < 32; ++i) {
+                const float y = x[i] * p.xs;
+                const float dlt = y - ref[i];
+                if (dlt > 64.f) {                    // first value, or a jump: re-base the sum
+                  sum[i] = fmaf(sum[i], ex2(-dlt), 1.f);
+                  ref[i] = y;
+                } else {
+                  sum[i] += ex2(dlt);
+                }
+              }
             }
-          });
-          const float mcol = transpose_reduce16<true>(m, lane);        // column 16k + (lane >> 1)
-          const float mref = (mcol == -CUDART_INF_F) ? 0.f : mcol * p.xs;
-          float nref[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) nref[i] = -__shfl_sync(0xffffffffu, mref, 2 * i);
-          // ---- pass B: sum of exp2(x*xs - max*xs)
-          float e[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) e[i] = 0.f;
-          for_tiles16(sbase + k * 16, p.NCP, ntile, [&](const float(&x)[16], int t) {
-            if (tok0 + (long long)t * kTileM < p.N) {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) e[i] += exp2f(fmaf(x[i], p.xs, nref[i]));
-            }
-          });
-          const float scol = transpose_reduce16<false>(e, lane);
-          if ((lane & 1) == 0) rb[q * p.NCP + 16 * k + (lane >> 1)] = make_float2(mcol, scol);
+          }
+          float mo, so;
+          transpose_merge32(ref, sum, lane, mo, so);                    // column 32*grp + lane
+          rb[q * p.NCP + grp * 32 + lane] = make_float2(mo, so);
         }
-        mbar_arrive(bar_rfull + 8 * (ui & 1));                       // 128 arrivals: all columns written
+        if (q == 0 && lane == 0) trace_stamp(p, ui, 7);
+        mbar_arrive(bar_rfull + 8 * (ui & 1));                        // 128 arrivals: all columns written
       }
     }
   } else if (warp == 2) {
     // ================================================================ statistics exchange
-    // Merge the 4 statistics warps into the CTA partial, publish it, and -- if
-    // this CTA is the last of the unit's token groups -- combine all partials
-    // into lse2 (fixed token-group order: deterministic) and mark it ready.
+    // Merge the 4 statistics warps into the CTA partial and publish it: one
+    // 64-bit word (max2, sum) per column, single-copy atomic, so a reader sees
+    // either 0 (not yet written) or the complete pair -- no flag, no fence.
     const float2* red = reinterpret_cast<const float2*>(smem + p.off_red);   // [2][4][NCP]
     uint32_t ui = 0;
     for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
@@ -562,119 +667,150 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const long long ubase = (long long)jb.b * p.U + u;
         mbar_wait(bar_rfull + 8 * (ui & 1), (ui >> 1) & 1);
         const float2* rb = red + (ui & 1) * 4 * p.NCP;
-        float2* mypart = p.part + (ubase * p.n_tg + jb.tg) * p.NC;
-        for (int c = lane; c < p.NC; c += 32) {
+        unsigned long long* mypart = p.part + (ubase * p.n_tg + jb.tg) * p.NCP;
+        for (int c = lane; c < p.NCP; c += 32) {
           float mm = -CUDART_INF_F, ss = 0.f;
+          if (c < p.NC) {
 #pragma unroll
-          for (int w = 0; w < 4; ++w) lse_merge(mm, ss, rb[w * p.NCP + c], p.xs);
-          mypart[c] = make_float2(mm, ss);
+            for (int w = 0; w < 4; ++w) merge2(mm, ss, rb[w * p.NCP + c].x, rb[w * p.NCP + c].y);
+          }
+          if (!(ss > 0.f)) { mm = -CUDART_INF_F; ss = -1.f; }          // written, but empty
+          st_relaxed_u64(mypart + c, pack_ms(mm, ss));
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_rempty + 8 * (ui & 1));
-        __threadfence();
-        __syncwarp();
-        unsigned old = 0;
         if (lane == 0) {
-          old = atomicAdd(p.cnt + ubase, 1u);
+          mbar_arrive(bar_rempty + 8 * (ui & 1));
           trace_stamp(p, ui, 3);
-        }
-        old = __shfl_sync(0xffffffffu, old, 0);
-        if (old == (unsigned)p.n_tg - 1) {
-          __threadfence();
-          const float2* src = p.part + ubase * p.n_tg * p.NC;
-          for (int c = lane; c < p.NC; c += 32) {
-            float mm = -CUDART_INF_F, ss = 0.f;
-            for (int s0 = 0; s0 < p.n_tg; s0 += 16) {
-              float2 v[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                v[j] = s0 + j < p.n_tg ? __ldcg(&src[(s0 + j) * p.NC + c]) : make_float2(-CUDART_INF_F, 0.f);
-#pragma unroll
-              for (int j = 0; j < 16; ++j) lse_merge(mm, ss, v[j], p.xs);
-            }
-            const float l2 = mm * p.xs + log2f(ss);
-            if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
-            p.lse_g[ubase * p.NC + c] = l2;
-          }
-          __threadfence();
-          __syncwarp();
-          if (lane == 0) {
-            atomicAdd(p.cnt + ubase, 1u);                               // n_tg + 1: lse2 ready
-            trace_stamp(p, ui, 4);
-          }
         }
       }
     }
   } else if (warp == 3) {
-    // ================================================================ lse2 fetch
-    // Waits for the unit's combined lse2 and stages it in SMEM for the
-    // aggregation warps (slot of the unit's TMEM buffer).
-    float* lse_s = reinterpret_cast<float*>(smem + p.off_lse);    // [kMaxBuf][NCP]
+    // ================================================================ lse2 gather
+    // Polls the unit's n_tg published partials (all loads of a batch in flight
+    // together; zero words are re-read until written), merges them in
+    // token-group order -- every CTA computes the same lse2 bit for bit -- and
+    // stages lse2 in SMEM for the aggregation warps.
+    float* lse_s = reinterpret_cast<float*>(smem + p.off_lse);    // [2][NCP]
     uint32_t ui = 0;
     for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
       const Job jb = decode_job(p, job);
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
-        const uint32_t slot = ui % p.nbuf, tpar = (ui / p.nbuf) & 1;
+        const uint32_t par = ui & 1;
         const long long ubase = (long long)jb.b * p.U + u;
-        mbar_wait(bar_tempty + 8 * slot, tpar ^ 1);                   // previous user of ls[slot] done
-        if (lane == 0) {
-          spin_geq(p.cnt + ubase, (unsigned)p.n_tg + 1u, p.err);
-          trace_stamp(p, ui, 5);
+        mbar_wait(bar_lempty + 8 * par, ((ui >> 1) & 1) ^ 1);          // aggregation done with ls[par]
+        float* ls = lse_s + par * p.NCP;
+        const unsigned long long* src = p.part + ubase * p.n_tg * p.NCP;
+        for (int c = lane; c < p.NCP; c += 32) {
+          float M = -CUDART_INF_F, S = 0.f;
+          for (int s0 = 0; s0 < p.n_tg; s0 += kMaxLseBatch) {
+            unsigned long long v[kMaxLseBatch];
+            uint32_t missing = 0;
+#pragma unroll
+            for (int j = 0; j < kMaxLseBatch; ++j) {
+              v[j] = (s0 + j < p.n_tg) ? ld_relaxed_u64(src + (long long)(s0 + j) * p.NCP + c) : pack_ms(0.f, -1.f);
+              missing |= (v[j] == 0ull ? 1u : 0u) << j;
+            }
+            long long it = 0;
+            while (__any_sync(0xffffffffu, missing != 0)) {
+              __nanosleep(it < 8 ? 64 : 200);
+#pragma unroll
+              for (int j = 0; j < kMaxLseBatch; ++j) {
+                if (missing & (1u << j)) {
+                  v[j] = ld_relaxed_u64(src + (long long)(s0 + j) * p.NCP + c);
+                  if (v[j] != 0ull) missing &= ~(1u << j);
+                }
+              }
+              if (++it > (1LL << 22)) {
+                set_err(p.err, kDevTimeout);
+#pragma unroll
+                for (int j = 0; j < kMaxLseBatch; ++j)
+                  if (missing & (1u << j)) v[j] = pack_ms(0.f, -1.f);
+                missing = 0;
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < kMaxLseBatch; ++j) {
+              const float2 w = unpack_ms(v[j]);
+              if (w.y > 0.f) merge2(M, S, w.x, w.y);
+            }
+          }
+          float l2 = 0.f;
+          if (c < p.NC) {
+            l2 = M + log2f(S);
+            if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
+          }
+          ls[c] = l2;
         }
+        if (lane == 0) trace_stamp(p, ui, 5);
+        mbar_arrive(bar_lfull + 8 * par);
         __syncwarp();
-        __threadfence();
-        float* ls = lse_s + slot * p.NCP;
-        for (int c = lane; c < p.NCP; c += 32) ls[c] = (c < p.NC) ? __ldcg(p.lse_g + ubase * p.NC + c) : 0.f;
-        mbar_arrive(bar_lfull + 8 * slot);
-        __syncwarp();
-        if (lane == 0) {
-          // self-cleaning counter: n_tg arrivals + 1 combine + n_tg readers; the last resets it
-          if (atomicAdd(p.cnt + ubase, 1u) == 2u * p.n_tg) atomicExch(p.cnt + ubase, 0u);
+        // the last of the n_tg readers re-zeroes the unit's partials and the counter
+        unsigned old = 0;
+        if (lane == 0) old = atomicAdd(p.cnt + ubase, 1u);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old == (unsigned)p.n_tg - 1) {
+          __threadfence();
+          unsigned long long* dst = p.part + ubase * p.n_tg * p.NCP;
+          for (long long e = lane; e < (long long)p.n_tg * p.NCP; e += 32) dst[e] = 0ull;
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence();
+            atomicExch(p.cnt + ubase, 0u);
+          }
         }
+        if (lane == 0) trace_stamp(p, ui, 4);
       }
     }
   } else if (warp >= kFinalWarp0) {
     // ================================================================ (l,h)-max aggregation
     const int q = warp & 3;
     float* acc = reinterpret_cast<float*>(smem + p.off_acc);      // [tpc][Rv][128]
-    float* lse_s = reinterpret_cast<float*>(smem + p.off_lse);    // [kMaxBuf][NCP]
+    const float* lse_s = reinterpret_cast<const float*>(smem + p.off_lse);    // [2][NCP]
     const int tok = q * 32 + lane;
-    uint32_t ui = 0;
+    uint32_t ui = 0, gt = 0;
     for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
       const Job jb = decode_job(p, job);
       const int ntile = jb.t_hi - jb.t_lo;
       for (int t = 0; t < ntile; ++t)
         for (int r = 0; r < p.Rv; ++r) acc[(t * p.Rv + r) * kTileM + tok] = -CUDART_INF_F;
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
-        const uint32_t slot = ui % p.nbuf, tpar = (ui / p.nbuf) & 1;
-        float* ls = lse_s + slot * p.NCP;
-        mbar_wait(bar_lfull + 8 * slot, tpar);
-        mbar_wait(bar_tfull + 8 * slot, tpar);
-        tc_fence_after();
-        const uint32_t sbase = tmem + ((uint32_t)(q * 32) << 16) + slot * p.slot_cols;
+        const uint32_t par = ui & 1;
+        mbar_wait(bar_lfull + 8 * par, (ui >> 1) & 1);
+        const float* ls = lse_s + par * p.NCP;
+        for (int t = 0; t < ntile; ++t, ++gt) {
+          const uint32_t slot = gt % nslots;
+          mbar_wait(bar_tfull + 8 * slot, (gt / nslots) & 1);
+          tc_fence_after();
+          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + slot * p.NCP;
+          float* arow = acc + (t * p.Rv) * kTileM + tok;
 #pragma unroll 1
-        for (int grp = 0; grp < p.NCP / 32; ++grp) {
-          float lv[32];
+          for (int k0 = 0; k0 < p.NCP / 16; k0 += 2) {
+            float xa[16], xb[16];
+            const bool two = k0 + 1 < p.NCP / 16;
+            tmem_ld16_issue(ta + k0 * 16, xa);
+            if (two) tmem_ld16_issue(ta + k0 * 16 + 16, xb);
+            tmem_wait();
+            tie16(xa);
+            tie16(xb);
 #pragma unroll
-          for (int i4 = 0; i4 < 8; ++i4) {
-            const float4 v4 = *reinterpret_cast<const float4*>(ls + grp * 32 + 4 * i4);
-            lv[4 * i4] = v4.x; lv[4 * i4 + 1] = v4.y; lv[4 * i4 + 2] = v4.z; lv[4 * i4 + 3] = v4.w;
-          }
-          auto fold = [&](const float(&x)[32], int t) {
-            float* arow = acc + (t * p.Rv) * kTileM + tok;
-            switch (p.G) {
-              case 1: fold_tile<1>(x, lv, p.xs, grp, p.NC, p.G, p.Rv, arow); break;
-              case 2: fold_tile<2>(x, lv, p.xs, grp, p.NC, p.G, p.Rv, arow); break;
-              case 4: fold_tile<4>(x, lv, p.xs, grp, p.NC, p.G, p.Rv, arow); break;
-              case 8: fold_tile<8>(x, lv, p.xs, grp, p.NC, p.G, p.Rv, arow); break;
-              default: fold_tile<0>(x, lv, p.xs, grp, p.NC, p.G, p.Rv, arow); break;
+            for (int h = 0; h < 2; ++h) {
+              if (h == 1 && !two) break;
+              const int k = k0 + h;
+              float lv[16];
+#pragma unroll
+              for (int i4 = 0; i4 < 4; ++i4) {
+                const float4 v4 = *reinterpret_cast<const float4*>(ls + k * 16 + 4 * i4);
+                lv[4 * i4] = v4.x; lv[4 * i4 + 1] = v4.y; lv[4 * i4 + 2] = v4.z; lv[4 * i4 + 3] = v4.w;
+              }
+              fold_tile<kG, 16>(h == 0 ? xa : xb, lv, p.xs, k, p.NC, p.G, p.Rv, arow);
             }
-          };
-          for_tiles(sbase + grp * 32, p.NCP, ntile, fold);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_tempty + 8 * slot);           // release the TMEM tile slot
         }
-        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_tempty + 8 * slot);
+        if (lane == 0) mbar_arrive(bar_lempty + 8 * par);
         if (q == 0 && lane == 0) trace_stamp(p, ui, 6);
       }
       // ---- job epilogue: importance = mean_r 2^acc (possibly across unit groups)
@@ -684,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           const long long i = (long long)(jb.t_lo + t) * kTileM + tok;
           if (i < p.N) {
             float s = 0.f;
-            for (int r = 0; r < p.Rv; ++r) s += exp2f(acc[(t * p.Rv + r) * kTileM + tok]);
+            for (int r = 0; r < p.Rv; ++r) s += ex2(acc[(t * p.Rv + r) * kTileM + tok]);
             p.imp[(long long)jb.b * p.N + i] = s * inv;
           }
         }
@@ -715,7 +851,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             float m = -CUDART_INF_F;
             for (int g = 0; g < p.n_ug; ++g)
               m = fmaxf(m, __ldcg(&p.accpart[(((long long)jb.b * p.n_ug + g) * p.Rv + r) * p.N + i]));
-            s += exp2f(m);
+            s += ex2(m);
           }
           p.imp[(long long)jb.b * p.N + i] = s * inv;
         }
@@ -757,12 +893,12 @@ PFN_encodeTiled_t encode_fn() {
 
 struct Plan {
   int P = 0, n_tg = 0, n_ug = 0, J = 0, T = 0, U = 0, tpc = 0, upc = 0;
-  int NC = 0, NCP = 0, W = 0, nkb = 0, stages = 0, nbuf = 0, slot_cols = 0;
+  int NC = 0, NCP = 0, W = 0, nkb = 0, stages = 0, nslots = 0;
   long long total_jobs = 0;
   uint32_t off_k = 0, off_q = 0, off_acc = 0, off_red = 0, off_lse = 0, off_comb = 0, off_bar = 0, smem = 0;
   uint32_t k_stage_bytes = 0, q_slot_bytes = 0;
-  size_t ws_part = 0, ws_lse = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0;
-  size_t ws_total() const { return ws_part + ws_lse + ws_cnt + ws_acc + ws_fin; }
+  size_t ws_part = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0;
+  size_t ws_total() const { return ws_part + ws_cnt + ws_acc + ws_fin; }
   bool ok = false;
 };
 
@@ -787,13 +923,13 @@ uint32_t carve(Plan& pl, int Rv, int stages) {
   pl.off_red = o;
   o += 2 * 4 * pl.NCP * 8;
   pl.off_lse = o;
-  o += kMaxBuf * pl.NCP * 4;
+  o += 2 * pl.NCP * 4;
   o = (o + 15) & ~15u;
   pl.off_comb = o;
   o += 16 + 4 * pl.NCP * 8;
   o = (o + 15) & ~15u;
   pl.off_bar = o;
-  o += (2 * stages + 8 + 3 * kMaxBuf) * 8 + 16;
+  o += (2 * stages + 12 + 2 * kMaxSlots) * 8 + 16;
   return o + 1024;                                   // slack for the manual 1024-byte alignment
 }
 
@@ -810,12 +946,14 @@ Plan make_plan(const Geom& g, bool allow_override = true) {
   pl.P = sm_count();
   pl.T = (int)((g.N + kTileM - 1) / kTileM);
   pl.U = g.L * g.Hkv;
-  // choose (n_tg, n_ug): J = n_tg*n_ug divides the grid so a request never
-  // straddles two waves of CTAs.  Time model in units of one K-tile load at an
-  // SM's share of HBM bandwidth: a unit costs max(tpc, chain/(nbuf-1)) where
-  // `chain` is the stats -> exchange -> aggregation latency that the nbuf TMEM
-  // slots must hide.
-  const double kChain = 6.0;
+  // choose (n_tg, n_ug): when a request needs more than one wave of CTAs
+  // (B*J > P), J = n_tg*n_ug must divide the grid so a request never straddles
+  // two waves (its CTAs exchange statistics and must be co-resident).  Time
+  // model in units of one K-tile load at an SM's share of HBM bandwidth: a tile
+  // holds its TMEM slot for about (tpc + chain) tile-times, so the ring of
+  // nslots slots sustains min(1, nslots / (tpc + chain)) tiles per tile-time.
+  pl.nslots = std::min(kMaxSlots, kTmemCols / pl.NCP);
+  const double kChain = 9.0;
   double best = 1e300;
   // test/tuning override: SP_FUSED_PLAN="n_tg,n_ug" (ignored unless valid for g)
   int force_tg = 0, force_ug = 0;
@@ -823,42 +961,37 @@ Plan make_plan(const Geom& g, bool allow_override = true) {
     if (std::sscanf(env, "%d,%d", &force_tg, &force_ug) != 2) force_tg = force_ug = 0;
   }
   for (int J = 1; J <= pl.P; ++J) {
-    if (pl.P % J) continue;
+    if ((long long)g.B * J > pl.P && pl.P % J) continue;
     for (int n_tg = 1; n_tg <= J; ++n_tg) {
       if (J % n_tg) continue;
       const int n_ug = J / n_tg;
       if (n_tg > pl.T || n_ug > pl.U) continue;
       const int tpc = (pl.T + n_tg - 1) / n_tg, upc = (pl.U + n_ug - 1) / n_ug;
-      if (tpc * pl.NCP > kTmemCols) continue;
+      if (tpc > pl.nslots) continue;                   // a unit's tiles must all be resident
       if (force_tg > 0 && (n_tg != force_tg || n_ug != force_ug)) continue;
-      const int nbuf = std::min(kMaxBuf, kTmemCols / (tpc * pl.NCP));
       const long long jobs = (long long)g.B * J;
       const int grid = (int)std::min<long long>(pl.P, jobs);
       const long long waves = (jobs + grid - 1) / grid;
       const double tile_scale = (double)pl.k_stage_bytes / 32768.0;
-      const double t_unit = nbuf >= 2 ? std::max((double)tpc * tile_scale, kChain / (nbuf - 1))
-                                      : tpc * tile_scale + kChain;
-      double cost = (double)upc * t_unit;
-      cost += upc * (n_tg * pl.NC * 8.0) / 32768.0 / 8.0;                  // combiner reads (L2)
+      const double rate = std::min(1.0, (double)pl.nslots / (tpc + kChain / tile_scale));
+      double cost = (double)upc * tpc * tile_scale / rate;
       cost += (n_ug > 1 ? 2.0 * g.Rv * tpc * kTileM * 4.0 / 32768.0 + kChain : 0.0);  // cross-group max
       cost *= (double)waves;
       if (cost < best * 0.999) {
         best = cost;
-        pl.J = J; pl.n_tg = n_tg; pl.n_ug = n_ug; pl.tpc = tpc; pl.upc = upc; pl.nbuf = nbuf;
+        pl.J = J; pl.n_tg = n_tg; pl.n_ug = n_ug; pl.tpc = tpc; pl.upc = upc;
       }
     }
   }
   if (pl.J == 0 && force_tg > 0) return make_plan(g, false);   // invalid override: plan normally
   if (pl.J == 0) return pl;
-  pl.slot_cols = pl.tpc * pl.NCP;
   pl.total_jobs = (long long)g.B * pl.J;
   int stages = kMaxStages;
   while (stages >= 2 && carve(pl, g.Rv, stages) > (uint32_t)kSmemLimit) --stages;
   if (stages < 2) return pl;
   pl.stages = stages;
   pl.smem = carve(pl, g.Rv, stages);
-  pl.ws_part = align256((size_t)g.B * pl.U * pl.NC * pl.n_tg * sizeof(float2));
-  pl.ws_lse = align256((size_t)g.B * pl.U * pl.NC * sizeof(float));
+  pl.ws_part = align256((size_t)g.B * pl.U * pl.NCP * pl.n_tg * sizeof(unsigned long long));
   pl.ws_cnt = align256((size_t)g.B * pl.U * sizeof(unsigned));
   pl.ws_acc = pl.n_ug > 1 ? align256((size_t)g.B * pl.n_ug * g.Rv * g.N * sizeof(float)) : 0;
   pl.ws_fin = align256((size_t)g.B * pl.n_tg * sizeof(unsigned));
@@ -926,7 +1059,7 @@ bool fused_plan_info(const Geom& g, long long out[9]) {
   Plan pl = make_plan(g);
   if (!pl.ok) return false;
   out[0] = std::min<long long>(pl.P, pl.total_jobs); out[1] = pl.J; out[2] = pl.n_tg; out[3] = pl.n_ug;
-  out[4] = pl.tpc; out[5] = pl.upc; out[6] = pl.nbuf; out[7] = pl.stages; out[8] = pl.smem;
+  out[4] = pl.tpc; out[5] = pl.upc; out[6] = pl.nslots; out[7] = pl.stages; out[8] = pl.smem;
   return true;
 }
 
@@ -947,8 +1080,8 @@ cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Ge
   if (!encode_maps(Q, K, g, lay, pl, &p.tmK, &p.tmQ)) return cudaErrorInvalidValue;
   p.B = g.B; p.L = g.L; p.Hkv = g.Hkv; p.G = g.G; p.Rv = g.Rv; p.d = g.d; p.N = (int)g.N;
   p.T = pl.T; p.U = pl.U; p.n_tg = pl.n_tg; p.n_ug = pl.n_ug; p.J = pl.J; p.total_jobs = pl.total_jobs;
-  p.NC = pl.NC; p.NCP = pl.NCP; p.W = pl.W; p.nkb = pl.nkb; p.stages = pl.stages; p.nbuf = pl.nbuf;
-  p.slot_cols = pl.slot_cols; p.tpc = pl.tpc;
+  p.NC = pl.NC; p.NCP = pl.NCP; p.W = pl.W; p.nkb = pl.nkb; p.stages = pl.stages; p.nslots = pl.nslots;
+  p.tpc = pl.tpc;
   p.xs = g.scale * kLog2e;
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(pl.NCP >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
   p.layout_type = pl.W == 64 ? 2u : (pl.W == 32 ? 4u : 6u);
@@ -960,14 +1093,13 @@ cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Ge
   w += pl.ws_cnt;
   p.fin_cnt = reinterpret_cast<unsigned*>(w);
   w += pl.ws_fin;
-  p.part = reinterpret_cast<float2*>(w);
+  p.part = reinterpret_cast<unsigned long long*>(w);
   w += pl.ws_part;
-  p.lse_g = reinterpret_cast<float*>(w);
-  w += pl.ws_lse;
   p.accpart = pl.ws_acc ? reinterpret_cast<float*>(w) : nullptr;
   p.imp = importance;
   p.err = device_error_flag();
   p.trace = nullptr;
+
   p.trace_units = 0;
   if (g_trace != nullptr) {
     const long long grid = std::min<long long>(pl.P, pl.total_jobs);
@@ -978,11 +1110,14 @@ cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Ge
     }
   }
 
-  static int configured_smem = -1;
-  if (configured_smem < (int)pl.smem) {
-    cudaError_t e = cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+  void (*kern)(FusedParams) = g.G == 1 ? k_fused<1> : g.G == 2 ? k_fused<2> : g.G == 4 ? k_fused<4>
+                                                     : g.G == 8 ? k_fused<8> : k_fused<0>;
+  static bool configured[5] = {false, false, false, false, false};
+  const int ki = g.G == 1 ? 0 : g.G == 2 ? 1 : g.G == 4 ? 2 : g.G == 8 ? 3 : 4;
+  if (!configured[ki]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (e != cudaSuccess) return e;
-    configured_smem = kSmemLimit;
+    configured[ki] = true;
   }
   const int grid = (int)std::min<long long>(pl.P, pl.total_jobs);
   cudaLaunchConfig_t cfg = {};
@@ -995,7 +1130,7 @@ cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Ge
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_fused, p);
+  return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 }  // namespace sp

@@ -92,7 +92,7 @@ def test_geometries(algo, variant):
     _small_case(w, algo)
 
 
-@pytest.mark.parametrize("plan,N", [("1,1", 2000), ("1,2", 2000), ("1,4", 2000), ("2,1", 5000), ("2,2", 5000),
+@pytest.mark.parametrize("plan,N", [("1,1", 2000), ("1,2", 2000), ("1,4", 2000), ("2,1", 4000), ("2,2", 4000),
                                     ("4,1", 5000), ("37,1", 5000), ("37,2", 5000), ("37,4", 5000)])
 def test_fused_forced_plans(plan, N, monkeypatch):
     """Every decomposition of the fused kernel (token groups x unit groups) gives

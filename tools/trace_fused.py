@@ -3,8 +3,8 @@
   python tools/trace_fused.py [--config C3] [--plan n_tg,n_ug]
 
 Event ids per (CTA, unit): 0 producer starts unit, 1 MMA starts (slot free),
-2 stats start, 3 CTA partial published, 4 lse combined (last CTA), 5 aggregation
-sees lse, 6 aggregation done.
+2 stats start, 3 CTA partial published, 4 partials cleanup done, 5 lse2 ready
+(this CTA combined all partials), 6 aggregation done, 7 stats compute done.
 """
 import argparse
 import os
@@ -48,8 +48,8 @@ def main():
         np.save(a.out, tr)
     print("plan", plan, "units/CTA", units)
     print("kernel span (us) %.1f" % np.nanmax(tr))
-    names = ["prod", "mma", "stats", "publ", "comb", "lseseen", "aggdone"]
-    for (x, y) in [(1, 2), (2, 3), (3, 5), (5, 6), (1, 6), (0, 1)]:
+    names = ["prod", "mma", "stats", "publ", "cleanup", "lseready", "aggdone", "statsend"]
+    for (x, y) in [(1, 2), (2, 7), (7, 3), (3, 5), (5, 6), (1, 6), (0, 1)]:
         d = tr[:, :, y] - tr[:, :, x]
         print(f"{names[x]:>8} -> {names[y]:<8} mean {np.nanmean(d):8.2f} us  p50 {np.nanmedian(d):8.2f}  max {np.nanmax(d):8.2f}")
     # per-unit period: successive MMA starts
