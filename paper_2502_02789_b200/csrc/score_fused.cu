@@ -48,6 +48,8 @@ constexpr int kFinalWarp0 = 8;
 constexpr int kMaxStages = 8;
 constexpr int kMaxChunks = 8;          // NCP <= 128 columns (16-column chunks)
 constexpr int kMaxSlots = 16;          // TMEM tile slots (512 columns / 32)
+constexpr int kLseRing = 8;
+constexpr int kPrefetchTiles = 0;      // L2 prefetch distance beyond the SMEM ring (tiles); measured: hurts            // lse2 buffers in SMEM (gather may run ahead of aggregation)
 constexpr int kMaxLseBatch = 20;       // float4 partial loads in flight per lane (40 token groups)
 constexpr int kTmemCols = 512;
 constexpr int kSmemLimit = 232448;     // sm_100 max dynamic shared memory per block
@@ -68,15 +70,17 @@ struct FusedParams {
   uint32_t off_k, off_q, off_acc, off_red, off_lse, off_comb, off_bar;
   uint32_t k_stage_bytes, q_slot_bytes;
   // workspace
-  unsigned long long* part;            // [B][U][n_tg][NCP] CTA partials: (m, s) packed in one 64-bit word,
-                                       // m = max raw logit, s = sum 2^((x-m)*xs); 0 = "not yet written"
-  unsigned* cnt;                       // [B][U]           readers done (the last one re-zeroes the partials)
+  unsigned long long* part;            // [2][B][U][n_tg][NCP] CTA partials, one buffer per launch parity:
+                                       // (max2, sum) packed in one 64-bit word; 0 = "not yet written"
+  unsigned* epoch;                     // [2] launch epoch (parity selects the partial buffer), CTAs done
   float* accpart;                      // [B][n_ug][Rv][N]
   unsigned* fin_cnt;                   // [B][n_tg]    finalize counters (self-cleaning)
   float* imp;                          // [B][N]
   int* err;
   unsigned long long* trace;           // optional [grid][trace_units][8] globaltimer stamps (debug)
   int trace_units;
+  int dbg;                             // timing experiments (SP_FUSED_DEBUG); 0 in production
+  int prefetch;                        // L2 prefetch distance in tiles beyond the SMEM ring (0 = off)
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -132,6 +136,12 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
       " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2_5d(const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4) {
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -445,6 +455,32 @@ __device__ __forceinline__ Job decode_job(const FusedParams& p, long long job) {
   return j;
 }
 
+// Walks a CTA's (job, unit, tile) sequence -- the order every role uses.
+struct TileCursor {
+  long long job;
+  Job jb;
+  int u, t;
+};
+__device__ __forceinline__ bool cursor_begin(const FusedParams& p, TileCursor& c) {
+  c.job = blockIdx.x;
+  if (c.job >= p.total_jobs) return false;
+  c.jb = decode_job(p, c.job);
+  c.u = c.jb.u_lo;
+  c.t = c.jb.t_lo;
+  return true;
+}
+__device__ __forceinline__ bool cursor_next(const FusedParams& p, TileCursor& c) {
+  if (++c.t < c.jb.t_hi) return true;
+  c.t = c.jb.t_lo;
+  if (++c.u < c.jb.u_hi) return true;
+  c.job += gridDim.x;
+  if (c.job >= p.total_jobs) return false;
+  c.jb = decode_job(p, c.job);
+  c.u = c.jb.u_lo;
+  c.t = c.jb.t_lo;
+  return true;
+}
+
 // ------------------------------------------------------------------ the kernel
 // Online (max, sum) merge in the log2 domain: (m, s) <- (m, s) (+) (m2, s2),
 // s = sum 2^(x - m).  Empty partials are (-inf, 0); two empties stay empty.
@@ -486,13 +522,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
   // barrier map: full[S] empty[S] qfull[2] qempty[2] tfull[kMaxSlots] tempty[kMaxSlots]
-  //              rfull[2] rempty[2] lfull[2] lempty[2]; then the TMEM base address
+  //              rfull[2] rempty[2] lfull[kLseRing] lempty[kLseRing]; then the TMEM base address
   const uint32_t bar_full = smem_u32(bars), bar_empty = bar_full + 8 * p.stages;
   const uint32_t bar_qfull = bar_empty + 8 * p.stages, bar_qempty = bar_qfull + 16;
   const uint32_t bar_tfull = bar_qempty + 16, bar_tempty = bar_tfull + 8 * kMaxSlots;
   const uint32_t bar_rfull = bar_tempty + 8 * kMaxSlots, bar_rempty = bar_rfull + 16;
-  const uint32_t bar_lfull = bar_rempty + 16, bar_lempty = bar_lfull + 16;
-  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 2 * p.stages + 12 + 2 * kMaxSlots);
+  const uint32_t bar_lfull = bar_rempty + 16, bar_lempty = bar_lfull + 8 * kLseRing;
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 2 * p.stages + 8 + 2 * kMaxSlots + 2 * kLseRing);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -508,6 +544,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       mbar_init(bar_qempty + 8 * s, 1);
       mbar_init(bar_rfull + 8 * s, 128);
       mbar_init(bar_rempty + 8 * s, 1);
+    }
+    for (int s = 0; s < kLseRing; ++s) {
       mbar_init(bar_lfull + 8 * s, 32);
       mbar_init(bar_lempty + 8 * s, 4);
     }
@@ -530,11 +568,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   tc_fence_after();
   const uint32_t tmem = *tmem_base_s;
   const uint32_t nslots = (uint32_t)p.nslots;
+  // this launch publishes into part[parity]; part[parity ^ 1] (the previous
+  // launch's) is re-zeroed off the critical path, for the launch after next
+  const uint32_t parity = ld_acquire(p.epoch) & 1u;
+  const long long part_half = (long long)p.B * p.U * p.n_tg * p.NCP;
+  unsigned long long* const part_cur = p.part + parity * part_half;
+  unsigned long long* const part_old = p.part + (parity ^ 1u) * part_half;
 
   if (warp == 0) {
     // ================================================================ TMA producer
     if (lane == 0) {
       uint32_t stage = 0, sphase = 0, ui = 0;
+      // L2 prefetch runs kPrefetchTiles ahead of the SMEM loads: HBM latency under
+      // full load is several us, longer than the SMEM ring alone can cover
+      TileCursor pf;
+      bool pf_ok = cursor_begin(p, pf);
+      auto prefetch_one = [&]() {
+        if (!pf_ok) return;
+        const int pl_ = pf.u / p.Hkv, pg = pf.u % p.Hkv;
+        for (int kb = 0; kb < p.nkb; ++kb) tma_prefetch_l2_5d(&p.tmK, kb * p.W, pf.t * kTileM, pg, pl_, pf.jb.b);
+        pf_ok = cursor_next(p, pf);
+      };
+      if (p.prefetch == 0) pf_ok = false;
+      for (int i = 0; i < p.prefetch + p.stages; ++i) prefetch_one();
       for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
         const Job jb = decode_job(p, job);
         for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
@@ -553,6 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             for (int kb = 0; kb < p.nkb; ++kb)
               tma_load_5d(kdst + kb * (kTileM * p.W * 2), &p.tmK, bar_full + 8 * stage, kb * p.W, t * kTileM, g, l,
                           jb.b);
+            prefetch_one();
             if (++stage == (uint32_t)p.stages) { stage = 0; sphase ^= 1; }
           }
         }
@@ -564,27 +621,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     // TMEM tile slots; a slot is released by the aggregation warps once they
     // have folded that tile (tile-granular reuse hides the exchange latency).
     if (lane == 0) {
-      uint32_t stage = 0, sphase = 0, ui = 0, gt = 0;
-      const uint32_t sbo = 8 * p.W * 2;
+      uint32_t stage = 0, sphase = 0, ui = 0, gt = 0, gslot = 0, gph = 0;
+      // UMMA smem descriptors: the high word (SBO, version, swizzle) is constant;
+      // the low word is (address >> 4) | LBO and a K step just adds to it.
+      const uint32_t desc_hi = (uint32_t)(make_sdesc(0, 8 * p.W * 2, p.layout_type) >> 32);
+      const uint32_t a_kb = (kTileM * p.W * 2) >> 4, b_kb = (p.NCP * p.W * 2) >> 4;
+      const int ksteps = p.W / 16;
       for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
         const Job jb = decode_job(p, job);
         for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
           const uint32_t qs = ui & 1, qpar = (ui >> 1) & 1;
           mbar_wait(bar_qfull + 8 * qs, qpar);
-          const uint32_t qbase = smem_u32(smem + p.off_q + qs * p.q_slot_bytes);
+          const uint32_t b_lo0 = ((smem_u32(smem + p.off_q + qs * p.q_slot_bytes) >> 4) & 0x3FFFu) | (1u << 16);
           for (int t = jb.t_lo; t < jb.t_hi; ++t, ++gt) {
-            const uint32_t slot = gt % nslots;
-            mbar_wait(bar_tempty + 8 * slot, ((gt / nslots) & 1) ^ 1);
+            const uint32_t slot = gslot;
+            mbar_wait(bar_tempty + 8 * slot, gph ^ 1);
+            if (++gslot == nslots) { gslot = 0; gph ^= 1; }
             if (t == jb.t_lo) trace_stamp(p, ui, 1);
             mbar_wait(bar_full + 8 * stage, sphase);
             tc_fence_after();
-            const uint32_t kbase = smem_u32(smem + p.off_k + stage * p.k_stage_bytes);
+            const uint32_t a_lo0 = ((smem_u32(smem + p.off_k + stage * p.k_stage_bytes) >> 4) & 0x3FFFu) | (1u << 16);
             const uint32_t dcol = tmem + slot * p.NCP;
-            for (int kb = 0; kb < p.nkb; ++kb) {
-              for (int ks = 0; ks < p.W / 16; ++ks) {
-                const uint64_t a = make_sdesc(kbase + kb * (kTileM * p.W * 2) + ks * 32, sbo, p.layout_type);
-                const uint64_t b = make_sdesc(qbase + kb * (p.NCP * p.W * 2) + ks * 32, sbo, p.layout_type);
-                umma_bf16(dcol, a, b, p.idesc, (kb | ks) != 0);
+            uint32_t accum = 0;
+            for (int kb = 0; kb < p.nkb && !(p.dbg & 16); ++kb) {
+              uint32_t a_lo = a_lo0 + kb * a_kb, b_lo = b_lo0 + kb * b_kb;
+              for (int ks = 0; ks < ksteps; ++ks, a_lo += 2, b_lo += 2) {
+                umma_bf16(dcol, ((uint64_t)desc_hi << 32) | a_lo, ((uint64_t)desc_hi << 32) | b_lo, p.idesc, accum);
+                accum = 1;
               }
             }
             umma_commit(bar_empty + 8 * stage);
@@ -595,7 +658,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         }
       }
     }
-  } else if (warp >= kStatsWarp0 && warp < kFinalWarp0) {
+  } else if (warp >= kStatsWarp0 && warp < kFinalWarp0 && !(p.dbg & 8)) {
     // ================================================================ softmax statistics
     // Progressive: each tile is folded as soon as its MMA completes into a
     // per-thread running (ref, sum) per column, sum = sum 2^(x*xs - ref) with
@@ -611,18 +674,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       const long long tok0 = (long long)jb.t_lo * kTileM + q * 32 + lane;
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
         const uint32_t gt0 = gt;
+        uint32_t slot0 = gt % nslots, ph0 = (gt / nslots) & 1;
         float2* rb = red + (ui & 1) * 4 * p.NCP;
         mbar_wait(bar_rempty + 8 * (ui & 1), ((ui >> 1) & 1) ^ 1);   // exchange warp done with rb
+        if (q == 0 && lane == 0) trace_stamp(p, ui, 2);
 #pragma unroll 1
         for (int grp = 0; grp < p.NCP / 32; ++grp) {
           float ref[32], sum[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) { ref[i] = -CUDART_INF_F; sum[i] = 0.f; }
           gt = gt0;
+          uint32_t slot = slot0, ph = ph0;
           for (int t = jb.t_lo; t < jb.t_hi; ++t, ++gt) {
-            const uint32_t slot = gt % nslots;
-            mbar_wait(bar_tfull + 8 * slot, (gt / nslots) & 1);
-            if (grp == 0 && t == jb.t_lo && q == 0 && lane == 0) trace_stamp(p, ui, 2);
+            mbar_wait(bar_tfull + 8 * slot, ph);
             tc_fence_after();
             float x[32];
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + slot * p.NCP + grp * 32;
@@ -632,19 +696,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             tmem_wait();
             tie16(*reinterpret_cast<float(*)[16]>(x0));
             tie16(*reinterpret_cast<float(*)[16]>(x0 + 16));
-            if (tok0 + (long long)(t - jb.t_lo) * kTileM < p.N) {
+            if (!(p.dbg & 1) && tok0 + (long long)(t - jb.t_lo) * kTileM < p.N) {
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
+                // one exp2 either way: first value (ref = -inf) or a jump > 2^64
+                // re-bases the sum on y, otherwise accumulate 2^(y - ref)
                 const float y = x[i] * p.xs;
                 const float dlt = y - ref[i];
-                if (dlt > 64.f) {                    // first value, or a jump: re-base the sum
-                  sum[i] = fmaf(sum[i], ex2(-dlt), 1.f);
-                  ref[i] = y;
-                } else {
-                  sum[i] += ex2(dlt);
-                }
+                const bool big = dlt > 64.f;
+                const float e = ex2(big ? -dlt : dlt);
+                sum[i] = big ? fmaf(sum[i], e, 1.f) : sum[i] + e;
+                ref[i] = big ? y : ref[i];
               }
             }
+            if (++slot == nslots) { slot = 0; ph ^= 1; }
           }
           float mo, so;
           transpose_merge32(ref, sum, lane, mo, so);                    // column 32*grp + lane
@@ -654,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         mbar_arrive(bar_rfull + 8 * (ui & 1));                        // 128 arrivals: all columns written
       }
     }
-  } else if (warp == 2) {
+  } else if (warp == 2 && !(p.dbg & 8)) {
     // ================================================================ statistics exchange
     // Merge the 4 statistics warps into the CTA partial and publish it: one
     // 64-bit word (max2, sum) per column, single-copy atomic, so a reader sees
@@ -667,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const long long ubase = (long long)jb.b * p.U + u;
         mbar_wait(bar_rfull + 8 * (ui & 1), (ui >> 1) & 1);
         const float2* rb = red + (ui & 1) * 4 * p.NCP;
-        unsigned long long* mypart = p.part + (ubase * p.n_tg + jb.tg) * p.NCP;
+        unsigned long long* mypart = part_cur + (ubase * p.n_tg + jb.tg) * p.NCP;
         for (int c = lane; c < p.NCP; c += 32) {
           float mm = -CUDART_INF_F, ss = 0.f;
           if (c < p.NC) {
@@ -684,23 +749,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         }
       }
     }
+    // re-zero this CTA's rows of the previous launch's buffer (read by nobody now)
+    for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
+      const Job jb = decode_job(p, job);
+      for (int u = jb.u_lo; u < jb.u_hi; ++u) {
+        unsigned long long* row = part_old + (((long long)jb.b * p.U + u) * p.n_tg + jb.tg) * p.NCP;
+        for (int c = lane; c < p.NCP; c += 32) row[c] = 0ull;
+      }
+    }
   } else if (warp == 3) {
     // ================================================================ lse2 gather
     // Polls the unit's n_tg published partials (all loads of a batch in flight
     // together; zero words are re-read until written), merges them in
     // token-group order -- every CTA computes the same lse2 bit for bit -- and
     // stages lse2 in SMEM for the aggregation warps.
-    float* lse_s = reinterpret_cast<float*>(smem + p.off_lse);    // [2][NCP]
+    float* lse_s = reinterpret_cast<float*>(smem + p.off_lse);    // [kLseRing][NCP]
     uint32_t ui = 0;
     for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
       const Job jb = decode_job(p, job);
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
-        const uint32_t par = ui & 1;
+        const uint32_t par = ui % kLseRing;
         const long long ubase = (long long)jb.b * p.U + u;
-        mbar_wait(bar_lempty + 8 * par, ((ui >> 1) & 1) ^ 1);          // aggregation done with ls[par]
+        mbar_wait(bar_lempty + 8 * par, ((ui / kLseRing) & 1) ^ 1);    // aggregation done with ls[par]
         float* ls = lse_s + par * p.NCP;
-        const unsigned long long* src = p.part + ubase * p.n_tg * p.NCP;
-        for (int c = lane; c < p.NCP; c += 32) {
+        const unsigned long long* src = part_cur + ubase * p.n_tg * p.NCP;
+        for (int c = lane; c < p.NCP && !(p.dbg & 8); c += 32) {
           float M = -CUDART_INF_F, S = 0.f;
           for (int s0 = 0; s0 < p.n_tg; s0 += kMaxLseBatch) {
             unsigned long long v[kMaxLseBatch];
@@ -711,6 +784,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
               missing |= (v[j] == 0ull ? 1u : 0u) << j;
             }
             long long it = 0;
+            if (p.dbg & 4) missing = 0;
             while (__any_sync(0xffffffffu, missing != 0)) {
               __nanosleep(it < 8 ? 64 : 200);
 #pragma unroll
@@ -737,27 +811,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           float l2 = 0.f;
           if (c < p.NC) {
             l2 = M + log2f(S);
-            if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
+            if (!isfinite(l2) && p.dbg == 0) set_err(p.err, kDevNonFinite);
           }
           ls[c] = l2;
         }
         if (lane == 0) trace_stamp(p, ui, 5);
         mbar_arrive(bar_lfull + 8 * par);
-        __syncwarp();
-        // the last of the n_tg readers re-zeroes the unit's partials and the counter
-        unsigned old = 0;
-        if (lane == 0) old = atomicAdd(p.cnt + ubase, 1u);
-        old = __shfl_sync(0xffffffffu, old, 0);
-        if (old == (unsigned)p.n_tg - 1) {
-          __threadfence();
-          unsigned long long* dst = p.part + ubase * p.n_tg * p.NCP;
-          for (long long e = lane; e < (long long)p.n_tg * p.NCP; e += 32) dst[e] = 0ull;
-          __syncwarp();
-          if (lane == 0) {
-            __threadfence();
-            atomicExch(p.cnt + ubase, 0u);
-          }
-        }
         if (lane == 0) trace_stamp(p, ui, 4);
       }
     }
@@ -765,7 +824,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     // ================================================================ (l,h)-max aggregation
     const int q = warp & 3;
     float* acc = reinterpret_cast<float*>(smem + p.off_acc);      // [tpc][Rv][128]
-    const float* lse_s = reinterpret_cast<const float*>(smem + p.off_lse);    // [2][NCP]
+    const float* lse_s = reinterpret_cast<const float*>(smem + p.off_lse);    // [kLseRing][NCP]
     const int tok = q * 32 + lane;
     uint32_t ui = 0, gt = 0;
     for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
@@ -774,17 +833,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       for (int t = 0; t < ntile; ++t)
         for (int r = 0; r < p.Rv; ++r) acc[(t * p.Rv + r) * kTileM + tok] = -CUDART_INF_F;
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
-        const uint32_t par = ui & 1;
-        mbar_wait(bar_lfull + 8 * par, (ui >> 1) & 1);
+        const uint32_t par = ui % kLseRing;
+        mbar_wait(bar_lfull + 8 * par, (ui / kLseRing) & 1);
         const float* ls = lse_s + par * p.NCP;
+        uint32_t slot = gt % nslots, ph = (gt / nslots) & 1;
         for (int t = 0; t < ntile; ++t, ++gt) {
-          const uint32_t slot = gt % nslots;
-          mbar_wait(bar_tfull + 8 * slot, (gt / nslots) & 1);
+          mbar_wait(bar_tfull + 8 * slot, ph);
           tc_fence_after();
           const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + slot * p.NCP;
           float* arow = acc + (t * p.Rv) * kTileM + tok;
 #pragma unroll 1
-          for (int k0 = 0; k0 < p.NCP / 16; k0 += 2) {
+          for (int k0 = 0; k0 < p.NCP / 16 && !(p.dbg & 8); k0 += 2) {
             float xa[16], xb[16];
             const bool two = k0 + 1 < p.NCP / 16;
             tmem_ld16_issue(ta + k0 * 16, xa);
@@ -802,12 +861,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
                 const float4 v4 = *reinterpret_cast<const float4*>(ls + k * 16 + 4 * i4);
                 lv[4 * i4] = v4.x; lv[4 * i4 + 1] = v4.y; lv[4 * i4 + 2] = v4.z; lv[4 * i4 + 3] = v4.w;
               }
-              fold_tile<kG, 16>(h == 0 ? xa : xb, lv, p.xs, k, p.NC, p.G, p.Rv, arow);
+              if (!(p.dbg & 2)) fold_tile<kG, 16>(h == 0 ? xa : xb, lv, p.xs, k, p.NC, p.G, p.Rv, arow);
             }
           }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_tempty + 8 * slot);           // release the TMEM tile slot
+          if (++slot == nslots) { slot = 0; ph ^= 1; }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_lempty + 8 * par);
@@ -870,6 +930,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
   }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(p.epoch + 1, 1u) == gridDim.x - 1) {       // last CTA: next launch uses the other buffer
+      atomicExch(p.epoch + 1, 0u);
+      atomicAdd(p.epoch, 1u);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -923,13 +990,13 @@ uint32_t carve(Plan& pl, int Rv, int stages) {
   pl.off_red = o;
   o += 2 * 4 * pl.NCP * 8;
   pl.off_lse = o;
-  o += 2 * pl.NCP * 4;
+  o += kLseRing * pl.NCP * 4;
   o = (o + 15) & ~15u;
   pl.off_comb = o;
   o += 16 + 4 * pl.NCP * 8;
   o = (o + 15) & ~15u;
   pl.off_bar = o;
-  o += (2 * stages + 12 + 2 * kMaxSlots) * 8 + 16;
+  o += (2 * stages + 8 + 2 * kMaxSlots + 2 * kLseRing) * 8 + 16;
   return o + 1024;                                   // slack for the manual 1024-byte alignment
 }
 
@@ -991,8 +1058,8 @@ Plan make_plan(const Geom& g, bool allow_override = true) {
   if (stages < 2) return pl;
   pl.stages = stages;
   pl.smem = carve(pl, g.Rv, stages);
-  pl.ws_part = align256((size_t)g.B * pl.U * pl.NCP * pl.n_tg * sizeof(unsigned long long));
-  pl.ws_cnt = align256((size_t)g.B * pl.U * sizeof(unsigned));
+  pl.ws_part = align256(2 * (size_t)g.B * pl.U * pl.NCP * pl.n_tg * sizeof(unsigned long long));
+  pl.ws_cnt = 256;                                   // launch epoch + CTAs-done counter
   pl.ws_acc = pl.n_ug > 1 ? align256((size_t)g.B * pl.n_ug * g.Rv * g.N * sizeof(float)) : 0;
   pl.ws_fin = align256((size_t)g.B * pl.n_tg * sizeof(unsigned));
   pl.ok = true;
@@ -1089,7 +1156,7 @@ cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Ge
   p.off_bar = pl.off_bar; p.k_stage_bytes = pl.k_stage_bytes; p.q_slot_bytes = pl.q_slot_bytes;
   char* w = reinterpret_cast<char*>(ws);
   // counters first: their offsets depend only on (B, U), not on the plan
-  p.cnt = reinterpret_cast<unsigned*>(w);
+  p.epoch = reinterpret_cast<unsigned*>(w);
   w += pl.ws_cnt;
   p.fin_cnt = reinterpret_cast<unsigned*>(w);
   w += pl.ws_fin;
@@ -1099,6 +1166,10 @@ cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Ge
   p.imp = importance;
   p.err = device_error_flag();
   p.trace = nullptr;
+  p.dbg = 0;
+  if (const char* dbg = std::getenv("SP_FUSED_DEBUG")) p.dbg = std::atoi(dbg);
+  p.prefetch = kPrefetchTiles;
+  if (const char* pf = std::getenv("SP_FUSED_PREFETCH")) p.prefetch = std::atoi(pf);
 
   p.trace_units = 0;
   if (g_trace != nullptr) {
