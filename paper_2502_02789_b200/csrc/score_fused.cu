@@ -48,9 +48,9 @@ constexpr int kFinalWarp0 = 8;
 constexpr int kMaxStages = 8;
 constexpr int kMaxChunks = 8;          // NCP <= 128 columns (16-column chunks)
 constexpr int kMaxSlots = 16;          // TMEM tile slots (512 columns / 32)
-constexpr int kLseRing = 8;
-constexpr int kPrefetchTiles = 0;      // L2 prefetch distance beyond the SMEM ring (tiles); measured: hurts            // lse2 buffers in SMEM (gather may run ahead of aggregation)
-constexpr int kMaxLseBatch = 20;       // float4 partial loads in flight per lane (40 token groups)
+constexpr int kLseRing = 8;            // lse2 buffers in SMEM (gather may run ahead of aggregation)
+constexpr int kPrefetchTiles = 0;      // L2 prefetch distance beyond the SMEM ring (tiles); measured: hurts
+constexpr int kMaxLseBatch = 20;       // 64-bit partial words in flight per lane
 constexpr int kTmemCols = 512;
 constexpr int kSmemLimit = 232448;     // sm_100 max dynamic shared memory per block
 
