@@ -205,8 +205,7 @@ def run_ours(args):
         sp.score(Q, K, R_valid=w.Rv, scale=w.scale, out=imp, algo=args.algo)
         if ev is not None:
             ev[1].record(stream)
-        sp.select(imp, w.keep, w.pool_k, w.chunk, w.pos0, ids=ids, pos=pos, n_kept=nk)
-        sp.gather(T, ids, nk, out=out)
+        sp.select(imp, w.keep, w.pool_k, w.chunk, w.pos0, ids=ids, pos=pos, n_kept=nk, tokens=T, out=out)
 
     for _ in range(args.warmup):
         step()
@@ -262,7 +261,7 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = run_e2e(args, w, Q, K, T, dev, stream, dist, world)
 
-    launches_per_step = {"fused": 1, "simt": 4, "auto": 1}[args.algo] + 2
+    launches_per_step = {"fused": 1, "simt": 4, "auto": 1}[args.algo] + 1     # + select_gather
     plan = sp.score_plan(Q, K, w.Rv) if args.algo != "simt" else None
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,

@@ -92,7 +92,7 @@ typedef struct sp_layout {
 /*
  * Selection parameters (sec:chunk_select P:121-123, sec:position_ids P:125-133).
  *   keep_rate  ratio of chunks kept, (0, 1]; K_c = sp_kept_chunks(n_c, keep_rate)
- *   pool_k     odd 1-D average-pool window >= 1, centred, shrinking at the edges (Z6)
+ *   pool_k     odd 1-D average-pool window, 1 <= pool_k <= 4097, centred, shrinking at the edges (Z6)
  *   chunk      contiguous chunk size >= 1; the last chunk may be partial (Z8)
  *   pos0       position id of prompt token 0 (kept positions are ids + pos0)
  */
@@ -187,6 +187,13 @@ sp_status sp_select(const float* importance, int32_t B, int64_t N, const sp_sele
                     int32_t* ids, int32_t* pos, int32_t* n_kept, void* ws, size_t ws_bytes,
                     sp_stream stream);
 
+/* sp_select + sp_gather in one launch: additionally out_tokens[b][j] =
+ * tokens[b][ids[b][j]] for j < n_kept[b] (bit-exact).  tokens / out_tokens:
+ * device int32 [B][N]; both NULL is the same as sp_select. */
+sp_status sp_select_gather(const float* importance, const int32_t* tokens, int32_t B, int64_t N,
+                           const sp_select_params* p, int32_t* ids, int32_t* pos, int32_t* n_kept,
+                           int32_t* out_tokens, void* ws, size_t ws_bytes, sp_stream stream);
+
 /* ------------------------------------------------------------------ gather
  * out[b][j] = tokens[b][ids[b][j]] for j < n_kept[b] (merge_requests input,
  * Alg.1).  tokens, ids, out: device int32 [B][N]; n_kept device int32 [B].
@@ -196,7 +203,7 @@ sp_status sp_gather(const int32_t* tokens, const int32_t* ids, const int32_t* n_
 
 /* ------------------------------------------------------------------ end to end from host buffers
  * The whole path with host inputs/outputs: copies Q, K and tokens host->device,
- * runs sp_score -> sp_select -> sp_gather, copies ids, pos, n_kept and the
+ * runs sp_score -> sp_select_gather, copies ids, pos, n_kept and the
  * gathered tokens device->host, all enqueued on `stream` (host buffers should
  * be pinned for the copies to be asynchronous).  Host Q/K use the same element
  * strides `lay` as the device copies; host outputs are [B][N] / [B]. */

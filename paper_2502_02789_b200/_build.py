@@ -36,11 +36,28 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found: the CUDA toolkit is required to build libspecprefill.so")
 
 
-def _newer(srcs, out) -> bool:
-    if not os.path.exists(out):
+def _digest(paths, extra: str = "") -> str:
+    import hashlib
+    h = hashlib.sha256(extra.encode())
+    for p in sorted(paths):
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
+def _newer(srcs, out, extra: str = "") -> bool:
+    """Content-based staleness: rebuild when the digest of the inputs (and flags)
+    differs from the one recorded next to the output."""
+    stamp = out + ".sha256"
+    d = _digest(srcs, extra)
+    if not os.path.exists(out) or not os.path.exists(stamp) or open(stamp).read() != d:
         return True
-    t = os.path.getmtime(out)
-    return any(os.path.getmtime(s) > t for s in srcs)
+    return False
+
+
+def _stamp(srcs, out, extra: str = ""):
+    with open(out + ".sha256", "w") as f:
+        f.write(_digest(srcs, extra))
 
 
 def _run(cmd):
@@ -56,21 +73,26 @@ def build(verbose: bool = False, force: bool = False) -> list[str]:
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         glob.glob(os.path.join(ROOT, "include", "*.h"))
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    flags = " ".join(ARCH + NVCC_FLAGS)
     jobs = []
     objs = []
     for s in sources:
         o = os.path.join(BUILD, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
-        if force or _newer([s] + headers, o):
-            jobs.append([nvcc, *ARCH, *NVCC_FLAGS, "-Xptxas", "-v", "-c", s, "-o", o])
+        if force or _newer([s] + headers, o, flags):
+            jobs.append(([nvcc, *ARCH, *NVCC_FLAGS, "-Xptxas", "-v", "-c", s, "-o", o], [s] + headers, o))
     logs = []
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        for out in ex.map(_run, jobs):
+        for out in ex.map(lambda j: _run(j[0]), jobs):
             logs.append(out)
+    for _, srcs, o in jobs:
+        _stamp(srcs, o, flags)
     if force or jobs or _newer(objs, LIB):
         logs.append(_run([nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]))
-    if force or _newer([GEN_SRC], GEN_LIB):
+        _stamp(objs, LIB)
+    if force or _newer([GEN_SRC], GEN_LIB, flags):
         logs.append(_run([nvcc, *ARCH, *NVCC_FLAGS, "-shared", GEN_SRC, "-o", GEN_LIB]))
+        _stamp([GEN_SRC], GEN_LIB, flags)
     if verbose:
         for x in logs:
             sys.stdout.write(x)

@@ -82,9 +82,11 @@ def score(Q, K, R_valid=None, scale=None, out=None, algo: str = "auto", stream=N
 
 
 def select(importance: torch.Tensor, keep: float, pool_k: int, chunk: int, pos0: int = 0, ids=None, pos=None,
-           n_kept=None, stream=None):
+           n_kept=None, stream=None, tokens=None, out=None):
     """(ids [B][N] int32, pos [B][N] int32, n_kept [B] int32); only the first
-    n_kept[b] entries of row b are meaningful (O5-O9)."""
+    n_kept[b] entries of row b are meaningful (O5-O9).  With
+    ``tokens`` the gather is fused into the same launch and the gathered
+    tokens are returned as a fourth element."""
     if importance.dtype != torch.float32 or importance.dim() != 2 or not importance.is_contiguous():
         raise ValueError("importance must be contiguous fp32 [B][N]")
     B, N = importance.shape
@@ -97,9 +99,17 @@ def select(importance: torch.Tensor, keep: float, pool_k: int, chunk: int, pos0:
     if nbytes == 0:
         check(_lib.SP_EINVAL, "sp_select")
     ws = workspace("select", nbytes, dev)
-    check(lib().sp_select(importance.data_ptr(), B, N, C.byref(p), ids.data_ptr(), pos.data_ptr(), n_kept.data_ptr(),
-                          ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_select")
-    return ids, pos, n_kept
+    if tokens is None:
+        check(lib().sp_select(importance.data_ptr(), B, N, C.byref(p), ids.data_ptr(), pos.data_ptr(),
+                              n_kept.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_select")
+        return ids, pos, n_kept
+    if tokens.dtype != torch.int32 or not tokens.is_contiguous() or tuple(tokens.shape) != (B, N):
+        raise ValueError("tokens must be contiguous int32 [B][N]")
+    out = torch.empty_like(tokens) if out is None else out
+    check(lib().sp_select_gather(importance.data_ptr(), tokens.data_ptr(), B, N, C.byref(p), ids.data_ptr(),
+                                 pos.data_ptr(), n_kept.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                 _stream_ptr(stream)), "sp_select_gather")
+    return ids, pos, n_kept, out
 
 
 def gather(tokens: torch.Tensor, ids: torch.Tensor, n_kept: torch.Tensor, out=None, stream=None) -> torch.Tensor:

@@ -1,25 +1,39 @@
-// Selection: 1-D average pool -> chunk means -> top-K_c chunks -> ids/positions.
+// Selection: 1-D average pool -> chunk means -> top-K_c chunks -> ids/positions
+// (+ optionally the token gather).
 //
 // PAPER.md sec:chunk_select: "we chunk the context contiguously and
 // average the token score within each block, and then we select the Top-K
 // blocks ... we apply a 1D average pooling before this"; sec:position_ids
-// (P:125-133): kept tokens keep their original position ids.
+// (P:125-133): kept tokens keep their original position ids; Alg.1
+// merge_requests takes the selected tokens.
 // Readings: shrinking pool edges (Z6), partial last chunk averaged
 // over its true size (Z8), K_c from the exact ppm rule (Z9, computed on the
 // host), ties to the lowest chunk index (Z10), ascending ids (Z11).
 //
-// One CTA of 1024 threads per request.  Selection is exact and deterministic:
-// a 4-pass 8-bit radix select finds the K_c-th largest chunk score (as its
-// IEEE bit pattern; scores are >= 0 so bit order == value order), then an
-// in-order block scan keeps every chunk above the threshold plus the
-// lowest-index chunks equal to it, and compacts their token ranges.
+// One CTA of 1024 threads per request:
+//   A. importance is staged in shared memory segment by segment (all loads of a
+//      segment in flight together), pooled, and summed per chunk in token order
+//      (deterministic) -> cs[c] (global workspace, L2-resident);
+//   B. a 4-pass 8-bit radix select on the IEEE bits of cs (scores are >= 0, so
+//      bit order == value order) finds the K_c-th largest value T; the digit
+//      search is a parallel suffix scan over the 256 bins;
+//   C. an in-order block scan keeps every chunk above T plus the lowest-index
+//      chunks equal to T (exactly K_c chunks), compacts their token ranges into
+//      ids/pos -- one warp per kept chunk, coalesced -- and, if requested,
+//      gathers the kept tokens in the same pass.
 #include "sp_internal.h"
+
+#include <cstdio>
+#include <cstdlib>
 
 namespace sp {
 namespace {
 
 constexpr int ST = 1024;
 constexpr int NW = ST / 32;
+constexpr int SEG = 16384;          // tokens of importance staged in SMEM per segment (64 KiB)
+constexpr int kMaxPool = 4097;      // largest pooling window (half-window staged on each side)
+constexpr int kSmemChunks = 8192;   // chunk scores kept in SMEM when n_c fits (else L2-resident workspace)
 
 struct ScanSmem {
   int warp_tot[NW];
@@ -59,65 +73,147 @@ __device__ __forceinline__ int block_excl_scan(int v, ScanSmem& sm, int* total) 
 __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all, long long N, int pool_k, int chunk,
                                                int pos0, long long K_c, int* __restrict__ ids_all,
                                                int* __restrict__ pos_all, int* __restrict__ n_kept,
-                                               float* __restrict__ cs_all) {
-  __shared__ float tile[ST];
+                                               float* __restrict__ cs_all, const int* __restrict__ tokens_all,
+                                               int* __restrict__ out_all, long long* __restrict__ dbg_ts) {
+#define SP_TS(k) if (dbg_ts && threadIdx.x == 0 && blockIdx.x == 0) dbg_ts[k] = clock64();
+  SP_TS(0)
+  extern __shared__ float seg[];                  // [SEG + 2w] staged importance, then [SEG] pooled
   __shared__ unsigned hist[256];
   __shared__ unsigned s_digit, s_remaining;
   __shared__ ScanSmem scan;
-  const int b = blockIdx.x, tid = threadIdx.x;
+  __shared__ int kept_c[ST];                      // kept chunk ids of one scan tile, in order
+  __shared__ int kept_off[ST];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long n_c = (N + chunk - 1) / chunk;
   const float* imp = imp_all + (long long)b * N;
-  float* cs = cs_all + (long long)b * n_c;
+  const long long w_ = (pool_k - 1) / 2;
+  float* cs = (n_c <= kSmemChunks) ? seg + 2 * SEG + 2 * w_ : cs_all + (long long)b * n_c;
   int* ids = ids_all + (long long)b * N;
   int* pos = pos_all + (long long)b * N;
   const long long w = (pool_k - 1) / 2;
 
-  // ---- A. pooled scores (centred window, shrinking edges) -> chunk sums, in token order
-  for (long long base = 0; base < N; base += ST) {
-    const long long i = base + tid;
-    if (i < N) {
-      long long lo = i - w < 0 ? 0 : i - w, hi = i + w > N - 1 ? N - 1 : i + w;
-      float s = 0.f;
-      for (long long j = lo; j <= hi; ++j) s += imp[j];
-      tile[tid] = s / (float)(hi - lo + 1);
+  // ---- A. pooled scores (centred window, shrinking edges) -> chunk sums
+  float* pooled = seg + SEG + 2 * w;                // [SEG]
+  const int wi = (int)w;
+  const float inv_k = 1.f / (float)pool_k;
+  const bool warp_chunks = chunk <= 32 && (chunk & (chunk - 1)) == 0;   // power of two <= 32
+  for (long long base = 0; base < N; base += SEG) {
+    const int len = (int)((base + SEG < N) ? SEG : N - base);           // tokens in this segment
+    const long long lo = base - w < 0 ? 0 : base - w, hi = base + len + w > N ? N : base + len + w;
+    const int off = (int)(base - lo);                                     // seg index of token `base`
+    {
+      // all loads of the segment in flight before any store (latency-bound otherwise)
+      constexpr int PER = SEG / ST;
+      const int n = (int)(hi - lo);
+      float r[PER];
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int i = tid + k * ST;
+        r[k] = i < n ? __ldg(imp + lo + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int i = tid + k * ST;
+        if (i < n) seg[i] = r[k];
+      }
+      for (int i = PER * ST + tid; i < n; i += ST) seg[i] = imp[lo + i];   // halo beyond SEG
     }
     __syncthreads();
-    const long long tend = (base + ST < N) ? base + ST : N;
-    const long long c_first = base / chunk, c_last = (tend - 1) / chunk;
-    for (long long c = c_first + tid; c <= c_last; c += ST) {
-      long long t0 = c * chunk > base ? c * chunk : base;
-      long long t1 = (c + 1) * chunk < tend ? (c + 1) * chunk : tend;
-      float s = (t0 == c * chunk) ? 0.f : cs[c];      // chunk continued from the previous tile
-      for (long long t = t0; t < t1; ++t) s += tile[t - base];
-      cs[c] = s;
+    if (base == 0) SP_TS(4)
+    // interior tokens [i_lo, i_hi) have the full window inside the sequence
+    const int i_lo = (int)(w - base > 0 ? w - base : 0);
+    const int i_hi = (int)(N - 1 - w - base + 1 < len ? N - 1 - w - base + 1 : len);
+#pragma unroll 4
+    for (int i = tid; i < len; i += ST) {                               // coalesced, conflict-free
+      float ws = 0.f;
+      if (i >= i_lo && i < i_hi) {                                      // interior: full window
+        const float* p0 = seg + off + i - wi;
+        for (int k = 0; k < pool_k; ++k) ws += p0[k];
+        pooled[i] = ws * inv_k;
+      } else {                                                            // sequence edges: shrink
+        const long long t = base + i;
+        const long long a = t - w < 0 ? 0 : t - w, e = t + w > N - 1 ? N - 1 : t + w;
+        for (long long j = a; j <= e; ++j) ws += seg[j - lo];
+        pooled[i] = ws / (float)(e - a + 1);
+      }
+    }
+    __syncthreads();
+    if (base == 0) SP_TS(5)
+    const long long c_first = base / chunk, c_last = (base + len - 1) / chunk;
+    if (warp_chunks && base % chunk == 0) {
+      // a warp sums 32 consecutive pooled values in groups of `chunk` lanes (tree
+      // order); SEG is a multiple of 32 so every chunk starts inside its segment
+      const int lg = __ffs(chunk) - 1;
+      const int cbase = (int)(base >> lg);
+#pragma unroll 4
+      for (int g0 = warp * 32; g0 < len; g0 += ST) {
+        float v = g0 + lane < len ? pooled[g0 + lane] : 0.f;
+        for (int o = chunk >> 1; o >= 1; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, chunk);
+        if ((lane & (chunk - 1)) == 0 && g0 + lane < len) cs[cbase + ((g0 + lane) >> lg)] = v;
+      }
+    } else {
+      // the owner thread walks its chunk's tokens in a rotated (fixed, hence
+      // deterministic) order so a warp's reads hit distinct banks
+      for (long long c = c_first + tid; c <= c_last; c += ST) {
+        const long long t0 = c * chunk > base ? c * chunk : base;
+        const long long t1 = (c + 1) * chunk < base + len ? (c + 1) * chunk : base + len;
+        const int n = (int)(t1 - t0), i0 = (int)(t0 - base);
+        float sacc = (t0 == c * chunk) ? 0.f : cs[c];                    // chunk continued from the previous segment
+        const int rot = (int)(c % n);
+        for (int j = 0; j < n; ++j) {
+          int k = j + rot;
+          if (k >= n) k -= n;
+          sacc += pooled[i0 + k];
+        }
+        cs[c] = sacc;
+      }
     }
     __syncthreads();
   }
   for (long long c = tid; c < n_c; c += ST) {
-    long long sz = ((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk;
+    const long long sz = ((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk;
     cs[c] = cs[c] / (float)sz;
   }
   __syncthreads();
 
+  SP_TS(1)
   // ---- B. radix select: threshold bit pattern T of the K_c-th largest score
   unsigned prefix = 0, pmask = 0;
   unsigned remaining = (unsigned)K_c;
   for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int k = tid; k < 256; k += ST) hist[k] = 0;
+    if (tid < 256) hist[tid] = 0;
     __syncthreads();
     for (long long c = tid; c < n_c; c += ST) {
-      unsigned key = __float_as_uint(cs[c]);
+      const unsigned key = __float_as_uint(cs[c]);
       if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
     }
     __syncthreads();
-    if (tid == 0) {
-      unsigned cum = 0, dgt = 0;
-      for (int k = 255; k >= 0; --k) {
-        if (cum + hist[k] >= remaining) { dgt = (unsigned)k; break; }
-        cum += hist[k];
+    // digit D: count(digits > D) < remaining <= count(digits >= D); warps 0-7 scan 256 bins
+    if (tid < 256) {
+      // suffix sums over bins (high digit first): bin d handled by thread 255 - d
+      const int d = 255 - tid;
+      unsigned v = hist[d];
+      unsigned x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
       }
-      s_digit = dgt;
-      s_remaining = remaining - cum;
+      if (lane == 31) scan.warp_tot[warp] = (int)x;
+      __syncwarp();
+      // (warps 0..7 only) combine warp totals below
+      kept_off[tid] = (int)x;                      // inclusive within warp
+    }
+    __syncthreads();
+    if (tid < 256) {
+      unsigned before = 0;
+      for (int ww = 0; ww < warp; ++ww) before += (unsigned)scan.warp_tot[ww];
+      const unsigned incl = before + (unsigned)kept_off[tid];   // count of digits >= d
+      const unsigned excl = incl - hist[255 - tid];             // count of digits > d
+      if (excl < remaining && incl >= remaining) {
+        s_digit = (unsigned)(255 - tid);
+        s_remaining = remaining - excl;
+      }
     }
     __syncthreads();
     prefix |= s_digit << shift;
@@ -128,30 +224,49 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
   const unsigned T = prefix;
   const int need_eq = (int)remaining;            // chunks equal to T to keep (lowest indices first)
 
-  // ---- C. keep flags in chunk order, compaction of the kept token ranges
+  SP_TS(2)
+  // ---- C. keep flags in chunk order, compaction (+ gather) of the kept token ranges
   int carry_eq = 0, carry_tok = 0;
+  const int* tokens = tokens_all ? tokens_all + (long long)b * N : nullptr;
+  int* out = out_all ? out_all + (long long)b * N : nullptr;
   for (long long base = 0; base < n_c; base += ST) {
     const long long c = base + tid;
-    unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
-    int eq = (c < n_c && key == T) ? 1 : 0;
-    int gt = (c < n_c && key > T) ? 1 : 0;
+    const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
+    const int eq = (c < n_c && key == T) ? 1 : 0;
+    const int gt = (c < n_c && key > T) ? 1 : 0;
     int tot;
-    int eq_rank = block_excl_scan(eq, scan, &tot) + carry_eq;
+    const int eq_rank = block_excl_scan(eq, scan, &tot) + carry_eq;
     carry_eq += tot;
-    int keep = gt | (eq & (eq_rank < need_eq ? 1 : 0));
+    const int keep = gt | (eq & (eq_rank < need_eq ? 1 : 0));
+    const int slot = block_excl_scan(keep, scan, &tot);          // index among kept chunks of this tile
+    const int nk = tot;
     int sz = 0;
     if (keep) sz = (int)(((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk);
-    int off = block_excl_scan(sz, scan, &tot) + carry_tok;
-    carry_tok += tot;
+    int tot2;
+    const int off = block_excl_scan(sz, scan, &tot2) + carry_tok;
     if (keep) {
-      const int t0 = (int)(c * chunk);
-      for (int j = 0; j < sz; ++j) {
-        ids[off + j] = t0 + j;
-        pos[off + j] = t0 + j + pos0;
+      kept_c[slot] = (int)c;
+      kept_off[slot] = off;
+    }
+    __syncthreads();
+    // one warp per kept chunk: coalesced ids / pos (/ gathered tokens)
+    for (int k = warp; k < nk; k += NW) {
+      const long long cc = kept_c[k];
+      const int t0 = (int)(cc * chunk);
+      const int csz = (int)(((cc + 1) * chunk < N ? (cc + 1) * chunk : N) - cc * chunk);
+      const int o = kept_off[k];
+      for (int j = lane; j < csz; j += 32) {
+        ids[o + j] = t0 + j;
+        pos[o + j] = t0 + j + pos0;
+        if (out) out[o + j] = tokens[t0 + j];
       }
     }
+    carry_tok += tot2;
+    __syncthreads();
   }
   if (tid == 0) n_kept[b] = carry_tok;
+  SP_TS(3)
+#undef SP_TS
 }
 
 }  // namespace
@@ -161,9 +276,31 @@ size_t select_ws_bytes(int B, long long N, int chunk) {
   return align256((size_t)B * n_c * sizeof(float));
 }
 
+bool select_supported(int pool_k) { return pool_k <= kMaxPool; }
+
 cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int chunk, int pos0, long long K_c,
-                          int* ids, int* pos, int* n_kept, void* ws, cudaStream_t st) {
-  k_select<<<B, ST, 0, st>>>(imp, N, pool_k, chunk, pos0, K_c, ids, pos, n_kept, reinterpret_cast<float*>(ws));
+                          int* ids, int* pos, int* n_kept, void* ws, cudaStream_t st, const int* tokens, int* out) {
+  static bool configured = false;
+  const size_t smem = (size_t)(2 * SEG + 2 * ((kMaxPool - 1) / 2) + kSmemChunks) * sizeof(float);
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const long long n_c = (N + chunk - 1) / chunk;
+  const size_t need = (size_t)(2 * SEG + 2 * ((pool_k - 1) / 2) + (n_c <= kSmemChunks ? n_c : 0)) * sizeof(float);
+  static long long* dbg = nullptr;
+  if (std::getenv("SP_SELECT_TS") && !dbg) cudaMalloc(&dbg, 64);
+  k_select<<<B, ST, need, st>>>(imp, N, pool_k, chunk, pos0, K_c, ids, pos, n_kept, reinterpret_cast<float*>(ws),
+                                tokens, out, dbg);
+  if (dbg) {
+    long long h[4];
+    long long h6[6];
+    cudaMemcpy(h6, dbg, 48, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < 4; ++i) h[i] = h6[i];
+    std::fprintf(stderr, "select phases (cycles): A %lld B %lld C %lld | seg0 stage %lld pool %lld\n", h[1] - h[0],
+                 h[2] - h[1], h[3] - h[2], h6[4] - h[0], h6[5] - h6[4]);
+  }
   return cudaGetLastError();
 }
 

@@ -77,6 +77,7 @@ sp_status check_select(int32_t B, int64_t N, const sp_select_params* p) {
   if (!(p->keep_rate > 0.0 && p->keep_rate <= 1.0)) return SP_EINVAL;
   if (p->pool_k < 1 || p->pool_k % 2 == 0) return SP_EINVAL;
   if (p->chunk < 1) return SP_EINVAL;
+  if (!select_supported(p->pool_k)) return SP_EUNSUPPORTED;
   if (p->pos0 < 0 || (long long)p->pos0 + N >= (1LL << 31)) return SP_EINVAL;
   return SP_OK;
 }
@@ -244,15 +245,22 @@ size_t sp_select_workspace_bytes(int32_t B, int64_t N, const sp_select_params* p
 
 sp_status sp_select(const float* importance, int32_t B, int64_t N, const sp_select_params* p, int32_t* ids,
                     int32_t* pos, int32_t* n_kept, void* ws, size_t ws_bytes, sp_stream stream) {
+  return sp_select_gather(importance, nullptr, B, N, p, ids, pos, n_kept, nullptr, ws, ws_bytes, stream);
+}
+
+sp_status sp_select_gather(const float* importance, const int32_t* tokens, int32_t B, int64_t N,
+                           const sp_select_params* p, int32_t* ids, int32_t* pos, int32_t* n_kept,
+                           int32_t* out_tokens, void* ws, size_t ws_bytes, sp_stream stream) {
   sp_status s = check_select(B, N, p);
   if (s != SP_OK) return s;
   if (importance == nullptr || ids == nullptr || pos == nullptr || n_kept == nullptr) return SP_EINVAL;
+  if ((tokens == nullptr) != (out_tokens == nullptr)) return SP_EINVAL;
   if ((s = check_device()) != SP_OK) return s;
   if (ws == nullptr || ws_bytes < select_ws_bytes(B, N, p->chunk)) return SP_EWORKSPACE;
   const long long n_c = (N + p->chunk - 1) / p->chunk;
   const long long K_c = sp_kept_chunks(n_c, p->keep_rate);
   return from_cuda(select_launch(importance, B, N, p->pool_k, p->chunk, p->pos0, K_c, ids, pos, n_kept, ws,
-                                 reinterpret_cast<cudaStream_t>(stream)));
+                                 reinterpret_cast<cudaStream_t>(stream), tokens, out_tokens));
 }
 
 sp_status sp_gather(const int32_t* tokens, const int32_t* ids, const int32_t* n_kept, int32_t B, int64_t N,
@@ -293,10 +301,10 @@ sp_status sp_run_host(const sp_host_io* host, const sp_device_bufs* dev, const s
   if ((s = sp_score(dev->Q, dev->K, g, lay, dev->importance, dev->ws, dev->ws_bytes, stream)) != SP_OK) return s;
   const size_t score_bytes = align256(score_ws(to_geom(*g), SP_SCORE_AUTO));
   if (dev->ws_bytes < score_bytes) return SP_EWORKSPACE;
-  if ((s = sp_select(dev->importance, g->B, g->N, p, dev->ids, dev->pos, dev->n_kept,
-                     reinterpret_cast<char*>(dev->ws) + score_bytes, dev->ws_bytes - score_bytes, stream)) != SP_OK)
+  if ((s = sp_select_gather(dev->importance, dev->tokens, g->B, g->N, p, dev->ids, dev->pos, dev->n_kept,
+                            dev->out_tokens, reinterpret_cast<char*>(dev->ws) + score_bytes,
+                            dev->ws_bytes - score_bytes, stream)) != SP_OK)
     return s;
-  if ((s = sp_gather(dev->tokens, dev->ids, dev->n_kept, g->B, g->N, dev->out_tokens, stream)) != SP_OK) return s;
   if (cudaMemcpyAsync(host->n_kept, dev->n_kept, (size_t)g->B * sizeof(int32_t), cudaMemcpyDeviceToHost, st) !=
           cudaSuccess ||
       cudaMemcpyAsync(host->ids, dev->ids, tok_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess ||

@@ -70,8 +70,10 @@ cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Ge
 
 // ---------------------------------------------------------------- select / gather (select.cu, gather.cu)
 size_t select_ws_bytes(int B, long long N, int chunk);
+bool select_supported(int pool_k);
 cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int chunk, int pos0,
-                          long long K_c, int* ids, int* pos, int* n_kept, void* ws, cudaStream_t st);
+                          long long K_c, int* ids, int* pos, int* n_kept, void* ws, cudaStream_t st,
+                          const int* tokens = nullptr, int* out = nullptr);
 cudaError_t gather_launch(const int* tokens, const int* ids, const int* n_kept, int B, long long N, int* out,
                           cudaStream_t st);
 

@@ -160,6 +160,23 @@ def test_select_keep_all_and_single_chunk():
     assert nk.tolist() == [3, 3] and ids[0, :3].tolist() == [0, 1, 2]
 
 
+@pytest.mark.parametrize("pool_k,chunk", [(5, 32), (3, 1), (1, 7)])
+def test_select_gather_fused(pool_k, chunk):
+    """sp_select_gather == sp_select followed by sp_gather, bit for bit."""
+    rng = np.random.default_rng(7 + chunk)
+    B, N = 3, 40000
+    imp = torch.tensor(rng.random((B, N)) ** 3 + 1e-6, dtype=torch.float32, device="cuda")
+    tok = torch.tensor(rng.integers(0, 128256, size=(B, N)), dtype=torch.int32, device="cuda")
+    ids, pos, nk = sp.select(imp, 0.3, pool_k, chunk, pos0=11)
+    out = sp.gather(tok, ids, nk)
+    ids2, pos2, nk2, out2 = sp.select(imp, 0.3, pool_k, chunk, pos0=11, tokens=tok)
+    assert torch.equal(nk, nk2)
+    for b in range(B):
+        n = int(nk[b])
+        assert torch.equal(ids[b, :n], ids2[b, :n]) and torch.equal(pos[b, :n], pos2[b, :n])
+        assert torch.equal(out[b, :n], out2[b, :n])
+
+
 def test_gather_bitexact():
     rng = np.random.default_rng(1)
     B, N = 3, 4000
