@@ -5,5 +5,6 @@ The compute lives in libspecprefill.so (C ABI: include/specprefill.h); this
 package is a thin binding plus the multi-GPU orchestration.
 """
 from .api import (gather, kept_chunks, make_geom, score, select, specprefill,  # noqa: F401
-                  check_device_error, run_host, run_workspace_bytes, score_plan, workspace)
+                  check_device_error, run_host, run_workspace_bytes, score_plan, workspace,
+                  score_stats, stats_combine, score_finish)
 from ._lib import LIB_PATH, SIGNATURES, SpError, lib  # noqa: F401

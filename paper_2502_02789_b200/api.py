@@ -133,6 +133,45 @@ def score_plan(Q, K, R_valid=None) -> dict:
     return dict(zip(keys, list(out)))
 
 
+def score_stats(Q, K, R_valid=None, scale=None, out=None, stream=None) -> torch.Tensor:
+    """Sequence-sharded split, step 1: local softmax statistics (log2 domain)
+    stats [B*L*H*R_valid][2] = (m2, l) over this shard's tokens."""
+    g, lay = make_geom(Q, K, R_valid, scale)
+    rows = g.B * g.L * g.H * g.R_valid
+    out = torch.empty((rows, 2), dtype=torch.float32, device=K.device) if out is None else out
+    nbytes = lib().sp_score_split_workspace_bytes(C.byref(g))
+    ws = workspace(("split", _geom_key(g), _split_algo()), nbytes, K.device)
+    check(lib().sp_score_stats(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), out.data_ptr(), ws.data_ptr(),
+                               ws.numel(), _stream_ptr(stream)), "sp_score_stats")
+    return out
+
+
+def stats_combine(parts: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    """Step 2: merge [P][rows][2] gathered statistics in rank order -> lse2 [rows]."""
+    if parts.dtype != torch.float32 or parts.dim() != 3 or parts.shape[2] != 2 or not parts.is_contiguous():
+        raise ValueError("parts must be contiguous fp32 [P][rows][2]")
+    P, rows = parts.shape[0], parts.shape[1]
+    out = torch.empty((rows,), dtype=torch.float32, device=parts.device) if out is None else out
+    check(lib().sp_stats_combine(parts.data_ptr(), P, rows, out.data_ptr(), _stream_ptr(stream)), "sp_stats_combine")
+    return out
+
+
+def score_finish(Q, K, lse2, R_valid=None, scale=None, out=None, stream=None) -> torch.Tensor:
+    """Step 3: importance over this shard's tokens given the global lse2."""
+    g, lay = make_geom(Q, K, R_valid, scale)
+    out = torch.empty((g.B, g.N), dtype=torch.float32, device=K.device) if out is None else out
+    nbytes = lib().sp_score_split_workspace_bytes(C.byref(g))
+    ws = workspace(("split", _geom_key(g), _split_algo()), nbytes, K.device)
+    check(lib().sp_score_finish(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), lse2.data_ptr(), out.data_ptr(),
+                                ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_score_finish")
+    return out
+
+
+def _split_algo():
+    import os
+    return os.environ.get("SP_SPLIT_ALGO", "auto")
+
+
 def kept_chunks(n_chunks: int, keep: float) -> int:
     k = lib().sp_kept_chunks(int(n_chunks), float(keep))
     if k < 0:

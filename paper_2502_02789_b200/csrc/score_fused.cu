@@ -42,6 +42,7 @@ namespace sp {
 namespace {
 
 constexpr int kThreads = 384;
+enum FusedMode : int { kModeFull = 0, kModeStats = 1, kModeFinish = 2 };
 constexpr int kTileM = 128;
 constexpr int kStatsWarp0 = 4;
 constexpr int kFinalWarp0 = 8;
@@ -79,7 +80,8 @@ struct FusedParams {
   int* err;
   unsigned long long* trace;           // optional [grid][trace_units][8] globaltimer stamps (debug)
   int trace_units;
-  int dbg;                             // timing experiments (SP_FUSED_DEBUG); 0 in production
+  int mode;                            // kModeFull / kModeStats (publish partials only) / kModeFinish (lse2 given)
+  const float* lse_in;                 // kModeFinish: lse2 per row ((b*L + l)*H + h)*Rv + r
   int prefetch;                        // L2 prefetch distance in tiles beyond the SMEM ring (0 = off)
 };
 
@@ -169,50 +171,7 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t 
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
-// tcgen05.ld of 32 consecutive fp32 columns of this warp's 32 TMEM lanes, WITHOUT
-// waiting: the registers are undefined until tmem_wait() + tie32().
-__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, float (&v)[32]) {
-  uint32_t* r = reinterpret_cast<uint32_t*>(v);
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-}
 __device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-// Re-define the registers after tmem_wait() so no use of them can be scheduled
-// before the wait (the compiler does not know tcgen05.ld is asynchronous).
-__device__ __forceinline__ void tie32(float (&v)[32]) {
-  asm volatile(""
-               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]),
-                 "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]), "+f"(v[14]),
-                 "+f"(v[15]), "+f"(v[16]), "+f"(v[17]), "+f"(v[18]), "+f"(v[19]), "+f"(v[20]), "+f"(v[21]),
-                 "+f"(v[22]), "+f"(v[23]), "+f"(v[24]), "+f"(v[25]), "+f"(v[26]), "+f"(v[27]), "+f"(v[28]),
-                 "+f"(v[29]), "+f"(v[30]), "+f"(v[31]));
-}
-// f(x[32], t) for every tile t < ntile of a TMEM column group; the load of tile
-// t+1 is in flight while tile t is processed.
-template <class F>
-__device__ __forceinline__ void for_tiles(uint32_t base, uint32_t stride, int ntile, F&& f) {
-  float a[32], b[32];
-  if (ntile <= 0) return;
-  tmem_ld32_issue(base, a);
-  for (int t = 0; t < ntile; t += 2) {
-    tmem_wait();
-    tie32(a);
-    if (t + 1 < ntile) tmem_ld32_issue(base + (uint32_t)(t + 1) * stride, b);
-    f(a, t);
-    if (t + 1 < ntile) {
-      tmem_wait();
-      tie32(b);
-      if (t + 2 < ntile) tmem_ld32_issue(base + (uint32_t)(t + 2) * stride, a);
-      f(b, t + 1);
-    }
-  }
-}
 
 __device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, float (&v)[16]) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
@@ -228,57 +187,7 @@ __device__ __forceinline__ void tie16(float (&v)[16]) {
                  "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]), "+f"(v[14]),
                  "+f"(v[15]));
 }
-template <class F>
-__device__ __forceinline__ void for_tiles16(uint32_t base, uint32_t stride, int ntile, F&& f) {
-  float a[16], b[16];
-  if (ntile <= 0) return;
-  tmem_ld16_issue(base, a);
-  for (int t = 0; t < ntile; t += 2) {
-    tmem_wait();
-    tie16(a);
-    if (t + 1 < ntile) tmem_ld16_issue(base + (uint32_t)(t + 1) * stride, b);
-    f(a, t);
-    if (t + 1 < ntile) {
-      tmem_wait();
-      tie16(b);
-      if (t + 2 < ntile) tmem_ld16_issue(base + (uint32_t)(t + 2) * stride, a);
-      f(b, t + 1);
-    }
-  }
-}
 
-// f(x, t) for every tile t < ntile, loading NB tiles per tcgen05.wait::ld so
-// that NB TMEM round trips overlap (tcgen05.ld latency is ~hundreds of cycles).
-template <int NB, class F>
-__device__ __forceinline__ void for_tiles16_batched(uint32_t base, uint32_t stride, int ntile, F&& f) {
-  for (int t0 = 0; t0 < ntile; t0 += NB) {
-    float x[NB][16];
-#pragma unroll
-    for (int j = 0; j < NB; ++j)
-      if (t0 + j < ntile) tmem_ld16_issue(base + (uint32_t)(t0 + j) * stride, x[j]);
-    tmem_wait();
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      tie16(x[j]);
-      if (t0 + j < ntile) f(x[j], t0 + j);
-    }
-  }
-}
-template <int NB, class F>
-__device__ __forceinline__ void for_tiles32_batched(uint32_t base, uint32_t stride, int ntile, F&& f) {
-  for (int t0 = 0; t0 < ntile; t0 += NB) {
-    float x[NB][32];
-#pragma unroll
-    for (int j = 0; j < NB; ++j)
-      if (t0 + j < ntile) tmem_ld32_issue(base + (uint32_t)(t0 + j) * stride, x[j]);
-    tmem_wait();
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      tie32(x[j]);
-      if (t0 + j < ntile) f(x[j], t0 + j);
-    }
-  }
-}
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -292,9 +201,6 @@ __device__ __forceinline__ unsigned long long pack_ms(float m, float s) {
 }
 __device__ __forceinline__ float2 unpack_ms(unsigned long long w) {
   return make_float2(__uint_as_float((unsigned)w), __uint_as_float((unsigned)(w >> 32)));
-}
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -319,36 +225,6 @@ __device__ __forceinline__ void spin_geq(const unsigned* p, unsigned target, int
   }
 }
 
-// Transposed butterfly over 16 columns x 32 lanes: returns, in every lane,
-// the reduction over all 32 lanes of column (lane >> 1).  15 + 1 shuffles.
-template <bool kMax>
-__device__ __forceinline__ float transpose_reduce16(float (&v)[16], int lane) {
-  auto op = [](float a, float b) { return kMax ? fmaxf(a, b) : a + b; };
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const bool up = lane & 16;
-    float send = up ? v[i] : v[i + 8], keep = up ? v[i + 8] : v[i];
-    v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, 16));
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const bool up = lane & 8;
-    float send = up ? v[i] : v[i + 4], keep = up ? v[i + 4] : v[i];
-    v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, 8));
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const bool up = lane & 4;
-    float send = up ? v[i] : v[i + 2], keep = up ? v[i + 2] : v[i];
-    v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, 4));
-  }
-  {
-    const bool up = lane & 2;
-    float send = up ? v[0] : v[1], keep = up ? v[1] : v[0];
-    v[0] = op(keep, __shfl_xor_sync(0xffffffffu, send, 2));
-  }
-  return op(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
-}
 
 // 2^x with one MUFU op (flush-to-zero: results below 2^-126 contribute nothing
 // measurable to a softmax denominator or a probability > 1e-30).
@@ -358,18 +234,6 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// Merge a partial (m, s) -- s = sum 2^((x - m) * xs) over a token subset, m the
-// subset's max raw logit -- into the running pair (M, S).  Empty partials (s == 0)
-// are skipped, so an all-masked subset (m = -inf) is harmless.
-__device__ __forceinline__ void lse_merge(float& M, float& S, float2 v, float xs) {
-  if (!(v.y > 0.f)) return;
-  if (v.x > M) {
-    S = S * ex2((M - v.x) * xs) + v.y;
-    M = v.x;
-  } else {
-    S += v.y * ex2((v.x - M) * xs);
-  }
-}
 
 // Debug trace: stamp event e of the CTA's ui-th unit (no-op unless enabled).
 __device__ __forceinline__ void trace_stamp(const FusedParams& p, uint32_t ui, int e) {
@@ -377,22 +241,6 @@ __device__ __forceinline__ void trace_stamp(const FusedParams& p, uint32_t ui, i
     p.trace[((size_t)blockIdx.x * p.trace_units + ui) * 8 + e] = globaltimer_ns();
 }
 
-// Transposed butterfly over 32 columns x 32 lanes: lane l returns the reduction
-// over all 32 lanes of column l.  16 + 8 + 4 + 2 + 1 = 31 shuffles.
-template <bool kMax>
-__device__ __forceinline__ float transpose_reduce32(float (&v)[32], int lane) {
-  auto op = [](float a, float b) { return kMax ? fmaxf(a, b) : a + b; };
-#pragma unroll
-  for (int w = 16; w >= 1; w >>= 1) {
-    const bool up = lane & w;
-#pragma unroll
-    for (int i = 0; i < w; ++i) {
-      const float send = up ? v[i] : v[i + w], keep = up ? v[i + w] : v[i];
-      v[i] = op(keep, __shfl_xor_sync(0xffffffffu, send, w));
-    }
-  }
-  return v[0];
-}
 
 // Fold one tile's 32 logit columns (group grp) into the running (l,h)-max of
 // this thread's token: acc[(t*Rv + r)*128 + tok] = max(acc, max_h (x*xs - lse2)).
@@ -643,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             const uint32_t a_lo0 = ((smem_u32(smem + p.off_k + stage * p.k_stage_bytes) >> 4) & 0x3FFFu) | (1u << 16);
             const uint32_t dcol = tmem + slot * p.NCP;
             uint32_t accum = 0;
-            for (int kb = 0; kb < p.nkb && !(p.dbg & 16); ++kb) {
+            for (int kb = 0; kb < p.nkb; ++kb) {
               uint32_t a_lo = a_lo0 + kb * a_kb, b_lo = b_lo0 + kb * b_kb;
               for (int ks = 0; ks < ksteps; ++ks, a_lo += 2, b_lo += 2) {
                 umma_bf16(dcol, ((uint64_t)desc_hi << 32) | a_lo, ((uint64_t)desc_hi << 32) | b_lo, p.idesc, accum);
@@ -658,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         }
       }
     }
-  } else if (warp >= kStatsWarp0 && warp < kFinalWarp0 && !(p.dbg & 8)) {
+  } else if (warp >= kStatsWarp0 && warp < kFinalWarp0 && p.mode != kModeFinish) {
     // ================================================================ softmax statistics
     // Progressive: each tile is folded as soon as its MMA completes into a
     // per-thread running (ref, sum) per column, sum = sum 2^(x*xs - ref) with
@@ -696,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             tmem_wait();
             tie16(*reinterpret_cast<float(*)[16]>(x0));
             tie16(*reinterpret_cast<float(*)[16]>(x0 + 16));
-            if (!(p.dbg & 1) && tok0 + (long long)(t - jb.t_lo) * kTileM < p.N) {
+            if (tok0 + (long long)(t - jb.t_lo) * kTileM < p.N) {
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
                 // one exp2 either way: first value (ref = -inf) or a jump > 2^64
@@ -719,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         mbar_arrive(bar_rfull + 8 * (ui & 1));                        // 128 arrivals: all columns written
       }
     }
-  } else if (warp == 2 && !(p.dbg & 8)) {
+  } else if (warp == 2 && p.mode != kModeFinish) {
     // ================================================================ statistics exchange
     // Merge the 4 statistics warps into the CTA partial and publish it: one
     // 64-bit word (max2, sum) per column, single-copy atomic, so a reader sees
@@ -757,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         for (int c = lane; c < p.NCP; c += 32) row[c] = 0ull;
       }
     }
-  } else if (warp == 3) {
+  } else if (warp == 3 && p.mode != kModeStats) {
     // ================================================================ lse2 gather
     // Polls the unit's n_tg published partials (all loads of a batch in flight
     // together; zero words are re-read until written), merges them in
@@ -773,7 +621,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         mbar_wait(bar_lempty + 8 * par, ((ui / kLseRing) & 1) ^ 1);    // aggregation done with ls[par]
         float* ls = lse_s + par * p.NCP;
         const unsigned long long* src = part_cur + ubase * p.n_tg * p.NCP;
-        for (int c = lane; c < p.NCP && !(p.dbg & 8); c += 32) {
+        for (int c = lane; c < p.NCP && p.mode == kModeFinish; c += 32) {
+          // lse2 supplied by the caller (sequence-sharded split: globally combined statistics)
+          float l2 = 0.f;
+          if (c < p.NC) {
+            const int l = u / p.Hkv, g = u % p.Hkv;
+            l2 = p.lse_in[(((long long)jb.b * p.L + l) * p.Hkv * p.G + g * p.G + c % p.G) * p.Rv + c / p.G];
+          }
+          ls[c] = l2;
+        }
+        for (int c = lane; c < p.NCP && p.mode == kModeFull; c += 32) {
           float M = -CUDART_INF_F, S = 0.f;
           for (int s0 = 0; s0 < p.n_tg; s0 += kMaxLseBatch) {
             unsigned long long v[kMaxLseBatch];
@@ -784,7 +641,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
               missing |= (v[j] == 0ull ? 1u : 0u) << j;
             }
             long long it = 0;
-            if (p.dbg & 4) missing = 0;
             while (__any_sync(0xffffffffu, missing != 0)) {
               __nanosleep(it < 8 ? 64 : 200);
 #pragma unroll
@@ -811,7 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           float l2 = 0.f;
           if (c < p.NC) {
             l2 = M + log2f(S);
-            if (!isfinite(l2) && p.dbg == 0) set_err(p.err, kDevNonFinite);
+            if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
           }
           ls[c] = l2;
         }
@@ -834,7 +690,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         for (int r = 0; r < p.Rv; ++r) acc[(t * p.Rv + r) * kTileM + tok] = -CUDART_INF_F;
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
         const uint32_t par = ui % kLseRing;
-        mbar_wait(bar_lfull + 8 * par, (ui / kLseRing) & 1);
+        if (p.mode != kModeStats) mbar_wait(bar_lfull + 8 * par, (ui / kLseRing) & 1);
         const float* ls = lse_s + par * p.NCP;
         uint32_t slot = gt % nslots, ph = (gt / nslots) & 1;
         for (int t = 0; t < ntile; ++t, ++gt) {
@@ -843,7 +699,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + slot * p.NCP;
           float* arow = acc + (t * p.Rv) * kTileM + tok;
 #pragma unroll 1
-          for (int k0 = 0; k0 < p.NCP / 16 && !(p.dbg & 8); k0 += 2) {
+          for (int k0 = 0; k0 < p.NCP / 16 && p.mode != kModeStats; k0 += 2) {
             float xa[16], xb[16];
             const bool two = k0 + 1 < p.NCP / 16;
             tmem_ld16_issue(ta + k0 * 16, xa);
@@ -861,7 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
                 const float4 v4 = *reinterpret_cast<const float4*>(ls + k * 16 + 4 * i4);
                 lv[4 * i4] = v4.x; lv[4 * i4 + 1] = v4.y; lv[4 * i4 + 2] = v4.z; lv[4 * i4 + 3] = v4.w;
               }
-              if (!(p.dbg & 2)) fold_tile<kG, 16>(h == 0 ? xa : xb, lv, p.xs, k, p.NC, p.G, p.Rv, arow);
+              fold_tile<kG, 16>(h == 0 ? xa : xb, lv, p.xs, k, p.NC, p.G, p.Rv, arow);
             }
           }
           tc_fence_before();
@@ -870,9 +726,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           if (++slot == nslots) { slot = 0; ph ^= 1; }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_lempty + 8 * par);
+        if (lane == 0 && p.mode != kModeStats) mbar_arrive(bar_lempty + 8 * par);
         if (q == 0 && lane == 0) trace_stamp(p, ui, 6);
       }
+      if (p.mode == kModeStats) continue;                             // no importance in stats-only mode
       // ---- job epilogue: importance = mean_r 2^acc (possibly across unit groups)
       const float inv = 1.f / (float)p.Rv;
       if (p.n_ug == 1) {
@@ -930,7 +787,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && p.mode != kModeFinish) {           // finish mode never touches the partials
     __threadfence();
     if (atomicAdd(p.epoch + 1, 1u) == gridDim.x - 1) {       // last CTA: next launch uses the other buffer
       atomicExch(p.epoch + 1, 0u);
@@ -1136,8 +993,38 @@ size_t fused_score_ws_bytes(const Geom& g) {
   return pl.ws_total();
 }
 
-cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
-                        float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
+namespace {
+
+// Stats-only mode epilogue: merge each unit's n_tg CTA partials (buffer of the
+// launch that just ran: its parity is epoch - 1) into per-row (m2, l) in the
+// sp_score_stats layout, row = ((b*L + l)*H + h)*Rv + r.
+__global__ void k_partials_to_stats(const unsigned long long* __restrict__ part, const unsigned* __restrict__ epoch,
+                                    int B, int L, int Hkv, int G, int Rv, int n_tg, int NC, int NCP,
+                                    float* __restrict__ stats) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long U = (long long)L * Hkv;
+  if (idx >= (long long)B * U * NC) return;
+  const int c = (int)(idx % NC);
+  const long long ubase = idx / NC;                  // b*U + u
+  const int u = (int)(ubase % U), b = (int)(ubase / U);
+  const int l = u / Hkv, g = u % Hkv;
+  const unsigned parity = (epoch[0] - 1u) & 1u;
+  const long long half = (long long)B * U * n_tg * NCP;
+  const unsigned long long* src = part + parity * half + ubase * n_tg * NCP + c;
+  float M = -CUDART_INF_F, S = 0.f;
+  for (int s2 = 0; s2 < n_tg; ++s2) {
+    const float2 w = unpack_ms(src[(long long)s2 * NCP]);
+    if (w.y > 0.f) merge2(M, S, w.x, w.y);
+  }
+  const long long row = (((long long)b * L + l) * Hkv * G + g * G + c % G) * Rv + c / G;
+  stats[row * 2] = M;
+  stats[row * 2 + 1] = S;
+}
+
+}  // namespace
+
+cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay, int mode,
+                         const float* lse_in, float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
   Plan pl = make_plan(g);
   if (!pl.ok || ws_bytes < pl.ws_total()) return cudaErrorInvalidValue;
   static FusedParams p;                               // large (two tensor maps); host-side scratch
@@ -1166,8 +1053,8 @@ cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Ge
   p.imp = importance;
   p.err = device_error_flag();
   p.trace = nullptr;
-  p.dbg = 0;
-  if (const char* dbg = std::getenv("SP_FUSED_DEBUG")) p.dbg = std::atoi(dbg);
+  p.mode = mode;
+  p.lse_in = lse_in;
   p.prefetch = kPrefetchTiles;
   if (const char* pf = std::getenv("SP_FUSED_PREFETCH")) p.prefetch = std::atoi(pf);
 
@@ -1202,6 +1089,30 @@ cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Ge
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                        float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
+  return fused_launch(Q, K, g, lay, kModeFull, nullptr, importance, ws, ws_bytes, st);
+}
+
+cudaError_t fused_score_stats(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                              float* stats, void* ws, size_t ws_bytes, cudaStream_t st) {
+  cudaError_t e = fused_launch(Q, K, g, lay, kModeStats, nullptr, nullptr, ws, ws_bytes, st);
+  if (e != cudaSuccess) return e;
+  Plan pl = make_plan(g);
+  const char* w = reinterpret_cast<const char*>(ws);
+  const unsigned* epoch = reinterpret_cast<const unsigned*>(w);
+  const unsigned long long* part = reinterpret_cast<const unsigned long long*>(w + pl.ws_cnt + pl.ws_fin);
+  const long long n = (long long)g.B * pl.U * pl.NC;
+  k_partials_to_stats<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, epoch, g.B, g.L, g.Hkv, g.G, g.Rv, pl.n_tg,
+                                                                   pl.NC, pl.NCP, stats);
+  return cudaGetLastError();
+}
+
+cudaError_t fused_score_finish(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                               const float* lse2, float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
+  return fused_launch(Q, K, g, lay, kModeFinish, lse2, importance, ws, ws_bytes, st);
 }
 
 }  // namespace sp

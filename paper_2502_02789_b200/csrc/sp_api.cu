@@ -3,6 +3,7 @@
 // Host-side argument validation, workspace carving and kernel dispatch.  No
 // exception crosses this boundary; every entry point returns an sp_status.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -198,9 +199,18 @@ sp_status sp_trace_enable(uint64_t* device_buffer, int64_t records) {
   return SP_OK;
 }
 
+// The split API runs the fused tensor-core kernel in its stats-only / finish-only
+// modes when the geometry is supported (SP_SPLIT_ALGO=simt forces the SIMT pair).
+bool split_fused(const Geom& g) {
+  const char* e = std::getenv("SP_SPLIT_ALGO");
+  if (e && std::strcmp(e, "simt") == 0) return false;
+  return fused_supported(g, Layout{}, nullptr, nullptr);
+}
+
 size_t sp_score_split_workspace_bytes(const sp_geom* g) {
   if (check_geom(g) != SP_OK) return 0;
   Geom G = to_geom(*g);
+  if (split_fused(G)) return fused_score_ws_bytes(G);
   size_t a = simt_split_ws_bytes(G);
   size_t b = align256((size_t)G.B * G.Rv * G.N * sizeof(unsigned));
   return a > b ? a : b;
@@ -214,8 +224,12 @@ sp_status sp_score_stats(const void* Q, const void* K, const sp_geom* g, const s
   if (stats == nullptr) return SP_EINVAL;
   if ((s = check_device()) != SP_OK) return s;
   if (ws == nullptr || ws_bytes < sp_score_split_workspace_bytes(g)) return SP_EWORKSPACE;
-  return from_cuda(simt_score_stats(reinterpret_cast<const __nv_bfloat16*>(Q), reinterpret_cast<const __nv_bfloat16*>(K),
-                                    to_geom(*g), to_layout(*lay), stats, ws, reinterpret_cast<cudaStream_t>(stream)));
+  const Geom G = to_geom(*g);
+  const auto* q = reinterpret_cast<const __nv_bfloat16*>(Q);
+  const auto* k = reinterpret_cast<const __nv_bfloat16*>(K);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (split_fused(G)) return from_cuda(fused_score_stats(q, k, G, to_layout(*lay), stats, ws, ws_bytes, st));
+  return from_cuda(simt_score_stats(q, k, G, to_layout(*lay), stats, ws, st));
 }
 
 sp_status sp_stats_combine(const float* parts, int32_t P, int64_t n_rows, float* lse2, sp_stream stream) {
@@ -233,9 +247,13 @@ sp_status sp_score_finish(const void* Q, const void* K, const sp_geom* g, const 
   if (lse2 == nullptr || importance == nullptr) return SP_EINVAL;
   if ((s = check_device()) != SP_OK) return s;
   if (ws == nullptr || ws_bytes < sp_score_split_workspace_bytes(g)) return SP_EWORKSPACE;
-  return from_cuda(simt_score_finish(reinterpret_cast<const __nv_bfloat16*>(Q),
-                                     reinterpret_cast<const __nv_bfloat16*>(K), to_geom(*g), to_layout(*lay), lse2,
-                                     importance, ws, reinterpret_cast<cudaStream_t>(stream)));
+  const Geom G = to_geom(*g);
+  const auto* q = reinterpret_cast<const __nv_bfloat16*>(Q);
+  const auto* k = reinterpret_cast<const __nv_bfloat16*>(K);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (split_fused(G))
+    return from_cuda(fused_score_finish(q, k, G, to_layout(*lay), lse2, importance, ws, ws_bytes, st));
+  return from_cuda(simt_score_finish(q, k, G, to_layout(*lay), lse2, importance, ws, st));
 }
 
 size_t sp_select_workspace_bytes(int32_t B, int64_t N, const sp_select_params* p) {

@@ -67,6 +67,10 @@ bool fused_plan_info(const Geom& g, long long out[9]);
 void fused_set_trace(unsigned long long* buf, long long records);
 cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                         float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t fused_score_stats(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                              float* stats, void* ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t fused_score_finish(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                               const float* lse2, float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
 
 // ---------------------------------------------------------------- select / gather (select.cu, gather.cu)
 size_t select_ws_bytes(int B, long long N, int chunk);

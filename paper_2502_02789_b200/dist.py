@@ -1,0 +1,84 @@
+"""Multi-GPU partitions of the hot path: one process per GPU,
+``torch.distributed`` (NCCL on GPUs, gloo in the CPU tests) for the plumbing.
+
+* Batch sharding -- requests are independent: rank p
+  scores and selects its own requests with the single-GPU kernels, no
+  collective on the data path.
+* Sequence sharding -- one request's prompt split along tokens.  The only real
+  exchange is the softmax statistics (the lse of every (layer, head, row) needs
+  all N keys):
+    1. local statistics (m2, l) per row            (sp_score_stats)
+    2. all-gather, merged in rank order -> lse2     (sp_stats_combine; identical on every rank)
+    3. local importance with the global lse2        (sp_score_finish)
+    4. all-gather of the importance shards (4 B/token) and the selection over
+       the whole prompt (sp_select_gather), so ids/positions are bit-identical
+       to the single-GPU path's for the same importance.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import api
+
+
+def batch_range(B: int, world: int, rank: int) -> tuple[int, int]:
+    """Requests [b0, b1) of rank `rank` (contiguous, sizes differ by at most 1)."""
+    return rank * B // world, (rank + 1) * B // world
+
+
+def token_range(N: int, world: int, rank: int, chunk: int = 1) -> tuple[int, int]:
+    """Prompt tokens [i0, i1) of rank `rank` for sequence sharding; N must be a
+    multiple of world (equal shards for the all-gathers)."""
+    if N % world:
+        raise ValueError(f"sequence sharding needs N ({N}) divisible by the number of ranks ({world})")
+    n = N // world
+    return rank * n, (rank + 1) * n
+
+
+class CudaBackend:
+    """The compute steps, all in libspecprefill.so kernels."""
+
+    @staticmethod
+    def score_stats(Q, K, R_valid, scale):
+        return api.score_stats(Q, K, R_valid, scale)
+
+    @staticmethod
+    def stats_combine(parts):
+        return api.stats_combine(parts)
+
+    @staticmethod
+    def score_finish(Q, K, lse2, R_valid, scale):
+        return api.score_finish(Q, K, lse2, R_valid, scale)
+
+    @staticmethod
+    def select(imp, keep, pool_k, chunk, pos0, tokens):
+        return api.select(imp, keep, pool_k, chunk, pos0, tokens=tokens)
+
+
+def seq_sharded_specprefill(Q, K_local, tokens, N_total: int, keep: float, pool_k: int, chunk: int,
+                            R_valid=None, scale=None, pos0: int = 0, group=None, backend=None) -> dict:
+    """Sequence-sharded path for one request (B = 1).  Q [1][L][R][H][d] is
+    replicated; K_local [1][L][Hkv][N_total/P][d] holds this rank's tokens
+    (rank order = token order); tokens [1][N_total] int32 replicated.
+    Returns importance [1][N_total], ids, pos, n_kept, out_tokens (replicated)."""
+    be = backend or CudaBackend
+    world = dist.get_world_size(group)
+    n_local = K_local.shape[3]
+    if n_local * world != N_total or Q.shape[0] != 1:
+        raise ValueError("K_local must hold N_total / world tokens of a single request")
+    stats = be.score_stats(Q, K_local, R_valid, scale)                       # [rows][2]
+    parts = torch.empty((world * stats.shape[0], 2), dtype=stats.dtype, device=stats.device)
+    dist.all_gather_into_tensor(parts, stats.contiguous(), group=group)      # concatenated in rank order
+    lse2 = be.stats_combine(parts.view(world, -1, 2))                        # [rows]
+    imp_local = be.score_finish(Q, K_local, lse2, R_valid, scale)            # [1][n_local]
+    imp = torch.empty((world * n_local,), dtype=imp_local.dtype, device=imp_local.device)
+    dist.all_gather_into_tensor(imp, imp_local.reshape(-1).contiguous(), group=group)
+    imp = imp.view(1, N_total)                                               # rank order = token order
+    ids, pos, n_kept, out = be.select(imp, keep, pool_k, chunk, pos0, tokens)
+    return dict(importance=imp, ids=ids, pos=pos, n_kept=n_kept, out_tokens=out, first_decode=N_total + pos0)
+
+
+def batch_sharded_specprefill(Q, K, tokens, keep, pool_k, chunk, R_valid=None, scale=None, pos0=0) -> dict:
+    """Batch sharding: the caller passes this rank's requests; no collective."""
+    return api.specprefill(Q, K, tokens, keep, pool_k, chunk, R_valid, scale, pos0)

@@ -260,3 +260,25 @@ def test_c4_keep_sweep():
     w = gen.CONFIGS["C4"]
     regimes = _full_config(w, "fused" if "fused" in ALGOS else "simt", [0], keeps=[i / 10.0 for i in range(1, 10)])
     assert len(regimes) == 9
+
+
+# ---------------------------------------------------------------- sequence-sharded split (virtual ranks)
+@pytest.mark.parametrize("split_algo", ["auto", "simt"])
+@pytest.mark.parametrize("P", [2, 4])
+def test_split_api_virtual_ranks(split_algo, P, monkeypatch):
+    """The sequence-sharded split (stats -> rank-order combine -> finish) run as P
+    virtual ranks on one GPU equals the oracle on the whole prompt, and the
+    selection over the gathered importance matches."""
+    monkeypatch.setenv("SP_SPLIT_ALGO", split_algo)
+    w = gen.CONFIGS["C1"].with_(N=4096, R_valid=6)
+    Q, K, T = spgen_cuda.make_inputs(w)
+    n = w.N // P
+    stats = [sp.score_stats(Q, K[:, :, :, p * n:(p + 1) * n], w.Rv, w.scale).clone() for p in range(P)]
+    lse2 = sp.stats_combine(torch.stack(stats).contiguous())
+    imp = torch.cat([sp.score_finish(Q, K[:, :, :, p * n:(p + 1) * n], lse2, w.Rv, w.scale) for p in range(P)], dim=1)
+    sp.check_device_error()
+    exact = _util.oracle_importance(w, 0)
+    assert _util.rel_err(imp[0].double().cpu().numpy(), exact) <= _util.REL_TOL
+    ids, pos, nk = sp.select(imp.contiguous(), w.keep, w.pool_k, w.chunk)
+    o = ref.select(exact, w.keep, w.pool_k, w.chunk)
+    _util.check_selection(ids[0].cpu().numpy(), pos[0].cpu().numpy(), int(nk[0]), o, w.chunk, w.N, 0)
