@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--config", default="C3", choices=["C0", "C1", "C2", "C3", "C4"])
     ap.add_argument("--algo", default="fused", choices=["fused", "simt", "auto"])
     ap.add_argument("--plan", default=None, help="fused-kernel decomposition override 'n_tg,n_ug'")
+    ap.add_argument("--shard", default="batch", choices=["batch", "seq"],
+                    help="N>1: batch = one request per rank, no collective (weak scaling); "
+                         "seq = the prompt split over ranks with the NCCL statistics exchange (strong scaling)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -190,9 +193,17 @@ def run_ours(args):
     w = workload(args.config)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
+    seq = world > 1 and args.shard == "seq"
+    if world > 1 and not seq:
+        w = w.with_(seed=w.seed + rank)              # batch sharding: each rank owns different requests
 
     # ---- inputs resident in HBM (device-side generator, bit-identical to spgen.gen)
-    Q, K, T = spgen_cuda.make_inputs(w, device=dev)
+    if seq:
+        from paper_2502_02789_b200 import dist as spd
+        i0, i1 = spd.token_range(w.N, world, rank)
+        Q, K, T = spgen_cuda.make_inputs(w, device=dev, i0=i0, n_local=i1 - i0)
+    else:
+        Q, K, T = spgen_cuda.make_inputs(w, device=dev)
     torch.cuda.synchronize()
     imp = torch.empty((w.B, w.N), dtype=torch.float32, device=dev)
     ids = torch.empty((w.B, w.N), dtype=torch.int32, device=dev)
@@ -210,6 +221,22 @@ def run_ours(args):
         score_only()
         select_only()
 
+    if seq:
+        def score_only():                              # noqa: F811 -- the sharded scoring (with its exchange)
+            nonlocal imp
+            st_ = sp.score_stats(Q, K, w.Rv, w.scale)
+            parts = torch.empty((world * st_.shape[0], 2), dtype=torch.float32, device=dev)
+            dist.all_gather_into_tensor(parts, st_)
+            lse2 = sp.stats_combine(parts.view(world, -1, 2))
+            loc = sp.score_finish(Q, K, lse2, w.Rv, w.scale)
+            full = torch.empty((world * loc.shape[1],), dtype=torch.float32, device=dev)
+            dist.all_gather_into_tensor(full, loc.reshape(-1))
+            imp = full.view(1, w.N)
+
+        def step():                                    # noqa: F811
+            score_only()
+            select_only()
+
     for _ in range(args.warmup):
         step()
     sp.check_device_error()
@@ -218,7 +245,7 @@ def run_ours(args):
     # roofline): replays cost one graph launch, no host work per kernel
     graph_note = "eager"
     run_step, run_score = step, score_only
-    if not args.no_graph:
+    if not args.no_graph and not seq:
         try:
             g_step, g_score = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
             with torch.cuda.graph(g_step):
@@ -269,13 +296,13 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_total, score_ms = tt.tolist()
     ms_step = ms_total / args.steps
-    tokens_per_step = w.B * w.N * world
+    tokens_per_step = w.B * w.N * (1 if seq else world)
     value = tokens_per_step / (ms_step / 1000.0)
 
     # ---- roofline of the dominant kernel (sp_score): algorithmic bytes / duration
     peak, peak_src = peaks()
     q_bytes = w.B * w.L * w.Rv * w.H * w.d * 2
-    alg_bytes = w.k_bytes + q_bytes + w.B * w.N * 4
+    alg_bytes = (w.k_bytes // world if seq else w.k_bytes) + q_bytes + w.B * w.N * 4
     achieved = alg_bytes / (score_ms / 1000.0) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -296,10 +323,13 @@ def run_ours(args):
     plan = sp.score_plan(Q, K, w.Rv) if args.algo != "simt" else None
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong" if seq else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{args.config} {w.name}", "B": w.B, "N": w.N, "L": w.L, "H": w.H, "Hkv": w.Hkv,
                        "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk,
-                       "algo": args.algo, "plan": plan, "launch": graph_note, "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "algo": args.algo, "plan": plan, "launch": graph_note, "shard": args.shard if world > 1 else None,
+                       "parallelism": (f"seq{world} (prompt split, NCCL stats all-gather)" if seq else
+                                       f"dp{world} (batch-sharded: one request per rank, no collective)")
+                       if world > 1 else "single",
                        "l2": f"inputs larger than L2 (K = {w.k_bytes / 2**30:.2f} GiB per GPU), no flush"},
             "roofline": roofline, "clocks": clk, "e2e": e2e, "gpu_launches": launches_per_step * args.steps}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

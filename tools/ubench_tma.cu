@@ -16,7 +16,7 @@ __device__ __forceinline__ void wait(uint32_t bar, uint32_t par) {
 }
 
 __global__ void __launch_bounds__(64, 1) k(const __grid_constant__ CUtensorMap map, const uint8_t* src, long long tiles_per_cta,
-                                           int stages, int mode) {
+                                           int stages, int mode, int reread) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* buf = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(buf + stages * 32768);
@@ -29,7 +29,11 @@ __global__ void __launch_bounds__(64, 1) k(const __grid_constant__ CUtensorMap m
   const long long t0 = blockIdx.x * tiles_per_cta;
   if (warp == 0 && threadIdx.x == 0) {
     int st = 0; uint32_t ph = 0;
-    for (long long t = 0; t < tiles_per_cta; ++t) {
+    const long long total = reread > 0 ? 2 * tiles_per_cta : tiles_per_cta;
+    for (long long it = 0; it < total; ++it) {
+      // reread > 0: every other load re-reads the tile `reread` tiles back (L2 hit if still resident)
+      long long t = reread > 0 ? it / 2 : it;
+      if (reread > 0 && (it & 1)) t = t - reread < 0 ? t : t - reread;
       wait(smem_u32(bars + stages + st), ph ^ 1);
       const uint32_t full = smem_u32(bars + st);
       expect_tx(full, 32768);
@@ -47,7 +51,8 @@ __global__ void __launch_bounds__(64, 1) k(const __grid_constant__ CUtensorMap m
     }
   } else if (warp == 1 && threadIdx.x == 32) {
     int st = 0; uint32_t ph = 0;
-    for (long long t = 0; t < tiles_per_cta; ++t) {
+    const long long total = reread > 0 ? 2 * tiles_per_cta : tiles_per_cta;
+    for (long long t = 0; t < total; ++t) {
       wait(smem_u32(bars + st), ph);
       arrive(smem_u32(bars + stages + st));
       if (++st == stages) { st = 0; ph ^= 1; }
@@ -68,27 +73,29 @@ int main() {
   CUtensorMap map;
   cuuint64_t dims[2] = {128, (cuuint64_t)rows}, strides[1] = {256};
   cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
-  for (int prom = 0; prom < 3; ++prom) {
+  for (int prom = 0; prom < 1; ++prom) {
     CUtensorMapL2promotion pr = prom == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : prom == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     ((Enc)fp)(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_128B, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    for (int mode = 0; mode < 2; ++mode) {
-      if (mode == 1 && prom > 0) continue;
-      for (int stages : {2, 4, 6}) {
+    for (int reread : {0, 8, 32, 64}) {
+    for (int mode = 0; mode < 1; ++mode) {
+      for (int stages : {4, 6}) {
         const int ctas = 148;
         const long long tpc = rows / 128 / ctas;
         size_t smem = stages * 32768 + 2048;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-        k<<<ctas, 64, smem>>>(map, d, tpc, stages, mode);
+        k<<<ctas, 64, smem>>>(map, d, tpc, stages, mode, reread);
         cudaEventRecord(a);
-        for (int r = 0; r < 5; ++r) k<<<ctas, 64, smem>>>(map, d, tpc, stages, mode);
+        for (int r = 0; r < 5; ++r) k<<<ctas, 64, smem>>>(map, d, tpc, stages, mode, reread);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b);
         double gbs = 5.0 * tpc * ctas * 32768 / (ms / 1000.0) / 1e9;
-        printf("mode %d prom %d stages %d: %.0f GB/s\n", mode, prom, stages, gbs);
+        printf("reread %d stages %d: HBM-equivalent %.0f GB/s (SMEM fill %.0f GB/s)\n", reread, stages, gbs,
+               gbs * (reread > 0 ? 2 : 1));
       }
+    }
     }
   }
   cudaError_t e = cudaGetLastError();
