@@ -50,7 +50,6 @@ constexpr int kMaxStages = 8;
 constexpr int kMaxChunks = 8;          // NCP <= 128 columns (16-column chunks)
 constexpr int kMaxSlots = 16;          // TMEM tile slots (512 columns / 32)
 constexpr int kLseRing = 8;            // lse2 buffers in SMEM (gather may run ahead of aggregation)
-constexpr int kPrefetchTiles = 0;      // L2 prefetch distance beyond the SMEM ring (tiles); measured: hurts
 constexpr int kMaxLseBatch = 20;       // 64-bit partial words in flight per lane
 constexpr int kTmemCols = 512;
 constexpr int kSmemLimit = 232448;     // sm_100 max dynamic shared memory per block
@@ -80,9 +79,10 @@ struct FusedParams {
   int* err;
   unsigned long long* trace;           // optional [grid][trace_units][8] globaltimer stamps (debug)
   int trace_units;
+  unsigned long long* tile_trace;      // optional [1000][8] per-tile MMA stamps of CTA 0 (debug)
   int mode;                            // kModeFull / kModeStats (publish partials only) / kModeFinish (lse2 given)
   const float* lse_in;                 // kModeFinish: lse2 per row ((b*L + l)*H + h)*Rv + r
-  int prefetch;                        // L2 prefetch distance in tiles beyond the SMEM ring (0 = off)
+  int debug_local;                     // timing experiment only: lse2 from the CTA's own partial (wrong results)
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -92,8 +92,15 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
+// The TMA / MMA helpers below are called by a whole (converged) warp and issue
+// from one elected lane: the loop state stays warp-uniform, so descriptors and
+// coordinates live in uniform registers (no per-instruction R2UR + elect loop).
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bar),
+      "r"(bytes)
+      : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -118,8 +125,7 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // backs off with __nanosleep so that idle waiters (up to half the CTA's warps at
 // any time) do not steal issue slots from the epilogue warps on their SMSP.
 // Bounded: a pipeline that never completes (a bug) traps after ~4 s.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  if (mbar_try_wait(bar, parity)) return;
+__device__ __noinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity) {
   uint64_t t0 = 0;
   for (uint32_t i = 1;; ++i) {
     if (mbar_try_wait(bar, parity)) return;
@@ -131,19 +137,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
   }
 }
+// Fast path inline (one try_wait); the back-off loop is out of line to keep
+// the warp roles' hot code small (they share the SM's instruction cache).
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity);
+}
 __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2,
                                             int c3, int c4) {
   asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];\n\t}" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
-}
-__device__ __forceinline__ void tma_prefetch_l2_5d(const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4) {
-  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global [%0, {%1, %2, %3, %4, %5}];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-               : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -162,14 +168,18 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t sbo_byte
 }
 __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+      : "memory");
 }
 __device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -242,6 +252,19 @@ __device__ __forceinline__ void trace_stamp(const FusedParams& p, uint32_t ui, i
 }
 
 
+// Debug wait accounting (trace mode only): mbar_wait plus the time it took.
+__device__ __forceinline__ void mbar_wait_acc(const FusedParams& p, uint32_t bar, uint32_t parity,
+                                              unsigned long long& acc) {
+  if (p.trace == nullptr) { mbar_wait(bar, parity); return; }
+  const long long t0 = clock64();
+  mbar_wait(bar, parity);
+  acc += clock64() - t0;
+}
+__device__ __forceinline__ void trace_waits(const FusedParams& p, int k, unsigned long long v) {
+  if (p.trace != nullptr && p.trace_units > 1)
+    p.trace[((size_t)blockIdx.x * p.trace_units + p.trace_units - 1) * 8 + k] = v;
+}
+
 // Fold one tile's 32 logit columns (group grp) into the running (l,h)-max of
 // this thread's token: acc[(t*Rv + r)*128 + tok] = max(acc, max_h (x*xs - lse2)).
 // Columns are r-major (c = r*G + h).  kG > 0: compile-time group size dividing 32.
@@ -290,7 +313,9 @@ __device__ __forceinline__ void fold_tile(const float (&x)[kW], const float (&lv
 struct Job {
   int b, tg, ug, t_lo, t_hi, u_lo, u_hi;
 };
-__device__ __forceinline__ Job decode_job(const FusedParams& p, long long job) {
+// Out of line: called once per job by every role; its 64-bit divisions would
+// otherwise be inlined into each role's code.
+__device__ __noinline__ Job decode_job(const FusedParams& p, long long job) {
   Job j;
   j.b = (int)(job / p.J);
   const int r = (int)(job % p.J);
@@ -301,32 +326,6 @@ __device__ __forceinline__ Job decode_job(const FusedParams& p, long long job) {
   j.u_lo = (int)((long long)j.ug * p.U / p.n_ug);
   j.u_hi = (int)((long long)(j.ug + 1) * p.U / p.n_ug);
   return j;
-}
-
-// Walks a CTA's (job, unit, tile) sequence -- the order every role uses.
-struct TileCursor {
-  long long job;
-  Job jb;
-  int u, t;
-};
-__device__ __forceinline__ bool cursor_begin(const FusedParams& p, TileCursor& c) {
-  c.job = blockIdx.x;
-  if (c.job >= p.total_jobs) return false;
-  c.jb = decode_job(p, c.job);
-  c.u = c.jb.u_lo;
-  c.t = c.jb.t_lo;
-  return true;
-}
-__device__ __forceinline__ bool cursor_next(const FusedParams& p, TileCursor& c) {
-  if (++c.t < c.jb.t_hi) return true;
-  c.t = c.jb.t_lo;
-  if (++c.u < c.jb.u_hi) return true;
-  c.job += gridDim.x;
-  if (c.job >= p.total_jobs) return false;
-  c.jb = decode_job(p, c.job);
-  c.u = c.jb.u_lo;
-  c.t = c.jb.t_lo;
-  return true;
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -366,7 +365,9 @@ template <int kG>
 __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ FusedParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index broadcast from lane 0: provably warp-uniform, so each role's
+  // loop state (descriptors, coordinates, phases) lives in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
   // barrier map: full[S] empty[S] qfull[2] qempty[2] tfull[kMaxSlots] tempty[kMaxSlots]
@@ -425,51 +426,47 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
 
   if (warp == 0) {
     // ================================================================ TMA producer
-    if (lane == 0) {
+    // (whole warp, warp-uniform loop; the helpers issue from one elected lane)
+    {
       uint32_t stage = 0, sphase = 0, ui = 0;
-      // L2 prefetch runs kPrefetchTiles ahead of the SMEM loads: HBM latency under
-      // full load is several us, longer than the SMEM ring alone can cover
-      TileCursor pf;
-      bool pf_ok = cursor_begin(p, pf);
-      auto prefetch_one = [&]() {
-        if (!pf_ok) return;
-        const int pl_ = pf.u / p.Hkv, pg = pf.u % p.Hkv;
-        for (int kb = 0; kb < p.nkb; ++kb) tma_prefetch_l2_5d(&p.tmK, kb * p.W, pf.t * kTileM, pg, pl_, pf.jb.b);
-        pf_ok = cursor_next(p, pf);
-      };
-      if (p.prefetch == 0) pf_ok = false;
-      for (int i = 0; i < p.prefetch + p.stages; ++i) prefetch_one();
+      unsigned long long w_empty = 0, w_q = 0;
       for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
         const Job jb = decode_job(p, job);
         for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
           const int l = u / p.Hkv, g = u % p.Hkv;
           const uint32_t qs = ui & 1, qpar = (ui >> 1) & 1;
-          mbar_wait(bar_qempty + 8 * qs, qpar ^ 1);
+          mbar_wait_acc(p, bar_qempty + 8 * qs, qpar ^ 1, w_q);
           trace_stamp(p, ui, 0);
           mbar_expect_tx(bar_qfull + 8 * qs, (uint32_t)(p.NC * p.d * 2));
           const uint32_t qdst = smem_u32(smem + p.off_q + qs * p.q_slot_bytes);
+          #pragma unroll 1
           for (int kb = 0; kb < p.nkb; ++kb)
             tma_load_5d(qdst + kb * (p.NCP * p.W * 2), &p.tmQ, bar_qfull + 8 * qs, kb * p.W, g * p.G, 0, l, jb.b);
           for (int t = jb.t_lo; t < jb.t_hi; ++t) {
-            mbar_wait(bar_empty + 8 * stage, sphase ^ 1);
+            mbar_wait_acc(p, bar_empty + 8 * stage, sphase ^ 1, w_empty);
             mbar_expect_tx(bar_full + 8 * stage, p.k_stage_bytes);
             const uint32_t kdst = smem_u32(smem + p.off_k + stage * p.k_stage_bytes);
+            #pragma unroll 1
             for (int kb = 0; kb < p.nkb; ++kb)
               tma_load_5d(kdst + kb * (kTileM * p.W * 2), &p.tmK, bar_full + 8 * stage, kb * p.W, t * kTileM, g, l,
                           jb.b);
-            prefetch_one();
             if (++stage == (uint32_t)p.stages) { stage = 0; sphase ^= 1; }
           }
         }
       }
+      trace_waits(p, 0, w_empty);
+      trace_waits(p, 1, w_q);
     }
   } else if (warp == 1) {
     // ================================================================ MMA issuer
     // Each tile's logits D[128 x NCP] go to the next slot of a ring of nslots
     // TMEM tile slots; a slot is released by the aggregation warps once they
     // have folded that tile (tile-granular reuse hides the exchange latency).
-    if (lane == 0) {
+    // Whole warp, warp-uniform loop; umma_* issue from one elected lane.
+    {
       uint32_t stage = 0, sphase = 0, ui = 0, gt = 0, gslot = 0, gph = 0;
+      unsigned long long w_qf = 0, w_slot = 0, w_full = 0, w_issue = 0;
+      const long long t_start = clock64();
       // UMMA smem descriptors: the high word (SBO, version, swizzle) is constant;
       // the low word is (address >> 4) | LBO and a K step just adds to it.
       const uint32_t desc_hi = (uint32_t)(make_sdesc(0, 8 * p.W * 2, p.layout_type) >> 32);
@@ -479,20 +476,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const Job jb = decode_job(p, job);
         for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
           const uint32_t qs = ui & 1, qpar = (ui >> 1) & 1;
-          mbar_wait(bar_qfull + 8 * qs, qpar);
+          mbar_wait_acc(p, bar_qfull + 8 * qs, qpar, w_qf);
           const uint32_t b_lo0 = ((smem_u32(smem + p.off_q + qs * p.q_slot_bytes) >> 4) & 0x3FFFu) | (1u << 16);
           for (int t = jb.t_lo; t < jb.t_hi; ++t, ++gt) {
             const uint32_t slot = gslot;
-            mbar_wait(bar_tempty + 8 * slot, gph ^ 1);
+            unsigned long long* tt = (p.tile_trace != nullptr && blockIdx.x == 0 && gt < 1000)
+                                         ? p.tile_trace + gt * 8 : nullptr;
+            if (tt && lane == 0) { tt[0] = clock64(); tt[4] = globaltimer_ns(); }
+            mbar_wait_acc(p, bar_tempty + 8 * slot, gph ^ 1, w_slot);
+            if (tt && lane == 0) tt[1] = clock64();
             if (++gslot == nslots) { gslot = 0; gph ^= 1; }
             if (t == jb.t_lo) trace_stamp(p, ui, 1);
-            mbar_wait(bar_full + 8 * stage, sphase);
+            mbar_wait_acc(p, bar_full + 8 * stage, sphase, w_full);
+            if (tt && lane == 0) tt[2] = clock64();
             tc_fence_after();
             const uint32_t a_lo0 = ((smem_u32(smem + p.off_k + stage * p.k_stage_bytes) >> 4) & 0x3FFFu) | (1u << 16);
             const uint32_t dcol = tmem + slot * p.NCP;
+            const long long ti0 = clock64();
             uint32_t accum = 0;
+            #pragma unroll 1
             for (int kb = 0; kb < p.nkb; ++kb) {
               uint32_t a_lo = a_lo0 + kb * a_kb, b_lo = b_lo0 + kb * b_kb;
+              #pragma unroll 4
               for (int ks = 0; ks < ksteps; ++ks, a_lo += 2, b_lo += 2) {
                 umma_bf16(dcol, ((uint64_t)desc_hi << 32) | a_lo, ((uint64_t)desc_hi << 32) | b_lo, p.idesc, accum);
                 accum = 1;
@@ -500,11 +505,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             }
             umma_commit(bar_empty + 8 * stage);
             umma_commit(bar_tfull + 8 * slot);
+            if (p.trace != nullptr) w_issue += clock64() - ti0;
+            if (tt && lane == 0) { tt[3] = clock64(); tt[5] = globaltimer_ns(); }
             if (++stage == (uint32_t)p.stages) { stage = 0; sphase ^= 1; }
           }
           umma_commit(bar_qempty + 8 * qs);
         }
       }
+      trace_waits(p, 2, w_qf);
+      trace_waits(p, 3, w_slot);
+      trace_waits(p, 4, w_full);
+      trace_waits(p, 5, clock64() - t_start);
+      trace_waits(p, 6, w_issue);
     }
   } else if (warp >= kStatsWarp0 && warp < kFinalWarp0 && p.mode != kModeFinish) {
     // ================================================================ softmax statistics
@@ -545,16 +557,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             tie16(*reinterpret_cast<float(*)[16]>(x0));
             tie16(*reinterpret_cast<float(*)[16]>(x0 + 16));
             if (tok0 + (long long)(t - jb.t_lo) * kTileM < p.N) {
+              if (t == jb.t_lo) {
+                // first tile: the reference is the first value, sum = 2^0
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                // one exp2 either way: first value (ref = -inf) or a jump > 2^64
-                // re-bases the sum on y, otherwise accumulate 2^(y - ref)
-                const float y = x[i] * p.xs;
-                const float dlt = y - ref[i];
-                const bool big = dlt > 64.f;
-                const float e = ex2(big ? -dlt : dlt);
-                sum[i] = big ? fmaf(sum[i], e, 1.f) : sum[i] + e;
-                ref[i] = big ? y : ref[i];
+                for (int i = 0; i < 32; ++i) { ref[i] = x[i] * p.xs; sum[i] = 1.f; }
+              } else {
+                // d = y - ref; the common case adds 2^d (FFMA, MUFU, FADD + a max);
+                // a jump d > 64 (rare) re-bases that column on y to keep fp32 finite
+                float dmax = -CUDART_INF_F;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  x[i] = fmaf(x[i], p.xs, -ref[i]);
+                  dmax = fmaxf(dmax, x[i]);
+                }
+                if (dmax <= 64.f) {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) sum[i] += ex2(x[i]);
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) {
+                    const bool big = x[i] > 64.f;
+                    const float e = ex2(big ? -x[i] : x[i]);
+                    sum[i] = big ? fmaf(sum[i], e, 1.f) : sum[i] + e;
+                    ref[i] = big ? ref[i] + x[i] : ref[i];
+                  }
+                }
               }
             }
             if (++slot == nslots) { slot = 0; ph ^= 1; }
@@ -620,7 +647,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const long long ubase = (long long)jb.b * p.U + u;
         mbar_wait(bar_lempty + 8 * par, ((ui / kLseRing) & 1) ^ 1);    // aggregation done with ls[par]
         float* ls = lse_s + par * p.NCP;
-        const unsigned long long* src = part_cur + ubase * p.n_tg * p.NCP;
+        const unsigned long long* src = part_cur + ubase * p.n_tg * p.NCP + (p.debug_local ? jb.tg * p.NCP : 0);
+        const int ntg = p.debug_local ? 1 : p.n_tg;
         for (int c = lane; c < p.NCP && p.mode == kModeFinish; c += 32) {
           // lse2 supplied by the caller (sequence-sharded split: globally combined statistics)
           float l2 = 0.f;
@@ -632,12 +660,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         }
         for (int c = lane; c < p.NCP && p.mode == kModeFull; c += 32) {
           float M = -CUDART_INF_F, S = 0.f;
-          for (int s0 = 0; s0 < p.n_tg; s0 += kMaxLseBatch) {
+          for (int s0 = 0; s0 < ntg; s0 += kMaxLseBatch) {
             unsigned long long v[kMaxLseBatch];
             uint32_t missing = 0;
 #pragma unroll
             for (int j = 0; j < kMaxLseBatch; ++j) {
-              v[j] = (s0 + j < p.n_tg) ? ld_relaxed_u64(src + (long long)(s0 + j) * p.NCP + c) : pack_ms(0.f, -1.f);
+              v[j] = (s0 + j < ntg) ? ld_relaxed_u64(src + (long long)(s0 + j) * p.NCP + c) : pack_ms(0.f, -1.f);
               missing |= (v[j] == 0ull ? 1u : 0u) << j;
             }
             long long it = 0;
@@ -1055,15 +1083,16 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   p.trace = nullptr;
   p.mode = mode;
   p.lse_in = lse_in;
-  p.prefetch = kPrefetchTiles;
-  if (const char* pf = std::getenv("SP_FUSED_PREFETCH")) p.prefetch = std::atoi(pf);
+  p.debug_local = std::getenv("SP_FUSED_DEBUG_LOCAL") != nullptr;
 
   p.trace_units = 0;
   if (g_trace != nullptr) {
     const long long grid = std::min<long long>(pl.P, pl.total_jobs);
-    const long long units = (g_trace_records / 8) / grid;
+    const long long tail = g_trace_records > 16000 ? 8000 : 0;   // per-tile stamps of CTA 0 at the end
+    const long long units = ((g_trace_records - tail) / 8) / grid;
     if (units > 0) {
       p.trace = g_trace;
+      p.tile_trace = tail ? g_trace + g_trace_records - tail : nullptr;
       p.trace_units = (int)std::min<long long>(units, 1 << 30);
     }
   }

@@ -34,20 +34,38 @@ def main():
     plan = sp.score_plan(Q, K, w.Rv)
     grid, upj = plan["grid"], plan["units_per_job"]
     units = upj * ((w.B * plan["jobs_per_request"] + grid - 1) // grid)
-    buf = torch.zeros(grid * units * 8, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(grid * (units + 1) * 8 + 1000 * 8, dtype=torch.int64, device="cuda")   # +1: wait accounting; CTA 0 tiles
     for _ in range(3):
         sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")
     sp.lib().sp_trace_enable(buf.data_ptr(), buf.numel())
     sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")
     torch.cuda.synchronize()
     sp.lib().sp_trace_enable(None, 0)
-    tr = buf.view(grid, units, 8).cpu().numpy().astype(np.float64)
+    tt = buf[grid * (units + 1) * 8:].view(1000, 8).cpu().numpy().astype(np.float64)
+    full = buf[:grid * (units + 1) * 8].view(grid, units + 1, 8).cpu().numpy().astype(np.float64)
+    waits = full[:, units, :7] / 1965.0                          # SM cycles -> us (1965 MHz)
+    tr = full[:, :units, :]
     t0 = tr[tr > 0].min()
     tr = np.where(tr > 0, (tr - t0) / 1000.0, np.nan)            # microseconds from the first stamp
     if a.out:
         np.save(a.out, tr)
     print("plan", plan, "units/CTA", units)
+    n = int((tt[:, 3] > 0).sum())
+    if n > 1:
+        t = tt[:n, :4] - tt[0, 0]
+        print("CTA 0 MMA per tile (cycles): wait slot / wait full / issue ; period")
+        for i in list(range(0, 24)) + list(range(n // 2, n // 2 + 16)):
+            if i < n:
+                print("  tile %4d  slot %6.0f  full %6.0f  issue %6.0f  period %6.0f" % (
+                    i, t[i, 1] - t[i, 0], t[i, 2] - t[i, 1], t[i, 3] - t[i, 2], (t[i, 0] - t[i - 1, 0]) if i else 0))
+        print("  globaltimer ns per tile (period): %.1f ; issue ns mean %.1f" % (np.mean(np.diff(tt[:n, 4])), np.mean(tt[:n, 5] - tt[:n, 4])))
+        print("  mean: slot %.0f full %.0f issue %.0f period %.0f" % (np.mean(t[:, 1] - t[:, 0]), np.mean(t[:, 2] - t[:, 1]),
+              np.mean(t[:, 3] - t[:, 2]), np.mean(np.diff(t[:, 0]))))
     print("kernel span (us) %.1f" % np.nanmax(tr))
+    wn = ["prod wait empty", "prod wait qempty", "mma wait qfull", "mma wait tmem slot", "mma wait tma full",
+          "mma span", "mma issue+commit"]
+    for k, nm in enumerate(wn):
+        print(f"{nm:>20}: mean {waits[:, k].mean():8.1f} us  min {waits[:, k].min():8.1f}  max {waits[:, k].max():8.1f}")
     names = ["prod", "mma", "stats", "publ", "cleanup", "lseready", "aggdone", "statsend"]
     for (x, y) in [(1, 2), (2, 7), (7, 3), (3, 5), (5, 6), (1, 6), (0, 1)]:
         d = tr[:, :, y] - tr[:, :, x]

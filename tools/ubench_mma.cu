@@ -14,15 +14,18 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   d |= (uint64_t)2 << 61;
   return d;
 }
-__global__ void __launch_bounds__(128, 1) k(int iters, int N, unsigned long long* out) {
+__global__ void __launch_bounds__(128, 1) k(int iters, int N, unsigned long long* out, int mode) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* buf = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
   __shared__ uint32_t tbase;
   __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t cbar[2];
   const int warp = threadIdx.x / 32;
   for (int i = threadIdx.x; i < 65536 / 4; i += 128) ((uint32_t*)buf)[i] = 0x3c003c00u;
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&cbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&cbar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("fence.proxy.async.shared::cta;");
@@ -46,6 +49,15 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int N, unsigned long long
           asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}"
                        ::"r"(tm + (uint32_t)((it % (512 / N)) * N)), "l"(a), "l"(b), "r"(idesc), "r"(acc));
         }
+      if (mode >= 1) {
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&cbar[0])));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&cbar[1])));
+      }
+      if (mode >= 2) asm volatile("tcgen05.fence::after_thread_sync;");
+      if (mode >= 3) {   // wait for this tile's MMAs to finish (serialised tiles)
+        const uint32_t par = it & 1;
+        asm volatile("{\n.reg .pred p;\nW%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W%=;\n}" ::"r"(smem_u32(&cbar[0])), "r"(par));
+      }
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
     asm volatile("{\n.reg .pred p;\nW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W;\n}" ::"r"(smem_u32(&bar)));
@@ -60,13 +72,14 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int N, unsigned long long
 int main() {
   unsigned long long* d; cudaMalloc(&d, 8);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
-  for (int N : {16, 32, 64, 128, 256}) {
+  for (int mode = 0; mode < 4; ++mode)
+  for (int N : {32, 64}) {
     const int iters = 2000;
-    k<<<148, 128, 100000>>>(iters, N, d);
+    k<<<148, 128, 100000>>>(iters, N, d, mode);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("N %d err %s\n", N, cudaGetErrorString(e)); return 1; }
     unsigned long long h; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-    printf("N %3d: %.1f cycles per MMA (M=128,K=16), %.1f cycles per 128x%dx128 tile\n", N, (double)h / (iters * 8), (double)h / iters, N);
+    printf("mode %d N %3d: %.1f cycles per MMA (M=128,K=16), %.1f cycles per 128x%dx128 tile\n", mode, N, (double)h / (iters * 8), (double)h / iters, N);
   }
   return 0;
 }
