@@ -116,6 +116,18 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Non-blocking probe of an mbarrier phase (no suspend): the cheap fast path.
+__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -140,7 +152,7 @@ __device__ __noinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity) {
 // Fast path inline (one try_wait); the back-off loop is out of line to keep
 // the warp roles' hot code small (they share the SM's instruction cache).
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity);
+  if (!mbar_test_wait(bar, parity)) mbar_wait_slow(bar, parity);
 }
 __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2,
                                             int c3, int c4) {
@@ -174,6 +186,18 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t 
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
+}
+// One tile's K steps (KS = d/16) with compile-time descriptor offsets; KSTEPS
+// K16 steps per swizzle block (W = 16*KSTEPS elements).
+template <int KS, int KSTEPS>
+__device__ __forceinline__ void issue_tile(uint32_t dcol, uint32_t a_lo0, uint32_t b_lo0, uint32_t desc_hi,
+                                           uint32_t b_kb, uint32_t idesc) {
+#pragma unroll
+  for (int j = 0; j < KS; ++j) {
+    const uint32_t kb = j / KSTEPS, ks = j % KSTEPS;
+    umma_bf16(dcol, ((uint64_t)desc_hi << 32) | (a_lo0 + kb * (256u * KSTEPS) + ks * 2u),
+              ((uint64_t)desc_hi << 32) | (b_lo0 + kb * b_kb + ks * 2u), idesc, j > 0 ? 1u : 0u);
+  }
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile(
@@ -493,14 +517,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             const uint32_t a_lo0 = ((smem_u32(smem + p.off_k + stage * p.k_stage_bytes) >> 4) & 0x3FFFu) | (1u << 16);
             const uint32_t dcol = tmem + slot * p.NCP;
             const long long ti0 = clock64();
-            uint32_t accum = 0;
-            #pragma unroll 1
-            for (int kb = 0; kb < p.nkb; ++kb) {
-              uint32_t a_lo = a_lo0 + kb * a_kb, b_lo = b_lo0 + kb * b_kb;
-              #pragma unroll 4
-              for (int ks = 0; ks < ksteps; ++ks, a_lo += 2, b_lo += 2) {
-                umma_bf16(dcol, ((uint64_t)desc_hi << 32) | a_lo, ((uint64_t)desc_hi << 32) | b_lo, p.idesc, accum);
-                accum = 1;
+            // straight-line issue for the common head dims (d = 64, 128, 256 with
+            // 64-element swizzle blocks): the descriptor arithmetic pipelines
+            // across the MMAs (a loop back-edge halves the issue rate)
+            if (ksteps == 4 && p.nkb == 2) {
+              issue_tile<8, 4>(dcol, a_lo0, b_lo0, desc_hi, b_kb, p.idesc);
+            } else if (ksteps == 4 && p.nkb == 1) {
+              issue_tile<4, 4>(dcol, a_lo0, b_lo0, desc_hi, b_kb, p.idesc);
+            } else if (ksteps == 4 && p.nkb == 4) {
+              issue_tile<16, 4>(dcol, a_lo0, b_lo0, desc_hi, b_kb, p.idesc);
+            } else {
+              uint32_t accum = 0;
+#pragma unroll 1
+              for (int kb = 0; kb < p.nkb; ++kb) {
+                uint32_t a_lo = a_lo0 + kb * a_kb, b_lo = b_lo0 + kb * b_kb;
+#pragma unroll 1
+                for (int ks = 0; ks < ksteps; ++ks, a_lo += 2, b_lo += 2) {
+                  umma_bf16(dcol, ((uint64_t)desc_hi << 32) | a_lo, ((uint64_t)desc_hi << 32) | b_lo, p.idesc, accum);
+                  accum = 1;
+                }
               }
             }
             umma_commit(bar_empty + 8 * stage);

@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int N, int mode, unsigned
   uint8_t* buf = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
   __shared__ uint32_t tbase;
   __shared__ __align__(8) uint64_t bar;
-  const int warp = threadIdx.x / 32;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 65536 / 4; i += 128) ((uint32_t*)buf)[i] = 0x3c003c00u;
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
@@ -59,6 +59,37 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int N, int mode, unsigned
         for (int ks = 0; ks < 4; ++ks)
           mma_warp(tm + (uint32_t)((it % (512 / N)) * N), sdesc(a0 + kb * 16384 + ks * 32),
                    sdesc(b0 + kb * N * 128 + ks * 32), idesc, (kb | ks) != 0);
+  } else if (mode >= 3 && warp == 0) {
+    // per-tile overheads of the real MMA loop: 3 = + two commits, 4 = + fence::after_thread_sync,
+    // 5 = + two test_waits of completed barriers, 6 = + commit only every 4th tile
+    __shared__ __align__(8) uint64_t cb[2];
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&cb[0])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&cb[1])));
+    }
+    __syncwarp();
+    const uint32_t alo = ((a0 >> 4) & 0x3FFF) | (1u << 16), blo = ((b0 >> 4) & 0x3FFF) | (1u << 16);
+    for (int it = 0; it < iters; ++it) {
+      if (mode >= 5) {
+        uint32_t ok;
+        asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.b32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(&bar)), "r"(1u) : "memory");
+        if (!ok) asm volatile("trap;");
+        asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.b32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(&bar)), "r"(1u) : "memory");
+        if (!ok) asm volatile("trap;");
+      }
+      if (mode >= 4) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t d = tm + (uint32_t)((it % (512 / N)) * N);
+#pragma unroll 1
+      for (int kb = 0; kb < 2; ++kb)
+#pragma unroll 4
+        for (int ks = 0; ks < 4; ++ks)
+          mma_warp(d, ((uint64_t)desc_hi << 32) | (alo + kb * 1024 + ks * 2),
+                   ((uint64_t)desc_hi << 32) | (blo + kb * N * 8 + ks * 2), idesc, (kb | ks) != 0);
+      if (mode != 6 || (it & 3) == 3) {
+        asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(smem_u32(&cb[0])));
+        asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(smem_u32(&cb[1])));
+      }
+    }
   } else if (mode == 2 && warp == 0) {
     // precomputed low words, 64-bit descriptors built by adding to the low word
     const uint32_t alo = ((a0 >> 4) & 0x3FFF) | (1u << 16), blo = ((b0 >> 4) & 0x3FFF) | (1u << 16);
@@ -86,8 +117,8 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int N, int mode, unsigned
 int main() {
   unsigned long long* d; cudaMalloc(&d, 8);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
-  for (int mode = 0; mode < 3; ++mode)
-    for (int N : {32, 64, 128}) {
+  for (int mode = 0; mode < 7; ++mode)
+    for (int N : {32}) {
       const int iters = 4000;
       k<<<148, 128, 100000>>>(iters, N, mode, d);
       cudaError_t e = cudaDeviceSynchronize();
