@@ -10,6 +10,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libspecprefill.so")
+# development A/B timing only (tools/ab_build.sh): load another build of the same ABI
+if os.environ.get("SP_LIB_AB"):
+    LIB_PATH = os.environ["SP_LIB_AB"]
 
 SP_OK, SP_EINVAL, SP_EUNSUPPORTED, SP_ECUDA, SP_ENONFINITE, SP_EEMPTY, SP_EWORKSPACE, SP_ETIMEOUT = 0, 1, 2, 3, 5, 6, 7, 8
 SP_SCORE_AUTO, SP_SCORE_FUSED, SP_SCORE_SIMT = 0, 1, 2

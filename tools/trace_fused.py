@@ -78,6 +78,25 @@ def main():
     # skew: for each unit index, spread of publish times across CTAs
     pub = tr[:, :, 3]
     print("publish skew across CTAs per unit (max-min): mean %.2f us" % np.nanmean(np.nanmax(pub, 0) - np.nanmin(pub, 0)))
+    # lateness of each CTA vs the median publish time of the CTAs sharing its units
+    n_tg, n_ug = plan["token_groups"], plan["unit_groups"]
+    late = np.full(grid, np.nan)
+    if w.B * plan["jobs_per_request"] <= grid:
+        for ug in range(n_ug):
+            ctas = [tg * n_ug + ug for tg in range(n_tg) if tg * n_ug + ug < grid]
+            med = np.nanmedian(pub[ctas], axis=0)
+            for c in ctas:
+                late[c] = np.nanmean(pub[c] - med)
+        order = np.argsort(-np.nan_to_num(late, nan=-1e9))
+        print("CTA lateness vs median publish (us): mean %.2f  p90 %.2f  max %.2f" % (
+            np.nanmean(late), np.nanpercentile(late, 90), np.nanmax(late)))
+        print("  latest CTAs:", ", ".join("%d(%.1f)" % (c, late[c]) for c in order[:12]))
+        # late CTA's own lag: when did it start each unit's stats relative to others
+        st = tr[:, :, 2]
+        print("  stats-start lateness of latest CTA per unit (first 10 units):",
+              " ".join("%.1f" % (st[order[0], u] - np.nanmedian(st[:, u])) for u in range(min(10, units))))
+        print("  end time per CTA (agg done last unit): min %.1f  median %.1f  max %.1f" % (
+            np.nanmin(tr[:, -1, 6]), np.nanmedian(tr[:, -1, 6]), np.nanmax(tr[:, -1, 6])))
     for c in [0, grid // 2, grid - 1]:
         print(f"CTA {c}: first units (us):")
         for u in range(min(4, units)):
