@@ -42,6 +42,14 @@ namespace sp {
 namespace {
 
 constexpr int kThreads = 384;
+// Timeline tracing (sp_trace_enable) is compiled in only with -DSP_FUSED_TRACE
+// (tools/ab_build.sh ... -DSP_FUSED_TRACE): the product kernel carries no
+// trace code (the warp roles share the SM's instruction cache).
+#ifdef SP_FUSED_TRACE
+constexpr bool kTrace = true;
+#else
+constexpr bool kTrace = false;
+#endif
 enum FusedMode : int { kModeFull = 0, kModeStats = 1, kModeFinish = 2 };
 constexpr int kTileM = 128;
 constexpr int kStatsWarp0 = 4;
@@ -271,6 +279,7 @@ __device__ __forceinline__ float ex2(float x) {
 
 // Debug trace: stamp event e of the CTA's ui-th unit (no-op unless enabled).
 __device__ __forceinline__ void trace_stamp(const FusedParams& p, uint32_t ui, int e) {
+  if constexpr (!kTrace) return;
   if (p.trace != nullptr && ui < (uint32_t)p.trace_units)
     p.trace[((size_t)blockIdx.x * p.trace_units + ui) * 8 + e] = globaltimer_ns();
 }
@@ -279,12 +288,13 @@ __device__ __forceinline__ void trace_stamp(const FusedParams& p, uint32_t ui, i
 // Debug wait accounting (trace mode only): mbar_wait plus the time it took.
 __device__ __forceinline__ void mbar_wait_acc(const FusedParams& p, uint32_t bar, uint32_t parity,
                                               unsigned long long& acc) {
-  if (p.trace == nullptr) { mbar_wait(bar, parity); return; }
+  if (!kTrace || p.trace == nullptr) { mbar_wait(bar, parity); return; }
   const long long t0 = clock64();
   mbar_wait(bar, parity);
   acc += clock64() - t0;
 }
 __device__ __forceinline__ void trace_waits(const FusedParams& p, int k, unsigned long long v) {
+  if constexpr (!kTrace) return;
   if (p.trace != nullptr && p.trace_units > 1)
     p.trace[((size_t)blockIdx.x * p.trace_units + p.trace_units - 1) * 8 + k] = v;
 }
@@ -490,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     {
       uint32_t stage = 0, sphase = 0, ui = 0, gt = 0, gslot = 0, gph = 0;
       unsigned long long w_qf = 0, w_slot = 0, w_full = 0, w_issue = 0;
-      const long long t_start = clock64();
+      const long long t_start = kTrace ? clock64() : 0;
       // UMMA smem descriptors: the high word (SBO, version, swizzle) is constant;
       // the low word is (address >> 4) | LBO and a K step just adds to it.
       const uint32_t desc_hi = (uint32_t)(make_sdesc(0, 8 * p.W * 2, p.layout_type) >> 32);
@@ -504,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           const uint32_t b_lo0 = ((smem_u32(smem + p.off_q + qs * p.q_slot_bytes) >> 4) & 0x3FFFu) | (1u << 16);
           for (int t = jb.t_lo; t < jb.t_hi; ++t, ++gt) {
             const uint32_t slot = gslot;
-            unsigned long long* tt = (p.tile_trace != nullptr && blockIdx.x == 0 && gt < 1000)
+            unsigned long long* tt = (kTrace && p.tile_trace != nullptr && blockIdx.x == 0 && gt < 1000)
                                          ? p.tile_trace + gt * 8 : nullptr;
             if (tt && lane == 0) { tt[0] = clock64(); tt[4] = globaltimer_ns(); }
             mbar_wait_acc(p, bar_tempty + 8 * slot, gph ^ 1, w_slot);
@@ -516,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             tc_fence_after();
             const uint32_t a_lo0 = ((smem_u32(smem + p.off_k + stage * p.k_stage_bytes) >> 4) & 0x3FFFu) | (1u << 16);
             const uint32_t dcol = tmem + slot * p.NCP;
-            const long long ti0 = clock64();
+            const long long ti0 = kTrace ? clock64() : 0;
             // straight-line issue for the common head dims (d = 64, 128, 256 with
             // 64-element swizzle blocks): the descriptor arithmetic pipelines
             // across the MMAs (a loop back-edge halves the issue rate)
@@ -540,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             }
             umma_commit(bar_empty + 8 * stage);
             umma_commit(bar_tfull + 8 * slot);
-            if (p.trace != nullptr) w_issue += clock64() - ti0;
+            if (kTrace && p.trace != nullptr) w_issue += clock64() - ti0;
             if (tt && lane == 0) { tt[3] = clock64(); tt[5] = globaltimer_ns(); }
             if (++stage == (uint32_t)p.stages) { stage = 0; sphase ^= 1; }
           }
@@ -550,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       trace_waits(p, 2, w_qf);
       trace_waits(p, 3, w_slot);
       trace_waits(p, 4, w_full);
-      trace_waits(p, 5, clock64() - t_start);
+      trace_waits(p, 5, kTrace ? clock64() - t_start : 0);
       trace_waits(p, 6, w_issue);
     }
   } else if (warp >= kStatsWarp0 && warp < kFinalWarp0 && p.mode != kModeFinish) {

@@ -1,9 +1,9 @@
 #!/bin/bash
 # Build libspecprefill.so from a git revision into build/ab/<name>.so for
 # back-to-back A/B timing on one GPU box:  tools/ab_build.sh <rev> <name>
-# then run with SP_LIB_AB=build/ab/<name>.so.
+# (extra nvcc flags after the name, e.g. -DSP_FUSED_TRACE), then run with SP_LIB_AB=build/ab/<name>.so.
 set -e
-rev=$1; name=$2
+rev=$1; name=$2; shift 2; extra=("$@")
 root=$(cd "$(dirname "$0")/.." && pwd)
 tmp=$(mktemp -d)
 git -C "$root" archive "$rev" paper_2502_02789_b200/csrc include | tar -x -C "$tmp"
@@ -11,7 +11,7 @@ mkdir -p "$root/build/ab"
 objs=()
 for f in "$tmp"/paper_2502_02789_b200/csrc/*.cu; do
   o="$tmp/$(basename "$f" .cu).o"
-  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr \
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr "${extra[@]}" \
     -I"$tmp/include" -c "$f" -o "$o" &
   objs+=("$o")
 done
