@@ -395,8 +395,11 @@ __device__ __forceinline__ void transpose_merge32(float (&m)[32], float (&s)[32]
 // instantiation per group size keeps the kernel's hot code small: the warp
 // roles run different code concurrently on each SMSP and share the
 // instruction cache.
-template <int kG>
+template <int kG, int kNCP>
 __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ FusedParams p) {
+  // kNCP > 0: compile-time padded column count (one 32-column TMEM group for
+  // the 8B geometry): the per-tile loops become straight-line code
+  const int NCP = kNCP > 0 ? kNCP : p.NCP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // warp index broadcast from lane 0: provably warp-uniform, so each role's
@@ -454,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   // this launch publishes into part[parity]; part[parity ^ 1] (the previous
   // launch's) is re-zeroed off the critical path, for the launch after next
   const uint32_t parity = ld_acquire(p.epoch) & 1u;
-  const long long part_half = (long long)p.B * p.U * p.n_tg * p.NCP;
+  const long long part_half = (long long)p.B * p.U * p.n_tg * NCP;
   unsigned long long* const part_cur = p.part + parity * part_half;
   unsigned long long* const part_old = p.part + (parity ^ 1u) * part_half;
 
@@ -475,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           const uint32_t qdst = smem_u32(smem + p.off_q + qs * p.q_slot_bytes);
           #pragma unroll 1
           for (int kb = 0; kb < p.nkb; ++kb)
-            tma_load_5d(qdst + kb * (p.NCP * p.W * 2), &p.tmQ, bar_qfull + 8 * qs, kb * p.W, g * p.G, 0, l, jb.b);
+            tma_load_5d(qdst + kb * (NCP * p.W * 2), &p.tmQ, bar_qfull + 8 * qs, kb * p.W, g * p.G, 0, l, jb.b);
           for (int t = jb.t_lo; t < jb.t_hi; ++t) {
             mbar_wait_acc(p, bar_empty + 8 * stage, sphase ^ 1, w_empty);
             mbar_expect_tx(bar_full + 8 * stage, p.k_stage_bytes);
@@ -504,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       // UMMA smem descriptors: the high word (SBO, version, swizzle) is constant;
       // the low word is (address >> 4) | LBO and a K step just adds to it.
       const uint32_t desc_hi = (uint32_t)(make_sdesc(0, 8 * p.W * 2, p.layout_type) >> 32);
-      const uint32_t a_kb = (kTileM * p.W * 2) >> 4, b_kb = (p.NCP * p.W * 2) >> 4;
+      const uint32_t a_kb = (kTileM * p.W * 2) >> 4, b_kb = (NCP * p.W * 2) >> 4;
       const int ksteps = p.W / 16;
       for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
         const Job jb = decode_job(p, job);
@@ -525,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             if (tt && lane == 0) tt[2] = clock64();
             tc_fence_after();
             const uint32_t a_lo0 = ((smem_u32(smem + p.off_k + stage * p.k_stage_bytes) >> 4) & 0x3FFFu) | (1u << 16);
-            const uint32_t dcol = tmem + slot * p.NCP;
+            const uint32_t dcol = tmem + slot * NCP;
             const long long ti0 = kTrace ? clock64() : 0;
             // straight-line issue for the common head dims (d = 64, 128, 256 with
             // 64-element swizzle blocks): the descriptor arithmetic pipelines
@@ -580,11 +583,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
         const uint32_t gt0 = gt;
         uint32_t slot0 = gt % nslots, ph0 = (gt / nslots) & 1;
-        float2* rb = red + (ui & 1) * 4 * p.NCP;
+        float2* rb = red + (ui & 1) * 4 * NCP;
         mbar_wait(bar_rempty + 8 * (ui & 1), ((ui >> 1) & 1) ^ 1);   // exchange warp done with rb
         if (q == 0 && lane == 0) trace_stamp(p, ui, 2);
 #pragma unroll 1
-        for (int grp = 0; grp < p.NCP / 32; ++grp) {
+        for (int grp = 0; grp < NCP / 32; ++grp) {
           float ref[32], sum[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) { ref[i] = -CUDART_INF_F; sum[i] = 0.f; }
@@ -594,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             mbar_wait(bar_tfull + 8 * slot, ph);
             tc_fence_after();
             float x[32];
-            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + slot * p.NCP + grp * 32;
+            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + slot * NCP + grp * 32;
             float* x0 = x;
             tmem_ld16_issue(ta, *reinterpret_cast<float(*)[16]>(x0));
             tmem_ld16_issue(ta + 16, *reinterpret_cast<float(*)[16]>(x0 + 16));
@@ -633,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           }
           float mo, so;
           transpose_merge32(ref, sum, lane, mo, so);                    // column 32*grp + lane
-          rb[q * p.NCP + grp * 32 + lane] = make_float2(mo, so);
+          rb[q * NCP + grp * 32 + lane] = make_float2(mo, so);
         }
         if (q == 0 && lane == 0) trace_stamp(p, ui, 7);
         mbar_arrive(bar_rfull + 8 * (ui & 1));                        // 128 arrivals: all columns written
@@ -651,13 +654,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
         const long long ubase = (long long)jb.b * p.U + u;
         mbar_wait(bar_rfull + 8 * (ui & 1), (ui >> 1) & 1);
-        const float2* rb = red + (ui & 1) * 4 * p.NCP;
-        unsigned long long* mypart = part_cur + (ubase * p.n_tg + jb.tg) * p.NCP;
-        for (int c = lane; c < p.NCP; c += 32) {
+        const float2* rb = red + (ui & 1) * 4 * NCP;
+        unsigned long long* mypart = part_cur + (ubase * p.n_tg + jb.tg) * NCP;
+        for (int c = lane; c < NCP; c += 32) {
           float mm = -CUDART_INF_F, ss = 0.f;
           if (c < p.NC) {
 #pragma unroll
-            for (int w = 0; w < 4; ++w) merge2(mm, ss, rb[w * p.NCP + c].x, rb[w * p.NCP + c].y);
+            for (int w = 0; w < 4; ++w) merge2(mm, ss, rb[w * NCP + c].x, rb[w * NCP + c].y);
           }
           if (!(ss > 0.f)) { mm = -CUDART_INF_F; ss = -1.f; }          // written, but empty
           st_relaxed_u64(mypart + c, pack_ms(mm, ss));
@@ -673,8 +676,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
       const Job jb = decode_job(p, job);
       for (int u = jb.u_lo; u < jb.u_hi; ++u) {
-        unsigned long long* row = part_old + (((long long)jb.b * p.U + u) * p.n_tg + jb.tg) * p.NCP;
-        for (int c = lane; c < p.NCP; c += 32) row[c] = 0ull;
+        unsigned long long* row = part_old + (((long long)jb.b * p.U + u) * p.n_tg + jb.tg) * NCP;
+        for (int c = lane; c < NCP; c += 32) row[c] = 0ull;
       }
     }
   } else if (warp == 3 && p.mode != kModeStats) {
@@ -691,10 +694,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const uint32_t par = ui % kLseRing;
         const long long ubase = (long long)jb.b * p.U + u;
         mbar_wait(bar_lempty + 8 * par, ((ui / kLseRing) & 1) ^ 1);    // aggregation done with ls[par]
-        float* ls = lse_s + par * p.NCP;
-        const unsigned long long* src = part_cur + ubase * p.n_tg * p.NCP + (p.debug_local ? jb.tg * p.NCP : 0);
+        float* ls = lse_s + par * NCP;
+        const unsigned long long* src = part_cur + ubase * p.n_tg * NCP + (p.debug_local ? jb.tg * NCP : 0);
         const int ntg = p.debug_local ? 1 : p.n_tg;
-        for (int c = lane; c < p.NCP && p.mode == kModeFinish; c += 32) {
+        for (int c = lane; c < NCP && p.mode == kModeFinish; c += 32) {
           // lse2 supplied by the caller (sequence-sharded split: globally combined statistics)
           float l2 = 0.f;
           if (c < p.NC) {
@@ -703,14 +706,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           }
           ls[c] = l2;
         }
-        for (int c = lane; c < p.NCP && p.mode == kModeFull; c += 32) {
+        for (int c = lane; c < NCP && p.mode == kModeFull; c += 32) {
           float M = -CUDART_INF_F, S = 0.f;
           for (int s0 = 0; s0 < ntg; s0 += kMaxLseBatch) {
             unsigned long long v[kMaxLseBatch];
             uint32_t missing = 0;
 #pragma unroll
             for (int j = 0; j < kMaxLseBatch; ++j) {
-              v[j] = (s0 + j < ntg) ? ld_relaxed_u64(src + (long long)(s0 + j) * p.NCP + c) : pack_ms(0.f, -1.f);
+              v[j] = (s0 + j < ntg) ? ld_relaxed_u64(src + (long long)(s0 + j) * NCP + c) : pack_ms(0.f, -1.f);
               missing |= (v[j] == 0ull ? 1u : 0u) << j;
             }
             long long it = 0;
@@ -719,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
 #pragma unroll
               for (int j = 0; j < kMaxLseBatch; ++j) {
                 if (missing & (1u << j)) {
-                  v[j] = ld_relaxed_u64(src + (long long)(s0 + j) * p.NCP + c);
+                  v[j] = ld_relaxed_u64(src + (long long)(s0 + j) * NCP + c);
                   if (v[j] != 0ull) missing &= ~(1u << j);
                 }
               }
@@ -764,17 +767,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
         const uint32_t par = ui % kLseRing;
         if (p.mode != kModeStats) mbar_wait(bar_lfull + 8 * par, (ui / kLseRing) & 1);
-        const float* ls = lse_s + par * p.NCP;
+        const float* ls = lse_s + par * NCP;
         uint32_t slot = gt % nslots, ph = (gt / nslots) & 1;
         for (int t = 0; t < ntile; ++t, ++gt) {
           mbar_wait(bar_tfull + 8 * slot, ph);
           tc_fence_after();
-          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + slot * p.NCP;
+          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + slot * NCP;
           float* arow = acc + (t * p.Rv) * kTileM + tok;
 #pragma unroll 1
-          for (int k0 = 0; k0 < p.NCP / 16 && p.mode != kModeStats; k0 += 2) {
+          for (int k0 = 0; k0 < NCP / 16 && p.mode != kModeStats; k0 += 2) {
             float xa[16], xb[16];
-            const bool two = k0 + 1 < p.NCP / 16;
+            const bool two = k0 + 1 < NCP / 16;
             tmem_ld16_issue(ta + k0 * 16, xa);
             if (two) tmem_ld16_issue(ta + k0 * 16 + 16, xb);
             tmem_wait();
@@ -1142,14 +1145,19 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
     }
   }
 
-  void (*kern)(FusedParams) = g.G == 1 ? k_fused<1> : g.G == 2 ? k_fused<2> : g.G == 4 ? k_fused<4>
-                                                     : g.G == 8 ? k_fused<8> : k_fused<0>;
-  static bool configured[5] = {false, false, false, false, false};
+  // one instantiation per (GQA group, one-column-group) pair
+  using KernFn = void (*)(FusedParams);
+  static const KernFn table[5][2] = {{k_fused<1, 0>, k_fused<1, 32>}, {k_fused<2, 0>, k_fused<2, 32>},
+                                     {k_fused<4, 0>, k_fused<4, 32>}, {k_fused<8, 0>, k_fused<8, 32>},
+                                     {k_fused<0, 0>, k_fused<0, 32>}};
+  static bool configured[5][2] = {};
   const int ki = g.G == 1 ? 0 : g.G == 2 ? 1 : g.G == 4 ? 2 : g.G == 8 ? 3 : 4;
-  if (!configured[ki]) {
+  const int kj = pl.NCP == 32 ? 1 : 0;
+  KernFn kern = table[ki][kj];
+  if (!configured[ki][kj]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (e != cudaSuccess) return e;
-    configured[ki] = true;
+    configured[ki][kj] = true;
   }
   const int grid = (int)std::min<long long>(pl.P, pl.total_jobs);
   cudaLaunchConfig_t cfg = {};
