@@ -60,6 +60,7 @@ constexpr int kMaxSlots = 16;          // TMEM tile slots (512 columns / 32)
 constexpr int kLseRing = 8;            // lse2 buffers in SMEM (gather may run ahead of aggregation)
 constexpr int kMaxLseBatch = 20;       // 64-bit partial words in flight per lane
 constexpr int kTmemCols = 512;
+constexpr double kSmHbmBytesPerUs = 7.0e6 / 148;   // one SM's share of ~7 TB/s, bytes per microsecond
 constexpr int kSmemLimit = 232448;     // sm_100 max dynamic shared memory per block
 
 // ------------------------------------------------------------------ parameters
@@ -949,11 +950,8 @@ Plan make_plan(const Geom& g, bool allow_override = true) {
   // choose (n_tg, n_ug): when a request needs more than one wave of CTAs
   // (B*J > P), J = n_tg*n_ug must divide the grid so a request never straddles
   // two waves (its CTAs exchange statistics and must be co-resident).  Time
-  // model in units of one K-tile load at an SM's share of HBM bandwidth: a tile
-  // holds its TMEM slot for about (tpc + chain) tile-times, so the ring of
-  // nslots slots sustains min(1, nslots / (tpc + chain)) tiles per tile-time.
+  // model below.
   pl.nslots = std::min(kMaxSlots, kTmemCols / pl.NCP);
-  const double kChain = 9.0;
   double best = 1e300;
   // test/tuning override: SP_FUSED_PLAN="n_tg,n_ug" (ignored unless valid for g)
   int force_tg = 0, force_ug = 0;
@@ -972,10 +970,21 @@ Plan make_plan(const Geom& g, bool allow_override = true) {
       const long long jobs = (long long)g.B * J;
       const int grid = (int)std::min<long long>(pl.P, jobs);
       const long long waves = (jobs + grid - 1) / grid;
-      const double tile_scale = (double)pl.k_stage_bytes / 32768.0;
-      const double rate = std::min(1.0, (double)pl.nslots / (tpc + kChain / tile_scale));
-      double cost = (double)upc * tpc * tile_scale / rate;
-      cost += (n_ug > 1 ? 2.0 * g.Rv * tpc * kTileM * 4.0 / 32768.0 + kChain : 0.0);  // cross-group max
+      // Time model (us, fitted to B200 measurements of C1-C4 plan sweeps): a
+      // tile streams at the SM's share of HBM; a unit's lse2 is known ~L after
+      // its last tile (cross-CTA skew + one L2 round trip per gather batch);
+      // the TMEM ring holds W units, so L - (W-1) unit-times stay exposed; the
+      // gather warp itself needs ~1.6 us per batch of kMaxLseBatch partials.
+      const double tile_us = (double)pl.k_stage_bytes / kSmHbmBytesPerUs;
+      const int batches = (n_tg + kMaxLseBatch - 1) / kMaxLseBatch;
+      const double L_us = 5.0 + 0.8 * batches;
+      const int W = std::max(1, pl.nslots / tpc);
+      const double exposed = std::max(0.0, L_us - (W - 1) * tpc * tile_us);
+      // (+0.4 us fixed per unit: Q load, statistics merge and publish)
+      const double per_unit = std::max(tpc * tile_us + exposed / W + 0.4, 1.6 * batches);
+      double cost = upc * per_unit + L_us;                                   // + pipeline fill
+      if (n_ug > 1)                                                          // cross-group max + its sync
+        cost += 2.0 * g.Rv * tpc * kTileM * 4.0 / kSmHbmBytesPerUs + 5.0 + 0.25 * n_ug;
       cost *= (double)waves;
       if (cost < best * 0.999) {
         best = cost;
