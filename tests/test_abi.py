@@ -126,3 +126,29 @@ def test_no_cpu_fallback_without_device():
     lay = _layout(g)
     rc = sp.lib().sp_score(FAKE, FAKE, C.byref(g), C.byref(lay), FAKE, FAKE, 1 << 30, None)
     assert rc in (_lib.SP_ECUDA, _lib.SP_EUNSUPPORTED)
+
+
+@pytest.mark.parametrize("name,variant", [("C0", {}), ("C1", {}), ("C2", {}), ("C3", {}), ("C4", {}),
+                                          ("C3", dict(R=4)), ("C3", dict(H=32, Hkv=32, R=1)),
+                                          ("C2", dict(B=200)), ("C1", dict(d=64)), ("C1", dict(d=256))])
+def test_fused_plan_invariants(name, variant):
+    """The fused kernel's host plan (no device needed: 148 SMs assumed): every
+    request's jobs fit one wave of co-resident CTAs, a unit's tiles fit the
+    TMEM ring, the SMEM carve fits the 227 KB limit."""
+    import torch
+    from spgen import gen
+    w = gen.CONFIGS[name].with_(**variant)
+    Q = torch.empty((w.B, w.L, w.R, w.H, w.d), dtype=torch.bfloat16, device="meta")
+    K = torch.empty((w.B, w.L, w.Hkv, w.N, w.d), dtype=torch.bfloat16, device="meta")
+    pl = sp.score_plan(Q, K, w.Rv)
+    P, J = 148, pl["jobs_per_request"]
+    T, U = -(-w.N // 128), w.L * w.Hkv
+    assert pl["token_groups"] * pl["unit_groups"] == J
+    assert pl["tiles_per_job"] == -(-T // pl["token_groups"]) and pl["units_per_job"] == -(-U // pl["unit_groups"])
+    assert pl["grid"] == min(P, w.B * J)
+    if w.B * J > P:
+        assert P % J == 0                      # a request never straddles two waves
+    assert pl["tiles_per_job"] <= pl["tmem_slots"]
+    assert 2 <= pl["stages"] and pl["smem_bytes"] <= 232448
+    if name == "C3" and not variant:
+        assert (pl["token_groups"], pl["unit_groups"]) == (37, 4)   # the plan the bench line is quoted on
