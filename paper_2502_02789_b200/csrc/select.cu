@@ -10,10 +10,12 @@
 // over its true size (Z8), K_c from the exact ppm rule (Z9, computed on the
 // host), ties to the lowest chunk index (Z10), ascending ids (Z11).
 //
-// One CTA of 1024 threads per request:
+// Phase A can run on many CTAs per request (kModeA: grid (B, chunk blocks),
+// writing cs to the workspace), phases B-C on one CTA of 1024 threads per
+// request (kModeBC); short prompts run all three in one launch (kModeAll):
 //   A. importance is staged in shared memory segment by segment (all loads of a
 //      segment in flight together), pooled, and summed per chunk in token order
-//      (deterministic) -> cs[c] (global workspace, L2-resident);
+//      (deterministic) -> cs[c];
 //   B. a 4-pass 8-bit radix select on the IEEE bits of cs (scores are >= 0, so
 //      bit order == value order) finds the K_c-th largest value T; the digit
 //      search is a parallel suffix scan over the 256 bins;
@@ -23,8 +25,7 @@
 //      gathers the kept tokens in the same pass.
 #include "sp_internal.h"
 
-#include <cstdio>
-#include <cstdlib>
+#include <algorithm>
 
 namespace sp {
 namespace {
@@ -34,6 +35,7 @@ constexpr int NW = ST / 32;
 constexpr int SEG = 16384;          // tokens of importance staged in SMEM per segment (64 KiB)
 constexpr int kMaxPool = 4097;      // largest pooling window (half-window staged on each side)
 constexpr int kSmemChunks = 8192;   // chunk scores kept in SMEM when n_c fits (else L2-resident workspace)
+enum SelectMode : int { kModeAll = 0, kModeA = 1, kModeBC = 2 };
 
 struct ScanSmem {
   int warp_tot[NW];
@@ -74,10 +76,8 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
                                                int pos0, long long K_c, int* __restrict__ ids_all,
                                                int* __restrict__ pos_all, int* __restrict__ n_kept,
                                                float* __restrict__ cs_all, const int* __restrict__ tokens_all,
-                                               int* __restrict__ out_all, long long* __restrict__ dbg_ts) {
-#define SP_TS(k) if (dbg_ts && threadIdx.x == 0 && blockIdx.x == 0) dbg_ts[k] = clock64();
-  SP_TS(0)
-  extern __shared__ float seg[];                  // [SEG + 2w] staged importance, then [SEG] pooled
+                                               int* __restrict__ out_all, int mode, int segcap, long long cpb) {
+  extern __shared__ float seg[];                  // [segcap + 2w] staged importance, then [segcap] pooled
   __shared__ unsigned hist[256];
   __shared__ unsigned s_digit, s_remaining;
   __shared__ ScanSmem scan;
@@ -87,18 +87,28 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
   const long long n_c = (N + chunk - 1) / chunk;
   const float* imp = imp_all + (long long)b * N;
   const long long w_ = (pool_k - 1) / 2;
-  float* cs = (n_c <= kSmemChunks) ? seg + 2 * SEG + 2 * w_ : cs_all + (long long)b * n_c;
+  // chunk scores: SMEM when this CTA runs phases B-C and n_c fits, else the workspace
+  float* cs = (mode != kModeA && n_c <= kSmemChunks) ? seg + 2 * segcap + 2 * w_ : cs_all + (long long)b * n_c;
   int* ids = ids_all + (long long)b * N;
   int* pos = pos_all + (long long)b * N;
   const long long w = (pool_k - 1) / 2;
 
-  // ---- A. pooled scores (centred window, shrinking edges) -> chunk sums
-  float* pooled = seg + SEG + 2 * w;                // [SEG]
+  if (mode == kModeBC) {
+    if (n_c <= kSmemChunks)
+      for (long long c = tid; c < n_c; c += ST) cs[c] = cs_all[(long long)b * n_c + c];
+    __syncthreads();
+  } else {
+  // ---- A. pooled scores (centred window, shrinking edges) -> chunk sums of
+  //      chunks [c_lo, c_hi) (all of them unless kModeA)
+  const long long c_lo = mode == kModeA ? (long long)blockIdx.y * cpb : 0;
+  const long long c_hi = mode == kModeA ? std::min(n_c, c_lo + cpb) : n_c;
+  const long long t_lo = c_lo * chunk, t_hi = std::min(N, c_hi * chunk);
+  float* pooled = seg + segcap + 2 * w;             // [segcap]
   const int wi = (int)w;
   const float inv_k = 1.f / (float)pool_k;
   const bool warp_chunks = chunk <= 32 && (chunk & (chunk - 1)) == 0;   // power of two <= 32
-  for (long long base = 0; base < N; base += SEG) {
-    const int len = (int)((base + SEG < N) ? SEG : N - base);           // tokens in this segment
+  for (long long base = t_lo; base < t_hi; base += segcap) {
+    const int len = (int)((base + segcap < t_hi) ? segcap : t_hi - base);  // tokens in this segment
     const long long lo = base - w < 0 ? 0 : base - w, hi = base + len + w > N ? N : base + len + w;
     const int off = (int)(base - lo);                                     // seg index of token `base`
     {
@@ -119,7 +129,6 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
       for (int i = PER * ST + tid; i < n; i += ST) seg[i] = imp[lo + i];   // halo beyond SEG
     }
     __syncthreads();
-    if (base == 0) SP_TS(4)
     // interior tokens [i_lo, i_hi) have the full window inside the sequence
     const int i_lo = (int)(w - base > 0 ? w - base : 0);
     const int i_hi = (int)(N - 1 - w - base + 1 < len ? N - 1 - w - base + 1 : len);
@@ -138,11 +147,10 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
       }
     }
     __syncthreads();
-    if (base == 0) SP_TS(5)
     const long long c_first = base / chunk, c_last = (base + len - 1) / chunk;
     if (warp_chunks && base % chunk == 0) {
       // a warp sums 32 consecutive pooled values in groups of `chunk` lanes (tree
-      // order); SEG is a multiple of 32 so every chunk starts inside its segment
+      // order); segcap is a multiple of 32 so every chunk starts inside its segment
       const int lg = __ffs(chunk) - 1;
       const int cbase = (int)(base >> lg);
 #pragma unroll 4
@@ -170,22 +178,28 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
     }
     __syncthreads();
   }
-  for (long long c = tid; c < n_c; c += ST) {
+  for (long long c = c_lo + tid; c < c_hi; c += ST) {
     const long long sz = ((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk;
     cs[c] = cs[c] / (float)sz;
   }
   __syncthreads();
+  }
+  if (mode == kModeA) return;
 
-  SP_TS(1)
   // ---- B. radix select: threshold bit pattern T of the K_c-th largest score
   unsigned prefix = 0, pmask = 0;
   unsigned remaining = (unsigned)K_c;
   for (int shift = 24; shift >= 0; shift -= 8) {
     if (tid < 256) hist[tid] = 0;
     __syncthreads();
-    for (long long c = tid; c < n_c; c += ST) {
-      const unsigned key = __float_as_uint(cs[c]);
-      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    // warp-aggregated: lanes with the same digit add once (the top digits of
+    // near-equal scores collide, and SMEM atomics on one address serialise)
+    for (long long c0 = (long long)warp * 32; c0 < n_c; c0 += ST) {
+      const long long c = c0 + lane;
+      const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
+      const unsigned digit = (c < n_c && (key & pmask) == prefix) ? (key >> shift) & 255u : 256u;
+      const unsigned peers = __match_any_sync(0xffffffffu, digit);
+      if (digit < 256u && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], (unsigned)__popc(peers));
     }
     __syncthreads();
     // digit D: count(digits > D) < remaining <= count(digits >= D); warps 0-7 scan 256 bins
@@ -224,7 +238,6 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
   const unsigned T = prefix;
   const int need_eq = (int)remaining;            // chunks equal to T to keep (lowest indices first)
 
-  SP_TS(2)
   // ---- C. keep flags in chunk order, compaction (+ gather) of the kept token ranges
   int carry_eq = 0, carry_tok = 0;
   const int* tokens = tokens_all ? tokens_all + (long long)b * N : nullptr;
@@ -265,8 +278,6 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
     __syncthreads();
   }
   if (tid == 0) n_kept[b] = carry_tok;
-  SP_TS(3)
-#undef SP_TS
 }
 
 }  // namespace
@@ -281,26 +292,34 @@ bool select_supported(int pool_k) { return pool_k <= kMaxPool; }
 cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int chunk, int pos0, long long K_c,
                           int* ids, int* pos, int* n_kept, void* ws, cudaStream_t st, const int* tokens, int* out) {
   static bool configured = false;
-  const size_t smem = (size_t)(2 * SEG + 2 * ((kMaxPool - 1) / 2) + kSmemChunks) * sizeof(float);
+  const size_t smem_max = (size_t)(2 * SEG + 2 * ((kMaxPool - 1) / 2) + kSmemChunks) * sizeof(float);
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   const long long n_c = (N + chunk - 1) / chunk;
-  const size_t need = (size_t)(2 * SEG + 2 * ((pool_k - 1) / 2) + (n_c <= kSmemChunks ? n_c : 0)) * sizeof(float);
-  static long long* dbg = nullptr;
-  if (std::getenv("SP_SELECT_TS") && !dbg) cudaMalloc(&dbg, 64);
-  k_select<<<B, ST, need, st>>>(imp, N, pool_k, chunk, pos0, K_c, ids, pos, n_kept, reinterpret_cast<float*>(ws),
-                                tokens, out, dbg);
-  if (dbg) {
-    long long h[4];
-    long long h6[6];
-    cudaMemcpy(h6, dbg, 48, cudaMemcpyDeviceToHost);
-    for (int i = 0; i < 4; ++i) h[i] = h6[i];
-    std::fprintf(stderr, "select phases (cycles): A %lld B %lld C %lld | seg0 stage %lld pool %lld\n", h[1] - h[0],
-                 h[2] - h[1], h[3] - h[2], h6[4] - h[0], h6[5] - h6[4]);
+  const long long w = (pool_k - 1) / 2;
+  float* cs = reinterpret_cast<float*>(ws);
+  // Long prompts: phase A (pooling + chunk sums, the bulk of the work) on
+  // ~kTokPerCta-token blocks of chunks spread over the SMs, then B-C per request.
+  constexpr long long kTokPerCta = 2048;
+  const long long cpb = std::max(1LL, kTokPerCta / chunk);
+  const long long nblk = (n_c + cpb - 1) / cpb;
+  if (nblk >= 4 && nblk <= 65535) {
+    const long long span = std::min(N, cpb * chunk);
+    const int segcap = (int)std::min<long long>(SEG, (span + 31) / 32 * 32);
+    const size_t needA = (size_t)(2 * segcap + 2 * w) * sizeof(float);
+    k_select<<<dim3(B, (unsigned)nblk), ST, needA, st>>>(imp, N, pool_k, chunk, pos0, K_c, ids, pos, n_kept, cs, tokens,
+                                                        out, kModeA, segcap, cpb);
+    const size_t needBC = (size_t)(2 * segcap + 2 * w + (n_c <= kSmemChunks ? n_c : 0)) * sizeof(float);
+    k_select<<<B, ST, needBC, st>>>(imp, N, pool_k, chunk, pos0, K_c, ids, pos, n_kept, cs, tokens, out, kModeBC,
+                                    segcap, cpb);
+    return cudaGetLastError();
   }
+  const size_t need = (size_t)(2 * SEG + 2 * w + (n_c <= kSmemChunks ? n_c : 0)) * sizeof(float);
+  k_select<<<B, ST, need, st>>>(imp, N, pool_k, chunk, pos0, K_c, ids, pos, n_kept, cs, tokens, out, kModeAll, SEG,
+                                n_c);
   return cudaGetLastError();
 }
 
