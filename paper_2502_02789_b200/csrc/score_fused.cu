@@ -770,6 +770,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         if (p.mode != kModeStats) mbar_wait(bar_lfull + 8 * par, (ui / kLseRing) & 1);
         const float* ls = lse_s + par * NCP;
         uint32_t slot = gt % nslots, ph = (gt / nslots) & 1;
+        if constexpr (kNCP == 32) {
+          // one 32-column group: the unit's lse2 stays in registers for all its tiles
+          float lv[32];
+#pragma unroll
+          for (int i4 = 0; i4 < 8; ++i4) {
+            const float4 v4 = *reinterpret_cast<const float4*>(ls + 4 * i4);
+            lv[4 * i4] = v4.x; lv[4 * i4 + 1] = v4.y; lv[4 * i4 + 2] = v4.z; lv[4 * i4 + 3] = v4.w;
+          }
+          for (int t = 0; t < ntile; ++t, ++gt) {
+            mbar_wait(bar_tfull + 8 * slot, ph);
+            tc_fence_after();
+            if (p.mode != kModeStats) {
+              const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + slot * 32;
+              float* arow = acc + (t * p.Rv) * kTileM + tok;
+              float xa[16], xb[16];
+              tmem_ld16_issue(ta, xa);
+              tmem_ld16_issue(ta + 16, xb);
+              tmem_wait();
+              tie16(xa);
+              tie16(xb);
+              fold_tile<kG, 16>(xa, *reinterpret_cast<const float(*)[16]>(&lv[0]), p.xs, 0, p.NC, p.G, p.Rv, arow);
+              fold_tile<kG, 16>(xb, *reinterpret_cast<const float(*)[16]>(&lv[16]), p.xs, 1, p.NC, p.G, p.Rv, arow);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_tempty + 8 * slot);         // release the TMEM tile slot
+            if (++slot == nslots) { slot = 0; ph ^= 1; }
+          }
+        } else
         for (int t = 0; t < ntile; ++t, ++gt) {
           mbar_wait(bar_tfull + 8 * slot, ph);
           tc_fence_after();
