@@ -151,6 +151,32 @@ def test_select_parity_random(pool_k, chunk):
         _util.check_selection(ids[b].cpu().numpy(), pos[b].cpu().numpy(), int(nk[b]), o, chunk, N, 0)
 
 
+@pytest.mark.parametrize("B,N,pool_k,chunk", [(2, 50000, 33, 24), (1, 20000, 1, 100), (1, 9000, 5, 1),
+                                               (1, 70000, 4097, 32), (2, 8197, 7, 3)])
+def test_select_multi_cta(B, N, pool_k, chunk):
+    """Long prompts run phase A (pooling + chunk sums) on many CTAs: pooling
+    windows and chunks straddle the CTA blocks, the chunk scores may exceed the
+    SMEM budget of the selecting CTA."""
+    rng = np.random.default_rng(N + chunk)
+    imp32 = (rng.random((B, N)) ** 4 + 1e-6).astype(np.float32)
+    ids, pos, nk = sp.select(torch.tensor(imp32, device="cuda"), 0.15, pool_k, chunk, pos0=3)
+    for b in range(B):
+        o = ref.select(imp32[b].astype(np.float64), 0.15, pool_k, chunk, 3)
+        _util.check_selection(ids[b].cpu().numpy(), pos[b].cpu().numpy(), int(nk[b]), o, chunk, N, 3)
+
+
+def test_select_multi_cta_dyadic_ties():
+    """Exact fp32 sums across CTA blocks: the tie-break must match bit for bit."""
+    rng = np.random.default_rng(5)
+    N, chunk = 12000, 8
+    imp = rng.integers(0, 4, size=(2, N)).astype(np.float64) / 64.0
+    ids, pos, nk = sp.select(torch.tensor(imp, dtype=torch.float32, device="cuda"), 0.25, 1, chunk)
+    for b in range(2):
+        o = ref.select(imp[b], 0.25, 1, chunk, 0)
+        n = int(nk[b])
+        assert n == len(o["ids"]) and np.array_equal(ids[b, :n].cpu().numpy(), o["ids"])
+
+
 def test_select_keep_all_and_single_chunk():
     imp = torch.rand((2, 77), device="cuda") + 0.01
     ids, pos, nk = sp.select(imp, 1.0, 3, 8, pos0=5)
