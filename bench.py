@@ -319,7 +319,12 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = run_e2e(args, w, Q, K, T, dev, stream, dist, world)
 
-    launches_per_step = {"fused": 1, "simt": 4, "auto": 1}[args.algo] + 1     # + select_gather
+    # select_gather is one launch, or two for long prompts (phase A over the SMs,
+    # then B-C): the rule of select_launch() in csrc/select.cu
+    n_c = -(-w.N // w.chunk)
+    cpb = max(1, 2048 // w.chunk)
+    select_launches = 2 if 4 <= -(-n_c // cpb) <= 65535 else 1
+    launches_per_step = {"fused": 1, "simt": 4, "auto": 1}[args.algo] + select_launches
     plan = sp.score_plan(Q, K, w.Rv) if args.algo != "simt" else None
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
