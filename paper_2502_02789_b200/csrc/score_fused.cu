@@ -58,7 +58,7 @@ constexpr int kMaxStages = 8;
 constexpr int kMaxChunks = 8;          // NCP <= 128 columns (16-column chunks)
 constexpr int kMaxSlots = 16;          // TMEM tile slots (512 columns / 32)
 constexpr int kLseRing = 8;            // lse2 buffers in SMEM (gather may run ahead of aggregation)
-constexpr int kMaxLseBatch = 20;       // 64-bit partial words in flight per lane
+constexpr int kMaxLseBatch = 10;       // 64-bit partial words in flight per lane
 constexpr int kTmemCols = 512;
 constexpr double kSmHbmBytesPerUs = 7.0e6 / 148;   // one SM's share of ~7 TB/s, bytes per microsecond
 constexpr int kSmemLimit = 232448;     // sm_100 max dynamic shared memory per block
@@ -711,27 +711,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           float M = -CUDART_INF_F, S = 0.f;
           for (int s0 = 0; s0 < ntg; s0 += kMaxLseBatch) {
             unsigned long long v[kMaxLseBatch];
-            uint32_t missing = 0;
+            unsigned long long missing = 0;
 #pragma unroll
             for (int j = 0; j < kMaxLseBatch; ++j) {
               v[j] = (s0 + j < ntg) ? ld_relaxed_u64(src + (long long)(s0 + j) * NCP + c) : pack_ms(0.f, -1.f);
-              missing |= (v[j] == 0ull ? 1u : 0u) << j;
+              missing |= (v[j] == 0ull ? 1ull : 0ull) << j;
             }
             long long it = 0;
             while (__any_sync(0xffffffffu, missing != 0)) {
               __nanosleep(it < 8 ? 64 : 200);
 #pragma unroll
               for (int j = 0; j < kMaxLseBatch; ++j) {
-                if (missing & (1u << j)) {
+                if (missing & (1ull << j)) {
                   v[j] = ld_relaxed_u64(src + (long long)(s0 + j) * NCP + c);
-                  if (v[j] != 0ull) missing &= ~(1u << j);
+                  if (v[j] != 0ull) missing &= ~(1ull << j);
                 }
               }
               if (++it > (1LL << 22)) {
                 set_err(p.err, kDevTimeout);
 #pragma unroll
                 for (int j = 0; j < kMaxLseBatch; ++j)
-                  if (missing & (1u << j)) v[j] = pack_ms(0.f, -1.f);
+                  if (missing & (1ull << j)) v[j] = pack_ms(0.f, -1.f);
                 missing = 0;
               }
             }
