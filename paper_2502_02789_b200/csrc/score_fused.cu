@@ -392,6 +392,22 @@ __device__ __forceinline__ void transpose_merge32(float (&m)[32], float (&s)[32]
   so = s[0];
 }
 
+// Transposed butterfly sum of 32 columns x 32 lanes: lane l returns column l
+// summed over all 32 lanes (fixed order, deterministic).  31 adds per lane.
+__device__ __forceinline__ float transpose_add32(float (&s)[32], int lane) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool up = lane & w;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? s[i] : s[i + w];
+      const float keep = up ? s[i + w] : s[i];
+      s[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+    }
+  }
+  return s[0];
+}
+
 // kG: compile-time GQA group size (1, 2, 4, 8) or 0 for any G.  One
 // instantiation per group size keeps the kernel's hot code small: the warp
 // roles run different code concurrently on each SMSP and share the
@@ -570,11 +586,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   } else if (warp >= kStatsWarp0 && warp < kFinalWarp0 && p.mode != kModeFinish) {
     // ================================================================ softmax statistics
     // Progressive: each tile is folded as soon as its MMA completes into a
-    // per-thread running (ref, sum) per column, sum = sum 2^(x*xs - ref) with
-    // ref the first value seen (re-based only if a value exceeds it by > 2^64,
-    // which keeps fp32 finite): one exp2 per logit, no per-tile shuffles.  At
-    // the end of the unit one transposed merge gives the warp's (max, sum) per
-    // column; the exchange warp merges the 4 warps and publishes.
+    // per-thread running sum 2^(x*xs - ref) per column.  The reference is
+    // shared by the warp: lane 0's value in the unit's first tile (a lane whose
+    // value later exceeds it by > 2^64 re-bases its own reference -- rare --
+    // which keeps fp32 finite).  One exp2 per logit, no per-tile shuffles; at
+    // the end of the unit a transposed butterfly sum gives the warp's (ref,
+    // sum) per column (a full (max, sum) merge only if some lane re-based).
+    // The exchange warp merges the 4 warps and publishes.
     const int q = warp & 3;                       // TMEM lane quarter
     float2* red = reinterpret_cast<float2*>(smem + p.off_red);   // [2][4][NCP]
     uint32_t ui = 0, gt = 0;
@@ -590,8 +608,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
 #pragma unroll 1
         for (int grp = 0; grp < NCP / 32; ++grp) {
           float ref[32], sum[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) { ref[i] = -CUDART_INF_F; sum[i] = 0.f; }
+          float myref = 0.f;                                            // ref of column 32*grp + lane
+          bool rebased = false;
           gt = gt0;
           uint32_t slot = slot0, ph = ph0;
           for (int t = jb.t_lo; t < jb.t_hi; ++t, ++gt) {
@@ -605,12 +623,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             tmem_wait();
             tie16(*reinterpret_cast<float(*)[16]>(x0));
             tie16(*reinterpret_cast<float(*)[16]>(x0 + 16));
-            if (tok0 + (long long)(t - jb.t_lo) * kTileM < p.N) {
-              if (t == jb.t_lo) {
-                // first tile: the reference is the first value, sum = 2^0
+            if (t == jb.t_lo) {
+              // lane 0's token is valid whenever any lane's is (lowest index)
 #pragma unroll
-                for (int i = 0; i < 32; ++i) { ref[i] = x[i] * p.xs; sum[i] = 1.f; }
-              } else {
+              for (int i = 0; i < 32; ++i) {
+                ref[i] = __shfl_sync(0xffffffffu, x[i] * p.xs, 0);
+                myref = lane == i ? ref[i] : myref;
+                sum[i] = 0.f;
+              }
+            }
+            if (tok0 + (long long)(t - jb.t_lo) * kTileM < p.N) {
+              {
                 // d = y - ref; the common case adds 2^d (FFMA, MUFU, FADD + a max);
                 // a jump d > 64 (rare) re-bases that column on y to keep fp32 finite
                 float dmax = -CUDART_INF_F;
@@ -623,6 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
 #pragma unroll
                   for (int i = 0; i < 32; ++i) sum[i] += ex2(x[i]);
                 } else {
+                  rebased = true;
 #pragma unroll
                   for (int i = 0; i < 32; ++i) {
                     const bool big = x[i] > 64.f;
@@ -636,7 +660,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             if (++slot == nslots) { slot = 0; ph ^= 1; }
           }
           float mo, so;
-          transpose_merge32(ref, sum, lane, mo, so);                    // column 32*grp + lane
+          if (__any_sync(0xffffffffu, rebased)) {
+            transpose_merge32(ref, sum, lane, mo, so);                  // references differ (rare)
+          } else {
+            so = transpose_add32(sum, lane);                            // column 32*grp + lane
+            mo = myref;
+          }
           rb[q * NCP + grp * 32 + lane] = make_float2(mo, so);
         }
         if (q == 0 && lane == 0) trace_stamp(p, ui, 7);
