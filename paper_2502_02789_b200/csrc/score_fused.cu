@@ -7,26 +7,30 @@
 //   acc[r,i]    = max_{l,h} (x - lse2)               (max over H and L, log domain)
 //   imp[b][i]   = (1/Rv) sum_{r<Rv} 2^acc[r,i]       (mean over the valid look-ahead rows)
 //
-// Design (DESIGN.md "Fused score kernel"):
+// Design (DESIGN.md §5.1):
 // * Persistent cooperative grid, one CTA per SM.  A request's N tokens are cut
 //   into 128-token tiles and its L*Hkv (layer, kv-head) "units" into groups; a
 //   job = (request, token group, unit group).  All jobs of one request run in
 //   the same wave of CTAs, so every CTA that shares a unit is co-resident.
 // * Warp roles (384 threads): warp 0 TMA producer, warp 1 tcgen05.mma issuer
-//   (+TMEM owner), warps 4-7 softmax statistics, warps 8-11 max-aggregation.
-// * K tiles [128 tokens x d] bf16 stream HBM -> SMEM by TMA (SWIZZLE_128B);
-//   the unit's query block [G*Rv x d] is the MMA B operand; the logits
-//   D[128 x G*Rv] fp32 accumulate in TMEM and STAY there: every tile of the
-//   unit is resident (tiles_per_cta * Ncols <= 256 columns, two unit slots).
-// * Statistics warps reduce each unit's columns over the CTA's tokens (online
-//   (m, l) in the log2 domain), publish the CTA partial to global memory and
-//   bump the unit's counter.  Aggregation warps wait for all token groups of
-//   the unit, combine the partials in fixed order (deterministic lse), re-read
-//   the logits from TMEM and fold max_h (x - lse2) into a per-token running
-//   max kept in SMEM.  K is read from HBM exactly once; logits never leave
-//   the chip.
+//   (+TMEM owner), warp 2 statistics exchange, warp 3 lse2 gather, warps 4-7
+//   softmax statistics, warps 8-11 max-aggregation.  The TMA/MMA warps run
+//   warp-uniform loops and issue from one elected lane.
+// * K tiles [128 tokens x d] bf16 stream HBM -> SMEM by TMA (swizzled); the
+//   unit's query block [G*Rv x d] is the MMA B operand; each tile's logits
+//   D[128 x NCP] fp32 go to the next slot of a 16-slot TMEM ring and stay
+//   there until aggregated: logits never leave the chip, K is read once.
+// * Statistics warps fold every tile into per-column running sums as soon as
+//   its MMA lands; the exchange warp publishes the CTA partial (one 64-bit
+//   (max, sum) word per column); the gather warp polls the unit's partials of
+//   all token groups and merges them in fixed order (bit-identical lse2 in
+//   every CTA); the aggregation warps fold max_h (x - lse2) into a per-token
+//   running max in SMEM and release the TMEM slots.
 // * Cross-unit-group max: partial acc maps go to the workspace and the CTAs of
 //   a token group split the final mean-of-exp2 among themselves.
+// * Instantiated per GQA group size and per "one 32-column group" (NCP = 32):
+//   the warp roles share the SM's instruction cache, so the executed code is
+//   kept small (measured: code size moved C3 by > 20 %).
 #include "sp_internal.h"
 
 #include <cuda.h>
