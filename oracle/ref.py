@@ -63,6 +63,25 @@ def attention_scores(Q: np.ndarray, K: np.ndarray, scale: float) -> np.ndarray:
     return A
 
 
+def softmax_lse(Q: np.ndarray, K: np.ndarray, scale: float) -> np.ndarray:
+    """O2's normaliser on its own: lse[l][h][r] = ln sum_i exp(s[l,h,r,i]) over
+    the prompt keys (Z2), s as in O1.  This is the per-row log-sum-exp
+    an attention kernel of the speculator returns: given it,
+    the softmax of O2 is exp(s - lse).
+
+    Q [L][R][H][d] f64, K [L][Hkv][N][d] f64 -> lse [L][H][R] f64.
+    """
+    L, R, H, d = Q.shape
+    G = H // K.shape[1]
+    out = np.empty((L, H, R), dtype=np.float64)
+    for l in range(L):
+        for h in range(H):
+            s = scale * (Q[l, :, h, :] @ K[l, h // G].T)      # [R][N]
+            m = s.max(axis=1)
+            out[l, h] = m + np.log(np.exp(s - m[:, None]).sum(axis=1))
+    return out
+
+
 # ------------------------------------------------------------------ O3-O4
 def aggregate_attention(A: np.ndarray, R_valid: int | None = None) -> np.ndarray:
     """Max-mean aggregation, P:117-119 (sec:attn_agg): "take the maximum over H

@@ -661,6 +661,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
                 }
               }
             }
+            if (p.mode == kModeStats && grp + 1 == NCP / 32) {
+              // statistics-only launch: no aggregation reads the tile, release it here
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(bar_tempty + 8 * slot);
+            }
             if (++slot == nslots) { slot = 0; ph ^= 1; }
           }
           float mo, so;
@@ -786,7 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         if (lane == 0) trace_stamp(p, ui, 4);
       }
     }
-  } else if (warp >= kFinalWarp0) {
+  } else if (warp >= kFinalWarp0 && p.mode != kModeStats) {
     // ================================================================ (l,h)-max aggregation
     const int q = warp & 3;
     float* acc = reinterpret_cast<float*>(smem + p.off_acc);      // [tpc][Rv][128]
@@ -800,7 +806,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         for (int r = 0; r < p.Rv; ++r) acc[(t * p.Rv + r) * kTileM + tok] = -CUDART_INF_F;
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
         const uint32_t par = ui % kLseRing;
-        if (p.mode != kModeStats) mbar_wait(bar_lfull + 8 * par, (ui / kLseRing) & 1);
+        mbar_wait(bar_lfull + 8 * par, (ui / kLseRing) & 1);
         const float* ls = lse_s + par * NCP;
         uint32_t slot = gt % nslots, ph = (gt / nslots) & 1;
         if constexpr (kNCP == 32) {
@@ -814,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           for (int t = 0; t < ntile; ++t, ++gt) {
             mbar_wait(bar_tfull + 8 * slot, ph);
             tc_fence_after();
-            if (p.mode != kModeStats) {
+            {
               const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + slot * 32;
               float* arow = acc + (t * p.Rv) * kTileM + tok;
               float xa[16], xb[16];
@@ -838,7 +844,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + slot * NCP;
           float* arow = acc + (t * p.Rv) * kTileM + tok;
 #pragma unroll 1
-          for (int k0 = 0; k0 < NCP / 16 && p.mode != kModeStats; k0 += 2) {
+          for (int k0 = 0; k0 < NCP / 16; k0 += 2) {
             float xa[16], xb[16];
             const bool two = k0 + 1 < NCP / 16;
             tmem_ld16_issue(ta + k0 * 16, xa);
@@ -865,10 +871,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           if (++slot == nslots) { slot = 0; ph ^= 1; }
         }
         __syncwarp();
-        if (lane == 0 && p.mode != kModeStats) mbar_arrive(bar_lempty + 8 * par);
+        if (lane == 0) mbar_arrive(bar_lempty + 8 * par);
         if (q == 0 && lane == 0) trace_stamp(p, ui, 6);
       }
-      if (p.mode == kModeStats) continue;                             // no importance in stats-only mode
       // ---- job epilogue: importance = mean_r 2^acc (possibly across unit groups)
       const float inv = 1.f / (float)p.Rv;
       if (p.n_ug == 1) {

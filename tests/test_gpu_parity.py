@@ -308,3 +308,37 @@ def test_split_api_virtual_ranks(split_algo, P, monkeypatch):
     ids, pos, nk = sp.select(imp.contiguous(), w.keep, w.pool_k, w.chunk)
     o = ref.select(exact, w.keep, w.pool_k, w.chunk)
     _util.check_selection(ids[0].cpu().numpy(), pos[0].cpu().numpy(), int(nk[0]), o, w.chunk, w.N, 0)
+
+
+# ---------------------------------------------------------------- row f2: lse handed over by the caller
+def test_lse_handover_f2():
+    """when the per-row log-sum-exp over the prompt keys is
+    supplied (an attention kernel of the speculator returns it), sp_score_finish
+    computes the importance in one pass over K with no statistics exchange."""
+    w = gen.CONFIGS["C1"].with_(N=2000, L=4, R_valid=6)
+    Q, K, T = spgen_cuda.make_inputs(w)
+    Qf = ref.bf16_to_f64(np.stack([gen.gen_Q(w, 0, l) for l in range(w.L)]))      # [L][R][H][d]
+    Kf = np.stack([_util.k_layer_f64(w, 0, l) for l in range(w.L)])              # [L][Hkv][N][d]
+    lse = ref.softmax_lse(Qf[:, :w.Rv], Kf, w.scale)                               # [L][H][Rv], natural log
+    lse2 = torch.tensor((lse / math.log(2.0)).reshape(-1), dtype=torch.float32, device="cuda")
+    imp = sp.score_finish(Q, K, lse2, w.Rv, w.scale)
+    sp.check_device_error()
+    exact = _util.oracle_importance(w, 0)
+    assert _util.rel_err(imp[0].double().cpu().numpy(), exact) <= _util.REL_TOL
+
+
+def test_split_stats_repeatable():
+    """Statistics-only launches, back to back: the TMEM ring is released by the
+    statistics warps (no aggregation runs), so the MMA can never lap a tile the
+    statistics have not read -- every launch gives the same bits."""
+    w = gen.CONFIGS["C3"].with_(N=8192)
+    Q, K, T = spgen_cuda.make_inputs(w)
+    first = sp.score_stats(Q, K, w.Rv, w.scale).clone()
+    for _ in range(40):
+        st = sp.score_stats(Q, K, w.Rv, w.scale)
+        assert torch.equal(st, first)
+    sp.check_device_error()
+    lse2 = sp.stats_combine(first[None].contiguous())
+    imp = sp.score_finish(Q, K, lse2, w.Rv, w.scale)
+    full = sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")
+    assert _util.rel_err(imp[0].double().cpu().numpy(), full[0].double().cpu().numpy()) <= 1e-5

@@ -327,3 +327,25 @@ def test_margin():
     assert ref.margin(np.array([3.0, 2.0, 1.0]), 3) == math.inf
     assert ref.margin(np.array([3.0, 2.0, 1.0]), 1) == pytest.approx(1 / 3)
     assert ref.margin(np.array([2.0, 2.0, 1.0]), 1) == 0.0
+
+
+# ---------------------------------------------------------------- O2 normaliser (row f2 hand-over)
+def test_softmax_lse_closed_forms_and_library():
+    """lse pins: uniform keys (all logits equal c) give c + ln N; the needle case
+    gives ln(e^{2s} + N - 1); in general it equals scipy's logsumexp of the
+    logits, and exp(s - lse) rows sum to one."""
+    N, d = 10, 16
+    Q = np.zeros((1, 1, 1, d)); Q[0, 0, 0, 0] = 1.0
+    K = np.zeros((1, 1, N, d)); K[0, 0, 3, 0] = 2.0
+    lse = ref.softmax_lse(Q, K, 0.5)
+    assert lse[0, 0, 0] == pytest.approx(math.log(math.exp(1.0) + N - 1), rel=1e-15)
+    K1 = np.zeros((1, 1, N, d)); K1[0, 0, :, 0] = 3.0            # every logit = 0.5 * 3
+    assert ref.softmax_lse(Q, K1, 0.5)[0, 0, 0] == pytest.approx(1.5 + math.log(N), rel=1e-15)
+    rng = np.random.default_rng(11)
+    Q, K = _rand_qk(rng, 2, 4, 2, 33, 8, 3, dyadic=False)
+    lse = ref.softmax_lse(Q, K, 0.3)
+    for l in range(2):
+        for h in range(4):
+            s = 0.3 * (Q[l, :, h, :] @ K[l, h // 2].T)
+            np.testing.assert_allclose(lse[l, h], scipy.special.logsumexp(s, axis=1), rtol=1e-14)
+            np.testing.assert_allclose(np.exp(s - lse[l, h][:, None]).sum(axis=1), 1.0, rtol=1e-13)
