@@ -173,6 +173,23 @@ sp_status sp_stats_combine(const float* parts, int32_t P, int64_t n_rows, float*
 sp_status sp_score_finish(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay,
                           const float* lse2, float* importance, void* ws, size_t ws_bytes, sp_stream stream);
 
+/* ------------------------------------------------------------------ score, head-sharded partition
+ * the (l, h)-max of O3 is
+ * order-free, so the query heads (with their kv heads: H and Hkv divided by the
+ * same P, G unchanged) can be split over P ranks.  Each rank passes its own
+ * Q/K heads; every lse is complete on its rank (all N tokens are local), so
+ * the only exchange is an elementwise MAX of
+ *   acc2 [B][R_valid][N] fp32 = max_{local l,h} (x - lse2)   (log2 domain, x = s*log2 e)
+ * followed by sp_acc_importance: importance[b][i] = (1/R_valid) sum_r 2^acc2[b][r][i]
+ * (the fused kernel's own epilogue arithmetic).  sp_score_acc runs the fused
+ * kernel only (SP_EUNSUPPORTED otherwise); its workspace is
+ * sp_score_workspace_bytes(g, SP_SCORE_FUSED).  acc2 is written for every
+ * valid (b, r, i); the caller owns it. */
+sp_status sp_score_acc(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, float* acc2,
+                       void* ws, size_t ws_bytes, sp_stream stream);
+sp_status sp_acc_importance(const float* acc2, int32_t B, int32_t R_valid, int64_t N, float* importance,
+                            sp_stream stream);
+
 /* ------------------------------------------------------------------ select
  * Pool, chunk means, top-K_c chunks, positions (O5-O9, Alg.1):
  *   pooled[i] = mean(importance[j] : |j-i| <= (pool_k-1)/2, 0 <= j < N)      (Z6)

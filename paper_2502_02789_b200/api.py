@@ -167,6 +167,30 @@ def score_finish(Q, K, lse2, R_valid=None, scale=None, out=None, stream=None) ->
     return out
 
 
+def score_acc(Q, K, R_valid=None, scale=None, out=None, stream=None) -> torch.Tensor:
+    """Head-sharded partition (row f1): acc2 [B][R_valid][N] = max over this
+    rank's (layer, head) of the log2-domain log-probability; MAX-reduce across
+    ranks, then acc_importance."""
+    g, lay = make_geom(Q, K, R_valid, scale)
+    out = torch.empty((g.B, g.R_valid, g.N), dtype=torch.float32, device=K.device) if out is None else out
+    nbytes = lib().sp_score_workspace_bytes(C.byref(g), _lib.SP_SCORE_FUSED)
+    ws = workspace(("score", "fused", _geom_key(g)), nbytes, K.device)
+    check(lib().sp_score_acc(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), out.data_ptr(), ws.data_ptr(),
+                             ws.numel(), _stream_ptr(stream)), "sp_score_acc")
+    return out
+
+
+def acc_importance(acc2, out=None, stream=None) -> torch.Tensor:
+    """importance[b][i] = mean_r 2^acc2[b][r][i] (after the cross-rank MAX)."""
+    if acc2.dtype != torch.float32 or not acc2.is_contiguous() or acc2.dim() != 3:
+        raise ValueError("acc2 must be contiguous fp32 [B][R_valid][N]")
+    B, Rv, N = acc2.shape
+    out = torch.empty((B, N), dtype=torch.float32, device=acc2.device) if out is None else out
+    check(lib().sp_acc_importance(acc2.data_ptr(), B, Rv, N, out.data_ptr(), _stream_ptr(stream)),
+          "sp_acc_importance")
+    return out
+
+
 def _split_algo():
     import os
     return os.environ.get("SP_SPLIT_ALGO", "auto")

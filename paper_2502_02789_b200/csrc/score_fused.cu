@@ -89,6 +89,7 @@ struct FusedParams {
   float* accpart;                      // [B][n_ug][Rv][N]
   unsigned* fin_cnt;                   // [B][n_tg]    finalize counters (self-cleaning)
   float* imp;                          // [B][N]
+  float* acc_out;                      // head-sharded partition: [B][Rv][N] log2-domain max instead of imp
   int* err;
   unsigned long long* trace;           // optional [grid][trace_units][8] globaltimer stamps (debug)
   int trace_units;
@@ -875,11 +876,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         if (q == 0 && lane == 0) trace_stamp(p, ui, 6);
       }
       // ---- job epilogue: importance = mean_r 2^acc (possibly across unit groups)
+      //      or, head-sharded (acc_out), the log2-domain max itself for a max-reduce across ranks
       const float inv = 1.f / (float)p.Rv;
       if (p.n_ug == 1) {
         for (int t = 0; t < ntile; ++t) {
           const long long i = (long long)(jb.t_lo + t) * kTileM + tok;
           if (i < p.N) {
+            if (p.acc_out != nullptr) {
+              for (int r = 0; r < p.Rv; ++r)
+                p.acc_out[((long long)jb.b * p.Rv + r) * p.N + i] = acc[(t * p.Rv + r) * kTileM + tok];
+              continue;
+            }
             float s = 0.f;
             for (int r = 0; r < p.Rv; ++r) s += ex2(acc[(t * p.Rv + r) * kTileM + tok]);
             p.imp[(long long)jb.b * p.N + i] = s * inv;
@@ -912,9 +919,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             float m = -CUDART_INF_F;
             for (int g = 0; g < p.n_ug; ++g)
               m = fmaxf(m, __ldcg(&p.accpart[(((long long)jb.b * p.n_ug + g) * p.Rv + r) * p.N + i]));
+            if (p.acc_out != nullptr) p.acc_out[((long long)jb.b * p.Rv + r) * p.N + i] = m;
             s += ex2(m);
           }
-          p.imp[(long long)jb.b * p.N + i] = s * inv;
+          if (p.acc_out == nullptr) p.imp[(long long)jb.b * p.N + i] = s * inv;
         }
         named_bar(2, 128);
         if (threadIdx.x == kFinalWarp0 * 32) {
@@ -1176,7 +1184,8 @@ __global__ void k_partials_to_stats(const unsigned long long* __restrict__ part,
 }  // namespace
 
 cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay, int mode,
-                         const float* lse_in, float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
+                         const float* lse_in, float* importance, void* ws, size_t ws_bytes, cudaStream_t st,
+                         float* acc_out = nullptr) {
   Plan pl = make_plan(g);
   if (!pl.ok || ws_bytes < pl.ws_total()) return cudaErrorInvalidValue;
   static FusedParams p;                               // large (two tensor maps); host-side scratch
@@ -1203,6 +1212,7 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   w += pl.ws_part;
   p.accpart = pl.ws_acc ? reinterpret_cast<float*>(w) : nullptr;
   p.imp = importance;
+  p.acc_out = acc_out;
   p.err = device_error_flag();
   p.trace = nullptr;
   p.mode = mode;
@@ -1271,6 +1281,30 @@ cudaError_t fused_score_stats(const __nv_bfloat16* Q, const __nv_bfloat16* K, co
 cudaError_t fused_score_finish(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                                const float* lse2, float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
   return fused_launch(Q, K, g, lay, kModeFinish, lse2, importance, ws, ws_bytes, st);
+}
+
+cudaError_t fused_score_acc(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                            float* acc2, void* ws, size_t ws_bytes, cudaStream_t st) {
+  return fused_launch(Q, K, g, lay, kModeFull, nullptr, nullptr, ws, ws_bytes, st, acc2);
+}
+
+namespace {
+// imp[b][i] = (1/Rv) sum_{r<Rv} 2^acc2[b][r][i] -- the fused epilogue's arithmetic,
+// applied after the head-sharded max-reduce.
+__global__ void k_acc_importance(const float* __restrict__ acc2, int B, int Rv, long long N, float* __restrict__ imp) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)B * N) return;
+  const long long b = idx / N, i = idx % N;
+  float s = 0.f;
+  for (int r = 0; r < Rv; ++r) s += ex2(acc2[(b * Rv + r) * N + i]);
+  imp[idx] = s * (1.f / (float)Rv);
+}
+}  // namespace
+
+cudaError_t acc_importance(const float* acc2, int B, int Rv, long long N, float* importance, cudaStream_t st) {
+  const long long n = (long long)B * N;
+  k_acc_importance<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(acc2, B, Rv, N, importance);
+  return cudaGetLastError();
 }
 
 }  // namespace sp

@@ -180,6 +180,30 @@ sp_status sp_score(const void* Q, const void* K, const sp_geom* g, const sp_layo
   return sp_score_ex(Q, K, g, lay, importance, ws, ws_bytes, SP_SCORE_AUTO, stream);
 }
 
+sp_status sp_score_acc(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, float* acc2, void* ws,
+                       size_t ws_bytes, sp_stream stream) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if ((s = check_layout(g, lay, Q, K)) != SP_OK) return s;
+  if (acc2 == nullptr) return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
+  const Geom G = to_geom(*g);
+  const Layout Lay = to_layout(*lay);
+  if (!fused_supported(G, Lay, Q, K)) return SP_EUNSUPPORTED;
+  const size_t need = score_ws(G, SP_SCORE_FUSED);
+  if (ws == nullptr || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return SP_EWORKSPACE;
+  return from_cuda(fused_score_acc(reinterpret_cast<const __nv_bfloat16*>(Q), reinterpret_cast<const __nv_bfloat16*>(K),
+                                   G, Lay, acc2, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sp_status sp_acc_importance(const float* acc2, int32_t B, int32_t R_valid, int64_t N, float* importance,
+                            sp_stream stream) {
+  if (acc2 == nullptr || importance == nullptr || B < 1 || R_valid < 1 || N < 1) return SP_EINVAL;
+  sp_status s = check_device();
+  if (s != SP_OK) return s;
+  return from_cuda(acc_importance(acc2, B, R_valid, N, importance, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 sp_status sp_score_plan(const sp_geom* g, int64_t out[9]) {
   sp_status s = check_geom(g);
   if (s != SP_OK) return s;

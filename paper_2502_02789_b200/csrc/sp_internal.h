@@ -71,6 +71,9 @@ cudaError_t fused_score_stats(const __nv_bfloat16* Q, const __nv_bfloat16* K, co
                               float* stats, void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t fused_score_finish(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                                const float* lse2, float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t fused_score_acc(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                            float* acc2, void* ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t acc_importance(const float* acc2, int B, int Rv, long long N, float* importance, cudaStream_t st);
 
 // ---------------------------------------------------------------- select / gather (select.cu, gather.cu)
 size_t select_ws_bytes(int B, long long N, int chunk);

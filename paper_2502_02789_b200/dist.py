@@ -4,6 +4,11 @@
 * Batch sharding -- requests are independent: rank p
   scores and selects its own requests with the single-GPU kernels, no
   collective on the data path.
+* Head sharding -- the query heads (with their kv heads)
+  split over the ranks: every lse is complete on its rank, the (l,h)-max is
+  order-free, so the one exchange is an elementwise MAX all-reduce of
+  acc2 [B][R_valid][N] (log2 domain), then importance = mean_r 2^acc2
+  (sp_score_acc -> all_reduce(MAX) -> sp_acc_importance) and the selection.
 * Sequence sharding -- one request's prompt split along tokens.  The only real
   exchange is the softmax statistics (the lse of every (layer, head, row) needs
   all N keys):
@@ -52,6 +57,14 @@ class CudaBackend:
         return api.score_finish(Q, K, lse2, R_valid, scale)
 
     @staticmethod
+    def score_acc(Q, K, R_valid, scale):
+        return api.score_acc(Q, K, R_valid, scale)
+
+    @staticmethod
+    def acc_importance(acc2):
+        return api.acc_importance(acc2)
+
+    @staticmethod
     def select(imp, keep, pool_k, chunk, pos0, tokens):
         return api.select(imp, keep, pool_k, chunk, pos0, tokens=tokens)
 
@@ -77,6 +90,30 @@ def seq_sharded_specprefill(Q, K_local, tokens, N_total: int, keep: float, pool_
     imp = imp.view(1, N_total)                                               # rank order = token order
     ids, pos, n_kept, out = be.select(imp, keep, pool_k, chunk, pos0, tokens)
     return dict(importance=imp, ids=ids, pos=pos, n_kept=n_kept, out_tokens=out, first_decode=N_total + pos0)
+
+
+def head_range(Hkv: int, world: int, rank: int) -> tuple[int, int]:
+    """kv heads [g0, g1) of rank `rank` for head sharding (query heads
+    [g0*G, g1*G)); Hkv must be a multiple of world (equal head groups)."""
+    if Hkv % world:
+        raise ValueError(f"head sharding needs Hkv ({Hkv}) divisible by the number of ranks ({world})")
+    n = Hkv // world
+    return rank * n, (rank + 1) * n
+
+
+def head_sharded_specprefill(Q_local, K_local, tokens, keep: float, pool_k: int, chunk: int, R_valid=None,
+                             scale=None, pos0: int = 0, group=None, backend=None) -> dict:
+    """Head-sharded path: Q_local [B][L][R][H/P][d] and K_local [B][L][Hkv/P][N][d]
+    hold this rank's heads (head_range); tokens [B][N] replicated.  The scale
+    must be given explicitly (it depends on d only, but keep it the caller's).
+    Returns importance [B][N], ids, pos, n_kept, out_tokens (replicated)."""
+    be = backend or CudaBackend
+    acc2 = be.score_acc(Q_local, K_local, R_valid, scale)                      # [B][Rv][N]
+    dist.all_reduce(acc2, op=dist.ReduceOp.MAX, group=group)                  # order-free: exact
+    imp = be.acc_importance(acc2.contiguous())
+    ids, pos, n_kept, out = be.select(imp, keep, pool_k, chunk, pos0, tokens)
+    N = imp.shape[1]
+    return dict(importance=imp, ids=ids, pos=pos, n_kept=n_kept, out_tokens=out, first_decode=N + pos0)
 
 
 def batch_sharded_specprefill(Q, K, tokens, keep, pool_k, chunk, R_valid=None, scale=None, pos0=0) -> dict:

@@ -342,3 +342,24 @@ def test_split_stats_repeatable():
     imp = sp.score_finish(Q, K, lse2, w.Rv, w.scale)
     full = sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")
     assert _util.rel_err(imp[0].double().cpu().numpy(), full[0].double().cpu().numpy()) <= 1e-5
+
+
+# ---------------------------------------------------------------- row f1: head-sharded partition (virtual ranks)
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_head_sharded_virtual_ranks(P):
+    """Row f1: the heads split over P virtual ranks on one GPU (strided views of
+    Q and K), sp_score_acc per rank, an elementwise MAX across ranks (what
+    all_reduce(MAX) computes) and sp_acc_importance equal the oracle on the
+    whole model, and the single-launch sp_score to fp32 rounding."""
+    w = gen.CONFIGS["C1"].with_(N=3000, R_valid=5)
+    Q, K, T = spgen_cuda.make_inputs(w)
+    n = w.Hkv // P
+    accs = [sp.score_acc(Q[:, :, :, p * n * w.G:(p + 1) * n * w.G], K[:, :, p * n:(p + 1) * n], w.Rv, w.scale)
+            for p in range(P)]
+    acc = torch.stack(accs).amax(dim=0).contiguous()
+    imp = sp.acc_importance(acc)
+    sp.check_device_error()
+    exact = _util.oracle_importance(w, 0)
+    assert _util.rel_err(imp[0].double().cpu().numpy(), exact) <= _util.REL_TOL
+    full = sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")
+    assert _util.rel_err(imp[0].double().cpu().numpy(), full[0].double().cpu().numpy()) <= 1e-5
