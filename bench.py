@@ -42,9 +42,10 @@ def parse():
     ap.add_argument("--config", default="C3", choices=["C0", "C1", "C2", "C3", "C4"])
     ap.add_argument("--algo", default="fused", choices=["fused", "simt", "auto"])
     ap.add_argument("--plan", default=None, help="fused-kernel decomposition override 'n_tg,n_ug'")
-    ap.add_argument("--shard", default="batch", choices=["batch", "seq"],
+    ap.add_argument("--shard", default="batch", choices=["batch", "seq", "head"],
                     help="N>1: batch = one request per rank, no collective (weak scaling); "
-                         "seq = the prompt split over ranks with the NCCL statistics exchange (strong scaling)")
+                         "seq = the prompt split over ranks with the NCCL statistics exchange (strong scaling); "
+                         "head = the heads split over ranks, NCCL MAX all-reduce of the log-domain maxima (strong)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -194,7 +195,8 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     seq = world > 1 and args.shard == "seq"
-    if world > 1 and not seq:
+    head = world > 1 and args.shard == "head"
+    if world > 1 and not (seq or head):
         w = w.with_(seed=w.seed + rank)              # batch sharding: each rank owns different requests
 
     # ---- inputs resident in HBM (device-side generator, bit-identical to spgen.gen)
@@ -204,6 +206,11 @@ def run_ours(args):
         Q, K, T = spgen_cuda.make_inputs(w, device=dev, i0=i0, n_local=i1 - i0)
     else:
         Q, K, T = spgen_cuda.make_inputs(w, device=dev)
+    if head:                                         # this rank's heads (strided views of the whole inputs)
+        from paper_2502_02789_b200 import dist as spd
+        g0, g1 = spd.head_range(w.Hkv, world, rank)
+        Qh_, Kh_ = Q[:, :, :, g0 * w.G:g1 * w.G], K[:, :, g0:g1]
+        acc_buf = torch.empty((w.B, w.Rv, w.N), dtype=torch.float32, device=dev)
     torch.cuda.synchronize()
     imp = torch.empty((w.B, w.N), dtype=torch.float32, device=dev)
     ids = torch.empty((w.B, w.N), dtype=torch.int32, device=dev)
@@ -237,6 +244,16 @@ def run_ours(args):
             score_only()
             select_only()
 
+    if head:
+        def score_only():                              # noqa: F811 -- head-sharded scoring + MAX all-reduce
+            sp.score_acc(Qh_, Kh_, w.Rv, w.scale, out=acc_buf)
+            dist.all_reduce(acc_buf, op=dist.ReduceOp.MAX)
+            sp.acc_importance(acc_buf, out=imp)
+
+        def step():                                    # noqa: F811
+            score_only()
+            select_only()
+
     for _ in range(args.warmup):
         step()
     sp.check_device_error()
@@ -245,7 +262,7 @@ def run_ours(args):
     # roofline): replays cost one graph launch, no host work per kernel
     graph_note = "eager"
     run_step, run_score = step, score_only
-    if not args.no_graph and not seq:
+    if not args.no_graph and not (seq or head):
         try:
             g_step, g_score = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
             with torch.cuda.graph(g_step):
@@ -296,13 +313,14 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_total, score_ms = tt.tolist()
     ms_step = ms_total / args.steps
-    tokens_per_step = w.B * w.N * (1 if seq else world)
+    tokens_per_step = w.B * w.N * (1 if (seq or head) else world)
     value = tokens_per_step / (ms_step / 1000.0)
 
     # ---- roofline of the dominant kernel (sp_score): algorithmic bytes / duration
     peak, peak_src = peaks()
     q_bytes = w.B * w.L * w.Rv * w.H * w.d * 2
-    alg_bytes = (w.k_bytes // world if seq else w.k_bytes) + q_bytes + w.B * w.N * 4
+    alg_bytes = ((w.k_bytes // world if (seq or head) else w.k_bytes) + (q_bytes // world if head else q_bytes)
+                 + w.B * w.N * 4)
     achieved = alg_bytes / (score_ms / 1000.0) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -316,7 +334,7 @@ def run_ours(args):
 
     # ---- end to end through the C ABI with host (pinned) buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not (seq or head):          # sp_run_host is the single-GPU / batch-sharded call
         e2e = run_e2e(args, w, Q, K, T, dev, stream, dist, world)
 
     # select_gather is one launch, or two for long prompts (phase A over the SMs,
@@ -328,11 +346,13 @@ def run_ours(args):
     plan = sp.score_plan(Q, K, w.Rv) if args.algo != "simt" else None
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if seq else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong" if (seq or head) else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{args.config} {w.name}", "B": w.B, "N": w.N, "L": w.L, "H": w.H, "Hkv": w.Hkv,
                        "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk,
                        "algo": args.algo, "plan": plan, "launch": graph_note, "shard": args.shard if world > 1 else None,
                        "parallelism": (f"seq{world} (prompt split, NCCL stats all-gather)" if seq else
+                                       f"tp{world} (head split, NCCL MAX all-reduce of the log-domain maxima)"
+                                       if head else
                                        f"dp{world} (batch-sharded: one request per rank, no collective)")
                        if world > 1 else "single",
                        "l2": f"inputs larger than L2 (K = {w.k_bytes / 2**30:.2f} GiB per GPU), no flush"},
