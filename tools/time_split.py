@@ -34,3 +34,11 @@ for name, fn in [("score (fused)", lambda: sp.score(Q, K, R_valid=w.Rv, scale=w.
                  ("score_finish", lambda: sp.score_finish(Q, K, lse2, w.Rv, w.scale))]:
     ms = timed(fn)
     print(f"{w.name} {name:14s} {ms:.4f} ms  {kb / ms:.2f} TB/s of K")
+
+# row f1: one rank's share of a P-way head split (the rest is an all-reduce of 4*Rv B/token)
+for P in (2, 8):
+    n = w.Hkv // P
+    Qh, Kh = Q[:, :, :, :n * w.G], K[:, :, :n]
+    acc = sp.score_acc(Qh, Kh, w.Rv, w.scale)
+    ms = timed(lambda: sp.score_acc(Qh, Kh, w.Rv, w.scale, out=acc))
+    print(f"{w.name} score_acc 1/{P} heads {ms:.4f} ms  {kb / P / ms:.2f} TB/s of K  (all-reduce {acc.numel() * 4 / 1e6:.1f} MB)")
