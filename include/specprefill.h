@@ -190,6 +190,33 @@ sp_status sp_score_acc(const void* Q, const void* K, const sp_geom* g, const sp_
 sp_status sp_acc_importance(const float* acc2, int32_t B, int32_t R_valid, int64_t N, float* importance,
                             sp_stream stream);
 
+/* ------------------------------------------------------------------ score, sequence-sharded single pass
+ * The prompt split along tokens over `world` ranks (<= 8), one launch per rank,
+ * K read once: the fused kernel's per-unit softmax-statistics exchange runs
+ * over peer memory.  Each CTA stores its 64-bit (max2, sum) partial words into
+ * EVERY rank's partial buffer (NVLink stores, st.relaxed.sys) and gathers the
+ * unit's world*n_tg partials from its own buffer in fixed (rank, token group)
+ * order, so every rank computes the same lse2 bit for bit; the importance of
+ * the rank's own tokens is written to importance [B][N_local].
+ * peer_buffers: host array of `world` device pointers (256-B aligned), entry r =
+ * rank r's partial buffer of sp_score_peer_buffer_bytes(g, world, sm_budget)
+ * bytes, mapped into this process (e.g. torch symmetric memory), zero-filled
+ * once before first use (the kernel leaves it re-zeroed).  All ranks pass the
+ * same geometry (equal shards), world and sm_budget, and their launches of one
+ * call must be co-resident (they wait for each other inside the kernel; a
+ * missing rank ends in a device timeout).  Consecutive calls must be separated
+ * by a cross-rank barrier (the importance all-gather that follows is one).
+ * sm_budget > 0 caps the CTAs per launch (0 = every SM), so several "ranks"
+ * can share one GPU (the virtual-rank tests).  ws: a private workspace of
+ * sp_score_peer_workspace_bytes(g, sm_budget) bytes, zero-filled once.
+ * sp_score_peer_plan reports the plan (as sp_score_plan) under sm_budget. */
+size_t sp_score_peer_buffer_bytes(const sp_geom* g, int32_t world, int32_t sm_budget);
+size_t sp_score_peer_workspace_bytes(const sp_geom* g, int32_t sm_budget);
+sp_status sp_score_peer_plan(const sp_geom* g, int32_t sm_budget, int64_t out[9]);
+sp_status sp_score_peer(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, int32_t rank,
+                        int32_t world, void* const* peer_buffers, int32_t sm_budget, float* importance, void* ws,
+                        size_t ws_bytes, sp_stream stream);
+
 /* ------------------------------------------------------------------ select
  * Pool, chunk means, top-K_c chunks, positions (O5-O9, Alg.1):
  *   pooled[i] = mean(importance[j] : |j-i| <= (pool_k-1)/2, 0 <= j < N)      (Z6)

@@ -191,6 +191,36 @@ def acc_importance(acc2, out=None, stream=None) -> torch.Tensor:
     return out
 
 
+def score_peer_buffer_bytes(Q, K, world: int, sm_budget: int = 0, R_valid=None) -> int:
+    """Bytes of one rank's partial buffer for score_peer (this rank's shard geometry)."""
+    g, _ = make_geom(Q, K, R_valid)
+    return int(lib().sp_score_peer_buffer_bytes(C.byref(g), world, sm_budget))
+
+
+def score_peer_plan(Q, K, sm_budget: int = 0, R_valid=None) -> dict:
+    g, _ = make_geom(Q, K, R_valid)
+    out = (C.c_int64 * 9)()
+    check(lib().sp_score_peer_plan(C.byref(g), sm_budget, out), "sp_score_peer_plan")
+    keys = ("grid", "jobs_per_request", "token_groups", "unit_groups", "tiles_per_job", "units_per_job",
+            "tmem_slots", "stages", "smem_bytes")
+    return dict(zip(keys, list(out)))
+
+
+def score_peer(Q, K, rank: int, world: int, peer_ptrs, sm_budget: int = 0, R_valid=None, scale=None, out=None,
+               stream=None, ws_tag=None) -> torch.Tensor:
+    """Sequence-sharded single pass: importance of this rank's tokens, the
+    statistics exchanged in-kernel through the peers' partial buffers
+    (peer_ptrs: `world` device addresses, rank order)."""
+    g, lay = make_geom(Q, K, R_valid, scale)
+    out = torch.empty((g.B, g.N), dtype=torch.float32, device=K.device) if out is None else out
+    nbytes = lib().sp_score_peer_workspace_bytes(C.byref(g), sm_budget)
+    ws = workspace(("peer", _geom_key(g), sm_budget, rank if ws_tag is None else ws_tag), nbytes, K.device)
+    ptrs = (C.c_void_p * world)(*[int(x) for x in peer_ptrs])
+    check(lib().sp_score_peer(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), rank, world, ptrs, sm_budget,
+                              out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_score_peer")
+    return out
+
+
 def _split_algo():
     import os
     return os.environ.get("SP_SPLIT_ALGO", "auto")

@@ -63,6 +63,7 @@ constexpr int kMaxChunks = 8;          // NCP <= 128 columns (16-column chunks)
 constexpr int kMaxSlots = 16;          // TMEM tile slots (512 columns / 32)
 constexpr int kLseRing = 8;            // lse2 buffers in SMEM (gather may run ahead of aggregation)
 constexpr int kMaxLseBatch = 10;       // 64-bit partial words in flight per lane
+constexpr int kMaxPeers = 8;           // ranks of a peer-memory statistics exchange
 constexpr int kTmemCols = 512;
 constexpr double kSmHbmBytesPerUs = 7.0e6 / 148;   // one SM's share of ~7 TB/s, bytes per microsecond
 constexpr int kSmemLimit = 232448;     // sm_100 max dynamic shared memory per block
@@ -96,7 +97,11 @@ struct FusedParams {
   unsigned long long* tile_trace;      // optional [1000][8] per-tile MMA stamps of CTA 0 (debug)
   int mode;                            // kModeFull / kModeStats (publish partials only) / kModeFinish (lse2 given)
   const float* lse_in;                 // kModeFinish: lse2 per row ((b*L + l)*H + h)*Rv + r
-  int debug_local;                     // timing experiment only: lse2 from the CTA's own partial (wrong results)
+  // peer-memory exchange (sequence-sharded single pass): world ranks each score
+  // their own tokens; a CTA publishes its partial into every rank's buffer and
+  // gathers the unit's world*n_tg partials from its own.  world = 1: local only.
+  int rank, world, ntg_all;            // ntg_all = world * n_tg partials per unit
+  unsigned long long* peer[kMaxPeers]; // every rank's partial buffer base ([2][B][U][ntg_all][NCP])
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -242,6 +247,14 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ unsigned long long pack_ms(float m, float s) {
@@ -479,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   // this launch publishes into part[parity]; part[parity ^ 1] (the previous
   // launch's) is re-zeroed off the critical path, for the launch after next
   const uint32_t parity = ld_acquire(p.epoch) & 1u;
-  const long long part_half = (long long)p.B * p.U * p.n_tg * NCP;
+  const long long part_half = (long long)p.B * p.U * p.ntg_all * NCP;
   unsigned long long* const part_cur = p.part + parity * part_half;
   unsigned long long* const part_old = p.part + (parity ^ 1u) * part_half;
 
@@ -696,7 +709,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const long long ubase = (long long)jb.b * p.U + u;
         mbar_wait(bar_rfull + 8 * (ui & 1), (ui >> 1) & 1);
         const float2* rb = red + (ui & 1) * 4 * NCP;
-        unsigned long long* mypart = part_cur + (ubase * p.n_tg + jb.tg) * NCP;
+        const long long row = (ubase * p.ntg_all + p.rank * p.n_tg + jb.tg) * NCP;
         for (int c = lane; c < NCP; c += 32) {
           float mm = -CUDART_INF_F, ss = 0.f;
           if (c < p.NC) {
@@ -704,7 +717,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             for (int w = 0; w < 4; ++w) merge2(mm, ss, rb[w * NCP + c].x, rb[w * NCP + c].y);
           }
           if (!(ss > 0.f)) { mm = -CUDART_INF_F; ss = -1.f; }          // written, but empty
-          st_relaxed_u64(mypart + c, pack_ms(mm, ss));
+          if (p.world == 1) {
+            st_relaxed_u64(part_cur + row + c, pack_ms(mm, ss));
+          } else {
+            for (int r = 0; r < p.world; ++r)                               // NVLink stores to the peers
+              st_relaxed_sys_u64(p.peer[r] + parity * part_half + row + c, pack_ms(mm, ss));
+          }
         }
         __syncwarp();
         if (lane == 0) {
@@ -717,8 +735,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
       const Job jb = decode_job(p, job);
       for (int u = jb.u_lo; u < jb.u_hi; ++u) {
-        unsigned long long* row = part_old + (((long long)jb.b * p.U + u) * p.n_tg + jb.tg) * NCP;
-        for (int c = lane; c < NCP; c += 32) row[c] = 0ull;
+        const long long row = (((long long)jb.b * p.U + u) * p.ntg_all + p.rank * p.n_tg + jb.tg) * NCP;
+        for (int r = 0; r < p.world; ++r)
+          for (int c = lane; c < NCP; c += 32) p.peer[r][(parity ^ 1u) * part_half + row + c] = 0ull;
       }
     }
   } else if (warp == 3 && p.mode != kModeStats) {
@@ -736,8 +755,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const long long ubase = (long long)jb.b * p.U + u;
         mbar_wait(bar_lempty + 8 * par, ((ui / kLseRing) & 1) ^ 1);    // aggregation done with ls[par]
         float* ls = lse_s + par * NCP;
-        const unsigned long long* src = part_cur + ubase * p.n_tg * NCP + (p.debug_local ? jb.tg * NCP : 0);
-        const int ntg = p.debug_local ? 1 : p.n_tg;
+        const unsigned long long* src = part_cur + ubase * p.ntg_all * NCP;
+        const int ntg = p.ntg_all;
         for (int c = lane; c < NCP && p.mode == kModeFinish; c += 32) {
           // lse2 supplied by the caller (sequence-sharded split: globally combined statistics)
           float l2 = 0.f;
@@ -754,7 +773,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             unsigned long long missing = 0;
 #pragma unroll
             for (int j = 0; j < kMaxLseBatch; ++j) {
-              v[j] = (s0 + j < ntg) ? ld_relaxed_u64(src + (long long)(s0 + j) * NCP + c) : pack_ms(0.f, -1.f);
+              v[j] = (s0 + j < ntg) ? ld_relaxed_sys_u64(src + (long long)(s0 + j) * NCP + c) : pack_ms(0.f, -1.f);
               missing |= (v[j] == 0ull ? 1ull : 0ull) << j;
             }
             long long it = 0;
@@ -763,7 +782,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
 #pragma unroll
               for (int j = 0; j < kMaxLseBatch; ++j) {
                 if (missing & (1ull << j)) {
-                  v[j] = ld_relaxed_u64(src + (long long)(s0 + j) * NCP + c);
+                  v[j] = ld_relaxed_sys_u64(src + (long long)(s0 + j) * NCP + c);
                   if (v[j] != 0ull) missing &= ~(1ull << j);
                 }
               }
@@ -1009,7 +1028,8 @@ uint32_t carve(Plan& pl, int Rv, int stages) {
   return o + 1024;                                   // slack for the manual 1024-byte alignment
 }
 
-Plan make_plan(const Geom& g, bool allow_override = true) {
+// sm_budget > 0: plan for at most that many CTAs (co-scheduled peer launches on one GPU, tests)
+Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0) {
   Plan pl;
   pl.NC = g.G * g.Rv;
   pl.NCP = ((pl.NC + 31) / 32) * 32;                  // TMEM column groups of 32 (one tcgen05.ld.x32)
@@ -1019,7 +1039,7 @@ Plan make_plan(const Geom& g, bool allow_override = true) {
   pl.k_stage_bytes = (uint32_t)kTileM * g.d * 2;
   pl.q_slot_bytes = (uint32_t)pl.NCP * g.d * 2;
   if (pl.q_slot_bytes * 2 > 64 * 1024) return pl;
-  pl.P = sm_count();
+  pl.P = sm_budget > 0 ? std::min(sm_count(), sm_budget) : sm_count();
   pl.T = (int)((g.N + kTileM - 1) / kTileM);
   pl.U = g.L * g.Hkv;
   // choose (n_tg, n_ug): when a request needs more than one wave of CTAs
@@ -1067,7 +1087,7 @@ Plan make_plan(const Geom& g, bool allow_override = true) {
       }
     }
   }
-  if (pl.J == 0 && force_tg > 0) return make_plan(g, false);   // invalid override: plan normally
+  if (pl.J == 0 && force_tg > 0) return make_plan(g, false, sm_budget);   // invalid override: plan normally
   if (pl.J == 0) return pl;
   pl.total_jobs = (long long)g.B * pl.J;
   int stages = kMaxStages;
@@ -1183,11 +1203,18 @@ __global__ void k_partials_to_stats(const unsigned long long* __restrict__ part,
 
 }  // namespace
 
+struct PeerArgs {
+  int rank = 0, world = 1, sm_budget = 0;
+  void* const* bufs = nullptr;                        // world partial buffers (fused_peer_buffer_bytes each)
+};
+
 cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay, int mode,
                          const float* lse_in, float* importance, void* ws, size_t ws_bytes, cudaStream_t st,
-                         float* acc_out = nullptr) {
-  Plan pl = make_plan(g);
+                         float* acc_out = nullptr, const PeerArgs& peer = PeerArgs()) {
+  Plan pl = make_plan(g, true, peer.sm_budget);
   if (!pl.ok || ws_bytes < pl.ws_total()) return cudaErrorInvalidValue;
+  if (peer.world < 1 || peer.world > kMaxPeers || peer.rank < 0 || peer.rank >= peer.world) return cudaErrorInvalidValue;
+  if (peer.world > 1 && (peer.bufs == nullptr || pl.n_tg * peer.world > kMaxLseBatch * 64)) return cudaErrorInvalidValue;
   static FusedParams p;                               // large (two tensor maps); host-side scratch
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
@@ -1211,18 +1238,26 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   p.part = reinterpret_cast<unsigned long long*>(w);
   w += pl.ws_part;
   p.accpart = pl.ws_acc ? reinterpret_cast<float*>(w) : nullptr;
+  p.rank = peer.rank;
+  p.world = peer.world;
+  p.ntg_all = pl.n_tg * peer.world;
+  if (peer.world > 1) {
+    for (int r = 0; r < peer.world; ++r) p.peer[r] = reinterpret_cast<unsigned long long*>(peer.bufs[r]);
+    p.part = p.peer[peer.rank];
+  } else {
+    p.peer[0] = p.part;
+  }
   p.imp = importance;
   p.acc_out = acc_out;
   p.err = device_error_flag();
   p.trace = nullptr;
   p.mode = mode;
   p.lse_in = lse_in;
-  p.debug_local = std::getenv("SP_FUSED_DEBUG_LOCAL") != nullptr;
 
   p.trace_units = 0;
   if (g_trace != nullptr) {
     const long long grid = std::min<long long>(pl.P, pl.total_jobs);
-    const long long tail = g_trace_records > 16000 ? 8000 : 0;   // per-tile stamps of CTA 0 at the end
+    const long long tail = g_trace_records > 16000 ? 8000 : 0;   // (trace builds only)   // per-tile stamps of CTA 0 at the end
     const long long units = ((g_trace_records - tail) / 8) / grid;
     if (units > 0) {
       p.trace = g_trace;
@@ -1286,6 +1321,36 @@ cudaError_t fused_score_finish(const __nv_bfloat16* Q, const __nv_bfloat16* K, c
 cudaError_t fused_score_acc(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                             float* acc2, void* ws, size_t ws_bytes, cudaStream_t st) {
   return fused_launch(Q, K, g, lay, kModeFull, nullptr, nullptr, ws, ws_bytes, st, acc2);
+}
+
+size_t fused_peer_buffer_bytes(const Geom& g, int world, int sm_budget) {
+  Plan pl = make_plan(g, true, sm_budget);
+  if (!pl.ok) return 0;
+  return align256(2 * (size_t)g.B * pl.U * pl.NCP * pl.n_tg * world * sizeof(unsigned long long));
+}
+
+size_t fused_peer_ws_bytes(const Geom& g, int sm_budget) {
+  Plan pl = make_plan(g, true, sm_budget);
+  return pl.ok ? pl.ws_total() : 0;
+}
+
+bool fused_peer_plan_info(const Geom& g, int sm_budget, long long out[9]) {
+  Plan pl = make_plan(g, true, sm_budget);
+  if (!pl.ok) return false;
+  out[0] = std::min<long long>(pl.P, pl.total_jobs); out[1] = pl.J; out[2] = pl.n_tg; out[3] = pl.n_ug;
+  out[4] = pl.tpc; out[5] = pl.upc; out[6] = pl.nslots; out[7] = pl.stages; out[8] = pl.smem;
+  return true;
+}
+
+cudaError_t fused_score_peer(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                             int rank, int world, void* const* bufs, int sm_budget, float* importance, void* ws,
+                             size_t ws_bytes, cudaStream_t st) {
+  PeerArgs pa;
+  pa.rank = rank;
+  pa.world = world;
+  pa.bufs = bufs;
+  pa.sm_budget = sm_budget;
+  return fused_launch(Q, K, g, lay, kModeFull, nullptr, importance, ws, ws_bytes, st, nullptr, pa);
 }
 
 namespace {

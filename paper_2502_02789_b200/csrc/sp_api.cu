@@ -204,6 +204,49 @@ sp_status sp_acc_importance(const float* acc2, int32_t B, int32_t R_valid, int64
   return from_cuda(acc_importance(acc2, B, R_valid, N, importance, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+size_t sp_score_peer_buffer_bytes(const sp_geom* g, int32_t world, int32_t sm_budget) {
+  if (check_geom(g) != SP_OK || world < 1 || world > 8) return 0;
+  return fused_peer_buffer_bytes(to_geom(*g), world, sm_budget);
+}
+
+size_t sp_score_peer_workspace_bytes(const sp_geom* g, int32_t sm_budget) {
+  if (check_geom(g) != SP_OK) return 0;
+  return fused_peer_ws_bytes(to_geom(*g), sm_budget);
+}
+
+sp_status sp_score_peer_plan(const sp_geom* g, int32_t sm_budget, int64_t out[9]) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if (out == nullptr) return SP_EINVAL;
+  long long o[9];
+  if (!fused_peer_plan_info(to_geom(*g), sm_budget, o)) return SP_EUNSUPPORTED;
+  for (int i = 0; i < 9; ++i) out[i] = o[i];
+  return SP_OK;
+}
+
+sp_status sp_score_peer(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, int32_t rank,
+                        int32_t world, void* const* peer_buffers, int32_t sm_budget, float* importance, void* ws,
+                        size_t ws_bytes, sp_stream stream) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if ((s = check_layout(g, lay, Q, K)) != SP_OK) return s;
+  if (importance == nullptr || world < 1 || world > 8 || rank < 0 || rank >= world || sm_budget < 0) return SP_EINVAL;
+  if (world > 1 && peer_buffers == nullptr) return SP_EINVAL;
+  if (world > 1)
+    for (int r = 0; r < world; ++r)
+      if (peer_buffers[r] == nullptr || (reinterpret_cast<uintptr_t>(peer_buffers[r]) & 255u) != 0) return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
+  const Geom G = to_geom(*g);
+  const Layout Lay = to_layout(*lay);
+  if (!fused_supported(G, Lay, Q, K)) return SP_EUNSUPPORTED;
+  const size_t need = fused_peer_ws_bytes(G, sm_budget);
+  if (need == 0) return SP_EUNSUPPORTED;
+  if (ws == nullptr || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return SP_EWORKSPACE;
+  return from_cuda(fused_score_peer(reinterpret_cast<const __nv_bfloat16*>(Q),
+                                    reinterpret_cast<const __nv_bfloat16*>(K), G, Lay, rank, world, peer_buffers,
+                                    sm_budget, importance, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 sp_status sp_score_plan(const sp_geom* g, int64_t out[9]) {
   sp_status s = check_geom(g);
   if (s != SP_OK) return s;

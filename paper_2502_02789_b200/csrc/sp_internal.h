@@ -74,6 +74,12 @@ cudaError_t fused_score_finish(const __nv_bfloat16* Q, const __nv_bfloat16* K, c
 cudaError_t fused_score_acc(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                             float* acc2, void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t acc_importance(const float* acc2, int B, int Rv, long long N, float* importance, cudaStream_t st);
+size_t fused_peer_buffer_bytes(const Geom& g, int world, int sm_budget);
+size_t fused_peer_ws_bytes(const Geom& g, int sm_budget);
+bool fused_peer_plan_info(const Geom& g, int sm_budget, long long out[9]);
+cudaError_t fused_score_peer(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                             int rank, int world, void* const* bufs, int sm_budget, float* importance, void* ws,
+                             size_t ws_bytes, cudaStream_t st);
 
 // ---------------------------------------------------------------- select / gather (select.cu, gather.cu)
 size_t select_ws_bytes(int B, long long N, int chunk);

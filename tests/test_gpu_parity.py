@@ -363,3 +363,20 @@ def test_head_sharded_virtual_ranks(P):
     assert _util.rel_err(imp[0].double().cpu().numpy(), exact) <= _util.REL_TOL
     full = sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")
     assert _util.rel_err(imp[0].double().cpu().numpy(), full[0].double().cpu().numpy()) <= 1e-5
+
+
+# ---------------------------------------------------------------- sequence-sharded single pass (peer exchange)
+@pytest.mark.parametrize("name,P,N", [("C1", 2, 4096), ("C1", 4, 4096), ("C3", 2, 8192), ("C0", 2, 64)])
+def test_peer_exchange_virtual_ranks(name, P, N):
+    """sp_score_peer as P virtual ranks on one GPU (P co-scheduled launches,
+    each capped at SMs/P CTAs, exchanging the softmax statistics through each
+    other's partial buffers): the importance equals the oracle on the whole
+    prompt and sp_score's to fp32 rounding, bit-identical over repeated calls."""
+    from tools import peer_virtual
+    w = gen.CONFIGS[name].with_(N=N, R_valid=max(1, gen.CONFIGS[name].R - 1))
+    plan, res, _, (Q, K) = peer_virtual.run(w, P, iters=3)
+    assert all(torch.equal(r, res[0]) for r in res)
+    exact = _util.oracle_importance(w, 0)
+    assert _util.rel_err(res[0][0].double().cpu().numpy(), exact) <= _util.REL_TOL
+    full = sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")
+    assert _util.rel_err(res[0][0].double().cpu().numpy(), full[0].double().cpu().numpy()) <= 1e-5
