@@ -42,9 +42,11 @@ def parse():
     ap.add_argument("--config", default="C3", choices=["C0", "C1", "C2", "C3", "C4"])
     ap.add_argument("--algo", default="fused", choices=["fused", "simt", "auto"])
     ap.add_argument("--plan", default=None, help="fused-kernel decomposition override 'n_tg,n_ug'")
-    ap.add_argument("--shard", default="batch", choices=["batch", "seq", "head"],
+    ap.add_argument("--shard", default="batch", choices=["batch", "seq", "seq-split", "head"],
                     help="N>1: batch = one request per rank, no collective (weak scaling); "
-                         "seq = the prompt split over ranks with the NCCL statistics exchange (strong scaling); "
+                         "seq = the prompt split over ranks, statistics exchanged inside the fused kernel over "
+                         "NVLink peer memory (one K read, strong scaling); seq-split = the same split with "
+                         "stats/finish launches and an NCCL statistics all-gather (two K reads); "
                          "head = the heads split over ranks, NCCL MAX all-reduce of the log-domain maxima (strong)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of replaying a CUDA graph")
@@ -194,7 +196,8 @@ def run_ours(args):
     w = workload(args.config)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
-    seq = world > 1 and args.shard == "seq"
+    seq = world > 1 and args.shard in ("seq", "seq-split")
+    seq_peer = seq and args.shard == "seq"
     head = world > 1 and args.shard == "head"
     if world > 1 and not (seq or head):
         w = w.with_(seed=w.seed + rank)              # batch sharding: each rank owns different requests
@@ -228,9 +231,18 @@ def run_ours(args):
         score_only()
         select_only()
 
+    if seq_peer:
+        from paper_2502_02789_b200 import dist as spd
+        peer_ptrs = spd._peer_buffers(Q, K, w.Rv, None)
     if seq:
         def score_only():                              # noqa: F811 -- the sharded scoring (with its exchange)
             nonlocal imp
+            if seq_peer:                               # one pass: the exchange runs in the kernel, over NVLink
+                loc = sp.score_peer(Q, K, rank, world, peer_ptrs, 0, w.Rv, w.scale)
+                full = torch.empty((world * loc.shape[1],), dtype=torch.float32, device=dev)
+                dist.all_gather_into_tensor(full, loc.reshape(-1))
+                imp = full.view(1, w.N)
+                return
             st_ = sp.score_stats(Q, K, w.Rv, w.scale)
             parts = torch.empty((world * st_.shape[0], 2), dtype=torch.float32, device=dev)
             dist.all_gather_into_tensor(parts, st_)
@@ -350,7 +362,9 @@ def run_ours(args):
             "config": {"workload": f"{args.config} {w.name}", "B": w.B, "N": w.N, "L": w.L, "H": w.H, "Hkv": w.Hkv,
                        "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk,
                        "algo": args.algo, "plan": plan, "launch": graph_note, "shard": args.shard if world > 1 else None,
-                       "parallelism": (f"seq{world} (prompt split, NCCL stats all-gather)" if seq else
+                       "parallelism": (f"seq{world} (prompt split, in-kernel statistics exchange over NVLink "
+                                       f"peer memory)" if seq_peer else
+                                       f"seq{world} (prompt split, NCCL stats all-gather)" if seq else
                                        f"tp{world} (head split, NCCL MAX all-reduce of the log-domain maxima)"
                                        if head else
                                        f"dp{world} (batch-sharded: one request per rank, no collective)")

@@ -9,7 +9,11 @@
   order-free, so the one exchange is an elementwise MAX all-reduce of
   acc2 [B][R_valid][N] (log2 domain), then importance = mean_r 2^acc2
   (sp_score_acc -> all_reduce(MAX) -> sp_acc_importance) and the selection.
-* Sequence sharding -- one request's prompt split along tokens.  The only real
+* Sequence sharding, single pass (seq_sharded_fused_specprefill) -- the fused
+  kernel exchanges the per-unit softmax statistics itself over peer memory
+  (torch symmetric memory buffers, NVLink stores; sp_score_peer), so each rank
+  reads its K shard once; then the importance all-gather and the selection.
+* Sequence sharding, split (seq_sharded_specprefill) -- one request's prompt split along tokens.  The only real
   exchange is the softmax statistics (the lse of every (layer, head, row) needs
   all N keys):
     1. local statistics (m2, l) per row            (sp_score_stats)
@@ -114,6 +118,47 @@ def head_sharded_specprefill(Q_local, K_local, tokens, keep: float, pool_k: int,
     ids, pos, n_kept, out = be.select(imp, keep, pool_k, chunk, pos0, tokens)
     N = imp.shape[1]
     return dict(importance=imp, ids=ids, pos=pos, n_kept=n_kept, out_tokens=out, first_decode=N + pos0)
+
+
+_PEER_CACHE: dict = {}
+
+
+def _peer_buffers(Q, K_local, R_valid, group):
+    """This rank's partial buffer in torch symmetric memory and every rank's
+    address of it (cached per geometry)."""
+    import torch.distributed._symmetric_memory as symm_mem
+    world = dist.get_world_size(group)
+    key = (tuple(K_local.shape), tuple(Q.shape), R_valid, world, id(group))
+    if key not in _PEER_CACHE:
+        nbytes = api.score_peer_buffer_bytes(Q, K_local, world, 0, R_valid)
+        buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=K_local.device)
+        buf.zero_()
+        pg = group if group is not None else dist.group.WORLD
+        hdl = symm_mem.rendezvous(buf, pg.group_name)
+        torch.cuda.synchronize()
+        dist.barrier(group)
+        _PEER_CACHE[key] = (buf, hdl, [int(x) for x in hdl.buffer_ptrs])
+    return _PEER_CACHE[key][2]
+
+
+def seq_sharded_fused_specprefill(Q, K_local, tokens, N_total: int, keep: float, pool_k: int, chunk: int,
+                                  R_valid=None, scale=None, pos0: int = 0, group=None) -> dict:
+    """Sequence-sharded single pass for one request (B = 1): the statistics
+    exchange runs inside the fused kernel over peer memory (one K read per
+    rank); the importance all-gather that follows also separates consecutive
+    calls (sp_score_peer's barrier requirement)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n_local = K_local.shape[3]
+    if n_local * world != N_total or Q.shape[0] != 1:
+        raise ValueError("K_local must hold N_total / world tokens of a single request")
+    ptrs = _peer_buffers(Q, K_local, R_valid, group)
+    imp_local = api.score_peer(Q, K_local, rank, world, ptrs, 0, R_valid, scale)
+    imp = torch.empty((world * n_local,), dtype=imp_local.dtype, device=imp_local.device)
+    dist.all_gather_into_tensor(imp, imp_local.reshape(-1).contiguous(), group=group)
+    imp = imp.view(1, N_total)
+    ids, pos, n_kept, out = api.select(imp, keep, pool_k, chunk, pos0, tokens=tokens)
+    return dict(importance=imp, ids=ids, pos=pos, n_kept=n_kept, out_tokens=out, first_decode=N_total + pos0)
 
 
 def batch_sharded_specprefill(Q, K, tokens, keep, pool_k, chunk, R_valid=None, scale=None, pos0=0) -> dict:
