@@ -48,6 +48,9 @@ def parse():
                          "NVLink peer memory (one K read, strong scaling); seq-split = the same split with "
                          "stats/finish launches and an NCCL statistics all-gather (two K reads); "
                          "head = the heads split over ranks, NCCL MAX all-reduce of the log-domain maxima (strong)")
+    ap.add_argument("--kv", default="bf16", choices=["bf16", "e4m3"],
+                    help="input element type: bf16 (the north_star's), or e4m3 codes with per-tensor scales "
+                         "(SURVEY 8(f) row f4, sp_score_e4m3; single GPU / batch sharding)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -214,6 +217,15 @@ def run_ours(args):
         g0, g1 = spd.head_range(w.Hkv, world, rank)
         Qh_, Kh_ = Q[:, :, :, g0 * w.G:g1 * w.G], K[:, :, g0:g1]
         acc_buf = torch.empty((w.B, w.Rv, w.N), dtype=torch.float32, device=dev)
+    f8 = args.kv == "e4m3"
+    if f8:
+        if seq or head:
+            raise SystemExit("--kv e4m3 runs single-GPU or batch-sharded")
+        from spgen import fp8
+        Q8 = fp8.to_e4m3_codes(Q, fp8.Q_INV_SCALE)
+        K8 = fp8.to_e4m3_codes(K, fp8.K_INV_SCALE)
+        del K
+        K = K8
     torch.cuda.synchronize()
     imp = torch.empty((w.B, w.N), dtype=torch.float32, device=dev)
     ids = torch.empty((w.B, w.N), dtype=torch.int32, device=dev)
@@ -222,7 +234,10 @@ def run_ours(args):
     out = torch.empty_like(ids)
 
     def score_only():
-        sp.score(Q, K, R_valid=w.Rv, scale=w.scale, out=imp, algo=args.algo)
+        if f8:
+            sp.score_e4m3(Q8, K8, 1.0 / fp8.Q_INV_SCALE, 1.0 / fp8.K_INV_SCALE, R_valid=w.Rv, scale=w.scale, out=imp)
+        else:
+            sp.score(Q, K, R_valid=w.Rv, scale=w.scale, out=imp, algo=args.algo)
 
     def select_only():
         sp.select(imp, w.keep, w.pool_k, w.chunk, w.pos0, ids=ids, pos=pos, n_kept=nk, tokens=T, out=out)
@@ -330,15 +345,17 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (sp_score): algorithmic bytes / duration
     peak, peak_src = peaks()
-    q_bytes = w.B * w.L * w.Rv * w.H * w.d * 2
-    alg_bytes = ((w.k_bytes // world if (seq or head) else w.k_bytes) + (q_bytes // world if head else q_bytes)
+    esz = 1 if f8 else 2
+    q_bytes = w.B * w.L * w.Rv * w.H * w.d * esz
+    k_bytes = w.k_bytes // 2 * esz
+    alg_bytes = ((k_bytes // world if (seq or head) else k_bytes) + (q_bytes // world if head else q_bytes)
                  + w.B * w.N * 4)
     achieved = alg_bytes / (score_ms / 1000.0) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(f"{args.config}/{args.algo}")
+            traffic = json.load(f).get(f"{args.config}/{args.algo}" + ("/e4m3" if f8 else ""))
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "sp_score", "kernel_ms": score_ms,
                 "algorithmic_bytes": alg_bytes, "peak_source": peak_src,
@@ -346,7 +363,7 @@ def run_ours(args):
 
     # ---- end to end through the C ABI with host (pinned) buffers
     e2e = None
-    if not args.no_e2e and not (seq or head):          # sp_run_host is the single-GPU / batch-sharded call
+    if not args.no_e2e and not (seq or head or f8):    # sp_run_host is the single-GPU / batch-sharded bf16 call
         e2e = run_e2e(args, w, Q, K, T, dev, stream, dist, world)
 
     # select_gather is one launch, or two for long prompts (phase A over the SMs,
@@ -355,11 +372,11 @@ def run_ours(args):
     cpb = max(1, 2048 // w.chunk)
     select_launches = 2 if 4 <= -(-n_c // cpb) <= 65535 else 1
     launches_per_step = {"fused": 1, "simt": 4, "auto": 1}[args.algo] + select_launches
-    plan = sp.score_plan(Q, K, w.Rv) if args.algo != "simt" else None
+    plan = (sp.score_e4m3_plan(Q8, K8, w.Rv) if f8 else sp.score_plan(Q, K, w.Rv)) if args.algo != "simt" else None
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if (seq or head) else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{args.config} {w.name}", "B": w.B, "N": w.N, "L": w.L, "H": w.H, "Hkv": w.Hkv,
+            "scaling": "strong" if (seq or head) else "weak", "vs_baseline": None, "dtype": args.kv, "data": "synthetic",
+            "config": {"workload": f"{args.config} {w.name}" + (" e4m3 K/Q" if f8 else ""), "B": w.B, "N": w.N, "L": w.L, "H": w.H, "Hkv": w.Hkv,
                        "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk,
                        "algo": args.algo, "plan": plan, "launch": graph_note, "shard": args.shard if world > 1 else None,
                        "parallelism": (f"seq{world} (prompt split, in-kernel statistics exchange over NVLink "
@@ -369,7 +386,7 @@ def run_ours(args):
                                        if head else
                                        f"dp{world} (batch-sharded: one request per rank, no collective)")
                        if world > 1 else "single",
-                       "l2": f"inputs larger than L2 (K = {w.k_bytes / 2**30:.2f} GiB per GPU), no flush"},
+                       "l2": f"inputs larger than L2 (K = {k_bytes / 2**30:.2f} GiB per GPU), no flush"},
             "roofline": roofline, "clocks": clk, "e2e": e2e, "gpu_launches": launches_per_step * args.steps}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w, args.cpu_sample_layers)

@@ -217,6 +217,24 @@ sp_status sp_score_peer(const void* Q, const void* K, const sp_geom* g, const sp
                         int32_t world, void* const* peer_buffers, int32_t sm_budget, float* importance, void* ws,
                         size_t ws_bytes, sp_stream stream);
 
+/* ------------------------------------------------------------------ score, FP8 (e4m3) inputs
+ * SURVEY 8(f) row f4 (an FP8 KV cache halves the K bytes, the path's cost).
+ * Q8, K8 hold OCP FP8 E4M3 codes (1 byte: sign, 4 exponent bits with bias 7,
+ * 3 mantissa bits; S.1111.111 is NaN, no infinities) with per-tensor
+ * dequantisation scales: Q = q_scale * e4m3(Q8), K = k_scale * e4m3(K8) (the
+ * usual FP8 attention formulation).  The scores are those of sp_score on these
+ * dequantised values, s = scale * <Q, K>, computed as
+ * (scale*q_scale*k_scale) * <e4m3(Q8), e4m3(K8)> with e4m3 x e4m3 products
+ * (exact in fp32) on the tensor cores (tcgen05.mma kind::f8f6f4), fp32
+ * accumulation; everything after the logits is sp_score's fused kernel.
+ * Layout: sp_layout strides in elements = bytes; rows 16-byte aligned;
+ * d % 32 == 0 (else SP_EUNSUPPORTED).  q_scale, k_scale finite and > 0.
+ * Workspace: sp_score_e4m3_workspace_bytes(g) bytes, same rules as sp_score. */
+size_t sp_score_e4m3_workspace_bytes(const sp_geom* g);
+sp_status sp_score_e4m3_plan(const sp_geom* g, int64_t out[9]);
+sp_status sp_score_e4m3(const void* Q8, const void* K8, float q_scale, float k_scale, const sp_geom* g,
+                        const sp_layout* lay, float* importance, void* ws, size_t ws_bytes, sp_stream stream);
+
 /* ------------------------------------------------------------------ select
  * Pool, chunk means, top-K_c chunks, positions (O5-O9, Alg.1):
  *   pooled[i] = mean(importance[j] : |j-i| <= (pool_k-1)/2, 0 <= j < N)      (Z6)

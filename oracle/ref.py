@@ -35,6 +35,21 @@ def bf16_to_f64(bits: np.ndarray) -> np.ndarray:
     return b.view(np.float32).astype(np.float64)
 
 
+def e4m3_to_f64(codes: np.ndarray) -> np.ndarray:
+    """Exact OCP FP8 E4M3 ("e4m3fn") -> float64, from the format's definition
+    (an FP8 KV cache): bit 7 sign, bits 6..3 exponent E with
+    bias 7, bits 2..0 mantissa M.  E > 0: (-1)^s * 2^(E-7) * (1 + M/8);
+    E = 0: (-1)^s * 2^-6 * (M/8) (subnormal); S.1111.111 is NaN; no infinities
+    (so E = 15 with M < 7 is a normal number, max 448)."""
+    c = np.asarray(codes, dtype=np.uint8).astype(np.int64)
+    sign = np.where(c >> 7, -1.0, 1.0)
+    E = (c >> 3) & 15
+    M = (c & 7).astype(np.float64)
+    mag = np.where(E > 0, np.ldexp(1.0 + M / 8.0, (E - 7).astype(np.int32)), np.ldexp(M / 8.0, -6))
+    out = sign * mag
+    return np.where((c & 0x7F) == 0x7F, np.nan, out)
+
+
 # ------------------------------------------------------------------ O1-O2
 def attention_scores(Q: np.ndarray, K: np.ndarray, scale: float) -> np.ndarray:
     """Speculator attention of the look-ahead rows over the prompt, one request.
@@ -201,6 +216,20 @@ def specprefill(Q_bits, K_bits, tokens, scale, keep, pool_k, chunk, R_valid=None
     merge)."""
     Q = bf16_to_f64(Q_bits)
     K = bf16_to_f64(K_bits)
+    imp = token_importance(Q, K, scale, R_valid)
+    out = select(imp, keep, pool_k, chunk, pos0)
+    out["imp"] = imp
+    out["out_tokens"] = gather(tokens, out["ids"])
+    return out
+
+
+def specprefill_e4m3(Q_codes, K_codes, q_scale, k_scale, tokens, scale, keep, pool_k, chunk, R_valid=None,
+                     pos0=0) -> dict:
+    """Row f4: the same path on FP8 inputs.  The dequantised values
+    Q = q_scale * e4m3(Q8), K = k_scale * e4m3(K8) are the speculator's query
+    rows and keys; everything after is ``specprefill``'s definition."""
+    Q = q_scale * e4m3_to_f64(Q_codes)
+    K = k_scale * e4m3_to_f64(K_codes)
     imp = token_importance(Q, K, scale, R_valid)
     out = select(imp, keep, pool_k, chunk, pos0)
     out["imp"] = imp

@@ -73,6 +73,9 @@ SIGNATURES = {
     "sp_score_peer_plan": (C.c_int, [_G, C.c_int32, C.POINTER(C.c_int64)]),
     "sp_score_peer": (C.c_int, [_P, _P, _G, _L, C.c_int32, C.c_int32, C.POINTER(C.c_void_p), C.c_int32, _P, _P,
                                 C.c_size_t, _P]),
+    "sp_score_e4m3_workspace_bytes": (C.c_size_t, [_G]),
+    "sp_score_e4m3_plan": (C.c_int, [_G, C.POINTER(C.c_int64)]),
+    "sp_score_e4m3": (C.c_int, [_P, _P, C.c_float, C.c_float, _G, _L, _P, _P, C.c_size_t, _P]),
     "sp_select_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int64, _S]),
     "sp_select": (C.c_int, [_P, C.c_int32, C.c_int64, _S, _P, _P, _P, _P, C.c_size_t, _P]),
     "sp_select_gather": (C.c_int, [_P, _P, C.c_int32, C.c_int64, _S, _P, _P, _P, _P, _P, C.c_size_t, _P]),

@@ -50,8 +50,15 @@ def _geom_key(g) -> tuple:
     return (g.B, g.L, g.H, g.Hkv, g.d, g.R, g.R_valid, g.N, os.environ.get("SP_FUSED_PLAN"))
 
 
-def make_geom(Q: torch.Tensor, K: torch.Tensor, R_valid: int | None = None, scale: float | None = None):
-    if Q.dtype != torch.bfloat16 or K.dtype != torch.bfloat16:
+_E4M3 = (torch.float8_e4m3fn, torch.uint8)
+
+
+def make_geom(Q: torch.Tensor, K: torch.Tensor, R_valid: int | None = None, scale: float | None = None,
+              e4m3: bool = False):
+    if e4m3:
+        if Q.dtype not in _E4M3 or K.dtype not in _E4M3:
+            raise TypeError("Q and K must be float8_e4m3fn (or uint8 holding e4m3 codes)")
+    elif Q.dtype != torch.bfloat16 or K.dtype != torch.bfloat16:
         raise TypeError("Q and K must be bfloat16")
     if Q.dim() != 5 or K.dim() != 5:
         raise ValueError("Q must be [B][L][R][H][d] and K [B][L][Hkv][N][d]")
@@ -79,6 +86,31 @@ def score(Q, K, R_valid=None, scale=None, out=None, algo: str = "auto", stream=N
     check(lib().sp_score_ex(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), out.data_ptr(), ws.data_ptr(),
                             ws.numel(), a, _stream_ptr(stream)), "sp_score")
     return out
+
+
+def score_e4m3(Q8, K8, q_scale: float = 1.0, k_scale: float = 1.0, R_valid=None, scale=None, out=None,
+               stream=None) -> torch.Tensor:
+    """Row f4: token importance [B][N] fp32 from FP8 e4m3 Q/K codes with
+    per-tensor dequantisation scales (Q = q_scale*Q8, K = k_scale*K8)."""
+    g, lay = make_geom(Q8, K8, R_valid, scale, e4m3=True)
+    if out is None:
+        out = torch.empty((g.B, g.N), dtype=torch.float32, device=K8.device)
+    nbytes = lib().sp_score_e4m3_workspace_bytes(C.byref(g))
+    if nbytes == 0:
+        check(_lib.SP_EUNSUPPORTED, "sp_score_e4m3")
+    ws = workspace(("score_e4m3", _geom_key(g)), nbytes, K8.device)
+    check(lib().sp_score_e4m3(Q8.data_ptr(), K8.data_ptr(), float(q_scale), float(k_scale), C.byref(g), C.byref(lay),
+                              out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_score_e4m3")
+    return out
+
+
+def score_e4m3_plan(Q8, K8, R_valid=None) -> dict:
+    g, _ = make_geom(Q8, K8, R_valid, e4m3=True)
+    out = (C.c_int64 * 9)()
+    check(lib().sp_score_e4m3_plan(C.byref(g), out), "sp_score_e4m3_plan")
+    keys = ("grid", "jobs_per_request", "token_groups", "unit_groups", "tiles_per_job", "units_per_job",
+            "tmem_slots", "stages", "smem_bytes")
+    return dict(zip(keys, list(out)))
 
 
 def select(importance: torch.Tensor, keep: float, pool_k: int, chunk: int, pos0: int = 0, ids=None, pos=None,

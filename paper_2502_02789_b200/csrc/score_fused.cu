@@ -77,6 +77,7 @@ struct FusedParams {
   int n_tg, n_ug, J;                   // token groups, unit groups, jobs per request
   long long total_jobs;
   int NC, NCP, W, nkb, stages, nslots, tpc;
+  int esz, swb, ksteps;                // element bytes (2 bf16, 1 e4m3), swizzle-block bytes, K steps per block
   float xs;                            // scale * log2(e)
   uint32_t idesc;                      // tcgen05 instruction descriptor
   uint32_t layout_type;                // UMMA smem descriptor swizzle code
@@ -197,24 +198,37 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t sbo_byte
   desc |= (uint64_t)(layout_type & 7u) << 61;                // [61,64) swizzle mode
   return desc;
 }
-__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
+// kF8: kind::f8f6f4 (e4m3 x e4m3, K = 32 per instruction) instead of kind::f16
+// (bf16 x bf16, K = 16); both step 32 bytes of a K-major row per instruction.
+template <bool kF8>
+__device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (kF8) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  }
 }
-// One tile's K steps (KS = d/16) with compile-time descriptor offsets; KSTEPS
-// K16 steps per swizzle block (W = 16*KSTEPS elements).
-template <int KS, int KSTEPS>
+// One tile's K steps (KS = d*esz/32) with compile-time descriptor offsets;
+// KSTEPS 32-byte steps per 128-byte swizzle block.
+template <int KS, int KSTEPS, bool kF8>
 __device__ __forceinline__ void issue_tile(uint32_t dcol, uint32_t a_lo0, uint32_t b_lo0, uint32_t desc_hi,
                                            uint32_t b_kb, uint32_t idesc) {
 #pragma unroll
   for (int j = 0; j < KS; ++j) {
     const uint32_t kb = j / KSTEPS, ks = j % KSTEPS;
-    umma_bf16(dcol, ((uint64_t)desc_hi << 32) | (a_lo0 + kb * (256u * KSTEPS) + ks * 2u),
+    umma<kF8>(dcol, ((uint64_t)desc_hi << 32) | (a_lo0 + kb * (256u * KSTEPS) + ks * 2u),
               ((uint64_t)desc_hi << 32) | (b_lo0 + kb * b_kb + ks * 2u), idesc, j > 0 ? 1u : 0u);
   }
 }
@@ -430,7 +444,8 @@ __device__ __forceinline__ float transpose_add32(float (&s)[32], int lane) {
 // instantiation per group size keeps the kernel's hot code small: the warp
 // roles run different code concurrently on each SMSP and share the
 // instruction cache.
-template <int kG, int kNCP>
+// kF8: e4m3 inputs (row f4), kind::f8f6f4 MMA; everything after the MMA is shared.
+template <int kG, int kNCP, bool kF8>
 __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ FusedParams p) {
   // kNCP > 0: compile-time padded column count (one 32-column TMEM group for
   // the 8B geometry): the per-tile loops become straight-line code
@@ -509,18 +524,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           const uint32_t qs = ui & 1, qpar = (ui >> 1) & 1;
           mbar_wait_acc(p, bar_qempty + 8 * qs, qpar ^ 1, w_q);
           trace_stamp(p, ui, 0);
-          mbar_expect_tx(bar_qfull + 8 * qs, (uint32_t)(p.NC * p.d * 2));
+          mbar_expect_tx(bar_qfull + 8 * qs, (uint32_t)(p.NC * p.d * p.esz));
           const uint32_t qdst = smem_u32(smem + p.off_q + qs * p.q_slot_bytes);
           #pragma unroll 1
           for (int kb = 0; kb < p.nkb; ++kb)
-            tma_load_5d(qdst + kb * (NCP * p.W * 2), &p.tmQ, bar_qfull + 8 * qs, kb * p.W, g * p.G, 0, l, jb.b);
+            tma_load_5d(qdst + kb * (NCP * p.swb), &p.tmQ, bar_qfull + 8 * qs, kb * p.W, g * p.G, 0, l, jb.b);
           for (int t = jb.t_lo; t < jb.t_hi; ++t) {
             mbar_wait_acc(p, bar_empty + 8 * stage, sphase ^ 1, w_empty);
             mbar_expect_tx(bar_full + 8 * stage, p.k_stage_bytes);
             const uint32_t kdst = smem_u32(smem + p.off_k + stage * p.k_stage_bytes);
             #pragma unroll 1
             for (int kb = 0; kb < p.nkb; ++kb)
-              tma_load_5d(kdst + kb * (kTileM * p.W * 2), &p.tmK, bar_full + 8 * stage, kb * p.W, t * kTileM, g, l,
+              tma_load_5d(kdst + kb * (kTileM * p.swb), &p.tmK, bar_full + 8 * stage, kb * p.W, t * kTileM, g, l,
                           jb.b);
             if (++stage == (uint32_t)p.stages) { stage = 0; sphase ^= 1; }
           }
@@ -541,9 +556,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       const long long t_start = kTrace ? clock64() : 0;
       // UMMA smem descriptors: the high word (SBO, version, swizzle) is constant;
       // the low word is (address >> 4) | LBO and a K step just adds to it.
-      const uint32_t desc_hi = (uint32_t)(make_sdesc(0, 8 * p.W * 2, p.layout_type) >> 32);
-      const uint32_t a_kb = (kTileM * p.W * 2) >> 4, b_kb = (NCP * p.W * 2) >> 4;
-      const int ksteps = p.W / 16;
+      const uint32_t desc_hi = (uint32_t)(make_sdesc(0, 8 * p.swb, p.layout_type) >> 32);
+      const uint32_t a_kb = (kTileM * p.swb) >> 4, b_kb = (NCP * p.swb) >> 4;
+      const int ksteps = p.ksteps;
       for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
         const Job jb = decode_job(p, job);
         for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
@@ -569,11 +584,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             // 64-element swizzle blocks): the descriptor arithmetic pipelines
             // across the MMAs (a loop back-edge halves the issue rate)
             if (ksteps == 4 && p.nkb == 2) {
-              issue_tile<8, 4>(dcol, a_lo0, b_lo0, desc_hi, b_kb, p.idesc);
+              issue_tile<8, 4, kF8>(dcol, a_lo0, b_lo0, desc_hi, b_kb, p.idesc);
             } else if (ksteps == 4 && p.nkb == 1) {
-              issue_tile<4, 4>(dcol, a_lo0, b_lo0, desc_hi, b_kb, p.idesc);
+              issue_tile<4, 4, kF8>(dcol, a_lo0, b_lo0, desc_hi, b_kb, p.idesc);
             } else if (ksteps == 4 && p.nkb == 4) {
-              issue_tile<16, 4>(dcol, a_lo0, b_lo0, desc_hi, b_kb, p.idesc);
+              issue_tile<16, 4, kF8>(dcol, a_lo0, b_lo0, desc_hi, b_kb, p.idesc);
             } else {
               uint32_t accum = 0;
 #pragma unroll 1
@@ -581,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
                 uint32_t a_lo = a_lo0 + kb * a_kb, b_lo = b_lo0 + kb * b_kb;
 #pragma unroll 1
                 for (int ks = 0; ks < ksteps; ++ks, a_lo += 2, b_lo += 2) {
-                  umma_bf16(dcol, ((uint64_t)desc_hi << 32) | a_lo, ((uint64_t)desc_hi << 32) | b_lo, p.idesc, accum);
+                  umma<kF8>(dcol, ((uint64_t)desc_hi << 32) | a_lo, ((uint64_t)desc_hi << 32) | b_lo, p.idesc, accum);
                   accum = 1;
                 }
               }
@@ -988,7 +1003,7 @@ PFN_encodeTiled_t encode_fn() {
 
 struct Plan {
   int P = 0, n_tg = 0, n_ug = 0, J = 0, T = 0, U = 0, tpc = 0, upc = 0;
-  int NC = 0, NCP = 0, W = 0, nkb = 0, stages = 0, nslots = 0;
+  int NC = 0, NCP = 0, W = 0, nkb = 0, stages = 0, nslots = 0, swb = 0;
   long long total_jobs = 0;
   uint32_t off_k = 0, off_q = 0, off_acc = 0, off_red = 0, off_lse = 0, off_comb = 0, off_bar = 0, smem = 0;
   uint32_t k_stage_bytes = 0, q_slot_bytes = 0;
@@ -1034,10 +1049,14 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0) {
   pl.NC = g.G * g.Rv;
   pl.NCP = ((pl.NC + 31) / 32) * 32;                  // TMEM column groups of 32 (one tcgen05.ld.x32)
   if (pl.NCP > 16 * kMaxChunks) return pl;
-  pl.W = (g.d % 64 == 0) ? 64 : (g.d % 32 == 0 ? 32 : 16);
+  // swizzle block = the widest of 128/64/32 bytes dividing a row of d elements
+  const int row_bytes = g.d * g.esz;
+  if (row_bytes % 32 != 0) return pl;
+  pl.swb = (row_bytes % 128 == 0) ? 128 : (row_bytes % 64 == 0 ? 64 : 32);
+  pl.W = pl.swb / g.esz;
   pl.nkb = g.d / pl.W;
-  pl.k_stage_bytes = (uint32_t)kTileM * g.d * 2;
-  pl.q_slot_bytes = (uint32_t)pl.NCP * g.d * 2;
+  pl.k_stage_bytes = (uint32_t)kTileM * row_bytes;
+  pl.q_slot_bytes = (uint32_t)pl.NCP * row_bytes;
   if (pl.q_slot_bytes * 2 > 64 * 1024) return pl;
   pl.P = sm_budget > 0 ? std::min(sm_count(), sm_budget) : sm_count();
   pl.T = (int)((g.N + kTileM - 1) / kTileM);
@@ -1107,36 +1126,38 @@ bool encode_maps(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, 
                  CUtensorMap* tmK, CUtensorMap* tmQ) {
   PFN_encodeTiled_t enc = encode_fn();
   if (enc == nullptr) return false;
-  const CUtensorMapSwizzle sw = pl.W == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                           : (pl.W == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  const CUtensorMapSwizzle sw = pl.swb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                               : (pl.swb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  const CUtensorMapDataType dt = g.esz == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const long long esz = g.esz;
   // strides of size-1 dims are irrelevant; give them a harmless contiguous value
-  auto fix = [](long long stride, long long prev_extent_bytes, long long size) -> cuuint64_t {
-    return (size == 1 || stride == 0) ? (cuuint64_t)prev_extent_bytes : (cuuint64_t)(stride * 2);
+  auto fix = [esz](long long stride, long long prev_extent_bytes, long long size) -> cuuint64_t {
+    return (size == 1 || stride == 0) ? (cuuint64_t)prev_extent_bytes : (cuuint64_t)(stride * esz);
   };
   {
     cuuint64_t dims[5] = {(cuuint64_t)g.d, (cuuint64_t)g.N, (cuuint64_t)g.Hkv, (cuuint64_t)g.L, (cuuint64_t)g.B};
-    cuuint64_t s1 = fix(lay.k_i, (long long)g.d * 2, g.N);
+    cuuint64_t s1 = fix(lay.k_i, (long long)g.d * esz, g.N);
     cuuint64_t s2 = fix(lay.k_g, (long long)s1 * g.N, g.Hkv);
     cuuint64_t s3 = fix(lay.k_l, (long long)s2 * g.Hkv, g.L);
     cuuint64_t s4 = fix(lay.k_b, (long long)s3 * g.L, g.B);
     cuuint64_t strides[4] = {s1, s2, s3, s4};
     cuuint32_t box[5] = {(cuuint32_t)pl.W, (cuuint32_t)kTileM, 1, 1, 1};
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    if (enc(tmK, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<__nv_bfloat16*>(K), dims, strides, box, es,
+    if (enc(tmK, dt, 5, const_cast<__nv_bfloat16*>(K), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
   }
   {
     cuuint64_t dims[5] = {(cuuint64_t)g.d, (cuuint64_t)g.H, (cuuint64_t)g.R, (cuuint64_t)g.L, (cuuint64_t)g.B};
-    cuuint64_t s1 = fix(lay.q_h, (long long)g.d * 2, g.H);
+    cuuint64_t s1 = fix(lay.q_h, (long long)g.d * esz, g.H);
     cuuint64_t s2 = fix(lay.q_r, (long long)s1 * g.H, g.R);
     cuuint64_t s3 = fix(lay.q_l, (long long)s2 * g.R, g.L);
     cuuint64_t s4 = fix(lay.q_b, (long long)s3 * g.L, g.B);
     cuuint64_t strides[4] = {s1, s2, s3, s4};
     cuuint32_t box[5] = {(cuuint32_t)pl.W, (cuuint32_t)g.G, (cuuint32_t)g.Rv, 1, 1};
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    if (enc(tmQ, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<__nv_bfloat16*>(Q), dims, strides, box, es,
+    if (enc(tmQ, dt, 5, const_cast<__nv_bfloat16*>(Q), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
@@ -1224,9 +1245,13 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   p.T = pl.T; p.U = pl.U; p.n_tg = pl.n_tg; p.n_ug = pl.n_ug; p.J = pl.J; p.total_jobs = pl.total_jobs;
   p.NC = pl.NC; p.NCP = pl.NCP; p.W = pl.W; p.nkb = pl.nkb; p.stages = pl.stages; p.nslots = pl.nslots;
   p.tpc = pl.tpc;
+  p.esz = g.esz; p.swb = pl.swb; p.ksteps = pl.swb / 32;
   p.xs = g.scale * kLog2e;
-  p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(pl.NCP >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
-  p.layout_type = pl.W == 64 ? 2u : (pl.W == 32 ? 4u : 6u);
+  // instruction descriptor: D fp32 (bit 4); A/B format bf16 (1) for kind::f16,
+  // e4m3 (0) for kind::f8f6f4; K-major A and B; N >> 3 at bit 17, M >> 4 at bit 24
+  const uint32_t ab_fmt = g.esz == 2 ? ((1u << 7) | (1u << 10)) : 0u;
+  p.idesc = (1u << 4) | ab_fmt | ((uint32_t)(pl.NCP >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
+  p.layout_type = pl.swb == 128 ? 2u : (pl.swb == 64 ? 4u : 6u);
   p.off_k = pl.off_k; p.off_q = pl.off_q; p.off_acc = pl.off_acc; p.off_red = pl.off_red; p.off_lse = pl.off_lse; p.off_comb = pl.off_comb;
   p.off_bar = pl.off_bar; p.k_stage_bytes = pl.k_stage_bytes; p.q_slot_bytes = pl.q_slot_bytes;
   char* w = reinterpret_cast<char*>(ws);
@@ -1266,19 +1291,24 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
     }
   }
 
-  // one instantiation per (GQA group, one-column-group) pair
+  // one instantiation per (GQA group, one-column-group, input type)
   using KernFn = void (*)(FusedParams);
-  static const KernFn table[5][2] = {{k_fused<1, 0>, k_fused<1, 32>}, {k_fused<2, 0>, k_fused<2, 32>},
-                                     {k_fused<4, 0>, k_fused<4, 32>}, {k_fused<8, 0>, k_fused<8, 32>},
-                                     {k_fused<0, 0>, k_fused<0, 32>}};
-  static bool configured[5][2] = {};
+  static const KernFn table[2][5][2] = {
+      {{k_fused<1, 0, false>, k_fused<1, 32, false>}, {k_fused<2, 0, false>, k_fused<2, 32, false>},
+       {k_fused<4, 0, false>, k_fused<4, 32, false>}, {k_fused<8, 0, false>, k_fused<8, 32, false>},
+       {k_fused<0, 0, false>, k_fused<0, 32, false>}},
+      {{k_fused<1, 0, true>, k_fused<1, 32, true>}, {k_fused<2, 0, true>, k_fused<2, 32, true>},
+       {k_fused<4, 0, true>, k_fused<4, 32, true>}, {k_fused<8, 0, true>, k_fused<8, 32, true>},
+       {k_fused<0, 0, true>, k_fused<0, 32, true>}}};
+  static bool configured[2][5][2] = {};
+  const int kt = g.esz == 1 ? 1 : 0;
   const int ki = g.G == 1 ? 0 : g.G == 2 ? 1 : g.G == 4 ? 2 : g.G == 8 ? 3 : 4;
   const int kj = pl.NCP == 32 ? 1 : 0;
-  KernFn kern = table[ki][kj];
-  if (!configured[ki][kj]) {
+  KernFn kern = table[kt][ki][kj];
+  if (!configured[kt][ki][kj]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (e != cudaSuccess) return e;
-    configured[ki][kj] = true;
+    configured[kt][ki][kj] = true;
   }
   const int grid = (int)std::min<long long>(pl.P, pl.total_jobs);
   cudaLaunchConfig_t cfg = {};

@@ -57,7 +57,8 @@ sp_status check_geom(const sp_geom* g) {
   return SP_OK;
 }
 
-sp_status check_layout(const sp_geom* g, const sp_layout* l, const void* Q, const void* K) {
+// esz: element bytes of Q and K (2 = bf16, 1 = e4m3)
+sp_status check_layout(const sp_geom* g, const sp_layout* l, const void* Q, const void* K, int esz = 2) {
   if (l == nullptr || Q == nullptr || K == nullptr) return SP_EINVAL;
   const long long ks[4] = {l->k_b, l->k_l, l->k_g, l->k_i};
   const long long kn[4] = {g->B, g->L, g->Hkv, g->N};
@@ -65,8 +66,8 @@ sp_status check_layout(const sp_geom* g, const sp_layout* l, const void* Q, cons
   const long long qn[4] = {g->B, g->L, g->R, g->H};
   for (int i = 0; i < 4; ++i) {
     if (ks[i] < 0 || qs[i] < 0) return SP_EINVAL;
-    if (kn[i] > 1 && (ks[i] * 2) % 16 != 0) return SP_EINVAL;   // TMA: strides multiple of 16 B
-    if (qn[i] > 1 && (qs[i] * 2) % 16 != 0) return SP_EINVAL;
+    if (kn[i] > 1 && (ks[i] * esz) % 16 != 0) return SP_EINVAL;   // TMA: strides multiple of 16 B
+    if (qn[i] > 1 && (qs[i] * esz) % 16 != 0) return SP_EINVAL;
   }
   if (l->k_i < g->d && g->N > 1) return SP_EINVAL;               // rows of one head may not overlap
   if (!aligned16(Q) || !aligned16(K)) return SP_EINVAL;
@@ -245,6 +246,55 @@ sp_status sp_score_peer(const void* Q, const void* K, const sp_geom* g, const sp
   return from_cuda(fused_score_peer(reinterpret_cast<const __nv_bfloat16*>(Q),
                                     reinterpret_cast<const __nv_bfloat16*>(K), G, Lay, rank, world, peer_buffers,
                                     sm_budget, importance, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+// Row f4: e4m3 inputs.  The per-tensor dequantisation scales fold into the
+// softmax scale (s = scale * q_scale * k_scale * <Q8, K8>, one fp32 product).
+static sp_status e4m3_geom(const sp_geom* g, float q_scale, float k_scale, Geom* out) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if (!(std::isfinite(q_scale) && q_scale > 0.f && std::isfinite(k_scale) && k_scale > 0.f)) return SP_EINVAL;
+  if (g->d % 32 != 0) return SP_EUNSUPPORTED;                    // 32-byte swizzle rows at 1 byte per element
+  Geom G = to_geom(*g);
+  G.esz = 1;
+  G.scale = g->scale * q_scale * k_scale;
+  if (!(std::isfinite(G.scale) && G.scale > 0.f)) return SP_EINVAL;
+  *out = G;
+  return SP_OK;
+}
+
+size_t sp_score_e4m3_workspace_bytes(const sp_geom* g) {
+  Geom G;
+  if (e4m3_geom(g, 1.f, 1.f, &G) != SP_OK) return 0;
+  return fused_supported(G, Layout{}, nullptr, nullptr) ? fused_score_ws_bytes(G) : 0;
+}
+
+sp_status sp_score_e4m3_plan(const sp_geom* g, int64_t out[9]) {
+  Geom G;
+  sp_status s = e4m3_geom(g, 1.f, 1.f, &G);
+  if (s != SP_OK) return s;
+  if (out == nullptr) return SP_EINVAL;
+  long long o[9];
+  if (!fused_plan_info(G, o)) return SP_EUNSUPPORTED;
+  for (int i = 0; i < 9; ++i) out[i] = o[i];
+  return SP_OK;
+}
+
+sp_status sp_score_e4m3(const void* Q8, const void* K8, float q_scale, float k_scale, const sp_geom* g,
+                        const sp_layout* lay, float* importance, void* ws, size_t ws_bytes, sp_stream stream) {
+  Geom G;
+  sp_status s = e4m3_geom(g, q_scale, k_scale, &G);
+  if (s != SP_OK) return s;
+  if ((s = check_layout(g, lay, Q8, K8, 1)) != SP_OK) return s;
+  if (importance == nullptr) return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
+  const Layout Lay = to_layout(*lay);
+  if (!fused_supported(G, Lay, Q8, K8)) return SP_EUNSUPPORTED;
+  if (ws == nullptr || ws_bytes < fused_score_ws_bytes(G) || (reinterpret_cast<uintptr_t>(ws) & 255u) != 0)
+    return SP_EWORKSPACE;
+  // the fused kernel takes the element type from G.esz; the pointer type is nominal
+  return from_cuda(fused_score(reinterpret_cast<const __nv_bfloat16*>(Q8), reinterpret_cast<const __nv_bfloat16*>(K8),
+                               G, Lay, importance, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 sp_status sp_score_plan(const sp_geom* g, int64_t out[9]) {

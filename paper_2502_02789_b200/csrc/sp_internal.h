@@ -24,6 +24,7 @@ struct Geom {
   int B, L, H, Hkv, d, R, Rv, G;
   long long N;
   float scale;
+  int esz = 2;          // input element bytes: 2 = bf16, 1 = e4m3 (row f4; scale then folds q_scale*k_scale)
 };
 
 struct Layout {

@@ -349,3 +349,40 @@ def test_softmax_lse_closed_forms_and_library():
             s = 0.3 * (Q[l, :, h, :] @ K[l, h // 2].T)
             np.testing.assert_allclose(lse[l, h], scipy.special.logsumexp(s, axis=1), rtol=1e-14)
             np.testing.assert_allclose(np.exp(s - lse[l, h][:, None]).sum(axis=1), 1.0, rtol=1e-13)
+
+
+# ------------------------------------------------------------------ row f4: e4m3 decoder
+def test_e4m3_decoder_format_values():
+    """Values the OCP E4M3 definition fixes: 1.0 = 0x38, max normal 448 = 0x7E,
+    min normal 2^-6 = 0x08, min subnormal 2^-9 = 0x01, -2 = 0xC0, NaN = 0x7F/0xFF."""
+    c = np.array([0x00, 0x80, 0x38, 0x7E, 0x08, 0x01, 0x07, 0xC0, 0x3C, 0x77], dtype=np.uint8)
+    want = [0.0, -0.0, 1.0, 448.0, 2.0 ** -6, 2.0 ** -9, 7 * 2.0 ** -9, -2.0, 1.5, 240.0]
+    np.testing.assert_array_equal(ref.e4m3_to_f64(c), want)
+    assert np.isnan(ref.e4m3_to_f64(np.array([0x7F, 0xFF], dtype=np.uint8))).all()
+
+
+def test_e4m3_decoder_vs_torch_all_codes():
+    """All 256 codes against torch's float8_e4m3fn (a library decoder)."""
+    codes = np.arange(256, dtype=np.uint8)
+    lib = torch.from_numpy(codes).view(torch.float8_e4m3fn).to(torch.float64).numpy()
+    mine = ref.e4m3_to_f64(codes)
+    nan = np.isnan(lib)
+    np.testing.assert_array_equal(np.isnan(mine), nan)
+    np.testing.assert_array_equal(mine[~nan], lib[~nan])
+
+
+def test_e4m3_path_equals_bf16_path_on_common_values():
+    """Values exactly representable in both formats give the same importance
+    through specprefill_e4m3 (with scales) and specprefill (bf16)."""
+    rng = np.random.default_rng(5)
+    L, R, H, Hkv, N, d = 2, 2, 4, 2, 24, 16
+    codes_q = rng.integers(0x30, 0x48, size=(L, R, H, d)).astype(np.uint8) | (rng.integers(0, 2, (L, R, H, d)) << 7).astype(np.uint8)
+    codes_k = rng.integers(0x28, 0x48, size=(L, Hkv, N, d)).astype(np.uint8)
+    Qv = 0.5 * ref.e4m3_to_f64(codes_q)
+    Kv = 0.25 * ref.e4m3_to_f64(codes_k)
+    to_bits = lambda x: (x.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)   # exact: <= 4 significant bits
+    tokens = np.arange(N)
+    a = ref.specprefill_e4m3(codes_q, codes_k, 0.5, 0.25, tokens, 0.25, 0.5, 3, 4)
+    b = ref.specprefill(to_bits(Qv), to_bits(Kv), tokens, 0.25, 0.5, 3, 4)
+    np.testing.assert_array_equal(a["imp"], b["imp"])
+    np.testing.assert_array_equal(a["ids"], b["ids"])
