@@ -62,6 +62,7 @@ constexpr int kMaxStages = 8;
 constexpr int kMaxChunks = 8;          // NCP <= 128 columns (16-column chunks)
 constexpr int kMaxSlots = 16;          // TMEM tile slots (512 columns / 32)
 constexpr int kLseRing = 8;            // lse2 buffers in SMEM (gather may run ahead of aggregation)
+constexpr int kMaxQSlots = 4;          // query blocks in SMEM (the producer loads up to nq - 1 units ahead)
 constexpr int kMaxLseBatch = 10;       // 64-bit partial words in flight per lane
 constexpr int kMaxPeers = 8;           // ranks of a peer-memory statistics exchange
 constexpr int kTmemCols = 512;
@@ -84,6 +85,7 @@ struct FusedParams {
   // smem carve (byte offsets from the 1024-aligned base)
   uint32_t off_k, off_q, off_acc, off_red, off_lse, off_comb, off_bar;
   uint32_t k_stage_bytes, q_slot_bytes;
+  int nq;                              // query slots (2 or 4, power of two)
   // workspace
   unsigned long long* part;            // [2][B][U][n_tg][NCP] CTA partials, one buffer per launch parity:
                                        // (max2, sum) packed in one 64-bit word; 0 = "not yet written"
@@ -457,14 +459,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
-  // barrier map: full[S] empty[S] qfull[2] qempty[2] tfull[kMaxSlots] tempty[kMaxSlots]
+  // barrier map: full[S] empty[S] qfull[kMaxQSlots] qempty[kMaxQSlots] tfull[kMaxSlots] tempty[kMaxSlots]
   //              rfull[2] rempty[2] lfull[kLseRing] lempty[kLseRing]; then the TMEM base address
   const uint32_t bar_full = smem_u32(bars), bar_empty = bar_full + 8 * p.stages;
-  const uint32_t bar_qfull = bar_empty + 8 * p.stages, bar_qempty = bar_qfull + 16;
-  const uint32_t bar_tfull = bar_qempty + 16, bar_tempty = bar_tfull + 8 * kMaxSlots;
+  const uint32_t bar_qfull = bar_empty + 8 * p.stages, bar_qempty = bar_qfull + 8 * kMaxQSlots;
+  const uint32_t bar_tfull = bar_qempty + 8 * kMaxQSlots, bar_tempty = bar_tfull + 8 * kMaxSlots;
   const uint32_t bar_rfull = bar_tempty + 8 * kMaxSlots, bar_rempty = bar_rfull + 16;
   const uint32_t bar_lfull = bar_rempty + 16, bar_lempty = bar_lfull + 8 * kLseRing;
-  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bars + 2 * p.stages + 8 + 2 * kMaxSlots + 2 * kLseRing);
+  uint32_t* tmem_base_s =
+      reinterpret_cast<uint32_t*>(bars + 2 * p.stages + 2 * kMaxQSlots + 2 * kMaxSlots + 4 + 2 * kLseRing);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -475,9 +478,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       mbar_init(bar_tfull + 8 * s, 1);
       mbar_init(bar_tempty + 8 * s, 4);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kMaxQSlots; ++s) {
       mbar_init(bar_qfull + 8 * s, 1);
       mbar_init(bar_qempty + 8 * s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(bar_rfull + 8 * s, 128);
       mbar_init(bar_rempty + 8 * s, 1);
     }
@@ -490,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     prefetch_tmap(&p.tmQ);
   }
   // zero both Q slots once: rows >= NC (MMA padding columns) are never written by TMA
-  for (uint32_t o = threadIdx.x * 16; o < 2 * p.q_slot_bytes; o += kThreads * 16)
+  for (uint32_t o = threadIdx.x * 16; o < (uint32_t)p.nq * p.q_slot_bytes; o += kThreads * 16)
     *reinterpret_cast<uint4*>(smem + p.off_q + o) = make_uint4(0, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == 1) {
@@ -521,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const Job jb = decode_job(p, job);
         for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
           const int l = u / p.Hkv, g = u % p.Hkv;
-          const uint32_t qs = ui & 1, qpar = (ui >> 1) & 1;
+          const uint32_t qs = ui & (p.nq - 1), qpar = (ui / p.nq) & 1;
           mbar_wait_acc(p, bar_qempty + 8 * qs, qpar ^ 1, w_q);
           trace_stamp(p, ui, 0);
           mbar_expect_tx(bar_qfull + 8 * qs, (uint32_t)(p.NC * p.d * p.esz));
@@ -562,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
         const Job jb = decode_job(p, job);
         for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
-          const uint32_t qs = ui & 1, qpar = (ui >> 1) & 1;
+          const uint32_t qs = ui & (p.nq - 1), qpar = (ui / p.nq) & 1;
           mbar_wait_acc(p, bar_qfull + 8 * qs, qpar, w_qf);
           const uint32_t b_lo0 = ((smem_u32(smem + p.off_q + qs * p.q_slot_bytes) >> 4) & 0x3FFFu) | (1u << 16);
           for (int t = jb.t_lo; t < jb.t_hi; ++t, ++gt) {
@@ -1007,6 +1012,7 @@ struct Plan {
   long long total_jobs = 0;
   uint32_t off_k = 0, off_q = 0, off_acc = 0, off_red = 0, off_lse = 0, off_comb = 0, off_bar = 0, smem = 0;
   uint32_t k_stage_bytes = 0, q_slot_bytes = 0;
+  int nq = 2;
   size_t ws_part = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0;
   size_t ws_total() const { return ws_part + ws_cnt + ws_acc + ws_fin; }
   bool ok = false;
@@ -1027,7 +1033,7 @@ uint32_t carve(Plan& pl, int Rv, int stages) {
   pl.off_k = o;
   o += (uint32_t)stages * pl.k_stage_bytes;
   pl.off_q = o;
-  o += 2 * pl.q_slot_bytes;
+  o += (uint32_t)pl.nq * pl.q_slot_bytes;
   pl.off_acc = o;
   o += (uint32_t)pl.tpc * Rv * kTileM * 4;
   pl.off_red = o;
@@ -1039,7 +1045,7 @@ uint32_t carve(Plan& pl, int Rv, int stages) {
   o += 16 + 4 * pl.NCP * 8;
   o = (o + 15) & ~15u;
   pl.off_bar = o;
-  o += (2 * stages + 8 + 2 * kMaxSlots + 2 * kLseRing) * 8 + 16;
+  o += (2 * stages + 2 * kMaxQSlots + 2 * kMaxSlots + 4 + 2 * kLseRing) * 8 + 16;
   return o + 1024;                                   // slack for the manual 1024-byte alignment
 }
 
@@ -1089,7 +1095,9 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0) {
       // its last tile (cross-CTA skew + one L2 round trip per gather batch);
       // the TMEM ring holds W units, so L - (W-1) unit-times stay exposed; the
       // gather warp itself needs ~1.6 us per batch of kMaxLseBatch partials.
-      const double tile_us = (double)pl.k_stage_bytes / kSmHbmBytesPerUs;
+      // (per-tile costs measured for bf16 hold for e4m3 too: the statistics,
+      // aggregation and exchange work per tile does not depend on the K bytes)
+      const double tile_us = (double)kTileM * g.d * 2 / kSmHbmBytesPerUs;
       const int batches = (n_tg + kMaxLseBatch - 1) / kMaxLseBatch;
       const double L_us = 5.0 + 0.8 * batches;
       const int W = std::max(1, pl.nslots / tpc);
@@ -1109,8 +1117,16 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0) {
   if (pl.J == 0 && force_tg > 0) return make_plan(g, false, sm_budget);   // invalid override: plan normally
   if (pl.J == 0) return pl;
   pl.total_jobs = (long long)g.B * pl.J;
-  int stages = kMaxStages;
-  while (stages >= 2 && carve(pl, g.Rv, stages) > (uint32_t)kSmemLimit) --stages;
+  // 4 query slots (Q loads issued 3 units ahead) unless that costs a K stage on long units
+  auto max_stages = [&](int nq) {
+    pl.nq = nq;
+    int s = kMaxStages;
+    while (s >= 2 && carve(pl, g.Rv, s) > (uint32_t)kSmemLimit) --s;
+    return s;
+  };
+  const int s2 = max_stages(2), s4 = max_stages(4);
+  pl.nq = (s4 >= 2 && (s4 >= s2 || pl.tpc <= 8)) ? 4 : 2;
+  int stages = pl.nq == 4 ? s4 : s2;
   if (stages < 2) return pl;
   pl.stages = stages;
   pl.smem = carve(pl, g.Rv, stages);
@@ -1254,6 +1270,7 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   p.layout_type = pl.swb == 128 ? 2u : (pl.swb == 64 ? 4u : 6u);
   p.off_k = pl.off_k; p.off_q = pl.off_q; p.off_acc = pl.off_acc; p.off_red = pl.off_red; p.off_lse = pl.off_lse; p.off_comb = pl.off_comb;
   p.off_bar = pl.off_bar; p.k_stage_bytes = pl.k_stage_bytes; p.q_slot_bytes = pl.q_slot_bytes;
+  p.nq = pl.nq;
   char* w = reinterpret_cast<char*>(ws);
   // counters first: their offsets depend only on (B, U), not on the plan
   p.epoch = reinterpret_cast<unsigned*>(w);

@@ -26,19 +26,31 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--plan", default=None)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--kv", default="bf16", choices=["bf16", "e4m3"])
     a = ap.parse_args()
     if a.plan:
         os.environ["SP_FUSED_PLAN"] = a.plan
     w = gen.CONFIGS[a.config]
     Q, K, T = spgen_cuda.make_inputs(w)
-    plan = sp.score_plan(Q, K, w.Rv)
+    if a.kv == "e4m3":
+        from spgen import fp8
+        Q8, K8 = fp8.to_e4m3_codes(Q, fp8.Q_INV_SCALE), fp8.to_e4m3_codes(K, fp8.K_INV_SCALE)
+        plan = sp.score_e4m3_plan(Q8, K8, w.Rv)
+
+        def run():
+            sp.score_e4m3(Q8, K8, 1 / fp8.Q_INV_SCALE, 1 / fp8.K_INV_SCALE, R_valid=w.Rv, scale=w.scale)
+    else:
+        plan = sp.score_plan(Q, K, w.Rv)
+
+        def run():
+            sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")
     grid, upj = plan["grid"], plan["units_per_job"]
     units = upj * ((w.B * plan["jobs_per_request"] + grid - 1) // grid)
     buf = torch.zeros(grid * (units + 1) * 8 + 1000 * 8, dtype=torch.int64, device="cuda")   # +1: wait accounting; CTA 0 tiles
     for _ in range(3):
-        sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")
+        run()
     sp.lib().sp_trace_enable(buf.data_ptr(), buf.numel())
-    sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")
+    run()
     torch.cuda.synchronize()
     sp.lib().sp_trace_enable(None, 0)
     tt = buf[grid * (units + 1) * 8:].view(1000, 8).cpu().numpy().astype(np.float64)
