@@ -51,6 +51,14 @@ def parse():
     ap.add_argument("--kv", default="bf16", choices=["bf16", "e4m3"],
                     help="input element type: bf16 (the north_star's), or e4m3 codes with per-tensor scales "
                          "(SURVEY 8(f) row f4, sp_score_e4m3; single GPU / batch sharding)")
+    ap.add_argument("--paged", type=int, default=0, metavar="BS",
+                    help="K in a paged cache of block size BS with a shuffled block table (row f3, sp_score_paged)")
+    ap.add_argument("--paged-layout", default="hnd", choices=["hnd", "nhd"],
+                    help="block storage: hnd = [Hkv][BS][d] per block (a head's rows contiguous), "
+                         "nhd = [BS][Hkv][d] (heads interleaved per token)")
+    ap.add_argument("--ragged", action="store_true",
+                    help="with --paged: per-request prompt lengths uniform in [N/4, N] (seeded); tokens/s counts "
+                         "the real tokens")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -226,6 +234,21 @@ def run_ours(args):
         K8 = fp8.to_e4m3_codes(K, fp8.K_INV_SCALE)
         del K
         K = K8
+    paged = args.paged > 0
+    seq_lens, n_tokens = None, w.B * w.N
+    if paged:
+        if seq or head or f8:
+            raise SystemExit("--paged runs single-GPU or batch-sharded with bf16 K")
+        from spgen.paged import to_paged
+        K_cache, btab = to_paged(K, args.paged, seed=rank, layout=args.paged_layout)
+        del K
+        K = K_cache
+        if args.ragged:
+            import numpy as np
+            lens = np.random.default_rng(1234 + rank).integers(w.N // 4, w.N + 1, size=w.B)
+            lens[0] = w.N
+            seq_lens = torch.tensor(lens, dtype=torch.int32, device=dev)
+            n_tokens = int(lens.sum())
     torch.cuda.synchronize()
     imp = torch.empty((w.B, w.N), dtype=torch.float32, device=dev)
     ids = torch.empty((w.B, w.N), dtype=torch.int32, device=dev)
@@ -234,12 +257,17 @@ def run_ours(args):
     out = torch.empty_like(ids)
 
     def score_only():
-        if f8:
+        if paged:
+            sp.score_paged(Q, K_cache, btab, seq_lens, N=w.N, R_valid=w.Rv, scale=w.scale, out=imp)
+        elif f8:
             sp.score_e4m3(Q8, K8, 1.0 / fp8.Q_INV_SCALE, 1.0 / fp8.K_INV_SCALE, R_valid=w.Rv, scale=w.scale, out=imp)
         else:
             sp.score(Q, K, R_valid=w.Rv, scale=w.scale, out=imp, algo=args.algo)
 
     def select_only():
+        if seq_lens is not None:
+            sp.select_ragged(imp, seq_lens, w.keep, w.pool_k, w.chunk, w.pos0, tokens=T)
+            return
         sp.select(imp, w.keep, w.pool_k, w.chunk, w.pos0, ids=ids, pos=pos, n_kept=nk, tokens=T, out=out)
 
     def step():
@@ -340,14 +368,14 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_total, score_ms = tt.tolist()
     ms_step = ms_total / args.steps
-    tokens_per_step = w.B * w.N * (1 if (seq or head) else world)
+    tokens_per_step = n_tokens * (1 if (seq or head) else world)
     value = tokens_per_step / (ms_step / 1000.0)
 
     # ---- roofline of the dominant kernel (sp_score): algorithmic bytes / duration
     peak, peak_src = peaks()
     esz = 1 if f8 else 2
     q_bytes = w.B * w.L * w.Rv * w.H * w.d * esz
-    k_bytes = w.k_bytes // 2 * esz
+    k_bytes = w.k_bytes // 2 * esz * n_tokens // (w.B * w.N)
     alg_bytes = ((k_bytes // world if (seq or head) else k_bytes) + (q_bytes // world if head else q_bytes)
                  + w.B * w.N * 4)
     achieved = alg_bytes / (score_ms / 1000.0) / 1e9
@@ -363,7 +391,7 @@ def run_ours(args):
 
     # ---- end to end through the C ABI with host (pinned) buffers
     e2e = None
-    if not args.no_e2e and not (seq or head or f8):    # sp_run_host is the single-GPU / batch-sharded bf16 call
+    if not args.no_e2e and not (seq or head or f8 or paged):    # sp_run_host is the single-GPU / batch-sharded bf16 call
         e2e = run_e2e(args, w, Q, K, T, dev, stream, dist, world)
 
     # select_gather is one launch, or two for long prompts (phase A over the SMs,
@@ -372,11 +400,15 @@ def run_ours(args):
     cpb = max(1, 2048 // w.chunk)
     select_launches = 2 if 4 <= -(-n_c // cpb) <= 65535 else 1
     launches_per_step = {"fused": 1, "simt": 4, "auto": 1}[args.algo] + select_launches
-    plan = (sp.score_e4m3_plan(Q8, K8, w.Rv) if f8 else sp.score_plan(Q, K, w.Rv)) if args.algo != "simt" else None
+    Kgeom = (torch.empty(w.d, dtype=torch.bfloat16, device=dev).as_strided((w.B, w.L, w.Hkv, w.N, w.d),
+                                                                          (0, 0, 0, 0, 1)) if paged else K)
+    plan = (sp.score_e4m3_plan(Q8, K8, w.Rv) if f8 else sp.score_plan(Q, Kgeom, w.Rv)) if args.algo != "simt" else None
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if (seq or head) else "weak", "vs_baseline": None, "dtype": args.kv, "data": "synthetic",
-            "config": {"workload": f"{args.config} {w.name}" + (" e4m3 K/Q" if f8 else ""), "B": w.B, "N": w.N, "L": w.L, "H": w.H, "Hkv": w.Hkv,
+            "config": {"workload": f"{args.config} {w.name}" + (" e4m3 K/Q" if f8 else "")
+                       + (f" paged bs{args.paged} {args.paged_layout}" if paged else "") + (" ragged" if seq_lens is not None else ""),
+                       "prompt_tokens_per_step": n_tokens, "B": w.B, "N": w.N, "L": w.L, "H": w.H, "Hkv": w.Hkv,
                        "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk,
                        "algo": args.algo, "plan": plan, "launch": graph_note, "shard": args.shard if world > 1 else None,
                        "parallelism": (f"seq{world} (prompt split, in-kernel statistics exchange over NVLink "

@@ -235,6 +235,40 @@ sp_status sp_score_e4m3_plan(const sp_geom* g, int64_t out[9]);
 sp_status sp_score_e4m3(const void* Q8, const void* K8, float q_scale, float k_scale, const sp_geom* g,
                         const sp_layout* lay, float* importance, void* ws, size_t ws_bytes, sp_stream stream);
 
+/* ------------------------------------------------------------------ score, paged K cache / ragged batch
+ * the speculator's K cache in the serving layout -- fixed-size
+ * blocks addressed through a block table (the "slot mapping" of the paper's vLLM
+ * integration; Alg.1) -- and requests of different prompt lengths.
+ * Per layer l the cache holds num_blocks blocks of block_size tokens:
+ *   K[l][blk][j][g][:]  at  cache + l*s_l + blk*s_blk + j*s_tok + g*s_g   (bf16, d contiguous)
+ * (vLLM's per-layer [num_blocks][block_size][Hkv][d] key cache with a uniform
+ * layer stride, e.g. one allocation for all layers).  Token i of request b is
+ * row i % block_size of physical block block_table[b][i / block_size].
+ *   block_size   8, 16, 32 or 64 (divides 128), or a multiple of 128
+ *   block_table  device int32 [B][max_blocks], max_blocks >= ceil(N / block_size);
+ *                entries past a request's last block are never read
+ *   seq_lens     device int32 [B]: request b's prompt length n_b (clamped to [1, N]),
+ *                or NULL: every request has N tokens.  g->N is the longest length.
+ * Scores are sp_score's over each request's own n_b tokens
+ * (softmax over its prompt keys only).  importance [B][N]: entries i < n_b are
+ * written, the rest of each row is left untouched.  Q and sp_layout's q_*
+ * strides as for sp_score (k_* are ignored).  Fused kernel only
+ * (SP_EUNSUPPORTED otherwise); workspace sp_score_paged_workspace_bytes(g),
+ * same rules as sp_score.  Alignment: cache and every stride*2 bytes multiples
+ * of 16 bytes. */
+typedef struct sp_paged_k {
+  const void* cache;
+  int64_t s_l, s_blk, s_tok, s_g;
+  int32_t num_blocks, block_size;
+  const int32_t* block_table;
+  int32_t max_blocks;
+  const int32_t* seq_lens;
+} sp_paged_k;
+
+size_t sp_score_paged_workspace_bytes(const sp_geom* g);
+sp_status sp_score_paged(const void* Q, const sp_paged_k* K, const sp_geom* g, const sp_layout* lay,
+                         float* importance, void* ws, size_t ws_bytes, sp_stream stream);
+
 /* ------------------------------------------------------------------ select
  * Pool, chunk means, top-K_c chunks, positions (O5-O9, Alg.1):
  *   pooled[i] = mean(importance[j] : |j-i| <= (pool_k-1)/2, 0 <= j < N)      (Z6)
@@ -254,6 +288,16 @@ sp_status sp_select(const float* importance, int32_t B, int64_t N, const sp_sele
  * device int32 [B][N]; both NULL is the same as sp_select. */
 sp_status sp_select_gather(const float* importance, const int32_t* tokens, int32_t B, int64_t N,
                            const sp_select_params* p, int32_t* ids, int32_t* pos, int32_t* n_kept,
+                           int32_t* out_tokens, void* ws, size_t ws_bytes, sp_stream stream);
+
+/* Ragged batch (row f3): sp_select_gather over per-request prompt lengths.
+ * seq_lens: device int32 [B], n_b clamped to [1, N]; request b's selection is
+ * the one above over importance[b][0 .. n_b) with n_c = ceil(n_b / chunk) and
+ * K_c = sp_kept_chunks(n_c, keep_rate) (evaluated on the device with the same
+ * integer rule).  Rows of every [B][N] array keep their stride N.  tokens /
+ * out_tokens may both be NULL. */
+sp_status sp_select_ragged(const float* importance, const int32_t* seq_lens, const int32_t* tokens, int32_t B,
+                           int64_t N, const sp_select_params* p, int32_t* ids, int32_t* pos, int32_t* n_kept,
                            int32_t* out_tokens, void* ws, size_t ws_bytes, sp_stream stream);
 
 /* ------------------------------------------------------------------ gather

@@ -33,6 +33,12 @@ class sp_select_params(C.Structure):
     _fields_ = [("keep_rate", C.c_double), ("pool_k", C.c_int32), ("chunk", C.c_int32), ("pos0", C.c_int32)]
 
 
+class sp_paged_k(C.Structure):
+    _fields_ = [("cache", C.c_void_p), ("s_l", C.c_int64), ("s_blk", C.c_int64), ("s_tok", C.c_int64),
+                ("s_g", C.c_int64), ("num_blocks", C.c_int32), ("block_size", C.c_int32),
+                ("block_table", C.c_void_p), ("max_blocks", C.c_int32), ("seq_lens", C.c_void_p)]
+
+
 class sp_host_io(C.Structure):
     _fields_ = [("Q", C.c_void_p), ("K", C.c_void_p), ("tokens", C.c_void_p), ("ids", C.c_void_p),
                 ("pos", C.c_void_p), ("n_kept", C.c_void_p), ("out_tokens", C.c_void_p),
@@ -76,6 +82,9 @@ SIGNATURES = {
     "sp_score_e4m3_workspace_bytes": (C.c_size_t, [_G]),
     "sp_score_e4m3_plan": (C.c_int, [_G, C.POINTER(C.c_int64)]),
     "sp_score_e4m3": (C.c_int, [_P, _P, C.c_float, C.c_float, _G, _L, _P, _P, C.c_size_t, _P]),
+    "sp_score_paged_workspace_bytes": (C.c_size_t, [_G]),
+    "sp_score_paged": (C.c_int, [_P, C.POINTER(sp_paged_k), _G, _L, _P, _P, C.c_size_t, _P]),
+    "sp_select_ragged": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int64, _S, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "sp_select_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int64, _S]),
     "sp_select": (C.c_int, [_P, C.c_int32, C.c_int64, _S, _P, _P, _P, _P, C.c_size_t, _P]),
     "sp_select_gather": (C.c_int, [_P, _P, C.c_int32, C.c_int64, _S, _P, _P, _P, _P, _P, C.c_size_t, _P]),
@@ -104,6 +113,8 @@ def lib():
                               "run __graft_entry__.build()")
         h = C.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("SP_LIB_AB") and not hasattr(h, name):
+                continue                       # A/B timing of an older build (tools/ab_build.sh)
             f = getattr(h, name)
             f.restype = res
             f.argtypes = args

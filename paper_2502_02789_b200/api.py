@@ -113,6 +113,73 @@ def score_e4m3_plan(Q8, K8, R_valid=None) -> dict:
     return dict(zip(keys, list(out)))
 
 
+def score_paged(Q, K_cache, block_table, seq_lens=None, N=None, R_valid=None, scale=None, out=None,
+                stream=None) -> torch.Tensor:
+    """Row f3: token importance [B][N] fp32 from a paged K cache.
+
+    K_cache: bf16 [L][num_blocks][block_size][Hkv][d] (any strides, d contiguous),
+    block_table: int32 [B][max_blocks] (device), seq_lens: int32 [B] (device) or
+    None, N: longest prompt (default max_blocks * block_size, capped by seq_lens
+    if given on the host side by the caller).  Entries i >= seq_lens[b] of the
+    output rows are left untouched."""
+    if Q.dtype != torch.bfloat16 or K_cache.dtype != torch.bfloat16:
+        raise TypeError("Q and K_cache must be bfloat16")
+    if K_cache.dim() != 5 or Q.dim() != 5 or K_cache.stride(-1) != 1 or Q.stride(-1) != 1:
+        raise ValueError("Q [B][L][R][H][d], K_cache [L][num_blocks][block_size][Hkv][d], d contiguous")
+    if block_table.dtype != torch.int32 or not block_table.is_contiguous() or block_table.dim() != 2:
+        raise ValueError("block_table must be contiguous int32 [B][max_blocks]")
+    B, L, R, H, d = Q.shape
+    Lk, nblk, bs, Hkv, dk = K_cache.shape
+    if (Lk, dk) != (L, d) or block_table.shape[0] != B:
+        raise ValueError("Q / K_cache / block_table disagree")
+    N = block_table.shape[1] * bs if N is None else int(N)
+    g = _lib.sp_geom(B=B, L=L, H=H, Hkv=Hkv, d=d, R=R, R_valid=R if R_valid is None else R_valid, N=N,
+                     scale=float(1.0 / math.sqrt(d)) if scale is None else float(scale))
+    lay = _lib.sp_layout(k_b=0, k_l=0, k_g=0, k_i=0, q_b=Q.stride(0), q_l=Q.stride(1), q_r=Q.stride(2),
+                         q_h=Q.stride(3))
+    if seq_lens is not None and (seq_lens.dtype != torch.int32 or not seq_lens.is_contiguous()):
+        raise ValueError("seq_lens must be contiguous int32 [B]")
+    pk = _lib.sp_paged_k(cache=K_cache.data_ptr(), s_l=K_cache.stride(0), s_blk=K_cache.stride(1),
+                         s_tok=K_cache.stride(2), s_g=K_cache.stride(3), num_blocks=nblk, block_size=bs,
+                         block_table=block_table.data_ptr(), max_blocks=block_table.shape[1],
+                         seq_lens=None if seq_lens is None else seq_lens.data_ptr())
+    if out is None:
+        out = torch.zeros((B, N), dtype=torch.float32, device=K_cache.device)
+    nbytes = lib().sp_score_paged_workspace_bytes(C.byref(g))
+    if nbytes == 0:
+        check(_lib.SP_EUNSUPPORTED, "sp_score_paged")
+    ws = workspace(("score_paged", _geom_key(g)), nbytes, K_cache.device)
+    check(lib().sp_score_paged(Q.data_ptr(), C.byref(pk), C.byref(g), C.byref(lay), out.data_ptr(), ws.data_ptr(),
+                               ws.numel(), _stream_ptr(stream)), "sp_score_paged")
+    return out
+
+
+def select_ragged(importance: torch.Tensor, seq_lens: torch.Tensor, keep: float, pool_k: int, chunk: int,
+                  pos0: int = 0, tokens=None, stream=None):
+    """Row f3: per-request selection over importance[b][:seq_lens[b]];
+    returns (ids, pos, n_kept) or (ids, pos, n_kept, gathered tokens)."""
+    if importance.dtype != torch.float32 or importance.dim() != 2 or not importance.is_contiguous():
+        raise ValueError("importance must be contiguous fp32 [B][N]")
+    if seq_lens.dtype != torch.int32 or not seq_lens.is_contiguous():
+        raise ValueError("seq_lens must be contiguous int32 [B]")
+    B, N = importance.shape
+    dev = importance.device
+    p = _lib.sp_select_params(keep_rate=float(keep), pool_k=int(pool_k), chunk=int(chunk), pos0=int(pos0))
+    ids = torch.empty((B, N), dtype=torch.int32, device=dev)
+    pos = torch.empty_like(ids)
+    n_kept = torch.empty((B,), dtype=torch.int32, device=dev)
+    out = torch.empty_like(ids) if tokens is not None else None
+    nbytes = lib().sp_select_workspace_bytes(B, N, C.byref(p))
+    if nbytes == 0:
+        check(_lib.SP_EINVAL, "sp_select_ragged")
+    ws = workspace("select", nbytes, dev)
+    check(lib().sp_select_ragged(importance.data_ptr(), seq_lens.data_ptr(),
+                                 None if tokens is None else tokens.data_ptr(), B, N, C.byref(p), ids.data_ptr(),
+                                 pos.data_ptr(), n_kept.data_ptr(), None if out is None else out.data_ptr(),
+                                 ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_select_ragged")
+    return (ids, pos, n_kept) if tokens is None else (ids, pos, n_kept, out)
+
+
 def select(importance: torch.Tensor, keep: float, pool_k: int, chunk: int, pos0: int = 0, ids=None, pos=None,
            n_kept=None, stream=None, tokens=None, out=None):
     """(ids [B][N] int32, pos [B][N] int32, n_kept [B] int32); only the first

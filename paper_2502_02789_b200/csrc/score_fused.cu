@@ -83,9 +83,14 @@ struct FusedParams {
   uint32_t idesc;                      // tcgen05 instruction descriptor
   uint32_t layout_type;                // UMMA smem descriptor swizzle code
   // smem carve (byte offsets from the 1024-aligned base)
-  uint32_t off_k, off_q, off_acc, off_red, off_lse, off_comb, off_bar;
+  uint32_t off_k, off_q, off_acc, off_red, off_lse, off_comb, off_bar, off_bt;
   uint32_t k_stage_bytes, q_slot_bytes;
   int nq;                              // query slots (2 or 4, power of two)
+  // row f3: paged K (tmK is then 5-D {d, Hkv, block_size, blocks, L}) and per-request lengths
+  int paged, bs;                       // paged: 1; tokens per block (8..64 dividing 128, or a multiple of 128)
+  const int* btab;                     // [B][max_blocks] physical block ids
+  int max_blocks;
+  const int* seq_lens;                 // [B] prompt lengths in [1, N] (clamped), or null: all N
   // workspace
   unsigned long long* part;            // [2][B][U][n_tg][NCP] CTA partials, one buffer per launch parity:
                                        // (max2, sum) packed in one 64-bit word; 0 = "not yet written"
@@ -182,6 +187,15 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
       "@e cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];\n\t}" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+// Per-lane variant (no election): every calling lane issues its own box.
+__device__ __forceinline__ void tma_load_5d_lane(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                                 int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
 }
@@ -381,6 +395,7 @@ __device__ __forceinline__ void fold_tile(const float (&x)[kW], const float (&lv
 
 struct Job {
   int b, tg, ug, t_lo, t_hi, u_lo, u_hi;
+  int n;                                   // this request's prompt tokens (N unless seq_lens)
 };
 // Out of line: called once per job by every role; its 64-bit divisions would
 // otherwise be inlined into each role's code.
@@ -390,11 +405,85 @@ __device__ __noinline__ Job decode_job(const FusedParams& p, long long job) {
   const int r = (int)(job % p.J);
   j.tg = r / p.n_ug;
   j.ug = r % p.n_ug;
-  j.t_lo = (int)((long long)j.tg * p.T / p.n_tg);
-  j.t_hi = (int)((long long)(j.tg + 1) * p.T / p.n_tg);
+  j.n = p.seq_lens ? min(max(p.seq_lens[j.b], 1), p.N) : p.N;
+  const int T = p.seq_lens ? (j.n + kTileM - 1) / kTileM : p.T;   // the request's tiles (ragged batch)
+  j.t_lo = (int)((long long)j.tg * T / p.n_tg);
+  j.t_hi = (int)((long long)(j.tg + 1) * T / p.n_tg);
   j.u_lo = (int)((long long)j.ug * p.U / p.n_ug);
   j.u_hi = (int)((long long)(j.ug + 1) * p.U / p.n_ug);
   return j;
+}
+
+// Row f3: one 128-token K tile of request jb.b from a paged cache (block table).
+// block_size >= 128: one box of 128 tokens inside one block; block_size < 128:
+// 128 / block_size boxes, one per block, each landing at its row offset of the
+// tile (block_size >= 8 rows keeps every box on a swizzle-atom boundary).
+// Blocks wholly past the request's length are not loaded (their rows are
+// masked downstream); expect_tx counts the bytes actually requested.  Out of
+// line: the producer's hot loop stays small for the contiguous layout.
+// bts: the job's block-table slice in SMEM (entry 0 = the block of token t_lo * 128).
+__device__ __noinline__ void paged_tile(const FusedParams& p, uint32_t kdst, uint32_t bar, const Job& jb, int t, int g,
+                                        int l, int lane, const int* bts) {
+  const long long tok0 = (long long)t * kTileM;
+  const long long blk0 = (long long)jb.t_lo * kTileM / p.bs;
+  if (p.bs >= kTileM) {
+    const int blk = bts[tok0 / p.bs - blk0];
+    const int off = (int)(tok0 % p.bs);
+    mbar_expect_tx(bar, p.k_stage_bytes);
+    for (int kb = 0; kb < p.nkb; ++kb) tma_load_5d(kdst + kb * (kTileM * p.swb), &p.tmK, bar, kb * p.W, g, off, blk, l);
+  } else {
+    // one lane per block: the boxes are issued in parallel
+    const int nb = kTileM / p.bs;
+    const int nvalid = min(nb, (int)((jb.n - tok0 + p.bs - 1) / p.bs));
+    mbar_expect_tx(bar, (uint32_t)(nvalid * p.bs * p.swb * p.nkb));
+    __syncwarp();
+    if (lane < nvalid) {
+      const int blk = bts[tok0 / p.bs - blk0 + lane];
+      for (int kb = 0; kb < p.nkb; ++kb)
+        tma_load_5d_lane(kdst + kb * (kTileM * p.swb) + lane * p.bs * p.swb, &p.tmK, bar, kb * p.W, g, 0, blk, l);
+    }
+    __syncwarp();
+  }
+}
+
+// The job's block-table entries -> SMEM (once per job, all lanes).
+__device__ __noinline__ void paged_job_table(const FusedParams& p, const Job& jb, int lane, int* bts) {
+  __syncwarp();
+  if (jb.t_hi > jb.t_lo) {
+    const long long b0 = (long long)jb.t_lo * kTileM / p.bs;
+    const long long b1 = min(((long long)jb.t_hi * kTileM + p.bs - 1) / p.bs, (long long)p.max_blocks);
+    const int* bt = p.btab + (long long)jb.b * p.max_blocks;
+    for (long long i = b0 + lane; i < b1; i += 32) bts[i - b0] = bt[i];
+  }
+  __syncwarp();
+}
+
+// Row f3 producer (whole warp 0): the contiguous producer's loop with the K
+// tiles read through the block table (out of line: the contiguous producer's
+// code stays as it was -- the warp roles share the instruction cache).
+__device__ __noinline__ void producer_paged(const FusedParams& p, uint8_t* smem, uint32_t bar_full, uint32_t bar_empty,
+                                            uint32_t bar_qfull, uint32_t bar_qempty, int lane) {
+  uint32_t stage = 0, sphase = 0, ui = 0;
+  int* bts = reinterpret_cast<int*>(smem + p.off_bt);
+  for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
+    const Job jb = decode_job(p, job);
+    paged_job_table(p, jb, lane, bts);
+    for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
+      const int l = u / p.Hkv, g = u % p.Hkv;
+      const uint32_t qs = ui & (p.nq - 1), qpar = (ui / p.nq) & 1;
+      mbar_wait(bar_qempty + 8 * qs, qpar ^ 1);
+      mbar_expect_tx(bar_qfull + 8 * qs, (uint32_t)(p.NC * p.d * p.esz));
+      const uint32_t qdst = smem_u32(smem + p.off_q + qs * p.q_slot_bytes);
+      for (int kb = 0; kb < p.nkb; ++kb)
+        tma_load_5d(qdst + kb * (p.NCP * p.swb), &p.tmQ, bar_qfull + 8 * qs, kb * p.W, g * p.G, 0, l, jb.b);
+      for (int t = jb.t_lo; t < jb.t_hi; ++t) {
+        mbar_wait(bar_empty + 8 * stage, sphase ^ 1);
+        const uint32_t kdst = smem_u32(smem + p.off_k + stage * p.k_stage_bytes);
+        paged_tile(p, kdst, bar_full + 8 * stage, jb, t, g, l, lane, bts);
+        if (++stage == (uint32_t)p.stages) { stage = 0; sphase ^= 1; }
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -516,7 +605,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   unsigned long long* const part_cur = p.part + parity * part_half;
   unsigned long long* const part_old = p.part + (parity ^ 1u) * part_half;
 
-  if (warp == 0) {
+  if (warp == 0 && p.paged) {
+    // ================================================================ TMA producer, paged K (row f3)
+    producer_paged(p, smem, bar_full, bar_empty, bar_qfull, bar_qempty, lane);
+  } else if (warp == 0) {
     // ================================================================ TMA producer
     // (whole warp, warp-uniform loop; the helpers issue from one elected lane)
     {
@@ -670,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
                 sum[i] = 0.f;
               }
             }
-            if (tok0 + (long long)(t - jb.t_lo) * kTileM < p.N) {
+            if (tok0 + (long long)(t - jb.t_lo) * kTileM < jb.n) {
               {
                 // d = y - ref; the common case adds 2^d (FFMA, MUFU, FADD + a max);
                 // a jump d > 64 (rare) re-bases that column on y to keep fp32 finite
@@ -734,9 +826,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           float mm = -CUDART_INF_F, ss = 0.f;
           if (c < p.NC) {
 #pragma unroll
-            for (int w = 0; w < 4; ++w) merge2(mm, ss, rb[w * NCP + c].x, rb[w * NCP + c].y);
+            for (int w = 0; w < 4; ++w) {                                // a warp with no valid token has sum 0
+              const float2 v = rb[w * NCP + c];                           // and an undefined ref: merge it as -inf
+              merge2(mm, ss, v.y > 0.f ? v.x : -CUDART_INF_F, v.y);
+            }
           }
-          if (!(ss > 0.f)) { mm = -CUDART_INF_F; ss = -1.f; }          // written, but empty
+          if (!(ss > 0.f) || jb.t_lo == jb.t_hi) { mm = -CUDART_INF_F; ss = -1.f; }   // written, but empty
+                                                                        // (an empty job of a ragged batch)
           if (p.world == 1) {
             st_relaxed_u64(part_cur + row + c, pack_ms(mm, ss));
           } else {
@@ -920,7 +1016,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       if (p.n_ug == 1) {
         for (int t = 0; t < ntile; ++t) {
           const long long i = (long long)(jb.t_lo + t) * kTileM + tok;
-          if (i < p.N) {
+          if (i < jb.n) {
             if (p.acc_out != nullptr) {
               for (int r = 0; r < p.Rv; ++r)
                 p.acc_out[((long long)jb.b * p.Rv + r) * p.N + i] = acc[(t * p.Rv + r) * kTileM + tok];
@@ -934,7 +1030,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       } else {
         for (int t = 0; t < ntile; ++t) {
           const long long i = (long long)(jb.t_lo + t) * kTileM + tok;
-          if (i < p.N)
+          if (i < jb.n)
             for (int r = 0; r < p.Rv; ++r)
               p.accpart[(((long long)jb.b * p.n_ug + jb.ug) * p.Rv + r) * p.N + i] = acc[(t * p.Rv + r) * kTileM + tok];
         }
@@ -949,8 +1045,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         named_bar(2, 128);
         // this CTA finalises slice ug of the token group's tokens
         const long long g_lo = (long long)jb.t_lo * kTileM;
-        const long long g_hi = min((long long)jb.t_hi * kTileM, (long long)p.N);
-        const long long n = g_hi - g_lo;
+        const long long g_hi = min((long long)jb.t_hi * kTileM, (long long)jb.n);
+        const long long n = max(0LL, g_hi - g_lo);
         const long long s_lo = g_lo + n * jb.ug / p.n_ug, s_hi = g_lo + n * (jb.ug + 1) / p.n_ug;
         for (long long i = s_lo + tok; i < s_hi; i += kTileM) {
           float s = 0.f;
@@ -1010,7 +1106,7 @@ struct Plan {
   int P = 0, n_tg = 0, n_ug = 0, J = 0, T = 0, U = 0, tpc = 0, upc = 0;
   int NC = 0, NCP = 0, W = 0, nkb = 0, stages = 0, nslots = 0, swb = 0;
   long long total_jobs = 0;
-  uint32_t off_k = 0, off_q = 0, off_acc = 0, off_red = 0, off_lse = 0, off_comb = 0, off_bar = 0, smem = 0;
+  uint32_t off_k = 0, off_q = 0, off_acc = 0, off_red = 0, off_lse = 0, off_comb = 0, off_bar = 0, off_bt = 0, smem = 0;
   uint32_t k_stage_bytes = 0, q_slot_bytes = 0;
   int nq = 2;
   size_t ws_part = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0;
@@ -1044,6 +1140,8 @@ uint32_t carve(Plan& pl, int Rv, int stages) {
   pl.off_comb = o;
   o += 16 + 4 * pl.NCP * 8;
   o = (o + 15) & ~15u;
+  pl.off_bt = o;                                     // paged K: the job's block-table slice
+  o += (kMaxSlots * kTileM / 8 + 8) * 4;
   pl.off_bar = o;
   o += (2 * stages + 2 * kMaxQSlots + 2 * kMaxSlots + 4 + 2 * kLseRing) * 8 + 16;
   return o + 1024;                                   // slack for the manual 1024-byte alignment
@@ -1245,9 +1343,33 @@ struct PeerArgs {
   void* const* bufs = nullptr;                        // world partial buffers (fused_peer_buffer_bytes each)
 };
 
+// Row f3: the paged-cache tensor map {d, Hkv, block_size, blocks, L}, box {W, 1, min(bs, 128), 1, 1}.
+bool encode_paged_map(const PagedK& pk, const Geom& g, const Plan& pl, CUtensorMap* tmK) {
+  PFN_encodeTiled_t enc = encode_fn();
+  if (enc == nullptr) return false;
+  const CUtensorMapSwizzle sw = pl.swb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                               : (pl.swb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  const CUtensorMapDataType dt = g.esz == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const long long esz = g.esz;
+  auto fix = [esz](long long stride, long long prev_extent_bytes, long long size) -> cuuint64_t {
+    return (size == 1 || stride == 0) ? (cuuint64_t)prev_extent_bytes : (cuuint64_t)(stride * esz);
+  };
+  cuuint64_t dims[5] = {(cuuint64_t)g.d, (cuuint64_t)g.Hkv, (cuuint64_t)pk.bs, (cuuint64_t)pk.num_blocks,
+                        (cuuint64_t)g.L};
+  cuuint64_t s1 = fix(pk.s_g, (long long)g.d * esz, g.Hkv);
+  cuuint64_t s2 = fix(pk.s_tok, (long long)s1 * g.Hkv, pk.bs);
+  cuuint64_t s3 = fix(pk.s_blk, (long long)s2 * pk.bs, pk.num_blocks);
+  cuuint64_t s4 = fix(pk.s_l, (long long)s3 * pk.num_blocks, g.L);
+  cuuint64_t strides[4] = {s1, s2, s3, s4};
+  cuuint32_t box[5] = {(cuuint32_t)pl.W, 1, (cuuint32_t)std::min(pk.bs, kTileM), 1, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return enc(tmK, dt, 5, const_cast<void*>(pk.cache), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay, int mode,
                          const float* lse_in, float* importance, void* ws, size_t ws_bytes, cudaStream_t st,
-                         float* acc_out = nullptr, const PeerArgs& peer = PeerArgs()) {
+                         float* acc_out = nullptr, const PeerArgs& peer = PeerArgs(), const PagedK* pk = nullptr) {
   Plan pl = make_plan(g, true, peer.sm_budget);
   if (!pl.ok || ws_bytes < pl.ws_total()) return cudaErrorInvalidValue;
   if (peer.world < 1 || peer.world > kMaxPeers || peer.rank < 0 || peer.rank >= peer.world) return cudaErrorInvalidValue;
@@ -1257,6 +1379,14 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   std::lock_guard<std::mutex> lk(mu);
   std::memset(&p, 0, sizeof(p));
   if (!encode_maps(Q, K, g, lay, pl, &p.tmK, &p.tmQ)) return cudaErrorInvalidValue;
+  if (pk != nullptr) {
+    if (!encode_paged_map(*pk, g, pl, &p.tmK)) return cudaErrorInvalidValue;
+    p.paged = 1;
+    p.bs = pk->bs;
+    p.btab = pk->btab;
+    p.max_blocks = pk->max_blocks;
+    p.seq_lens = pk->seq_lens;
+  }
   p.B = g.B; p.L = g.L; p.Hkv = g.Hkv; p.G = g.G; p.Rv = g.Rv; p.d = g.d; p.N = (int)g.N;
   p.T = pl.T; p.U = pl.U; p.n_tg = pl.n_tg; p.n_ug = pl.n_ug; p.J = pl.J; p.total_jobs = pl.total_jobs;
   p.NC = pl.NC; p.NCP = pl.NCP; p.W = pl.W; p.nkb = pl.nkb; p.stages = pl.stages; p.nslots = pl.nslots;
@@ -1269,7 +1399,7 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   p.idesc = (1u << 4) | ab_fmt | ((uint32_t)(pl.NCP >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
   p.layout_type = pl.swb == 128 ? 2u : (pl.swb == 64 ? 4u : 6u);
   p.off_k = pl.off_k; p.off_q = pl.off_q; p.off_acc = pl.off_acc; p.off_red = pl.off_red; p.off_lse = pl.off_lse; p.off_comb = pl.off_comb;
-  p.off_bar = pl.off_bar; p.k_stage_bytes = pl.k_stage_bytes; p.q_slot_bytes = pl.q_slot_bytes;
+  p.off_bar = pl.off_bar; p.off_bt = pl.off_bt; p.k_stage_bytes = pl.k_stage_bytes; p.q_slot_bytes = pl.q_slot_bytes;
   p.nq = pl.nq;
   char* w = reinterpret_cast<char*>(ws);
   // counters first: their offsets depend only on (B, U), not on the plan
@@ -1344,6 +1474,14 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
 cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                         float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
   return fused_launch(Q, K, g, lay, kModeFull, nullptr, importance, ws, ws_bytes, st);
+}
+
+cudaError_t fused_score_paged(const __nv_bfloat16* Q, const PagedK& K, const Geom& g, const Layout& lay,
+                              float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
+  Layout l2 = lay;
+  l2.k_b = l2.k_l = l2.k_g = l2.k_i = 0;                    // (the contiguous map is replaced by the paged one)
+  return fused_launch(Q, reinterpret_cast<const __nv_bfloat16*>(K.cache), g, l2, kModeFull, nullptr, importance, ws,
+                      ws_bytes, st, nullptr, PeerArgs(), &K);
 }
 
 cudaError_t fused_score_stats(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,

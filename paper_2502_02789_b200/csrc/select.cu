@@ -72,8 +72,12 @@ __device__ __forceinline__ int block_excl_scan(int v, ScanSmem& sm, int* total) 
   return res;
 }
 
-__global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all, long long N, int pool_k, int chunk,
-                                               int pos0, long long K_c, int* __restrict__ ids_all,
+// Nrow: row length of the [B][Nrow] arrays; seq_lens (optional, row f3): the
+// request's own prompt length n_b (clamped to [1, Nrow]), else Nrow.  K_c is
+// computed per request from the keep rate in parts per million (Z9's integer rule).
+__global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all, long long Nrow,
+                                               const int* __restrict__ seq_lens, int pool_k, int chunk,
+                                               int pos0, long long ppm, int* __restrict__ ids_all,
                                                int* __restrict__ pos_all, int* __restrict__ n_kept,
                                                float* __restrict__ cs_all, const int* __restrict__ tokens_all,
                                                int* __restrict__ out_all, int mode, int segcap, long long cpb) {
@@ -84,23 +88,28 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
   __shared__ int kept_c[ST];                      // kept chunk ids of one scan tile, in order
   __shared__ int kept_off[ST];
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long N = seq_lens ? std::min<long long>(std::max(seq_lens[b], 1), Nrow) : Nrow;
   const long long n_c = (N + chunk - 1) / chunk;
-  const float* imp = imp_all + (long long)b * N;
+  const long long n_c_row = (Nrow + chunk - 1) / chunk;
+  const long long K_c = std::min(n_c, std::max(1LL, (ppm * n_c + 999999) / 1000000));
+  const float* imp = imp_all + (long long)b * Nrow;
   const long long w_ = (pool_k - 1) / 2;
   // chunk scores: SMEM when this CTA runs phases B-C and n_c fits, else the workspace
-  float* cs = (mode != kModeA && n_c <= kSmemChunks) ? seg + 2 * segcap + 2 * w_ : cs_all + (long long)b * n_c;
-  int* ids = ids_all + (long long)b * N;
-  int* pos = pos_all + (long long)b * N;
+  // (decided on the row's chunk count, as the launch sized the SMEM: a ragged request may have fewer)
+  const bool cs_smem = mode != kModeA && n_c_row <= kSmemChunks;
+  float* cs = cs_smem ? seg + 2 * segcap + 2 * w_ : cs_all + (long long)b * n_c_row;
+  int* ids = ids_all + (long long)b * Nrow;
+  int* pos = pos_all + (long long)b * Nrow;
   const long long w = (pool_k - 1) / 2;
 
   if (mode == kModeBC) {
-    if (n_c <= kSmemChunks)
-      for (long long c = tid; c < n_c; c += ST) cs[c] = cs_all[(long long)b * n_c + c];
+    if (cs_smem)
+      for (long long c = tid; c < n_c; c += ST) cs[c] = cs_all[(long long)b * n_c_row + c];
     __syncthreads();
   } else {
   // ---- A. pooled scores (centred window, shrinking edges) -> chunk sums of
   //      chunks [c_lo, c_hi) (all of them unless kModeA)
-  const long long c_lo = mode == kModeA ? (long long)blockIdx.y * cpb : 0;
+  const long long c_lo = mode == kModeA ? std::min(n_c, (long long)blockIdx.y * cpb) : 0;
   const long long c_hi = mode == kModeA ? std::min(n_c, c_lo + cpb) : n_c;
   const long long t_lo = c_lo * chunk, t_hi = std::min(N, c_hi * chunk);
   float* pooled = seg + segcap + 2 * w;             // [segcap]
@@ -240,8 +249,8 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
 
   // ---- C. keep flags in chunk order, compaction (+ gather) of the kept token ranges
   int carry_eq = 0, carry_tok = 0;
-  const int* tokens = tokens_all ? tokens_all + (long long)b * N : nullptr;
-  int* out = out_all ? out_all + (long long)b * N : nullptr;
+  const int* tokens = tokens_all ? tokens_all + (long long)b * Nrow : nullptr;
+  int* out = out_all ? out_all + (long long)b * Nrow : nullptr;
   for (long long base = 0; base < n_c; base += ST) {
     const long long c = base + tid;
     const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
@@ -289,8 +298,9 @@ size_t select_ws_bytes(int B, long long N, int chunk) {
 
 bool select_supported(int pool_k) { return pool_k <= kMaxPool; }
 
-cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int chunk, int pos0, long long K_c,
-                          int* ids, int* pos, int* n_kept, void* ws, cudaStream_t st, const int* tokens, int* out) {
+cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int chunk, int pos0, long long ppm,
+                          int* ids, int* pos, int* n_kept, void* ws, cudaStream_t st, const int* tokens, int* out,
+                          const int* seq_lens) {
   static bool configured = false;
   const size_t smem_max = (size_t)(2 * SEG + 2 * ((kMaxPool - 1) / 2) + kSmemChunks) * sizeof(float);
   if (!configured) {
@@ -310,15 +320,15 @@ cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int 
     const long long span = std::min(N, cpb * chunk);
     const int segcap = (int)std::min<long long>(SEG, (span + 31) / 32 * 32);
     const size_t needA = (size_t)(2 * segcap + 2 * w) * sizeof(float);
-    k_select<<<dim3(B, (unsigned)nblk), ST, needA, st>>>(imp, N, pool_k, chunk, pos0, K_c, ids, pos, n_kept, cs, tokens,
+    k_select<<<dim3(B, (unsigned)nblk), ST, needA, st>>>(imp, N, seq_lens, pool_k, chunk, pos0, ppm, ids, pos, n_kept, cs, tokens,
                                                         out, kModeA, segcap, cpb);
     const size_t needBC = (size_t)(2 * segcap + 2 * w + (n_c <= kSmemChunks ? n_c : 0)) * sizeof(float);
-    k_select<<<B, ST, needBC, st>>>(imp, N, pool_k, chunk, pos0, K_c, ids, pos, n_kept, cs, tokens, out, kModeBC,
+    k_select<<<B, ST, needBC, st>>>(imp, N, seq_lens, pool_k, chunk, pos0, ppm, ids, pos, n_kept, cs, tokens, out, kModeBC,
                                     segcap, cpb);
     return cudaGetLastError();
   }
   const size_t need = (size_t)(2 * SEG + 2 * w + (n_c <= kSmemChunks ? n_c : 0)) * sizeof(float);
-  k_select<<<B, ST, need, st>>>(imp, N, pool_k, chunk, pos0, K_c, ids, pos, n_kept, cs, tokens, out, kModeAll, SEG,
+  k_select<<<B, ST, need, st>>>(imp, N, seq_lens, pool_k, chunk, pos0, ppm, ids, pos, n_kept, cs, tokens, out, kModeAll, SEG,
                                 n_c);
   return cudaGetLastError();
 }

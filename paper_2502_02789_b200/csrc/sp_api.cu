@@ -84,6 +84,10 @@ sp_status check_select(int32_t B, int64_t N, const sp_select_params* p) {
   return SP_OK;
 }
 
+// keep rate snapped to parts per million (Z9); the kernels evaluate
+// K_c = clamp(ceil(ppm * n_c / 1e6), 1, n_c) in integers, as sp_kept_chunks does
+long long keep_ppm(double keep_rate) { return (long long)std::floor(keep_rate * 1000000.0 + 0.5); }
+
 sp_status from_cuda(cudaError_t e) {
   if (e == cudaSuccess) return SP_OK;
   cudaGetLastError();
@@ -125,7 +129,7 @@ const char* sp_status_string(sp_status s) {
 
 int64_t sp_kept_chunks(int64_t n_chunks, double keep_rate) {
   if (n_chunks < 1 || !(keep_rate > 0.0 && keep_rate <= 1.0)) return -1;
-  const long long ppm = (long long)std::floor(keep_rate * 1000000.0 + 0.5);
+  const long long ppm = keep_ppm(keep_rate);
   long long k = (ppm * n_chunks + 999999) / 1000000;
   if (k < 1) k = 1;
   if (k > n_chunks) k = n_chunks;
@@ -297,6 +301,49 @@ sp_status sp_score_e4m3(const void* Q8, const void* K8, float q_scale, float k_s
                                G, Lay, importance, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+// Row f3: paged K cache + block table (+ per-request lengths).
+size_t sp_score_paged_workspace_bytes(const sp_geom* g) {
+  if (check_geom(g) != SP_OK) return 0;
+  const Geom G = to_geom(*g);
+  return fused_supported(G, Layout{}, nullptr, nullptr) ? fused_score_ws_bytes(G) : 0;
+}
+
+sp_status sp_score_paged(const void* Q, const sp_paged_k* K, const sp_geom* g, const sp_layout* lay,
+                         float* importance, void* ws, size_t ws_bytes, sp_stream stream) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if (K == nullptr || importance == nullptr) return SP_EINVAL;
+  if (K->cache == nullptr || K->block_table == nullptr || (reinterpret_cast<uintptr_t>(K->cache) & 15u) != 0)
+    return SP_EINVAL;
+  const int bs = K->block_size;
+  if (!((bs >= 8 && bs < 128 && 128 % bs == 0) || (bs >= 128 && bs % 128 == 0))) return SP_EINVAL;
+  if (K->num_blocks < 1 || K->max_blocks < (g->N + bs - 1) / bs) return SP_EINVAL;
+  const long long ks[4] = {K->s_l, K->s_blk, K->s_tok, K->s_g};
+  const long long kn[4] = {g->L, K->num_blocks, bs, g->Hkv};
+  for (int i = 0; i < 4; ++i) {
+    if (ks[i] < 0) return SP_EINVAL;
+    if (kn[i] > 1 && (ks[i] * 2) % 16 != 0) return SP_EINVAL;
+  }
+  // Q strides: reuse the contiguous-layout check with a dummy K view of the same geometry
+  sp_layout ql = *lay;
+  ql.k_b = ql.k_l = ql.k_g = 0;
+  ql.k_i = g->d;
+  if ((s = check_layout(g, &ql, Q, K->cache)) != SP_OK) return s;
+  if ((s = check_device()) != SP_OK) return s;
+  const Geom G = to_geom(*g);
+  const Layout Lay = to_layout(*lay);
+  if (!fused_supported(G, Lay, Q, K->cache)) return SP_EUNSUPPORTED;
+  if (ws == nullptr || ws_bytes < fused_score_ws_bytes(G) || (reinterpret_cast<uintptr_t>(ws) & 255u) != 0)
+    return SP_EWORKSPACE;
+  PagedK pk;
+  pk.cache = K->cache;
+  pk.s_l = K->s_l; pk.s_blk = K->s_blk; pk.s_tok = K->s_tok; pk.s_g = K->s_g;
+  pk.num_blocks = K->num_blocks; pk.bs = bs;
+  pk.btab = K->block_table; pk.max_blocks = K->max_blocks; pk.seq_lens = K->seq_lens;
+  return from_cuda(fused_score_paged(reinterpret_cast<const __nv_bfloat16*>(Q), pk, G, Lay, importance, ws, ws_bytes,
+                                     reinterpret_cast<cudaStream_t>(stream)));
+}
+
 sp_status sp_score_plan(const sp_geom* g, int64_t out[9]) {
   sp_status s = check_geom(g);
   if (s != SP_OK) return s;
@@ -392,10 +439,22 @@ sp_status sp_select_gather(const float* importance, const int32_t* tokens, int32
   if ((tokens == nullptr) != (out_tokens == nullptr)) return SP_EINVAL;
   if ((s = check_device()) != SP_OK) return s;
   if (ws == nullptr || ws_bytes < select_ws_bytes(B, N, p->chunk)) return SP_EWORKSPACE;
-  const long long n_c = (N + p->chunk - 1) / p->chunk;
-  const long long K_c = sp_kept_chunks(n_c, p->keep_rate);
-  return from_cuda(select_launch(importance, B, N, p->pool_k, p->chunk, p->pos0, K_c, ids, pos, n_kept, ws,
-                                 reinterpret_cast<cudaStream_t>(stream), tokens, out_tokens));
+  return from_cuda(select_launch(importance, B, N, p->pool_k, p->chunk, p->pos0, keep_ppm(p->keep_rate), ids, pos,
+                                 n_kept, ws, reinterpret_cast<cudaStream_t>(stream), tokens, out_tokens));
+}
+
+sp_status sp_select_ragged(const float* importance, const int32_t* seq_lens, const int32_t* tokens, int32_t B,
+                           int64_t N, const sp_select_params* p, int32_t* ids, int32_t* pos, int32_t* n_kept,
+                           int32_t* out_tokens, void* ws, size_t ws_bytes, sp_stream stream) {
+  sp_status s = check_select(B, N, p);
+  if (s != SP_OK) return s;
+  if (importance == nullptr || seq_lens == nullptr || ids == nullptr || pos == nullptr || n_kept == nullptr)
+    return SP_EINVAL;
+  if ((tokens == nullptr) != (out_tokens == nullptr)) return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
+  if (ws == nullptr || ws_bytes < select_ws_bytes(B, N, p->chunk)) return SP_EWORKSPACE;
+  return from_cuda(select_launch(importance, B, N, p->pool_k, p->chunk, p->pos0, keep_ppm(p->keep_rate), ids, pos,
+                                 n_kept, ws, reinterpret_cast<cudaStream_t>(stream), tokens, out_tokens, seq_lens));
 }
 
 sp_status sp_gather(const int32_t* tokens, const int32_t* ids, const int32_t* n_kept, int32_t B, int64_t N,

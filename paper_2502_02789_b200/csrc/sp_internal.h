@@ -45,6 +45,16 @@ inline Layout to_layout(const sp_layout& l) {
   return o;
 }
 
+// Row f3: a paged K cache (element strides; d contiguous) + block table + lengths.
+struct PagedK {
+  const void* cache;
+  long long s_l, s_blk, s_tok, s_g;
+  int num_blocks, bs;
+  const int* btab;
+  int max_blocks;
+  const int* seq_lens;
+};
+
 // Round up to a multiple of 256 bytes (workspace carving).
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -74,6 +84,8 @@ cudaError_t fused_score_finish(const __nv_bfloat16* Q, const __nv_bfloat16* K, c
                                const float* lse2, float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t fused_score_acc(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                             float* acc2, void* ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t fused_score_paged(const __nv_bfloat16* Q, const PagedK& K, const Geom& g, const Layout& lay,
+                              float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t acc_importance(const float* acc2, int B, int Rv, long long N, float* importance, cudaStream_t st);
 size_t fused_peer_buffer_bytes(const Geom& g, int world, int sm_budget);
 size_t fused_peer_ws_bytes(const Geom& g, int sm_budget);
@@ -85,9 +97,11 @@ cudaError_t fused_score_peer(const __nv_bfloat16* Q, const __nv_bfloat16* K, con
 // ---------------------------------------------------------------- select / gather (select.cu, gather.cu)
 size_t select_ws_bytes(int B, long long N, int chunk);
 bool select_supported(int pool_k);
+// ppm: keep rate in parts per million (K_c per request, Z9); seq_lens: optional
+// device [B] per-request prompt lengths (row f3), rows of the arrays stay N long
 cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int chunk, int pos0,
-                          long long K_c, int* ids, int* pos, int* n_kept, void* ws, cudaStream_t st,
-                          const int* tokens = nullptr, int* out = nullptr);
+                          long long ppm, int* ids, int* pos, int* n_kept, void* ws, cudaStream_t st,
+                          const int* tokens = nullptr, int* out = nullptr, const int* seq_lens = nullptr);
 cudaError_t gather_launch(const int* tokens, const int* ids, const int* n_kept, int B, long long N, int* out,
                           cudaStream_t st);
 
