@@ -383,7 +383,8 @@ def run_ours(args):
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(f"{args.config}/{args.algo}" + ("/e4m3" if f8 else ""))
+            traffic = json.load(f).get(f"{args.config}/{args.algo}" + ("/e4m3" if f8 else "")
+                                       + (f"/paged{args.paged}" if paged else ""))
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "sp_score", "kernel_ms": score_ms,
                 "algorithmic_bytes": alg_bytes, "peak_source": peak_src,

@@ -12,3 +12,11 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_fu
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_select -s 6 -c 1 -o gpurun_out/prof_select -f \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-graph > /dev/null 2>&1
 ls -la gpurun_out/launches.csv gpurun_out/*.ncu-rep
+# secondary lines (rows f3 / f4) and the e4m3 kernel's DRAM traffic
+for a in "--kv e4m3" "--kv e4m3 --config C2" "--paged 16" "--paged 256" "--paged 16 --config C2 --ragged"; do
+  n=$(echo "$a" | tr -d ' -'); timeout 300 python bench.py $a --no-cpu-baseline > gpurun_out/bench_$n.json 2>/dev/null; tail -c 400 gpurun_out/bench_$n.json
+done
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k_fused -c 2 --csv \
+  --log-file gpurun_out/f4_traffic.csv python bench.py --kv e4m3 --steps 1 --warmup 3 --no-cpu-baseline --no-graph > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k_fused -c 2 --csv \
+  --log-file gpurun_out/f3_traffic.csv python bench.py --paged 16 --steps 1 --warmup 3 --no-cpu-baseline --no-graph > /dev/null 2>&1
