@@ -235,6 +235,31 @@ sp_status sp_score_e4m3_plan(const sp_geom* g, int64_t out[9]);
 sp_status sp_score_e4m3(const void* Q8, const void* K8, float q_scale, float k_scale, const sp_geom* g,
                         const sp_layout* lay, float* importance, void* ws, size_t ws_bytes, sp_stream stream);
 
+/* ------------------------------------------------------------------ score, look-ahead-key denominator
+ * SURVEY 8(f) row f4, reading Z2': each look-ahead
+ * row's softmax also covers the look-ahead tokens' own keys -- "softmax over
+ * ALL keys visible to that row (context plus any earlier decoded tokens) ...
+ * sliced to the first M context entries WITHOUT renormalization".  Row r sees
+ * the N prompt keys and K_la[b][l][g][j] for j <= r - la_shift (causal):
+ * la_shift = 0 when row r is the r-th look-ahead token (its own key is
+ * K_la[.., r]); 1 when row 0 is the last prompt token (whose key is in K) and
+ * row r >= 1 the r-th decoded token (key K_la[.., r - 1]).
+ *   s_la[j] = scale * <Q[b][l][r][h], K_la[b][l][h/G][j]>
+ *   lse'    = log( sum_i exp(s[i]) + sum_{j <= r - la_shift} exp(s_la[j]) )
+ *   acc[r,i] = max_{l,h} (s[l,h,r,i] - lse'),  importance = mean_r exp(acc)
+ * K_la: bf16, element strides s_b, s_l, s_g, s_j (d contiguous), at least
+ * R_valid - la_shift rows per (b, l, g).  Fused kernel only; workspace
+ * sp_score_lookahead_workspace_bytes(g) bytes (zero-filled once, as sp_score's). */
+typedef struct sp_lookahead_k {
+  const void* K_la;
+  int64_t s_b, s_l, s_g, s_j;
+  int32_t la_shift;
+} sp_lookahead_k;
+
+size_t sp_score_lookahead_workspace_bytes(const sp_geom* g);
+sp_status sp_score_lookahead(const void* Q, const void* K, const sp_lookahead_k* la, const sp_geom* g,
+                             const sp_layout* lay, float* importance, void* ws, size_t ws_bytes, sp_stream stream);
+
 /* ------------------------------------------------------------------ score, paged K cache / ragged batch
  * the speculator's K cache in the serving layout -- fixed-size
  * blocks addressed through a block table (the "slot mapping" of the paper's vLLM

@@ -97,6 +97,33 @@ def softmax_lse(Q: np.ndarray, K: np.ndarray, scale: float) -> np.ndarray:
     return out
 
 
+def attention_scores_lookahead(Q: np.ndarray, K: np.ndarray, K_la: np.ndarray, scale: float,
+                               la_shift: int = 0) -> np.ndarray:
+    """Reading Z2' ("softmax over ALL keys visible
+    to that row (context plus any earlier decoded tokens) ... sliced to the first
+    M context entries WITHOUT renormalization"): look-ahead row r attends to the
+    N prompt keys and to the look-ahead tokens' keys K_la[j], j <= r - la_shift
+    (causal; la_shift = 0: row r's own key is K_la[r]; 1: row 0 is the last
+    prompt token and sees none).  The softmax runs over that whole key set and
+    is then sliced to the prompt entries (P:105-107's a_ij, i < M).
+
+    Q [L][R][H][d], K [L][Hkv][N][d], K_la [L][Hkv][R][d]  ->  A [R][L][N][H].
+    """
+    L, R, H, d = Q.shape
+    Hkv, N = K.shape[1], K.shape[2]
+    G = H // Hkv
+    A = np.empty((R, L, N, H), dtype=np.float64)
+    for l in range(L):
+        for h in range(H):
+            for r in range(R):
+                n_la = max(0, r + 1 - la_shift)
+                keys = np.concatenate([K[l, h // G], K_la[l, h // G, :n_la]], axis=0)   # prompt, then look-ahead
+                s = scale * (keys @ Q[l, r, h])
+                e = np.exp(s - s.max())
+                A[r, l, :, h] = e[:N] / e.sum()                    # slice, no renormalisation
+    return A
+
+
 # ------------------------------------------------------------------ O3-O4
 def aggregate_attention(A: np.ndarray, R_valid: int | None = None) -> np.ndarray:
     """Max-mean aggregation, P:117-119 (sec:attn_agg): "take the maximum over H

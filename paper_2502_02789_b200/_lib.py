@@ -39,6 +39,11 @@ class sp_paged_k(C.Structure):
                 ("block_table", C.c_void_p), ("max_blocks", C.c_int32), ("seq_lens", C.c_void_p)]
 
 
+class sp_lookahead_k(C.Structure):
+    _fields_ = [("K_la", C.c_void_p), ("s_b", C.c_int64), ("s_l", C.c_int64), ("s_g", C.c_int64),
+                ("s_j", C.c_int64), ("la_shift", C.c_int32)]
+
+
 class sp_host_io(C.Structure):
     _fields_ = [("Q", C.c_void_p), ("K", C.c_void_p), ("tokens", C.c_void_p), ("ids", C.c_void_p),
                 ("pos", C.c_void_p), ("n_kept", C.c_void_p), ("out_tokens", C.c_void_p),
@@ -82,6 +87,8 @@ SIGNATURES = {
     "sp_score_e4m3_workspace_bytes": (C.c_size_t, [_G]),
     "sp_score_e4m3_plan": (C.c_int, [_G, C.POINTER(C.c_int64)]),
     "sp_score_e4m3": (C.c_int, [_P, _P, C.c_float, C.c_float, _G, _L, _P, _P, C.c_size_t, _P]),
+    "sp_score_lookahead_workspace_bytes": (C.c_size_t, [_G]),
+    "sp_score_lookahead": (C.c_int, [_P, _P, C.POINTER(sp_lookahead_k), _G, _L, _P, _P, C.c_size_t, _P]),
     "sp_score_paged_workspace_bytes": (C.c_size_t, [_G]),
     "sp_score_paged": (C.c_int, [_P, C.POINTER(sp_paged_k), _G, _L, _P, _P, C.c_size_t, _P]),
     "sp_select_ragged": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int64, _S, _P, _P, _P, _P, _P, C.c_size_t, _P]),

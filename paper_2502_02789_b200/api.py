@@ -113,6 +113,25 @@ def score_e4m3_plan(Q8, K8, R_valid=None) -> dict:
     return dict(zip(keys, list(out)))
 
 
+def score_lookahead(Q, K, K_la, la_shift: int = 0, R_valid=None, scale=None, out=None, stream=None) -> torch.Tensor:
+    """Row f4, reading Z2': importance [B][N] with the look-ahead tokens' keys
+    K_la (bf16 [B][L][Hkv][R][d], d contiguous) in each row's softmax denominator."""
+    g, lay = make_geom(Q, K, R_valid, scale)
+    if K_la.dtype != torch.bfloat16 or K_la.dim() != 5 or K_la.stride(-1) != 1:
+        raise ValueError("K_la must be bf16 [B][L][Hkv][R][d] with d contiguous")
+    la = _lib.sp_lookahead_k(K_la=K_la.data_ptr(), s_b=K_la.stride(0), s_l=K_la.stride(1), s_g=K_la.stride(2),
+                             s_j=K_la.stride(3), la_shift=int(la_shift))
+    if out is None:
+        out = torch.empty((g.B, g.N), dtype=torch.float32, device=K.device)
+    nbytes = lib().sp_score_lookahead_workspace_bytes(C.byref(g))
+    if nbytes == 0:
+        check(_lib.SP_EUNSUPPORTED, "sp_score_lookahead")
+    ws = workspace(("score_la", _geom_key(g)), nbytes, K.device)
+    check(lib().sp_score_lookahead(Q.data_ptr(), K.data_ptr(), C.byref(la), C.byref(g), C.byref(lay), out.data_ptr(),
+                                   ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_score_lookahead")
+    return out
+
+
 def score_paged(Q, K_cache, block_table, seq_lens=None, N=None, R_valid=None, scale=None, out=None,
                 stream=None) -> torch.Tensor:
     """Row f3: token importance [B][N] fp32 from a paged K cache.

@@ -91,6 +91,7 @@ struct FusedParams {
   const int* btab;                     // [B][max_blocks] physical block ids
   int max_blocks;
   const int* seq_lens;                 // [B] prompt lengths in [1, N] (clamped), or null: all N
+  const float2* la;                    // Z2' (row f4): [B][U][NCP] look-ahead keys' (max2, sum) per column, or null
   // workspace
   unsigned long long* part;            // [2][B][U][n_tg][NCP] CTA partials, one buffer per launch parity:
                                        // (max2, sum) packed in one 64-bit word; 0 = "not yet written"
@@ -916,6 +917,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
               if (w.y > 0.f) merge2(M, S, w.x, w.y);
             }
           }
+          if (p.la != nullptr && c < p.NC) {                         // the look-ahead keys' share (Z2')
+            const float2 v = p.la[ubase * NCP + c];
+            if (v.y > 0.f) merge2(M, S, v.x, v.y);
+          }
           float l2 = 0.f;
           if (c < p.NC) {
             l2 = M + log2f(S);
@@ -1369,7 +1374,8 @@ bool encode_paged_map(const PagedK& pk, const Geom& g, const Plan& pl, CUtensorM
 
 cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay, int mode,
                          const float* lse_in, float* importance, void* ws, size_t ws_bytes, cudaStream_t st,
-                         float* acc_out = nullptr, const PeerArgs& peer = PeerArgs(), const PagedK* pk = nullptr) {
+                         float* acc_out = nullptr, const PeerArgs& peer = PeerArgs(), const PagedK* pk = nullptr,
+                         const float2* la = nullptr) {
   Plan pl = make_plan(g, true, peer.sm_budget);
   if (!pl.ok || ws_bytes < pl.ws_total()) return cudaErrorInvalidValue;
   if (peer.world < 1 || peer.world > kMaxPeers || peer.rank < 0 || peer.rank >= peer.world) return cudaErrorInvalidValue;
@@ -1425,6 +1431,7 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   p.trace = nullptr;
   p.mode = mode;
   p.lse_in = lse_in;
+  p.la = la;
 
   p.trace_units = 0;
   if (g_trace != nullptr) {
@@ -1474,6 +1481,58 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
 cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                         float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
   return fused_launch(Q, K, g, lay, kModeFull, nullptr, importance, ws, ws_bytes, st);
+}
+
+// Z2' (row f4): the look-ahead keys' (max2, sum) per (request, unit, column), one
+// warp per (b, l, h, r): x_j = xs * <Q[b][l][r][h], K_la[b][l][h/G][j]> for
+// j <= r - shift (fp32 FMA of exact bf16 products), log2 domain.
+__global__ void k_la_stats(const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ Kla, Layout lay,
+                           LookaheadK la, int B, int L, int H, int Hkv, int Rv, int d, int NCP, float xs,
+                           float2* __restrict__ out) {
+  const long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= (long long)B * L * H * Rv) return;
+  const int r = (int)(row % Rv), h = (int)((row / Rv) % H), l = (int)((row / ((long long)Rv * H)) % L);
+  const int b = (int)(row / ((long long)Rv * H * L));
+  const int G = H / Hkv, g = h / G;
+  const __nv_bfloat16* q = Q + b * lay.q_b + l * lay.q_l + r * lay.q_r + h * lay.q_h;
+  float qv[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) qv[k] = lane + 32 * k < d ? __bfloat162float(q[lane + 32 * k]) : 0.f;
+  float m = -CUDART_INF_F, s = 0.f;
+  const int n_la = r + 1 - la.shift;
+  for (int j = 0; j < n_la; ++j) {
+    const __nv_bfloat16* kr = Kla + b * la.s_b + l * la.s_l + g * la.s_g + j * la.s_j;
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (lane + 32 * k < d) acc = fmaf(qv[k], __bfloat162float(kr[lane + 32 * k]), acc);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    merge2(m, s, acc * xs, 1.f);
+  }
+  if (lane == 0) out[((long long)b * L * Hkv + (long long)l * Hkv + g) * NCP + r * G + (h % G)] = make_float2(m, s);
+}
+
+size_t fused_la_ws_bytes(const Geom& g) {
+  const size_t base = fused_score_ws_bytes(g);
+  if (base == 0) return 0;
+  const int NCP = ((g.G * g.Rv + 31) / 32) * 32;
+  return align256(base) + align256((size_t)g.B * g.L * g.Hkv * NCP * sizeof(float2));
+}
+
+cudaError_t fused_score_la(const __nv_bfloat16* Q, const __nv_bfloat16* K, const LookaheadK& la, const Geom& g,
+                           const Layout& lay, float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const size_t base = align256(fused_score_ws_bytes(g));
+  if (base == 0 || ws_bytes < fused_la_ws_bytes(g)) return cudaErrorInvalidValue;
+  const int NCP = ((g.G * g.Rv + 31) / 32) * 32;
+  float2* lab = reinterpret_cast<float2*>(reinterpret_cast<char*>(ws) + base);
+  const long long rows = (long long)g.B * g.L * g.H * g.Rv;
+  k_la_stats<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(Q, reinterpret_cast<const __nv_bfloat16*>(la.K), lay, la,
+                                                         g.B, g.L, g.H, g.Hkv, g.Rv, g.d, NCP, g.scale * kLog2e, lab);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return fused_launch(Q, K, g, lay, kModeFull, nullptr, importance, ws, base, st, nullptr, PeerArgs(), nullptr, lab);
 }
 
 cudaError_t fused_score_paged(const __nv_bfloat16* Q, const PagedK& K, const Geom& g, const Layout& lay,

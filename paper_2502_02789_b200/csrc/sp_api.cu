@@ -301,6 +301,36 @@ sp_status sp_score_e4m3(const void* Q8, const void* K8, float q_scale, float k_s
                                G, Lay, importance, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+// Row f4, reading Z2': the look-ahead tokens' keys join each row's softmax denominator.
+size_t sp_score_lookahead_workspace_bytes(const sp_geom* g) {
+  if (check_geom(g) != SP_OK) return 0;
+  const Geom G = to_geom(*g);
+  return fused_supported(G, Layout{}, nullptr, nullptr) ? fused_la_ws_bytes(G) : 0;
+}
+
+sp_status sp_score_lookahead(const void* Q, const void* K, const sp_lookahead_k* la, const sp_geom* g,
+                             const sp_layout* lay, float* importance, void* ws, size_t ws_bytes, sp_stream stream) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if ((s = check_layout(g, lay, Q, K)) != SP_OK) return s;
+  if (la == nullptr || la->K_la == nullptr || importance == nullptr) return SP_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(la->K_la) & 1u) != 0) return SP_EINVAL;
+  if (la->s_b < 0 || la->s_l < 0 || la->s_g < 0 || la->s_j < 0 || (la->la_shift != 0 && la->la_shift != 1))
+    return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
+  const Geom G = to_geom(*g);
+  const Layout Lay = to_layout(*lay);
+  if (!fused_supported(G, Lay, Q, K)) return SP_EUNSUPPORTED;
+  if (ws == nullptr || ws_bytes < fused_la_ws_bytes(G) || (reinterpret_cast<uintptr_t>(ws) & 255u) != 0)
+    return SP_EWORKSPACE;
+  LookaheadK lk;
+  lk.K = la->K_la;
+  lk.s_b = la->s_b; lk.s_l = la->s_l; lk.s_g = la->s_g; lk.s_j = la->s_j;
+  lk.shift = la->la_shift;
+  return from_cuda(fused_score_la(reinterpret_cast<const __nv_bfloat16*>(Q), reinterpret_cast<const __nv_bfloat16*>(K),
+                                  lk, G, Lay, importance, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 // Row f3: paged K cache + block table (+ per-request lengths).
 size_t sp_score_paged_workspace_bytes(const sp_geom* g) {
   if (check_geom(g) != SP_OK) return 0;

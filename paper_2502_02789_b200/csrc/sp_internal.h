@@ -55,6 +55,13 @@ struct PagedK {
   const int* seq_lens;
 };
 
+// Z2' (row f4): the look-ahead tokens' keys K_la[b][l][g][j][:] (element strides).
+struct LookaheadK {
+  const void* K;
+  long long s_b, s_l, s_g, s_j;
+  int shift;
+};
+
 // Round up to a multiple of 256 bytes (workspace carving).
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -86,6 +93,9 @@ cudaError_t fused_score_acc(const __nv_bfloat16* Q, const __nv_bfloat16* K, cons
                             float* acc2, void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t fused_score_paged(const __nv_bfloat16* Q, const PagedK& K, const Geom& g, const Layout& lay,
                               float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t fused_la_ws_bytes(const Geom& g);
+cudaError_t fused_score_la(const __nv_bfloat16* Q, const __nv_bfloat16* K, const LookaheadK& la, const Geom& g,
+                           const Layout& lay, float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t acc_importance(const float* acc2, int B, int Rv, long long N, float* importance, cudaStream_t st);
 size_t fused_peer_buffer_bytes(const Geom& g, int world, int sm_budget);
 size_t fused_peer_ws_bytes(const Geom& g, int sm_budget);

@@ -386,3 +386,45 @@ def test_e4m3_path_equals_bf16_path_on_common_values():
     b = ref.specprefill(to_bits(Qv), to_bits(Kv), tokens, 0.25, 0.5, 3, 4)
     np.testing.assert_array_equal(a["imp"], b["imp"])
     np.testing.assert_array_equal(a["ids"], b["ids"])
+
+
+# ------------------------------------------------------------------ row f4: look-ahead-key denominator (Z2')
+def test_lookahead_denominator_closed_form():
+    """All logits equal (Q = 0): every visible key has probability 1/(N + n_la(r)),
+    so the importance of each prompt token is mean_r 1/(N + r + 1 - shift)."""
+    L, R, H, Hkv, N, d = 2, 3, 4, 2, 10, 8
+    Q = np.zeros((L, R, H, d))
+    rng = np.random.default_rng(0)
+    K = rng.normal(size=(L, Hkv, N, d))
+    K_la = rng.normal(size=(L, Hkv, R, d))
+    for shift in (0, 1):
+        A = ref.attention_scores_lookahead(Q, K, K_la, 0.5, shift)
+        imp = ref.aggregate_attention(A)
+        want = np.mean([1.0 / (N + max(0, r + 1 - shift)) for r in range(R)])
+        np.testing.assert_allclose(imp, want, rtol=1e-14)
+
+
+def test_lookahead_denominator_vs_library_softmax():
+    """One (l, h, r) slice equals scipy's softmax over the concatenated key set,
+    sliced to the prompt entries; prompt + look-ahead probabilities sum to 1."""
+    rng = np.random.default_rng(1)
+    L, R, H, Hkv, N, d = 1, 4, 2, 1, 7, 5
+    Q, K, K_la = rng.normal(size=(L, R, H, d)), rng.normal(size=(L, Hkv, N, d)), rng.normal(size=(L, Hkv, R, d))
+    A = ref.attention_scores_lookahead(Q, K, K_la, 0.7, 0)
+    for r in range(R):
+        for h in range(H):
+            keys = np.concatenate([K[0, 0], K_la[0, 0, :r + 1]])
+            p = scipy.special.softmax(0.7 * keys @ Q[0, r, h])
+            np.testing.assert_allclose(A[r, 0, :, h], p[:N], rtol=1e-13)
+            assert A[r, 0, :, h].sum() < 1.0
+
+
+def test_lookahead_denominator_shift_one_row0_is_plain():
+    """la_shift = 1: row 0 sees no look-ahead key, so it equals the plain (Z2) row."""
+    rng = np.random.default_rng(2)
+    L, R, H, Hkv, N, d = 2, 3, 4, 2, 9, 6
+    Q, K, K_la = rng.normal(size=(L, R, H, d)), rng.normal(size=(L, Hkv, N, d)), rng.normal(size=(L, Hkv, R, d))
+    A1 = ref.attention_scores_lookahead(Q, K, K_la, 0.3, 1)
+    A0 = ref.attention_scores(Q, K, 0.3)
+    np.testing.assert_allclose(A1[0], A0[0], rtol=1e-13)
+    assert (A1[1:] < A0[1:]).all()
