@@ -269,7 +269,7 @@ sp_status sp_score_lookahead(const void* Q, const void* K, const sp_lookahead_k*
  * (vLLM's per-layer [num_blocks][block_size][Hkv][d] key cache with a uniform
  * layer stride, e.g. one allocation for all layers).  Token i of request b is
  * row i % block_size of physical block block_table[b][i / block_size].
- *   block_size   8, 16, 32 or 64 (divides 128), or a multiple of 128
+ *   block_size   a power of two >= 8 (8 ... 64 divide a 128-token tile; >= 128 hold whole tiles)
  *   block_table  device int32 [B][max_blocks], max_blocks >= ceil(N / block_size);
  *                entries past a request's last block are never read
  *   seq_lens     device int32 [B]: request b's prompt length n_b (clamped to [1, N]),

@@ -87,7 +87,7 @@ struct FusedParams {
   uint32_t k_stage_bytes, q_slot_bytes;
   int nq;                              // query slots (2 or 4, power of two)
   // row f3: paged K (tmK is then 5-D {d, Hkv, block_size, blocks, L}) and per-request lengths
-  int paged, bs;                       // paged: 1; tokens per block (8..64 dividing 128, or a multiple of 128)
+  int paged, bs, bs_log2;              // paged: 1; tokens per block (a power of two >= 8), its log2
   const int* btab;                     // [B][max_blocks] physical block ids
   int max_blocks;
   const int* seq_lens;                 // [B] prompt lengths in [1, N] (clamped), or null: all N
@@ -425,21 +425,22 @@ __device__ __noinline__ Job decode_job(const FusedParams& p, long long job) {
 // bts: the job's block-table slice in SMEM (entry 0 = the block of token t_lo * 128).
 __device__ __noinline__ void paged_tile(const FusedParams& p, uint32_t kdst, uint32_t bar, const Job& jb, int t, int g,
                                         int l, int lane, const int* bts) {
-  const long long tok0 = (long long)t * kTileM;
-  const long long blk0 = (long long)jb.t_lo * kTileM / p.bs;
+  // (32-bit shifts: the block size is a power of two; token indices < 2^31)
+  const int tok0 = t * kTileM;
+  const int blk0 = (jb.t_lo * kTileM) >> p.bs_log2;
   if (p.bs >= kTileM) {
-    const int blk = bts[tok0 / p.bs - blk0];
-    const int off = (int)(tok0 % p.bs);
+    const int blk = bts[(tok0 >> p.bs_log2) - blk0];
+    const int off = tok0 & (p.bs - 1);
     mbar_expect_tx(bar, p.k_stage_bytes);
     for (int kb = 0; kb < p.nkb; ++kb) tma_load_5d(kdst + kb * (kTileM * p.swb), &p.tmK, bar, kb * p.W, g, off, blk, l);
   } else {
     // one lane per block: the boxes are issued in parallel
-    const int nb = kTileM / p.bs;
-    const int nvalid = min(nb, (int)((jb.n - tok0 + p.bs - 1) / p.bs));
+    const int nb = kTileM >> p.bs_log2;
+    const int nvalid = min(nb, (jb.n - tok0 + p.bs - 1) >> p.bs_log2);
     mbar_expect_tx(bar, (uint32_t)(nvalid * p.bs * p.swb * p.nkb));
     __syncwarp();
     if (lane < nvalid) {
-      const int blk = bts[tok0 / p.bs - blk0 + lane];
+      const int blk = bts[(tok0 >> p.bs_log2) - blk0 + lane];
       for (int kb = 0; kb < p.nkb; ++kb)
         tma_load_5d_lane(kdst + kb * (kTileM * p.swb) + lane * p.bs * p.swb, &p.tmK, bar, kb * p.W, g, 0, blk, l);
     }
@@ -1389,6 +1390,7 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
     if (!encode_paged_map(*pk, g, pl, &p.tmK)) return cudaErrorInvalidValue;
     p.paged = 1;
     p.bs = pk->bs;
+    p.bs_log2 = __builtin_ctz((unsigned)pk->bs);
     p.btab = pk->btab;
     p.max_blocks = pk->max_blocks;
     p.seq_lens = pk->seq_lens;

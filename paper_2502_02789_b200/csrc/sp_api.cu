@@ -346,7 +346,7 @@ sp_status sp_score_paged(const void* Q, const sp_paged_k* K, const sp_geom* g, c
   if (K->cache == nullptr || K->block_table == nullptr || (reinterpret_cast<uintptr_t>(K->cache) & 15u) != 0)
     return SP_EINVAL;
   const int bs = K->block_size;
-  if (!((bs >= 8 && bs < 128 && 128 % bs == 0) || (bs >= 128 && bs % 128 == 0))) return SP_EINVAL;
+  if (bs < 8 || (bs & (bs - 1)) != 0) return SP_EINVAL;            // a power of two >= 8
   if (K->num_blocks < 1 || K->max_blocks < (g->N + bs - 1) / bs) return SP_EINVAL;
   const long long ks[4] = {K->s_l, K->s_blk, K->s_tok, K->s_g};
   const long long kn[4] = {g->L, K->num_blocks, bs, g->Hkv};

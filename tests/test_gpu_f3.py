@@ -104,7 +104,7 @@ def test_paged_invalid_block_size():
     w = gen.CONFIGS["C0"].with_(d=64, N=100)
     Qb, Kb, _ = gen.gen_batch(w)
     Q, K = _dev(Qb), _dev(Kb)
-    for bs in (4, 24, 192):
+    for bs in (4, 24, 192, 384):
         cache = torch.zeros((w.L, 64, bs, w.Hkv, w.d), dtype=torch.bfloat16, device="cuda")
         bt = torch.zeros((1, -(-w.N // bs)), dtype=torch.int32, device="cuda")
         with pytest.raises(sp.SpError) as e:
