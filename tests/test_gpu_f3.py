@@ -31,12 +31,15 @@ def _dev(bits):
     return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).cuda()
 
 
+@pytest.mark.parametrize("d", [64, 128, 256])
 @pytest.mark.parametrize("layout", ["nhd", "hnd"])
 @pytest.mark.parametrize("bs", [8, 16, 32, 64, 128, 256])
-def test_paged_uniform_bitexact_vs_contiguous(bs, layout):
-    """Paging only changes where the TMA reads a tile from: the importance is
-    bit-identical to sp_score on the contiguous cache, and within 1e-3 of the oracle."""
-    w = gen.CONFIGS["C0"].with_(L=3, H=8, Hkv=2, d=64, R=3, N=1000, B=2)
+def test_paged_uniform_bitexact_vs_contiguous(bs, layout, d):
+    """Paging only changes where the TMA reads a tile from (d >= 128 with blocks
+    < 128 tokens: one box per block, kb halves interleaved per 8-row group): the
+    importance is bit-identical to sp_score on the contiguous cache, and within
+    1e-3 of the oracle."""
+    w = gen.CONFIGS["C0"].with_(L=3, H=8, Hkv=2, d=d, R=3, N=1000, B=2)
     Qb, Kb, _ = gen.gen_batch(w)
     Q, K = _dev(Qb), _dev(Kb)
     cache, bt = _paged(K, bs, seed=bs, layout=layout)
@@ -48,13 +51,14 @@ def test_paged_uniform_bitexact_vs_contiguous(bs, layout):
         assert _util.rel_err(imp[b].double().cpu().numpy(), _oracle_req(Qb[b], Kb[b], w, w.N)) <= _util.REL_TOL
 
 
+@pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("bs", [16, 128])
 @pytest.mark.parametrize("lens", [(1000, 337, 77), (64, 1, 129), (5000, 4999, 128, 2500)])
-def test_ragged_paged_vs_oracle(bs, lens):
+def test_ragged_paged_vs_oracle(bs, lens, d):
     """Requests of different lengths in one launch: each request's softmax runs
     over its own prompt keys; the selection over its own chunks."""
     N = max(lens)
-    w = gen.CONFIGS["C0"].with_(L=2, H=8, Hkv=2, d=64, R=3, N=N, B=len(lens), keep=0.3, pool_k=5, chunk=8)
+    w = gen.CONFIGS["C0"].with_(L=2, H=8, Hkv=2, d=d, R=3, N=N, B=len(lens), keep=0.3, pool_k=5, chunk=8)
     Qb, Kb, tok = gen.gen_batch(w)
     Q, K = _dev(Qb), _dev(Kb)
     cache, bt = _paged(K, bs)
