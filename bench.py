@@ -237,8 +237,8 @@ def run_ours(args):
     paged = args.paged > 0
     seq_lens, n_tokens = None, w.B * w.N
     if paged:
-        if seq or head or f8:
-            raise SystemExit("--paged runs single-GPU or batch-sharded with bf16 K")
+        if seq or head:
+            raise SystemExit("--paged runs single-GPU or batch-sharded")
         from spgen.paged import to_paged
         K_cache, btab = to_paged(K, args.paged, seed=rank, layout=args.paged_layout)
         del K
@@ -257,7 +257,10 @@ def run_ours(args):
     out = torch.empty_like(ids)
 
     def score_only():
-        if paged:
+        if paged and f8:
+            sp.score_paged(Q8, K_cache, btab, seq_lens, N=w.N, R_valid=w.Rv, scale=w.scale, out=imp,
+                           q_scale=1.0 / fp8.Q_INV_SCALE, k_scale=1.0 / fp8.K_INV_SCALE)
+        elif paged:
             sp.score_paged(Q, K_cache, btab, seq_lens, N=w.N, R_valid=w.Rv, scale=w.scale, out=imp)
         elif f8:
             sp.score_e4m3(Q8, K8, 1.0 / fp8.Q_INV_SCALE, 1.0 / fp8.K_INV_SCALE, R_valid=w.Rv, scale=w.scale, out=imp)
@@ -403,7 +406,10 @@ def run_ours(args):
     launches_per_step = {"fused": 1, "simt": 4, "auto": 1}[args.algo] + select_launches
     Kgeom = (torch.empty(w.d, dtype=torch.bfloat16, device=dev).as_strided((w.B, w.L, w.Hkv, w.N, w.d),
                                                                           (0, 0, 0, 0, 1)) if paged else K)
-    plan = (sp.score_e4m3_plan(Q8, K8, w.Rv) if f8 else sp.score_plan(Q, Kgeom, w.Rv)) if args.algo != "simt" else None
+    Kgeom8 = (torch.empty(w.d, dtype=torch.uint8, device=dev).as_strided((w.B, w.L, w.Hkv, w.N, w.d),
+                                                                        (0, 0, 0, 0, 1)) if paged and f8 else None)
+    plan = ((sp.score_e4m3_plan(Q8, Kgeom8 if paged else K8, w.Rv) if f8 else sp.score_plan(Q, Kgeom, w.Rv))
+            if args.algo != "simt" else None)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if (seq or head) else "weak", "vs_baseline": None, "dtype": args.kv, "data": "synthetic",

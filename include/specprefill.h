@@ -294,6 +294,12 @@ size_t sp_score_paged_workspace_bytes(const sp_geom* g);
 sp_status sp_score_paged(const void* Q, const sp_paged_k* K, const sp_geom* g, const sp_layout* lay,
                          float* importance, void* ws, size_t ws_bytes, sp_stream stream);
 
+/* Rows f3 x f4: a paged FP8 cache (vLLM's fp8 KV cache) -- Q8 and the cache hold
+ * e4m3 codes with per-tensor scales as in sp_score_e4m3; strides in elements =
+ * bytes (multiples of 16), d % 32 == 0.  Workspace sp_score_e4m3_workspace_bytes(g). */
+sp_status sp_score_paged_e4m3(const void* Q8, const sp_paged_k* K, float q_scale, float k_scale, const sp_geom* g,
+                              const sp_layout* lay, float* importance, void* ws, size_t ws_bytes, sp_stream stream);
+
 /* ------------------------------------------------------------------ select
  * Pool, chunk means, top-K_c chunks, positions (O5-O9, Alg.1):
  *   pooled[i] = mean(importance[j] : |j-i| <= (pool_k-1)/2, 0 <= j < N)      (Z6)

@@ -91,6 +91,8 @@ SIGNATURES = {
     "sp_score_lookahead": (C.c_int, [_P, _P, C.POINTER(sp_lookahead_k), _G, _L, _P, _P, C.c_size_t, _P]),
     "sp_score_paged_workspace_bytes": (C.c_size_t, [_G]),
     "sp_score_paged": (C.c_int, [_P, C.POINTER(sp_paged_k), _G, _L, _P, _P, C.c_size_t, _P]),
+    "sp_score_paged_e4m3": (C.c_int, [_P, C.POINTER(sp_paged_k), C.c_float, C.c_float, _G, _L, _P, _P, C.c_size_t,
+                                      _P]),
     "sp_select_ragged": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int64, _S, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "sp_select_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int64, _S]),
     "sp_select": (C.c_int, [_P, C.c_int32, C.c_int64, _S, _P, _P, _P, _P, C.c_size_t, _P]),

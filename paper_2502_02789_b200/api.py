@@ -133,7 +133,7 @@ def score_lookahead(Q, K, K_la, la_shift: int = 0, R_valid=None, scale=None, out
 
 
 def score_paged(Q, K_cache, block_table, seq_lens=None, N=None, R_valid=None, scale=None, out=None,
-                stream=None) -> torch.Tensor:
+                stream=None, q_scale=None, k_scale=None) -> torch.Tensor:
     """Row f3: token importance [B][N] fp32 from a paged K cache.
 
     K_cache: bf16 [L][num_blocks][block_size][Hkv][d] (any strides, d contiguous),
@@ -141,7 +141,11 @@ def score_paged(Q, K_cache, block_table, seq_lens=None, N=None, R_valid=None, sc
     None, N: longest prompt (default max_blocks * block_size, capped by seq_lens
     if given on the host side by the caller).  Entries i >= seq_lens[b] of the
     output rows are left untouched."""
-    if Q.dtype != torch.bfloat16 or K_cache.dtype != torch.bfloat16:
+    e4m3 = q_scale is not None
+    if e4m3:
+        if Q.dtype not in _E4M3 or K_cache.dtype not in _E4M3:
+            raise TypeError("with q_scale/k_scale, Q and K_cache must hold e4m3 codes")
+    elif Q.dtype != torch.bfloat16 or K_cache.dtype != torch.bfloat16:
         raise TypeError("Q and K_cache must be bfloat16")
     if K_cache.dim() != 5 or Q.dim() != 5 or K_cache.stride(-1) != 1 or Q.stride(-1) != 1:
         raise ValueError("Q [B][L][R][H][d], K_cache [L][num_blocks][block_size][Hkv][d], d contiguous")
@@ -164,6 +168,15 @@ def score_paged(Q, K_cache, block_table, seq_lens=None, N=None, R_valid=None, sc
                          seq_lens=None if seq_lens is None else seq_lens.data_ptr())
     if out is None:
         out = torch.zeros((B, N), dtype=torch.float32, device=K_cache.device)
+    if e4m3:
+        nbytes = lib().sp_score_e4m3_workspace_bytes(C.byref(g))
+        if nbytes == 0:
+            check(_lib.SP_EUNSUPPORTED, "sp_score_paged_e4m3")
+        ws = workspace(("score_paged_e4m3", _geom_key(g)), nbytes, K_cache.device)
+        check(lib().sp_score_paged_e4m3(Q.data_ptr(), C.byref(pk), float(q_scale), float(k_scale), C.byref(g),
+                                        C.byref(lay), out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
+              "sp_score_paged_e4m3")
+        return out
     nbytes = lib().sp_score_paged_workspace_bytes(C.byref(g))
     if nbytes == 0:
         check(_lib.SP_EUNSUPPORTED, "sp_score_paged")

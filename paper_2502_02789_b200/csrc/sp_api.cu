@@ -338,11 +338,15 @@ size_t sp_score_paged_workspace_bytes(const sp_geom* g) {
   return fused_supported(G, Layout{}, nullptr, nullptr) ? fused_score_ws_bytes(G) : 0;
 }
 
-sp_status sp_score_paged(const void* Q, const sp_paged_k* K, const sp_geom* g, const sp_layout* lay,
-                         float* importance, void* ws, size_t ws_bytes, sp_stream stream) {
+// esz = 1: e4m3 codes with the dequantisation scales folded into the softmax scale (row f4)
+static sp_status score_paged_impl(const void* Q, const sp_paged_k* K, const sp_geom* g, const sp_layout* lay,
+                                  float* importance, void* ws, size_t ws_bytes, sp_stream stream, int esz,
+                                  float q_scale, float k_scale) {
   sp_status s = check_geom(g);
   if (s != SP_OK) return s;
-  if (K == nullptr || importance == nullptr) return SP_EINVAL;
+  Geom G = to_geom(*g);
+  if (esz == 1 && (s = e4m3_geom(g, q_scale, k_scale, &G)) != SP_OK) return s;
+  if (K == nullptr || importance == nullptr || lay == nullptr) return SP_EINVAL;
   if (K->cache == nullptr || K->block_table == nullptr || (reinterpret_cast<uintptr_t>(K->cache) & 15u) != 0)
     return SP_EINVAL;
   const int bs = K->block_size;
@@ -352,15 +356,14 @@ sp_status sp_score_paged(const void* Q, const sp_paged_k* K, const sp_geom* g, c
   const long long kn[4] = {g->L, K->num_blocks, bs, g->Hkv};
   for (int i = 0; i < 4; ++i) {
     if (ks[i] < 0) return SP_EINVAL;
-    if (kn[i] > 1 && (ks[i] * 2) % 16 != 0) return SP_EINVAL;
+    if (kn[i] > 1 && (ks[i] * esz) % 16 != 0) return SP_EINVAL;
   }
   // Q strides: reuse the contiguous-layout check with a dummy K view of the same geometry
   sp_layout ql = *lay;
   ql.k_b = ql.k_l = ql.k_g = 0;
   ql.k_i = g->d;
-  if ((s = check_layout(g, &ql, Q, K->cache)) != SP_OK) return s;
+  if ((s = check_layout(g, &ql, Q, K->cache, esz)) != SP_OK) return s;
   if ((s = check_device()) != SP_OK) return s;
-  const Geom G = to_geom(*g);
   const Layout Lay = to_layout(*lay);
   if (!fused_supported(G, Lay, Q, K->cache)) return SP_EUNSUPPORTED;
   if (ws == nullptr || ws_bytes < fused_score_ws_bytes(G) || (reinterpret_cast<uintptr_t>(ws) & 255u) != 0)
@@ -372,6 +375,16 @@ sp_status sp_score_paged(const void* Q, const sp_paged_k* K, const sp_geom* g, c
   pk.btab = K->block_table; pk.max_blocks = K->max_blocks; pk.seq_lens = K->seq_lens;
   return from_cuda(fused_score_paged(reinterpret_cast<const __nv_bfloat16*>(Q), pk, G, Lay, importance, ws, ws_bytes,
                                      reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sp_status sp_score_paged(const void* Q, const sp_paged_k* K, const sp_geom* g, const sp_layout* lay,
+                         float* importance, void* ws, size_t ws_bytes, sp_stream stream) {
+  return score_paged_impl(Q, K, g, lay, importance, ws, ws_bytes, stream, 2, 1.f, 1.f);
+}
+
+sp_status sp_score_paged_e4m3(const void* Q8, const sp_paged_k* K, float q_scale, float k_scale, const sp_geom* g,
+                              const sp_layout* lay, float* importance, void* ws, size_t ws_bytes, sp_stream stream) {
+  return score_paged_impl(Q8, K, g, lay, importance, ws, ws_bytes, stream, 1, q_scale, k_scale);
 }
 
 sp_status sp_score_plan(const sp_geom* g, int64_t out[9]) {

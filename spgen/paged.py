@@ -21,11 +21,12 @@ def to_paged(K: torch.Tensor, bs: int, seed: int = 0, spare: int = 3, layout: st
     nblk = B * mb + spare
     g = torch.Generator().manual_seed(seed)
     perm = torch.randperm(nblk, generator=g)[:B * mb].view(B, mb)
+    fill = 0x7F if K.dtype == torch.uint8 else float("nan")          # (e4m3 codes: 0x7F is NaN)
     if layout == "hnd":
-        store = torch.full((L, nblk, Hkv, bs, d), float("nan"), dtype=K.dtype, device=K.device)
+        store = torch.full((L, nblk, Hkv, bs, d), fill, dtype=K.dtype, device=K.device)
         cache = store.permute(0, 1, 3, 2, 4)
     else:
-        cache = torch.full((L, nblk, bs, Hkv, d), float("nan"), dtype=K.dtype, device=K.device)
+        cache = torch.full((L, nblk, bs, Hkv, d), fill, dtype=K.dtype, device=K.device)
     for b in range(B):
         Kp = torch.nn.functional.pad(K[b], (0, 0, 0, mb * bs - N))                 # [L][Hkv][mb*bs][d]
         Kp = Kp.view(L, Hkv, mb, bs, d).permute(0, 2, 3, 1, 4)                     # [L][mb][bs][Hkv][d]

@@ -149,3 +149,21 @@ def test_paged_ragged_c2_sampled():
         assert _util.rel_err(imp[b, :n].double().cpu().numpy(), exact) <= _util.REL_TOL, b
         o = ref.select(exact, w.keep, w.pool_k, w.chunk)
         _util.check_selection(ids[b].cpu().numpy(), pos[b].cpu().numpy(), int(nk[b]), o, w.chunk, n, 0)
+
+
+@pytest.mark.parametrize("d,bs", [(128, 16), (128, 128), (256, 16), (64, 32)])
+def test_paged_e4m3_bitexact_vs_contiguous(d, bs):
+    """Rows f3 x f4: an FP8 paged cache gives the e4m3 contiguous path's bits."""
+    from spgen import fp8
+    w = gen.CONFIGS["C0"].with_(L=3, H=8, Hkv=2, d=d, R=3, N=1000, B=2)
+    Qb, Kb, _ = gen.gen_batch(w)
+    Q8, K8 = fp8.to_e4m3_codes(_dev(Qb), fp8.Q_INV_SCALE), fp8.to_e4m3_codes(_dev(Kb), fp8.K_INV_SCALE)
+    qs, ks = 1 / fp8.Q_INV_SCALE, 1 / fp8.K_INV_SCALE
+    cache, bt = _paged(K8, bs, layout="hnd")
+    a = sp.score_paged(Q8, cache, bt, N=w.N, R_valid=w.Rv, scale=w.scale, q_scale=qs, k_scale=ks)
+    b = sp.score_e4m3(Q8, K8, qs, ks, R_valid=w.Rv, scale=w.scale)
+    sp.check_device_error()
+    assert torch.equal(a, b)
+    exact = ref.token_importance(qs * ref.e4m3_to_f64(Q8[0].cpu().numpy()), ks * ref.e4m3_to_f64(K8[0].cpu().numpy()),
+                                 w.scale, w.Rv)
+    assert _util.rel_err(a[0].double().cpu().numpy(), exact) <= _util.REL_TOL
