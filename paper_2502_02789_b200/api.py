@@ -136,11 +136,11 @@ def score_paged(Q, K_cache, block_table, seq_lens=None, N=None, R_valid=None, sc
                 stream=None, q_scale=None, k_scale=None) -> torch.Tensor:
     """Row f3: token importance [B][N] fp32 from a paged K cache.
 
-    K_cache: bf16 [L][num_blocks][block_size][Hkv][d] (any strides, d contiguous),
-    block_table: int32 [B][max_blocks] (device), seq_lens: int32 [B] (device) or
-    None, N: longest prompt (default max_blocks * block_size, capped by seq_lens
-    if given on the host side by the caller).  Entries i >= seq_lens[b] of the
-    output rows are left untouched."""
+    K_cache: bf16 (or, with q_scale/k_scale, e4m3 codes) [L][num_blocks][block_size][Hkv][d],
+    any strides with d contiguous (vLLM NHD storage, or an HND store viewed this way);
+    block_table: int32 [B][max_blocks] (device); seq_lens: int32 [B] (device) or None;
+    N: the longest prompt, the row length of the output (default max_blocks * block_size).
+    Entries i >= seq_lens[b] of the output rows are left untouched."""
     e4m3 = q_scale is not None
     if e4m3:
         if Q.dtype not in _E4M3 or K_cache.dtype not in _E4M3:
