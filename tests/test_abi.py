@@ -152,3 +152,51 @@ def test_fused_plan_invariants(name, variant):
     assert 2 <= pl["stages"] and pl["smem_bytes"] <= 232448
     if name == "C3" and not variant:
         assert (pl["token_groups"], pl["unit_groups"]) == (37, 4)   # the plan the bench line is quoted on
+
+
+# ---------------------------------------------------------------- rows f3 / f4 host-side validation
+def test_e4m3_validation():
+    g = _geom(d=32)
+    lay = _layout(g)
+    e = sp.lib().sp_score_e4m3
+    assert e(FAKE, FAKE, 0.0, 1.0, C.byref(g), C.byref(lay), FAKE, FAKE, 1 << 20, None) == _lib.SP_EINVAL
+    assert e(FAKE, FAKE, 1.0, float("inf"), C.byref(g), C.byref(lay), FAKE, FAKE, 1 << 20, None) == _lib.SP_EINVAL
+    g16 = _geom(d=16)
+    assert e(FAKE, FAKE, 1.0, 1.0, C.byref(g16), C.byref(_layout(g16)), FAKE, FAKE, 1 << 20, None) == \
+        _lib.SP_EUNSUPPORTED                              # d % 32 != 0: no 32-byte swizzle rows
+    lay.k_i = 40                                          # 40 B rows: not a multiple of 16 B
+    assert e(FAKE, FAKE, 1.0, 1.0, C.byref(g), C.byref(lay), FAKE, FAKE, 1 << 20, None) == _lib.SP_EINVAL
+
+
+def _paged(g, **kw):
+    pk = dict(cache=FAKE, s_l=64 * 16 * g.Hkv * g.d, s_blk=16 * g.Hkv * g.d, s_tok=g.Hkv * g.d, s_g=g.d,
+              num_blocks=64, block_size=16, block_table=FAKE, max_blocks=-(-g.N // 16), seq_lens=None)
+    pk.update(kw)
+    return _lib.sp_paged_k(**pk)
+
+
+@pytest.mark.parametrize("kw", [dict(block_size=4), dict(block_size=24), dict(block_size=384),
+                                dict(max_blocks=1), dict(num_blocks=0), dict(cache=0), dict(block_table=0),
+                                dict(s_tok=-8), dict(cache=FAKE + 8)])
+def test_paged_validation(kw):
+    g = _geom(d=64)
+    pk = _paged(g, **kw)
+    if "block_size" in kw:
+        pk.max_blocks = 1 << 20
+    rc = sp.lib().sp_score_paged(FAKE, C.byref(pk), C.byref(g), C.byref(_layout(g)), FAKE, FAKE, 1 << 20, None)
+    assert rc == _lib.SP_EINVAL
+
+
+def test_lookahead_and_ragged_validation():
+    g = _geom()
+    lay = _layout(g)
+    la = _lib.sp_lookahead_k(K_la=FAKE, s_b=0, s_l=0, s_g=0, s_j=g.d, la_shift=2)
+    f = sp.lib().sp_score_lookahead
+    assert f(FAKE, FAKE, C.byref(la), C.byref(g), C.byref(lay), FAKE, FAKE, 1 << 20, None) == _lib.SP_EINVAL
+    la.la_shift, la.s_j = 0, -1
+    assert f(FAKE, FAKE, C.byref(la), C.byref(g), C.byref(lay), FAKE, FAKE, 1 << 20, None) == _lib.SP_EINVAL
+    assert f(FAKE, FAKE, None, C.byref(g), C.byref(lay), FAKE, FAKE, 1 << 20, None) == _lib.SP_EINVAL
+    p = _lib.sp_select_params(keep_rate=0.5, pool_k=3, chunk=4, pos0=0)
+    r = sp.lib().sp_select_ragged
+    assert r(FAKE, None, None, 2, 100, C.byref(p), FAKE, FAKE, FAKE, None, FAKE, 1 << 20, None) == _lib.SP_EINVAL
+    assert r(FAKE, FAKE, FAKE, 2, 100, C.byref(p), FAKE, FAKE, FAKE, None, FAKE, 1 << 20, None) == _lib.SP_EINVAL
