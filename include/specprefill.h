@@ -146,6 +146,20 @@ sp_status sp_score_ex(const void* Q, const void* K, const sp_geom* g, const sp_l
  * dynamic SMEM bytes.  Returns SP_EUNSUPPORTED if the fused kernel cannot run g. */
 sp_status sp_score_plan(const sp_geom* g, int64_t out[9]);
 
+/* Measured plan choice.  sp_score_tune times the fused kernel's best model
+ * candidates (token groups x unit groups; at most 6, within 1.3x of the model's
+ * best) on this device with private workspaces (allocated and freed inside the
+ * call: not for the hot path; synchronises `stream`) and registers the fastest
+ * for g: every later sp_score / plan / workspace query of g uses it.  out[0..1]
+ * = (token groups, unit groups); *ms_per_launch = its mean launch time.
+ * sp_score_set_plan registers a plan explicitly (n_tg = 0 clears; an invalid
+ * plan is ignored at plan time).  After either call, re-query
+ * sp_score_workspace_bytes(g) and use a freshly zero-filled workspace: the
+ * partial-statistics layout depends on the plan. */
+sp_status sp_score_tune(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, int64_t out[2],
+                        float* ms_per_launch, sp_stream stream);
+sp_status sp_score_set_plan(const sp_geom* g, int32_t n_tg, int32_t n_ug);
+
 /* Debug tracing of the fused kernel (not for production runs): while enabled,
  * every sp_score launch writes globaltimer stamps (ns) into device_buffer laid
  * out as [grid CTA][unit index within the CTA][8] uint64:

@@ -46,8 +46,12 @@ def workspace(tag, nbytes: int, device) -> torch.Tensor:
 
 
 def _geom_key(g) -> tuple:
+    """Workspace cache key: the geometry and the fused plan it runs with (the
+    partial-statistics layout depends on the plan: env override, sp_score_tune)."""
     import os
-    return (g.B, g.L, g.H, g.Hkv, g.d, g.R, g.R_valid, g.N, os.environ.get("SP_FUSED_PLAN"))
+    out = (C.c_int64 * 9)()
+    plan = tuple(out)[2:4] if lib().sp_score_plan(C.byref(g), out) == _lib.SP_OK else None
+    return (g.B, g.L, g.H, g.Hkv, g.d, g.R, g.R_valid, g.N, os.environ.get("SP_FUSED_PLAN"), plan)
 
 
 _E4M3 = (torch.float8_e4m3fn, torch.uint8)
@@ -252,6 +256,17 @@ def gather(tokens: torch.Tensor, ids: torch.Tensor, n_kept: torch.Tensor, out=No
     check(lib().sp_gather(tokens.data_ptr(), ids.data_ptr(), n_kept.data_ptr(), B, N, out.data_ptr(),
                           _stream_ptr(stream)), "sp_gather")
     return out
+
+
+def score_tune(Q, K, R_valid=None, scale=None, stream=None) -> dict:
+    """Time the fused kernel's best plan candidates on these inputs and register
+    the fastest for this geometry (sp_score_tune; synchronises, allocates)."""
+    g, lay = make_geom(Q, K, R_valid, scale)
+    out = (C.c_int64 * 2)()
+    ms = C.c_float()
+    check(lib().sp_score_tune(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), out, C.byref(ms),
+                              _stream_ptr(stream)), "sp_score_tune")
+    return {"token_groups": out[0], "unit_groups": out[1], "ms_per_launch": ms.value}
 
 
 def score_plan(Q, K, R_valid=None) -> dict:

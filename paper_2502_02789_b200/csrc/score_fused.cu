@@ -40,7 +40,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
+#include <vector>
 
 namespace sp {
 namespace {
@@ -1164,8 +1167,24 @@ uint32_t carve(Plan& pl, int Rv, int stages) {
   return o + 1024;                                   // slack for the manual 1024-byte alignment
 }
 
-// sm_budget > 0: plan for at most that many CTAs (co-scheduled peer launches on one GPU, tests)
-Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0) {
+// Measured plan choices (sp_score_tune / sp_score_set_plan), per geometry.
+using PlanKey = std::tuple<int, int, int, int, int, int, int, long long, int, int>;
+std::map<PlanKey, std::pair<int, int>>& plan_registry() {
+  static std::map<PlanKey, std::pair<int, int>> m;
+  return m;
+}
+std::mutex& plan_registry_mu() {
+  static std::mutex mu;
+  return mu;
+}
+PlanKey plan_key(const Geom& g, int sm_budget) {
+  return PlanKey(g.B, g.L, g.H, g.Hkv, g.d, g.R, g.Rv, g.N, g.esz, sm_budget);
+}
+
+// sm_budget > 0: plan for at most that many CTAs (co-scheduled peer launches on one GPU, tests).
+// cands (optional): every valid (model cost, n_tg, n_ug), for the tuner.
+Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
+               std::vector<std::tuple<double, int, int>>* cands = nullptr) {
   Plan pl;
   pl.NC = g.G * g.Rv;
   pl.NCP = ((pl.NC + 31) / 32) * 32;                  // TMEM column groups of 32 (one tcgen05.ld.x32)
@@ -1192,6 +1211,11 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0) {
   int force_tg = 0, force_ug = 0;
   if (const char* env = allow_override ? std::getenv("SP_FUSED_PLAN") : nullptr) {
     if (std::sscanf(env, "%d,%d", &force_tg, &force_ug) != 2) force_tg = force_ug = 0;
+  }
+  if (allow_override && force_tg == 0) {                  // a measured choice for this geometry
+    std::lock_guard<std::mutex> lk(plan_registry_mu());
+    auto it = plan_registry().find(plan_key(g, sm_budget));
+    if (it != plan_registry().end()) { force_tg = it->second.first; force_ug = it->second.second; }
   }
   for (int J = 1; J <= pl.P; ++J) {
     if ((long long)g.B * J > pl.P && pl.P % J) continue;
@@ -1223,6 +1247,7 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0) {
       if (n_ug > 1)                                                          // cross-group max + its sync
         cost += 2.0 * g.Rv * tpc * kTileM * 4.0 / kSmHbmBytesPerUs + 5.0 + 0.25 * n_ug;
       cost *= (double)waves;
+      if (cands != nullptr) cands->emplace_back(cost, n_tg, n_ug);
       if (cost < best * 0.999) {
         best = cost;
         pl.J = J; pl.n_tg = n_tg; pl.n_ug = n_ug; pl.tpc = tpc; pl.upc = upc;
@@ -1593,6 +1618,68 @@ cudaError_t fused_score_paged(const __nv_bfloat16* Q, const PagedK& K, const Geo
   l2.k_b = l2.k_l = l2.k_g = l2.k_i = 0;                    // (the contiguous map is replaced by the paged one)
   return fused_launch(Q, reinterpret_cast<const __nv_bfloat16*>(K.cache), g, l2, kModeFull, nullptr, importance, ws,
                       ws_bytes, st, nullptr, PeerArgs(), &K);
+}
+
+// Measured plan choice (sp_score_tune): the model's best candidates (cost within
+// 1.3x, at most 6) each timed over 5 launches on private zeroed workspaces; the
+// fastest is registered for g and used by every later plan query of g.
+cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                       cudaStream_t st, int* tg_out, int* ug_out, float* ms_out) {
+  std::vector<std::tuple<double, int, int>> cands;
+  {
+    std::lock_guard<std::mutex> lk(plan_registry_mu());
+    plan_registry().erase(plan_key(g, 0));
+  }
+  Plan base = make_plan(g, false, 0, &cands);
+  if (!base.ok) return cudaErrorInvalidValue;
+  std::sort(cands.begin(), cands.end());
+  const double best_cost = std::get<0>(cands.front());
+  float best_ms = 1e30f;
+  int best_tg = base.n_tg, best_ug = base.n_ug;
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return cudaGetLastError();
+  float* imp = nullptr;
+  cudaError_t err = cudaMalloc(&imp, (size_t)g.B * g.N * sizeof(float));
+  for (size_t i = 0; err == cudaSuccess && i < cands.size() && i < 6; ++i) {
+    if (std::get<0>(cands[i]) > 1.3 * best_cost) break;
+    const int tg = std::get<1>(cands[i]), ug = std::get<2>(cands[i]);
+    {
+      std::lock_guard<std::mutex> lk(plan_registry_mu());
+      plan_registry()[plan_key(g, 0)] = {tg, ug};
+    }
+    Plan pl = make_plan(g);
+    if (!pl.ok || pl.n_tg != tg || pl.n_ug != ug) continue;
+    void* ws = nullptr;
+    if ((err = cudaMalloc(&ws, pl.ws_total())) != cudaSuccess) break;
+    cudaMemsetAsync(ws, 0, pl.ws_total(), st);
+    for (int w = 0; w < 2 && err == cudaSuccess; ++w) err = fused_score(Q, K, g, lay, imp, ws, pl.ws_total(), st);
+    cudaEventRecord(e0, st);
+    for (int r = 0; r < 5 && err == cudaSuccess; ++r) err = fused_score(Q, K, g, lay, imp, ws, pl.ws_total(), st);
+    cudaEventRecord(e1, st);
+    if (err == cudaSuccess) err = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    if (err == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
+    cudaFree(ws);
+    if (err == cudaSuccess && ms < best_ms) { best_ms = ms; best_tg = tg; best_ug = ug; }
+  }
+  cudaFree(imp);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  {
+    std::lock_guard<std::mutex> lk(plan_registry_mu());
+    plan_registry()[plan_key(g, 0)] = {best_tg, best_ug};
+  }
+  *tg_out = best_tg;
+  *ug_out = best_ug;
+  *ms_out = best_ms / 5.f;
+  return err;
+}
+
+bool fused_set_plan(const Geom& g, int n_tg, int n_ug) {
+  std::lock_guard<std::mutex> lk(plan_registry_mu());
+  if (n_tg <= 0) { plan_registry().erase(plan_key(g, 0)); return true; }
+  plan_registry()[plan_key(g, 0)] = {n_tg, n_ug};
+  return true;
 }
 
 cudaError_t fused_score_stats(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,

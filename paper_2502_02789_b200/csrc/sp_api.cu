@@ -387,6 +387,32 @@ sp_status sp_score_paged_e4m3(const void* Q8, const sp_paged_k* K, float q_scale
   return score_paged_impl(Q8, K, g, lay, importance, ws, ws_bytes, stream, 1, q_scale, k_scale);
 }
 
+sp_status sp_score_tune(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, int64_t out[2],
+                        float* ms_per_launch, sp_stream stream) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if ((s = check_layout(g, lay, Q, K)) != SP_OK) return s;
+  if ((s = check_device()) != SP_OK) return s;
+  const Geom G = to_geom(*g);
+  const Layout Lay = to_layout(*lay);
+  if (!fused_supported(G, Lay, Q, K)) return SP_EUNSUPPORTED;
+  int tg = 0, ug = 0;
+  float ms = 0.f;
+  s = from_cuda(fused_tune(reinterpret_cast<const __nv_bfloat16*>(Q), reinterpret_cast<const __nv_bfloat16*>(K), G,
+                           Lay, reinterpret_cast<cudaStream_t>(stream), &tg, &ug, &ms));
+  if (out != nullptr) { out[0] = tg; out[1] = ug; }
+  if (ms_per_launch != nullptr) *ms_per_launch = ms;
+  return s;
+}
+
+sp_status sp_score_set_plan(const sp_geom* g, int32_t n_tg, int32_t n_ug) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if (n_tg > 0 && n_ug < 1) return SP_EINVAL;
+  fused_set_plan(to_geom(*g), n_tg, n_ug);
+  return SP_OK;
+}
+
 sp_status sp_score_plan(const sp_geom* g, int64_t out[9]) {
   sp_status s = check_geom(g);
   if (s != SP_OK) return s;

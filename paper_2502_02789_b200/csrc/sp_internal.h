@@ -96,6 +96,9 @@ cudaError_t fused_score_paged(const __nv_bfloat16* Q, const PagedK& K, const Geo
 size_t fused_la_ws_bytes(const Geom& g);
 cudaError_t fused_score_la(const __nv_bfloat16* Q, const __nv_bfloat16* K, const LookaheadK& la, const Geom& g,
                            const Layout& lay, float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
+cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                       cudaStream_t st, int* tg_out, int* ug_out, float* ms_out);
+bool fused_set_plan(const Geom& g, int n_tg, int n_ug);
 cudaError_t acc_importance(const float* acc2, int B, int Rv, long long N, float* importance, cudaStream_t st);
 size_t fused_peer_buffer_bytes(const Geom& g, int world, int sm_budget);
 size_t fused_peer_ws_bytes(const Geom& g, int sm_budget);

@@ -380,3 +380,25 @@ def test_peer_exchange_virtual_ranks(name, P, N):
     assert _util.rel_err(res[0][0].double().cpu().numpy(), exact) <= _util.REL_TOL
     full = sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")
     assert _util.rel_err(res[0][0].double().cpu().numpy(), full[0].double().cpu().numpy()) <= 1e-5
+
+
+# ---------------------------------------------------------------- measured plan choice
+def test_tune_registers_a_valid_plan():
+    """sp_score_tune times the model's best candidates and registers the fastest;
+    sp_score then runs it (new workspace key) and still matches the oracle."""
+    w = gen.CONFIGS["C1"]
+    Q, K, T = spgen_cuda.make_inputs(w)
+    before = sp.score_plan(Q, K, w.Rv)
+    t = sp.score_tune(Q, K, w.Rv, w.scale)
+    after = sp.score_plan(Q, K, w.Rv)
+    assert (after["token_groups"], after["unit_groups"]) == (t["token_groups"], t["unit_groups"])
+    assert t["ms_per_launch"] > 0
+    imp = _score(Q, K, w, "fused")
+    exact = _util.oracle_importance(w, 0)
+    assert _util.rel_err(imp[0].double().cpu().numpy(), exact) <= _util.REL_TOL
+    g, _ = sp.make_geom(Q, K, w.Rv)
+    import ctypes as C
+    g = C.byref(g)
+    assert sp.lib().sp_score_set_plan(g, 0, 0) == 0
+    cleared = sp.score_plan(Q, K, w.Rv)
+    assert (cleared["token_groups"], cleared["unit_groups"]) == (before["token_groups"], before["unit_groups"])
