@@ -61,7 +61,7 @@ def parse():
                          "the real tokens")
     ap.add_argument("--no-tune", action="store_true",
                     help="skip sp_score_tune (the fused plan measured among the model's best candidates during "
-                         "warm-up, untimed); single-GPU / batch-sharded contiguous bf16 only")
+                         "warm-up, untimed); single-GPU / batch-sharded contiguous inputs only")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -316,8 +316,11 @@ def run_ours(args):
             select_only()
 
     tuned = None
-    if not (args.no_tune or args.plan or seq or head or f8 or paged or args.algo == "simt"):
-        tuned = sp.score_tune(Q, K, w.Rv, w.scale)         # setup, not timed; later calls use the winner
+    if not (args.no_tune or args.plan or seq or head or paged or args.algo == "simt"):
+        if f8:
+            tuned = sp.score_e4m3_tune(Q8, K8, 1.0 / fp8.Q_INV_SCALE, 1.0 / fp8.K_INV_SCALE, w.Rv, w.scale)
+        else:
+            tuned = sp.score_tune(Q, K, w.Rv, w.scale)     # setup, not timed; later calls use the winner
     for _ in range(args.warmup):
         step()
     sp.check_device_error()

@@ -248,6 +248,9 @@ size_t sp_score_e4m3_workspace_bytes(const sp_geom* g);
 sp_status sp_score_e4m3_plan(const sp_geom* g, int64_t out[9]);
 sp_status sp_score_e4m3(const void* Q8, const void* K8, float q_scale, float k_scale, const sp_geom* g,
                         const sp_layout* lay, float* importance, void* ws, size_t ws_bytes, sp_stream stream);
+/* sp_score_tune for the e4m3 path (its plans are registered separately from bf16's). */
+sp_status sp_score_e4m3_tune(const void* Q8, const void* K8, float q_scale, float k_scale, const sp_geom* g,
+                             const sp_layout* lay, int64_t out[2], float* ms_per_launch, sp_stream stream);
 
 /* ------------------------------------------------------------------ score, look-ahead-key denominator
  * SURVEY 8(f) row f4, reading Z2': each look-ahead

@@ -73,6 +73,8 @@ SIGNATURES = {
     "sp_score_ex": (C.c_int, [_P, _P, _G, _L, _P, _P, C.c_size_t, C.c_int, _P]),
     "sp_score_plan": (C.c_int, [_G, C.POINTER(C.c_int64)]),
     "sp_score_tune": (C.c_int, [_P, _P, _G, _L, C.POINTER(C.c_int64), C.POINTER(C.c_float), _P]),
+    "sp_score_e4m3_tune": (C.c_int, [_P, _P, C.c_float, C.c_float, _G, _L, C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_float), _P]),
     "sp_score_set_plan": (C.c_int, [_G, C.c_int32, C.c_int32]),
     "sp_trace_enable": (C.c_int, [_P, C.c_int64]),
     "sp_score_split_workspace_bytes": (C.c_size_t, [_G]),

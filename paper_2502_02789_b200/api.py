@@ -102,7 +102,9 @@ def score_e4m3(Q8, K8, q_scale: float = 1.0, k_scale: float = 1.0, R_valid=None,
     nbytes = lib().sp_score_e4m3_workspace_bytes(C.byref(g))
     if nbytes == 0:
         check(_lib.SP_EUNSUPPORTED, "sp_score_e4m3")
-    ws = workspace(("score_e4m3", _geom_key(g)), nbytes, K8.device)
+    pl = (C.c_int64 * 9)()
+    lib().sp_score_e4m3_plan(C.byref(g), pl)
+    ws = workspace(("score_e4m3", _geom_key(g), tuple(pl)[2:4]), nbytes, K8.device)
     check(lib().sp_score_e4m3(Q8.data_ptr(), K8.data_ptr(), float(q_scale), float(k_scale), C.byref(g), C.byref(lay),
                               out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_score_e4m3")
     return out
@@ -266,6 +268,16 @@ def score_tune(Q, K, R_valid=None, scale=None, stream=None) -> dict:
     ms = C.c_float()
     check(lib().sp_score_tune(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), out, C.byref(ms),
                               _stream_ptr(stream)), "sp_score_tune")
+    return {"token_groups": out[0], "unit_groups": out[1], "ms_per_launch": ms.value}
+
+
+def score_e4m3_tune(Q8, K8, q_scale: float = 1.0, k_scale: float = 1.0, R_valid=None, scale=None,
+                    stream=None) -> dict:
+    g, lay = make_geom(Q8, K8, R_valid, scale, e4m3=True)
+    out = (C.c_int64 * 2)()
+    ms = C.c_float()
+    check(lib().sp_score_e4m3_tune(Q8.data_ptr(), K8.data_ptr(), float(q_scale), float(k_scale), C.byref(g),
+                                   C.byref(lay), out, C.byref(ms), _stream_ptr(stream)), "sp_score_e4m3_tune")
     return {"token_groups": out[0], "unit_groups": out[1], "ms_per_launch": ms.value}
 
 

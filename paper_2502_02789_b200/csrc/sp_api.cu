@@ -405,6 +405,24 @@ sp_status sp_score_tune(const void* Q, const void* K, const sp_geom* g, const sp
   return s;
 }
 
+sp_status sp_score_e4m3_tune(const void* Q8, const void* K8, float q_scale, float k_scale, const sp_geom* g,
+                             const sp_layout* lay, int64_t out[2], float* ms_per_launch, sp_stream stream) {
+  Geom G;
+  sp_status s = e4m3_geom(g, q_scale, k_scale, &G);
+  if (s != SP_OK) return s;
+  if ((s = check_layout(g, lay, Q8, K8, 1)) != SP_OK) return s;
+  if ((s = check_device()) != SP_OK) return s;
+  const Layout Lay = to_layout(*lay);
+  if (!fused_supported(G, Lay, Q8, K8)) return SP_EUNSUPPORTED;
+  int tg = 0, ug = 0;
+  float ms = 0.f;
+  s = from_cuda(fused_tune(reinterpret_cast<const __nv_bfloat16*>(Q8), reinterpret_cast<const __nv_bfloat16*>(K8), G,
+                           Lay, reinterpret_cast<cudaStream_t>(stream), &tg, &ug, &ms));
+  if (out != nullptr) { out[0] = tg; out[1] = ug; }
+  if (ms_per_launch != nullptr) *ms_per_launch = ms;
+  return s;
+}
+
 sp_status sp_score_set_plan(const sp_geom* g, int32_t n_tg, int32_t n_ug) {
   sp_status s = check_geom(g);
   if (s != SP_OK) return s;
