@@ -195,10 +195,29 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
   }
   if (mode == kModeA) return;
 
-  // ---- B. radix select: threshold bit pattern T of the K_c-th largest score
+  // ---- B. radix select: threshold bit pattern T of the K_c-th largest score.
+  //      Up to kRankMax chunks the rank is counted directly instead:
+  //      rank(c) = #{c' : cs[c'] > cs[c], or cs[c'] == cs[c] and c' < c} (the
+  //      (score desc, index asc) order), kept iff rank < K_c -- one pass, no
+  //      barrier rounds (measured: 2 us faster at 128 chunks, 29 us slower at 1024).
+  constexpr int kRankMax = 256;
+  const bool by_rank = n_c <= kRankMax;
   unsigned prefix = 0, pmask = 0;
   unsigned remaining = (unsigned)K_c;
-  for (int shift = 24; shift >= 0; shift -= 8) {
+  int rank_keep = 0;
+  if (by_rank) {
+    if (tid < n_c) {
+      const float mine = cs[tid];
+      int rank = 0;
+#pragma unroll 8
+      for (int c2 = 0; c2 < (int)n_c; ++c2) {
+        const float o = cs[c2];                      // same address in every lane: broadcast
+        rank += (o > mine || (o == mine && c2 < tid)) ? 1 : 0;
+      }
+      rank_keep = rank < K_c ? 1 : 0;
+    }
+  }
+  for (int shift = 24; shift >= 0 && !by_rank; shift -= 8) {
     if (tid < 256) hist[tid] = 0;
     __syncthreads();
     // warp-aggregated: lanes with the same digit add once (the top digits of
@@ -259,7 +278,7 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
     int tot;
     const int eq_rank = block_excl_scan(eq, scan, &tot) + carry_eq;
     carry_eq += tot;
-    const int keep = gt | (eq & (eq_rank < need_eq ? 1 : 0));
+    const int keep = by_rank ? rank_keep : (gt | (eq & (eq_rank < need_eq ? 1 : 0)));
     const int slot = block_excl_scan(keep, scan, &tot);          // index among kept chunks of this tile
     const int nk = tot;
     int sz = 0;
