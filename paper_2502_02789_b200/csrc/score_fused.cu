@@ -1623,6 +1623,14 @@ cudaError_t fused_score_paged(const __nv_bfloat16* Q, const PagedK& K, const Geo
 // Measured plan choice (sp_score_tune): the model's best candidates (cost within
 // 1.3x, at most 6) each timed over 5 launches on private zeroed workspaces; the
 // fastest is registered for g and used by every later plan query of g.
+#ifndef SP_TUNE_MAX
+#define SP_TUNE_MAX 6
+#endif
+#ifndef SP_TUNE_SPAN
+#define SP_TUNE_SPAN 1.3
+#endif
+constexpr int kTuneMax = SP_TUNE_MAX;        // candidates timed
+constexpr double kTuneSpan = SP_TUNE_SPAN;   // ... within this factor of the model's best cost
 cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                        cudaStream_t st, int* tg_out, int* ug_out, float* ms_out) {
   std::vector<std::tuple<double, int, int>> cands;
@@ -1640,8 +1648,8 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return cudaGetLastError();
   float* imp = nullptr;
   cudaError_t err = cudaMalloc(&imp, (size_t)g.B * g.N * sizeof(float));
-  for (size_t i = 0; err == cudaSuccess && i < cands.size() && i < 6; ++i) {
-    if (std::get<0>(cands[i]) > 1.3 * best_cost) break;
+  for (size_t i = 0; err == cudaSuccess && i < cands.size() && i < (size_t)kTuneMax; ++i) {
+    if (std::get<0>(cands[i]) > kTuneSpan * best_cost) break;
     const int tg = std::get<1>(cands[i]), ug = std::get<2>(cands[i]);
     {
       std::lock_guard<std::mutex> lk(plan_registry_mu());
