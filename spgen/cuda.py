@@ -5,6 +5,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+import numpy as np
 import torch
 
 from . import gen
@@ -20,8 +21,8 @@ def _lib():
             raise ImportError(f"{_PATH} missing; run __graft_entry__.build()")
         h = C.CDLL(_PATH)
         L, I, V, U = C.c_longlong, C.c_int, C.c_void_p, C.c_ulonglong
-        h.spgen_fill_K.argtypes = [V, L, L, L, L, I, I, I, I, L, L, L, U, V, V]
-        h.spgen_fill_Q.argtypes = [V, L, L, L, L, I, I, I, I, I, I, U, V]
+        h.spgen_fill_K.argtypes = [V, L, L, L, L, I, I, I, I, L, L, L, U, V, I, V, I, I, V]
+        h.spgen_fill_Q.argtypes = [V, L, L, L, L, I, I, I, I, I, I, U, I, V]
         h.spgen_fill_tokens.argtypes = [V, I, L, U, V]
         for f in (h.spgen_fill_K, h.spgen_fill_Q, h.spgen_fill_tokens):
             f.restype = C.c_int
@@ -46,17 +47,21 @@ def fill_K(K: torch.Tensor, w: gen.Workload, i0: int = 0):
     with global tokens [i0, i0 + n_local) of workload w."""
     B, L, Hkv, n, d = K.shape
     sp = spans_tensor(w, K.device)
+    tiers = None
+    if w.planted:
+        tiers = torch.tensor(np.stack([gen.planted_tiers(w, b) for b in range(B)]).astype(np.int8), device=K.device)
     rc = _lib().spgen_fill_K(K.data_ptr(), K.stride(0), K.stride(1), K.stride(2), K.stride(3), B, L, Hkv, d,
-                             w.N, i0, n, w.seed, sp.data_ptr(), _stream())
+                             w.N, i0, n, w.seed, sp.data_ptr(), int(w.values == "randn"),
+                             None if tiers is None else tiers.data_ptr(), w.chunk, w.pool_k, _stream())
     if rc:
         raise RuntimeError(f"spgen_fill_K failed ({rc})")
-    torch.cuda.current_stream().synchronize()        # keep `sp` alive until the kernel ran
+    torch.cuda.current_stream().synchronize()        # keep `sp` / `tiers` alive until the kernel ran
 
 
 def fill_Q(Q: torch.Tensor, w: gen.Workload):
     B, L, R, H, d = Q.shape
     rc = _lib().spgen_fill_Q(Q.data_ptr(), Q.stride(0), Q.stride(1), Q.stride(2), Q.stride(3), B, L, R, H, w.Hkv, d,
-                             w.seed, _stream())
+                             w.seed, int(w.values == "randn"), _stream())
     if rc:
         raise RuntimeError(f"spgen_fill_Q failed ({rc})")
 

@@ -12,6 +12,17 @@ from spgen import gen
 REL_TOL = 1e-3          # importance / chunk-score tolerance (BASELINE.json north_star)
 _POOL = cf.ThreadPoolExecutor(max_workers=max(1, min(32, os.cpu_count() or 1)))
 
+# Parity report ("report the fraction of (config, seed, keep) cases
+# in each regime"): every full-size case appends a record; tests/conftest.py
+# prints the table at the end of the session and writes gpurun_out/parity_regimes.json.
+RECORDS: list[dict] = []
+
+
+def record(w: gen.Workload, keep: float, b: int, regime: str, margin: float, rel_err: float, where: str):
+    RECORDS.append(dict(where=where, config=w.name, N=w.N, B=w.B, seed=w.seed, values=w.values,
+                        planted=w.planted, request=b, keep=keep, regime=regime,
+                        margin=None if margin == float("inf") else float(margin), max_rel_err=float(rel_err)))
+
 
 def k_layer_f64(w: gen.Workload, b: int, l: int, i0: int = 0, i1: int | None = None) -> np.ndarray:
     """K[b][l] as float64 [Hkv][n][d], kv heads generated in parallel."""

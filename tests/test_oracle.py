@@ -47,6 +47,31 @@ def test_paper_position_example():
     assert decoding == g["decoding_pos_ids_prefix"]
 
 
+def test_gather_paper_example():
+    """O10 pinned by the paper's worked example: with the prompt's
+    tokens standing for their original positions [0..9], gathering the kept
+    tokens [0, 1, 3, 6, 7] must give the "Speculated Pos Ids" row."""
+    g = _golden("paper_position_ids.json")
+    tokens = np.array(g["original_pos_ids"], dtype=np.int32)
+    assert list(ref.gather(tokens, np.array(g["kept"]))) == g["speculated_pos_ids"]
+
+
+def test_gather_closed_forms():
+    """O10 closed forms: tokens[i] = a + b*i gathers to a + b*ids; gathering a
+    gather composes the index maps; on the whole path, tokens = arange(N)
+    returns the kept ids themselves."""
+    rng = np.random.default_rng(7)
+    ids = np.sort(rng.choice(1000, size=137, replace=False))
+    assert (ref.gather(5 + 3 * np.arange(1000), ids) == 5 + 3 * ids).all()
+    tok = rng.integers(0, 128256, size=1000)
+    sub = np.sort(rng.choice(137, size=40, replace=False))
+    assert (ref.gather(ref.gather(tok, ids), sub) == tok[ids[sub]]).all()
+    w = gen.CONFIGS["C0"]
+    Qb, Kb, _ = gen.gen_request(w, 0)
+    r = ref.specprefill(Qb, Kb, np.arange(w.N, dtype=np.int32), w.scale, w.keep, w.pool_k, w.chunk)
+    assert (r["out_tokens"] == r["ids"]).all() and len(r["ids"]) == r["n_kept"]
+
+
 def test_position_offset_and_partial_chunk():
     ids, pos, first = ref.restore_position_ids(np.array([0, 2]), chunk=4, N=10, pos0=100)
     assert list(ids) == [0, 1, 2, 3, 8, 9]          # chunk 2 is the partial tail [8, 10)
