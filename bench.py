@@ -42,12 +42,15 @@ def parse():
     ap.add_argument("--config", default="C3", choices=["C0", "C1", "C2", "C3", "C4"])
     ap.add_argument("--algo", default="fused", choices=["fused", "simt", "auto"])
     ap.add_argument("--plan", default=None, help="fused-kernel decomposition override 'n_tg,n_ug'")
-    ap.add_argument("--shard", default="batch", choices=["batch", "seq", "seq-split", "head"],
-                    help="N>1: batch = one request per rank, no collective (weak scaling); "
+    ap.add_argument("--shard", default="auto", choices=["auto", "batch", "replica", "seq", "seq-split", "head"],
+                    help="N>1: batch = the batch's requests split over ranks (dist.batch_range), no collective "
+                         "(strong scaling); replica = every rank runs its own copy of the workload (weak); "
                          "seq = the prompt split over ranks, statistics exchanged inside the fused kernel over "
-                         "NVLink peer memory (one K read, strong scaling); seq-split = the same split with "
-                         "stats/finish launches and an NCCL statistics all-gather (two K reads); "
-                         "head = the heads split over ranks, NCCL MAX all-reduce of the log-domain maxima (strong)")
+                         "NVLink peer memory (one K read) + the sharded selection (candidate all-gather/merge; "
+                         "strong); seq-split = the same split with stats/finish launches and an NCCL statistics "
+                         "all-gather (two K reads); head = the heads split over ranks, NCCL MAX all-reduce of the "
+                         "log-domain maxima (strong).  auto: C2 -> batch, C3/C4 -> seq (BASELINE.json configs), "
+                         "C0/C1 -> replica")
     ap.add_argument("--kv", default="bf16", choices=["bf16", "e4m3"],
                     help="input element type: bf16 (the north_star's), or e4m3 codes with per-tensor scales "
                          "(SURVEY 8(f) row f4, sp_score_e4m3; single GPU / batch sharding)")
@@ -65,6 +68,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-read-peak", action="store_true", help="skip measuring the read-only stream peak")
     ap.add_argument("--cpu-sample-layers", type=int, default=32)
     return ap.parse_args()
 
@@ -139,6 +143,14 @@ def workload(name):
     return gen.CONFIGS[name]
 
 
+def resolve_shard(args, world: int) -> str | None:
+    if world == 1:
+        return None
+    if args.shard != "auto":
+        return args.shard
+    return {"C2": "batch", "C3": "seq", "C4": "seq"}.get(args.config, "replica")
+
+
 # ---------------------------------------------------------------- cpu baseline (oracle)
 def cpu_baseline(w, n_layers: int):
     """The float64 oracle as it stands, on this host's cores, on a bounded
@@ -167,27 +179,48 @@ def cpu_baseline(w, n_layers: int):
 
 def run_reference(args):
     """--impl reference: the oracle is the reference arm (no reference code
-    exists for this paper).  Rank 0 only; other ranks exit without work."""
+    exists for this paper).  Rank 0 only; other ranks exit without work.
+
+    Each step is a bounded sample of the workload, timed as it runs: the
+    float64 scoring of request 0's first `layers` layers over all N prompt
+    tokens plus the full selection (the inputs are generated once, untimed).
+    ms_per_step is that sample's measured time, so steps x ms_per_step is the
+    arm's timed wall clock; value counts the prompt-token equivalent of the
+    work done per step, N * layers / L tokens."""
+    import numpy as np
+
+    from oracle import ref
+    from spgen import gen
+    from threadpoolctl import threadpool_info
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     w = workload(args.config)
     layers = max(1, min(w.L, 2))
+    Q = ref.bf16_to_f64(np.stack([gen.gen_Q(w, 0, l) for l in range(layers)]))
+    Ks = [ref.bf16_to_f64(np.stack([gen.gen_K(w, 0, l, g) for g in range(w.Hkv)])) for l in range(layers)]
     times = []
-    cb = None
-    for s in range(args.warmup + args.steps):
-        cb = cpu_baseline(w, layers)
-        if s >= args.warmup:
-            times.append(w.N / cb["value"])
+    for s_ in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        imp = ref.token_importance(Q, lambda l: Ks[l], w.scale, w.Rv)
+        ref.select(imp, w.keep, w.pool_k, w.chunk)
+        t1 = time.perf_counter()
+        if s_ >= args.warmup:
+            times.append(t1 - t0)
     ms = 1000.0 * statistics.mean(times)
-    val = w.N / (ms / 1000.0)
+    tok_equiv = w.N * layers / w.L
+    val = tok_equiv / (ms / 1000.0)
+    threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    sample = (f"request 0 of {w.name}: float64 scoring of layers 0..{layers - 1} of {w.L} over all {w.N} tokens "
+              f"+ the full selection per step ({tok_equiv:g} prompt-token equivalents per step)")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config} {w.name}", "B": w.B, "N": w.N, "L": w.L, "H": w.H,
-                       "Hkv": w.Hkv, "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cb["cores"], "kind": "oracle",
-                             "sample": cb["sample"]},
+                       "Hkv": w.Hkv, "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk,
+                       "sampled_layers": layers, "prompt_token_equiv_per_step": tok_equiv},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                             "host_cpus": os.cpu_count()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -210,11 +243,18 @@ def run_ours(args):
     w = workload(args.config)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
-    seq = world > 1 and args.shard in ("seq", "seq-split")
-    seq_peer = seq and args.shard == "seq"
-    head = world > 1 and args.shard == "head"
-    if world > 1 and not (seq or head):
-        w = w.with_(seed=w.seed + rank)              # batch sharding: each rank owns different requests
+    shard = resolve_shard(args, world)
+    seq = shard in ("seq", "seq-split")
+    seq_peer = shard == "seq"
+    head = shard == "head"
+    bsplit = shard == "batch"
+    if shard == "replica":
+        w = w.with_(seed=w.seed + rank)              # replicas: every rank its own copy of the workload
+    if bsplit:
+        from paper_2502_02789_b200 import dist as spd
+        b0, b1 = spd.batch_range(w.B, world, rank)
+        if b1 <= b0:
+            raise SystemExit(f"--shard batch needs B >= world (B = {w.B})")
 
     # ---- inputs resident in HBM (device-side generator, bit-identical to spgen.gen)
     if seq:
@@ -223,6 +263,10 @@ def run_ours(args):
         Q, K, T = spgen_cuda.make_inputs(w, device=dev, i0=i0, n_local=i1 - i0)
     else:
         Q, K, T = spgen_cuda.make_inputs(w, device=dev)
+    if bsplit:                                       # this rank's requests [b0, b1) of the batch
+        Q, K, T = Q[b0:b1].clone(), K[b0:b1].clone(), T[b0:b1].clone()
+        w = w.with_(B=b1 - b0)
+        torch.cuda.empty_cache()
     if head:                                         # this rank's heads (strided views of the whole inputs)
         from paper_2502_02789_b200 import dist as spd
         g0, g1 = spd.head_range(w.Hkv, world, rank)
@@ -282,28 +326,25 @@ def run_ours(args):
 
     if seq_peer:
         from paper_2502_02789_b200 import dist as spd
-        peer_ptrs = spd._peer_buffers(Q, K, w.Rv, None)
+        peer_ptrs, peer_ws = spd._peer_buffers(Q, K, w.Rv, None)
     if seq:
+        from paper_2502_02789_b200 import dist as spd
+        imp_loc = torch.empty((w.B, K.shape[3]), dtype=torch.float32, device=dev)
+
         def score_only():                              # noqa: F811 -- the sharded scoring (with its exchange)
-            nonlocal imp
             if seq_peer:                               # one pass: the exchange runs in the kernel, over NVLink
-                loc = sp.score_peer(Q, K, rank, world, peer_ptrs, 0, w.Rv, w.scale)
-                full = torch.empty((world * loc.shape[1],), dtype=torch.float32, device=dev)
-                dist.all_gather_into_tensor(full, loc.reshape(-1))
-                imp = full.view(1, w.N)
+                sp.score_peer(Q, K, rank, world, peer_ptrs, 0, w.Rv, w.scale, out=imp_loc, ws=peer_ws)
                 return
             st_ = sp.score_stats(Q, K, w.Rv, w.scale)
             parts = torch.empty((world * st_.shape[0], 2), dtype=torch.float32, device=dev)
             dist.all_gather_into_tensor(parts, st_)
             lse2 = sp.stats_combine(parts.view(world, -1, 2))
-            loc = sp.score_finish(Q, K, lse2, w.Rv, w.scale)
-            full = torch.empty((world * loc.shape[1],), dtype=torch.float32, device=dev)
-            dist.all_gather_into_tensor(full, loc.reshape(-1))
-            imp = full.view(1, w.N)
+            sp.score_finish(Q, K, lse2, w.Rv, w.scale, out=imp_loc)
 
         def step():                                    # noqa: F811
             score_only()
-            select_only()
+            # the sharded selection: edges + candidate all-gathers, global merge (no importance all-gather)
+            spd.seq_sharded_select(imp_loc, w.N, w.keep, w.pool_k, w.chunk, w.pos0, T)
 
     if head:
         def score_only():                              # noqa: F811 -- head-sharded scoring + MAX all-reduce
@@ -380,7 +421,13 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_total, score_ms = tt.tolist()
     ms_step = ms_total / args.steps
-    tokens_per_step = n_tokens * (1 if (seq or head) else world)
+    # seq / head: every rank works on the same prompt (strong scaling); batch split and
+    # replicas: the ranks' own requests add up (batch split: the one batch, strong)
+    tokens_per_step = n_tokens
+    if world > 1 and not (seq or head):
+        tt = torch.tensor([n_tokens], device=dev, dtype=torch.int64)
+        dist.all_reduce(tt)
+        tokens_per_step = int(tt.item())
     value = tokens_per_step / (ms_step / 1000.0)
 
     # ---- roofline of the dominant kernel (sp_score): algorithmic bytes / duration
@@ -391,28 +438,46 @@ def run_ours(args):
     alg_bytes = ((k_bytes // world if (seq or head) else k_bytes) + (q_bytes // world if head else q_bytes)
                  + w.B * w.N * 4)
     achieved = alg_bytes / (score_ms / 1000.0) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and not (seq or head or bsplit):
         with open(tp) as f:
-            traffic = json.load(f).get(f"{args.config}/{args.algo}" + ("/e4m3" if f8 else "")
-                                       + (f"/paged{args.paged}" if paged else ""))
+            tj = json.load(f)
+        key = f"{args.config}/{args.algo}" + ("/e4m3" if f8 else "") + (f"/paged{args.paged}" if paged else "")
+        traffic = tj.get(key)
+        traffic_src = tj.get("_source", {}).get(key) if traffic is not None else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "sp_score", "kernel_ms": score_ms,
+                "traffic": traffic, "traffic_source": traffic_src, "kernel": "sp_score", "kernel_ms": score_ms,
                 "algorithmic_bytes": alg_bytes, "peak_source": peak_src,
                 "frac_of_8TBs": achieved / SPEC_HBM_GBS, "score_share_of_step": score_ms / ms_step}
 
     # ---- end to end through the C ABI with host (pinned) buffers
     e2e = None
     if not args.no_e2e and not (seq or head or f8 or paged):    # sp_run_host is the single-GPU / batch-sharded bf16 call
-        e2e = run_e2e(args, w, Q, K, T, dev, stream, dist, world)
+        e2e = run_e2e(args, w, Q, K, T, dev, stream, dist, tokens_per_step)
+    read_peak = None
+    if not args.no_read_peak:
+        from spgen import cuda as spgen_cuda2
+        rp = spgen_cuda2.read_stream_gbs(dev)
+        best = max(rp.values())
+        read_peak = {"gbs": best, "frac": achieved / best, "probes_gbs": rp,
+                     "how": "best of 10 passes over a 2 GiB buffer: 1-D TMA bulk copies into a 6-stage SMEM ring "
+                            "(one CTA per SM) and 128-bit ld.global.nc read-xor (spgen/probe.cu), CUDA events"}
+    roofline["read_peak"] = read_peak
 
     # select_gather is one launch, or two for long prompts (phase A over the SMs,
-    # then B-C): the rule of select_launch() in csrc/select.cu
-    n_c = -(-w.N // w.chunk)
-    cpb = max(1, 2048 // w.chunk)
-    select_launches = 2 if 4 <= -(-n_c // cpb) <= 65535 else 1
-    launches_per_step = {"fused": 1, "simt": 4, "auto": 1}[args.algo] + select_launches
+    # then B-C): the rule of launch_select() in csrc/select.cu
+    def sel_launches(n_tok):
+        n_c = -(-n_tok // w.chunk)
+        cpb = max(1, 2048 // w.chunk)
+        return 2 if 4 <= -(-n_c // cpb) <= 65535 else 1
+    if seq:
+        n_loc = w.N // world
+        sel = (1 if w.pool_k > 1 else 0) + sel_launches(n_loc) + 1         # edges, candidates, merge
+        launches_per_step = (1 if seq_peer else 2 + 1) + sel                 # score_peer | stats+combine+finish
+    else:
+        launches_per_step = {"fused": 1, "simt": 4, "auto": 1}[args.algo] + sel_launches(w.N) \
+            + (1 if head else 0)
     Kgeom = (torch.empty(w.d, dtype=torch.bfloat16, device=dev).as_strided((w.B, w.L, w.Hkv, w.N, w.d),
                                                                           (0, 0, 0, 0, 1)) if paged else K)
     Kgeom8 = (torch.empty(w.d, dtype=torch.uint8, device=dev).as_strided((w.B, w.L, w.Hkv, w.N, w.d),
@@ -421,18 +486,20 @@ def run_ours(args):
             if args.algo != "simt" else None)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if (seq or head) else "weak", "vs_baseline": None, "dtype": args.kv, "data": "synthetic",
+            "scaling": "strong" if (seq or head or bsplit) else "weak", "vs_baseline": None, "dtype": args.kv, "data": "synthetic",
             "config": {"workload": f"{args.config} {w.name}" + (" e4m3 K/Q" if f8 else "")
                        + (f" paged bs{args.paged} {args.paged_layout}" if paged else "") + (" ragged" if seq_lens is not None else ""),
                        "prompt_tokens_per_step": n_tokens, "B": w.B, "N": w.N, "L": w.L, "H": w.H, "Hkv": w.Hkv,
                        "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk,
-                       "algo": args.algo, "plan": plan, "plan_tuned": tuned, "launch": graph_note, "shard": args.shard if world > 1 else None,
+                       "algo": args.algo, "plan": plan, "plan_tuned": tuned, "launch": graph_note, "shard": shard,
                        "parallelism": (f"seq{world} (prompt split, in-kernel statistics exchange over NVLink "
-                                       f"peer memory)" if seq_peer else
-                                       f"seq{world} (prompt split, NCCL stats all-gather)" if seq else
+                                       f"peer memory, sharded select: candidate all-gather + merge)" if seq_peer else
+                                       f"seq{world} (prompt split, NCCL stats all-gather, sharded select)" if seq else
                                        f"tp{world} (head split, NCCL MAX all-reduce of the log-domain maxima)"
                                        if head else
-                                       f"dp{world} (batch-sharded: one request per rank, no collective)")
+                                       f"dp{world} (batch split: requests [{b0}, {b1}) on rank {rank}, no collective)"
+                                       if bsplit else
+                                       f"replica{world} (every rank its own copy, no collective)")
                        if world > 1 else "single",
                        "l2": f"inputs larger than L2 (K = {k_bytes / 2**30:.2f} GiB per GPU), no flush"},
             "roofline": roofline, "clocks": clk, "e2e": e2e, "gpu_launches": launches_per_step * args.steps}
@@ -444,7 +511,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(args, w, Q, K, T, dev, stream, dist, world):
+def run_e2e(args, w, Q, K, T, dev, stream, dist, job_tokens):
     """Same metric through sp_run_host: H2D of the step's inputs from pinned
     host memory, score/select/gather, D2H of ids/pos/n_kept/tokens."""
     import torch
@@ -480,7 +547,7 @@ def run_e2e(args, w, Q, K, T, dev, stream, dist, world):
         ms = t.item()
     h2d = Qh.numel() * 2 + Kh.numel() * 2 + Th.numel() * 4
     d2h = 3 * w.B * w.N * 4 + w.B * 4
-    return {"value": w.B * w.N * world / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+    return {"value": job_tokens / (ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps}
 
 

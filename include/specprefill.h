@@ -82,7 +82,8 @@ typedef struct sp_geom {
  *   K[b][l][g][i][:]  at  K + b*k_b + l*k_l + g*k_g + i*k_i     (bf16)
  *   Q[b][l][r][h][:]  at  Q + b*q_b + l*q_l + r*q_r + h*q_h     (bf16)
  * Alignment: K, Q and every stride*2 bytes must be multiples of 16 bytes
- * (TMA tensor maps), strides must be non-negative.
+ * (TMA tensor maps), strides must be non-negative, and a dimension of size > 1
+ * may not have stride 0 (no broadcast views, e.g. K.expand(B, ...): SP_EINVAL).
  */
 typedef struct sp_layout {
   int64_t k_b, k_l, k_g, k_i;
@@ -347,6 +348,41 @@ sp_status sp_select_gather(const float* importance, const int32_t* tokens, int32
 sp_status sp_select_ragged(const float* importance, const int32_t* seq_lens, const int32_t* tokens, int32_t B,
                            int64_t N, const sp_select_params* p, int32_t* ids, int32_t* pos, int32_t* n_kept,
                            int32_t* out_tokens, void* ws, size_t ws_bytes, sp_stream stream);
+
+/* ------------------------------------------------------------------ sequence-sharded select
+ * Row e: one request's prompt split along tokens over
+ * P ranks (the paper's TP=8 placement), rank p holding the
+ * importance of tokens [p*N/P, (p+1)*N/P).  The selection of O5-O9 (Alg.1 P:163,
+ * chunk_select_from_smoothed_attention) is computed without gathering the
+ * importance vector:
+ *   1. sp_seq_edges: this rank's first w and last w importance values
+ *      (w = (pool_k-1)/2), edges [B][2w];
+ *   2. the caller all-gathers them -> edges_all [P][B][2w] (rank order);
+ *   3. sp_seq_candidates: pool (windows reach into the neighbours' edges), chunk
+ *      means and the local top M = min(K_c, n_c/P) chunks in (cs desc, c asc)
+ *      order, written in chunk order as 64-bit keys (float bits of cs << 32 |
+ *      ~global chunk index): compared as unsigned integers they follow the
+ *      same total order; cand [B][M];
+ *   4. the caller all-gathers them -> cand_all [P][B][M];
+ *   5. sp_seq_merge: the global top-K_c of the P*M candidates (identical on
+ *      every rank) -> ids / pos / n_kept for the whole prompt, as sp_select
+ *      writes them, and the gathered tokens when tokens (replicated [B][N]) is
+ *      given.  The global top-K_c is contained in the union of the local top-M
+ *      lists because every rank ranks by the same total order.
+ * Chunk scores are computed in the same order as sp_select's, so for the same
+ * importance values the result is bit-identical to sp_select_gather on the
+ * concatenated vector.  Requires N % P == 0, (N/P) % chunk == 0 and
+ * w <= N/P (SP_EINVAL otherwise).  All device buffers are caller-owned. */
+int64_t sp_seq_candidate_count(int64_t N, int32_t world, const sp_select_params* p);   /* M, or -1 if invalid */
+size_t sp_seq_select_workspace_bytes(int32_t B, int64_t N, int32_t world, const sp_select_params* p);
+sp_status sp_seq_edges(const float* imp_local, int32_t B, int64_t N, int32_t world, const sp_select_params* p,
+                       float* edges, sp_stream stream);
+sp_status sp_seq_candidates(const float* imp_local, const float* edges_all, int32_t rank, int32_t world, int32_t B,
+                            int64_t N, const sp_select_params* p, uint64_t* cand, void* ws, size_t ws_bytes,
+                            sp_stream stream);
+sp_status sp_seq_merge(const uint64_t* cand_all, int32_t world, int32_t B, int64_t N, const sp_select_params* p,
+                       const int32_t* tokens, int32_t* ids, int32_t* pos, int32_t* n_kept, int32_t* out_tokens,
+                       void* ws, size_t ws_bytes, sp_stream stream);
 
 /* ------------------------------------------------------------------ gather
  * out[b][j] = tokens[b][ids[b][j]] for j < n_kept[b] (merge_requests input,

@@ -1,7 +1,8 @@
 """In-tree build of the native libraries (nvcc, sm_100a only).
 
 * paper_2502_02789_b200/libspecprefill.so  <- paper_2502_02789_b200/csrc/*.cu
-* spgen/libspgen.so                        <- spgen/gen.cu (input generator, not product code)
+* spgen/libspgen.so                        <- spgen/gen.cu, spgen/probe.cu (input generator and the
+                                              bench's read-stream probe; not product code)
 
 Objects go to build/ (git-ignored); the .so files stay in-tree so gpurun ships
 them to the GPU box.  Rebuilds only what changed (sources or headers newer
@@ -22,6 +23,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libspecprefill.so")
 GEN_SRC = os.path.join(ROOT, "spgen", "gen.cu")
+PROBE_SRC = os.path.join(ROOT, "spgen", "probe.cu")
 GEN_LIB = os.path.join(ROOT, "spgen", "libspgen.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -90,9 +92,9 @@ def build(verbose: bool = False, force: bool = False) -> list[str]:
     if force or jobs or _newer(objs, LIB):
         logs.append(_run([nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]))
         _stamp(objs, LIB)
-    if force or _newer([GEN_SRC], GEN_LIB, flags):
-        logs.append(_run([nvcc, *ARCH, *NVCC_FLAGS, "-shared", GEN_SRC, "-o", GEN_LIB]))
-        _stamp([GEN_SRC], GEN_LIB, flags)
+    if force or _newer([GEN_SRC, PROBE_SRC], GEN_LIB, flags):
+        logs.append(_run([nvcc, *ARCH, *NVCC_FLAGS, "-shared", GEN_SRC, PROBE_SRC, "-o", GEN_LIB]))
+        _stamp([GEN_SRC, PROBE_SRC], GEN_LIB, flags)
     if verbose:
         for x in logs:
             sys.stdout.write(x)

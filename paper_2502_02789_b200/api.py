@@ -12,6 +12,7 @@ Tensor layouts (strides are passed through, the head dim must be contiguous):
 """
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import math
 
@@ -22,7 +23,8 @@ from ._lib import check, lib
 
 ALGOS = {"auto": _lib.SP_SCORE_AUTO, "fused": _lib.SP_SCORE_FUSED, "simt": _lib.SP_SCORE_SIMT}
 
-_ws_cache: dict = {}
+_ws_cache: "collections.OrderedDict" = collections.OrderedDict()
+_WS_MAX = 64
 
 
 def _stream_ptr(stream) -> int:
@@ -30,18 +32,28 @@ def _stream_ptr(stream) -> int:
     return s.cuda_stream
 
 
-def workspace(tag, nbytes: int, device) -> torch.Tensor:
-    """Zero-initialised, cached device workspace.  The fused kernel leaves its
-    counters at zero after every call, but their position depends on the
-    geometry, so a workspace is only ever reused for the same ``tag`` (which
-    includes the geometry): see include/specprefill.h, "Ownership"."""
-    key = (tag, torch.device(device).index)
+def workspace(tag, nbytes: int, device, stream=None) -> torch.Tensor:
+    """Zero-initialised, cached device workspace, one per (tag, device, stream).
+    The fused kernel leaves its counters at zero after every call, but their
+    position depends on the geometry, so a workspace is only ever reused for
+    the same ``tag`` (which includes the geometry) and the same stream (two
+    streams never share a launch epoch or partial buffers): see
+    include/specprefill.h, "Ownership".  Least-recently-used entries beyond 64
+    are dropped; a buffer used on a non-current stream is recorded on it, so
+    the caching allocator does not hand its memory out while a kernel on that
+    stream may still use it."""
+    dev = torch.device(device)
+    key = (tag, dev.index, _stream_ptr(stream))
     buf = _ws_cache.get(key)
     if buf is None or buf.numel() < nbytes:
-        if len(_ws_cache) > 64:
-            _ws_cache.clear()
-        buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+        while len(_ws_cache) >= _WS_MAX:
+            _ws_cache.popitem(last=False)
+        buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=dev)
         _ws_cache[key] = buf
+    else:
+        _ws_cache.move_to_end(key)
+    if stream is not None and stream != torch.cuda.current_stream(dev):
+        buf.record_stream(stream)
     return buf
 
 
@@ -86,7 +98,7 @@ def score(Q, K, R_valid=None, scale=None, out=None, algo: str = "auto", stream=N
         out = torch.empty((g.B, g.N), dtype=torch.float32, device=K.device)
     a = ALGOS[algo]
     nbytes = lib().sp_score_workspace_bytes(C.byref(g), a)
-    ws = workspace(("score", algo, _geom_key(g)), nbytes, K.device)
+    ws = workspace(("score", algo, _geom_key(g)), nbytes, K.device, stream)
     check(lib().sp_score_ex(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), out.data_ptr(), ws.data_ptr(),
                             ws.numel(), a, _stream_ptr(stream)), "sp_score")
     return out
@@ -104,7 +116,7 @@ def score_e4m3(Q8, K8, q_scale: float = 1.0, k_scale: float = 1.0, R_valid=None,
         check(_lib.SP_EUNSUPPORTED, "sp_score_e4m3")
     pl = (C.c_int64 * 9)()
     lib().sp_score_e4m3_plan(C.byref(g), pl)
-    ws = workspace(("score_e4m3", _geom_key(g), tuple(pl)[2:4]), nbytes, K8.device)
+    ws = workspace(("score_e4m3", _geom_key(g), tuple(pl)[2:4]), nbytes, K8.device, stream)
     check(lib().sp_score_e4m3(Q8.data_ptr(), K8.data_ptr(), float(q_scale), float(k_scale), C.byref(g), C.byref(lay),
                               out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_score_e4m3")
     return out
@@ -132,7 +144,7 @@ def score_lookahead(Q, K, K_la, la_shift: int = 0, R_valid=None, scale=None, out
     nbytes = lib().sp_score_lookahead_workspace_bytes(C.byref(g))
     if nbytes == 0:
         check(_lib.SP_EUNSUPPORTED, "sp_score_lookahead")
-    ws = workspace(("score_la", _geom_key(g)), nbytes, K.device)
+    ws = workspace(("score_la", _geom_key(g)), nbytes, K.device, stream)
     check(lib().sp_score_lookahead(Q.data_ptr(), K.data_ptr(), C.byref(la), C.byref(g), C.byref(lay), out.data_ptr(),
                                    ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_score_lookahead")
     return out
@@ -178,7 +190,9 @@ def score_paged(Q, K_cache, block_table, seq_lens=None, N=None, R_valid=None, sc
         nbytes = lib().sp_score_e4m3_workspace_bytes(C.byref(g))
         if nbytes == 0:
             check(_lib.SP_EUNSUPPORTED, "sp_score_paged_e4m3")
-        ws = workspace(("score_paged_e4m3", _geom_key(g)), nbytes, K_cache.device)
+        pl = (C.c_int64 * 9)()
+        lib().sp_score_e4m3_plan(C.byref(g), pl)
+        ws = workspace(("score_paged_e4m3", _geom_key(g), tuple(pl)[2:4]), nbytes, K_cache.device, stream)
         check(lib().sp_score_paged_e4m3(Q.data_ptr(), C.byref(pk), float(q_scale), float(k_scale), C.byref(g),
                                         C.byref(lay), out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
               "sp_score_paged_e4m3")
@@ -186,7 +200,7 @@ def score_paged(Q, K_cache, block_table, seq_lens=None, N=None, R_valid=None, sc
     nbytes = lib().sp_score_paged_workspace_bytes(C.byref(g))
     if nbytes == 0:
         check(_lib.SP_EUNSUPPORTED, "sp_score_paged")
-    ws = workspace(("score_paged", _geom_key(g)), nbytes, K_cache.device)
+    ws = workspace(("score_paged", _geom_key(g)), nbytes, K_cache.device, stream)
     check(lib().sp_score_paged(Q.data_ptr(), C.byref(pk), C.byref(g), C.byref(lay), out.data_ptr(), ws.data_ptr(),
                                ws.numel(), _stream_ptr(stream)), "sp_score_paged")
     return out
@@ -210,7 +224,7 @@ def select_ragged(importance: torch.Tensor, seq_lens: torch.Tensor, keep: float,
     nbytes = lib().sp_select_workspace_bytes(B, N, C.byref(p))
     if nbytes == 0:
         check(_lib.SP_EINVAL, "sp_select_ragged")
-    ws = workspace("select", nbytes, dev)
+    ws = workspace("select", nbytes, dev, stream)
     check(lib().sp_select_ragged(importance.data_ptr(), seq_lens.data_ptr(),
                                  None if tokens is None else tokens.data_ptr(), B, N, C.byref(p), ids.data_ptr(),
                                  pos.data_ptr(), n_kept.data_ptr(), None if out is None else out.data_ptr(),
@@ -235,7 +249,7 @@ def select(importance: torch.Tensor, keep: float, pool_k: int, chunk: int, pos0:
     nbytes = lib().sp_select_workspace_bytes(B, N, C.byref(p))
     if nbytes == 0:
         check(_lib.SP_EINVAL, "sp_select")
-    ws = workspace("select", nbytes, dev)
+    ws = workspace("select", nbytes, dev, stream)
     if tokens is None:
         check(lib().sp_select(importance.data_ptr(), B, N, C.byref(p), ids.data_ptr(), pos.data_ptr(),
                               n_kept.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_select")
@@ -247,6 +261,86 @@ def select(importance: torch.Tensor, keep: float, pool_k: int, chunk: int, pos0:
                                  pos.data_ptr(), n_kept.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(),
                                  _stream_ptr(stream)), "sp_select_gather")
     return ids, pos, n_kept, out
+
+
+def _seq_params(keep, pool_k, chunk, pos0=0):
+    return _lib.sp_select_params(keep_rate=float(keep), pool_k=int(pool_k), chunk=int(chunk), pos0=int(pos0))
+
+
+def seq_candidate_count(N: int, world: int, keep: float, pool_k: int, chunk: int) -> int:
+    """M = min(K_c, n_c / world): candidates per rank of the sequence-sharded select."""
+    p = _seq_params(keep, pool_k, chunk)
+    m = lib().sp_seq_candidate_count(int(N), int(world), C.byref(p))
+    if m < 0:
+        check(_lib.SP_EINVAL, "sp_seq_candidate_count")
+    return int(m)
+
+
+def seq_edges(imp_local: torch.Tensor, world: int, N: int, keep: float, pool_k: int, chunk: int,
+              stream=None) -> torch.Tensor:
+    """Sequence-sharded select, step 1: this rank's first and last (pool_k-1)/2
+    importance values, edges [B][2w] fp32 (all-gathered by the caller)."""
+    if imp_local.dtype != torch.float32 or imp_local.dim() != 2 or not imp_local.is_contiguous():
+        raise ValueError("imp_local must be contiguous fp32 [B][N/world]")
+    B = imp_local.shape[0]
+    w = (int(pool_k) - 1) // 2
+    edges = torch.empty((B, 2 * w), dtype=torch.float32, device=imp_local.device)
+    p = _seq_params(keep, pool_k, chunk)
+    check(lib().sp_seq_edges(imp_local.data_ptr(), B, int(N), int(world), C.byref(p),
+                             edges.data_ptr() if w else None, _stream_ptr(stream)), "sp_seq_edges")
+    return edges
+
+
+def seq_candidates(imp_local: torch.Tensor, edges_all, rank: int, world: int, N: int, keep: float, pool_k: int,
+                   chunk: int, stream=None) -> torch.Tensor:
+    """Step 3: pool + chunk means of this rank's chunks and its top-M
+    candidates, int64 [B][M] keys (fp32 score bits << 32 | ~global chunk id;
+    unsigned order = (score desc, index asc)), in chunk order."""
+    if imp_local.dtype != torch.float32 or imp_local.dim() != 2 or not imp_local.is_contiguous():
+        raise ValueError("imp_local must be contiguous fp32 [B][N/world]")
+    B = imp_local.shape[0]
+    p = _seq_params(keep, pool_k, chunk)
+    M = seq_candidate_count(N, world, keep, pool_k, chunk)
+    cand = torch.empty((B, M), dtype=torch.int64, device=imp_local.device)
+    nbytes = lib().sp_seq_select_workspace_bytes(B, int(N), int(world), C.byref(p))
+    if nbytes == 0:
+        check(_lib.SP_EINVAL, "sp_seq_candidates")
+    ws = workspace("seq_sel", nbytes, imp_local.device, stream)
+    if edges_all is not None and (edges_all.dtype != torch.float32 or not edges_all.is_contiguous()):
+        raise ValueError("edges_all must be contiguous fp32 [world][B][2w]")
+    check(lib().sp_seq_candidates(imp_local.data_ptr(), None if edges_all is None or edges_all.numel() == 0
+                                  else edges_all.data_ptr(), int(rank), int(world), B, int(N), C.byref(p),
+                                  cand.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
+          "sp_seq_candidates")
+    return cand
+
+
+def seq_merge(cand_all: torch.Tensor, world: int, N: int, keep: float, pool_k: int, chunk: int, pos0: int = 0,
+              tokens=None, stream=None):
+    """Step 5: global top-K_c of the gathered candidates [world][B][M] ->
+    (ids, pos, n_kept[, gathered tokens]) for the whole prompt, as select()."""
+    if cand_all.dtype != torch.int64 or cand_all.dim() != 3 or not cand_all.is_contiguous():
+        raise ValueError("cand_all must be contiguous int64 [world][B][M]")
+    B = cand_all.shape[1]
+    dev = cand_all.device
+    p = _seq_params(keep, pool_k, chunk, pos0)
+    ids = torch.empty((B, N), dtype=torch.int32, device=dev)
+    pos = torch.empty_like(ids)
+    n_kept = torch.empty((B,), dtype=torch.int32, device=dev)
+    out = None
+    if tokens is not None:
+        if tokens.dtype != torch.int32 or not tokens.is_contiguous() or tuple(tokens.shape) != (B, N):
+            raise ValueError("tokens must be contiguous int32 [B][N]")
+        out = torch.empty_like(tokens)
+    nbytes = lib().sp_seq_select_workspace_bytes(B, int(N), int(world), C.byref(p))
+    if nbytes == 0:
+        check(_lib.SP_EINVAL, "sp_seq_merge")
+    ws = workspace("seq_sel", nbytes, dev, stream)
+    check(lib().sp_seq_merge(cand_all.data_ptr(), int(world), B, int(N), C.byref(p),
+                             None if tokens is None else tokens.data_ptr(), ids.data_ptr(), pos.data_ptr(),
+                             n_kept.data_ptr(), None if out is None else out.data_ptr(), ws.data_ptr(), ws.numel(),
+                             _stream_ptr(stream)), "sp_seq_merge")
+    return (ids, pos, n_kept) if tokens is None else (ids, pos, n_kept, out)
 
 
 def gather(tokens: torch.Tensor, ids: torch.Tensor, n_kept: torch.Tensor, out=None, stream=None) -> torch.Tensor:
@@ -298,7 +392,7 @@ def score_stats(Q, K, R_valid=None, scale=None, out=None, stream=None) -> torch.
     rows = g.B * g.L * g.H * g.R_valid
     out = torch.empty((rows, 2), dtype=torch.float32, device=K.device) if out is None else out
     nbytes = lib().sp_score_split_workspace_bytes(C.byref(g))
-    ws = workspace(("split", _geom_key(g), _split_algo()), nbytes, K.device)
+    ws = workspace(("split", _geom_key(g), _split_algo()), nbytes, K.device, stream)
     check(lib().sp_score_stats(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), out.data_ptr(), ws.data_ptr(),
                                ws.numel(), _stream_ptr(stream)), "sp_score_stats")
     return out
@@ -319,7 +413,7 @@ def score_finish(Q, K, lse2, R_valid=None, scale=None, out=None, stream=None) ->
     g, lay = make_geom(Q, K, R_valid, scale)
     out = torch.empty((g.B, g.N), dtype=torch.float32, device=K.device) if out is None else out
     nbytes = lib().sp_score_split_workspace_bytes(C.byref(g))
-    ws = workspace(("split", _geom_key(g), _split_algo()), nbytes, K.device)
+    ws = workspace(("split", _geom_key(g), _split_algo()), nbytes, K.device, stream)
     check(lib().sp_score_finish(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), lse2.data_ptr(), out.data_ptr(),
                                 ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_score_finish")
     return out
@@ -332,7 +426,7 @@ def score_acc(Q, K, R_valid=None, scale=None, out=None, stream=None) -> torch.Te
     g, lay = make_geom(Q, K, R_valid, scale)
     out = torch.empty((g.B, g.R_valid, g.N), dtype=torch.float32, device=K.device) if out is None else out
     nbytes = lib().sp_score_workspace_bytes(C.byref(g), _lib.SP_SCORE_FUSED)
-    ws = workspace(("score", "fused", _geom_key(g)), nbytes, K.device)
+    ws = workspace(("score", "fused", _geom_key(g)), nbytes, K.device, stream)
     check(lib().sp_score_acc(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), out.data_ptr(), ws.data_ptr(),
                              ws.numel(), _stream_ptr(stream)), "sp_score_acc")
     return out
@@ -364,15 +458,26 @@ def score_peer_plan(Q, K, sm_budget: int = 0, R_valid=None) -> dict:
     return dict(zip(keys, list(out)))
 
 
+def score_peer_workspace_bytes(Q, K, sm_budget: int = 0, R_valid=None) -> int:
+    g, _ = make_geom(Q, K, R_valid)
+    return int(lib().sp_score_peer_workspace_bytes(C.byref(g), sm_budget))
+
+
 def score_peer(Q, K, rank: int, world: int, peer_ptrs, sm_budget: int = 0, R_valid=None, scale=None, out=None,
-               stream=None, ws_tag=None) -> torch.Tensor:
+               stream=None, ws_tag=None, ws=None) -> torch.Tensor:
     """Sequence-sharded single pass: importance of this rank's tokens, the
     statistics exchanged in-kernel through the peers' partial buffers
-    (peer_ptrs: `world` device addresses, rank order)."""
+    (peer_ptrs: `world` device addresses, rank order).  ``ws``: a zeroed
+    workspace owned together with the peer buffers (its launch epoch selects
+    the half of the peer buffers a launch writes, so the two must live and die
+    together); by default one from the cache."""
     g, lay = make_geom(Q, K, R_valid, scale)
     out = torch.empty((g.B, g.N), dtype=torch.float32, device=K.device) if out is None else out
     nbytes = lib().sp_score_peer_workspace_bytes(C.byref(g), sm_budget)
-    ws = workspace(("peer", _geom_key(g), sm_budget, rank if ws_tag is None else ws_tag), nbytes, K.device)
+    if ws is None:
+        ws = workspace(("peer", _geom_key(g), sm_budget, rank if ws_tag is None else ws_tag), nbytes, K.device, stream)
+    elif ws.numel() < nbytes:
+        raise ValueError("peer workspace too small")
     ptrs = (C.c_void_p * world)(*[int(x) for x in peer_ptrs])
     check(lib().sp_score_peer(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), rank, world, ptrs, sm_budget,
                               out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_score_peer")

@@ -1,11 +1,13 @@
 // Selection: 1-D average pool -> chunk means -> top-K_c chunks -> ids/positions
-// (+ optionally the token gather).
+// (+ optionally the token gather), and its sequence-sharded split into a
+// rank-local candidate select and a global candidate merge.
 //
 // PAPER.md sec:chunk_select: "we chunk the context contiguously and
 // average the token score within each block, and then we select the Top-K
 // blocks ... we apply a 1D average pooling before this"; sec:position_ids
 // (P:125-133): kept tokens keep their original position ids; Alg.1
-// merge_requests takes the selected tokens.
+// merge_requests takes the selected tokens.  Under the paper's TP=8 placement
+// the prompt is split along tokens.
 // Readings: shrinking pool edges (Z6), partial last chunk averaged
 // over its true size (Z8), K_c from the exact ppm rule (Z9, computed on the
 // host), ties to the lowest chunk index (Z10), ascending ids (Z11).
@@ -14,15 +16,27 @@
 // writing cs to the workspace), phases B-C on one CTA of 1024 threads per
 // request (kModeBC); short prompts run all three in one launch (kModeAll):
 //   A. importance is staged in shared memory segment by segment (all loads of a
-//      segment in flight together), pooled, and summed per chunk in token order
-//      (deterministic) -> cs[c];
+//      segment in flight together), pooled, and summed per chunk (a canonical
+//      order that depends only on the chunk: segments are chunk-aligned, so the
+//      single-GPU, multi-CTA and sequence-sharded runs give the same bits);
 //   B. a 4-pass 8-bit radix select on the IEEE bits of cs (scores are >= 0, so
-//      bit order == value order) finds the K_c-th largest value T; the digit
+//      bit order == value order) finds the K-th largest value T; the digit
 //      search is a parallel suffix scan over the 256 bins;
 //   C. an in-order block scan keeps every chunk above T plus the lowest-index
-//      chunks equal to T (exactly K_c chunks), compacts their token ranges into
+//      chunks equal to T (exactly K chunks), compacts their token ranges into
 //      ids/pos -- one warp per kept chunk, coalesced -- and, if requested,
 //      gathers the kept tokens in the same pass.
+// Variants (template parameter V):
+//   kPlain -- the whole prompt on one GPU (sp_select, sp_select_gather, ragged);
+//   kCand  -- sequence shard: phase A over this rank's chunks (pooling windows
+//             reach into the neighbours' importance through the exchanged edge
+//             values), B-C with K = M = min(K_c, n_c / P), and the kept chunks
+//             written as 64-bit candidate keys (score bits << 32 | ~chunk): as
+//             unsigned integers they order exactly as (score desc, index asc);
+//   kMerge -- the P ranks' gathered candidates scattered into the dense chunk
+//             array (absent chunks marked invalid), B-C with K = K_c over the
+//             whole prompt: the global top-K_c is a subset of the union of the
+//             local top-M lists because every rank ranks by the same total order.
 #include "sp_internal.h"
 
 #include <algorithm>
@@ -35,7 +49,33 @@ constexpr int NW = ST / 32;
 constexpr int SEG = 16384;          // tokens of importance staged in SMEM per segment (64 KiB)
 constexpr int kMaxPool = 4097;      // largest pooling window (half-window staged on each side)
 constexpr int kSmemChunks = 8192;   // chunk scores kept in SMEM when n_c fits (else L2-resident workspace)
+constexpr unsigned kInvalid = 0xFFFFFFFFu;   // merge: chunk with no candidate (never a score: scores are >= 0)
 enum SelectMode : int { kModeAll = 0, kModeA = 1, kModeBC = 2 };
+enum Variant : int { kPlain = 0, kCand = 1, kMerge = 2 };
+
+struct SelArgs {
+  const float* imp;          // [B][row] importance (kCand: this rank's shard)
+  long long row;             // row length of imp / ids / pos / tokens / out
+  const int* seq_lens;       // kPlain, optional [B]: per-request prompt length (row f3)
+  int pool_k, chunk, pos0;
+  long long ppm;             // keep rate in parts per million (K_c, Z9)
+  int* ids;
+  int* pos;
+  int* n_kept;
+  float* cs_ws;              // [B][n_c_row] chunk scores (workspace)
+  const int* tokens;         // optional gather source [B][row]
+  int* out;                  // optional gathered tokens [B][row]
+  int mode, segcap;
+  long long cpb;             // chunks per CTA in kModeA
+  // sequence sharding
+  long long i0;              // kCand: global index of this shard's first token
+  long long n_glob;          // kCand / kMerge: prompt length N (kPlain: row / seq_lens)
+  const float* edges;        // kCand: [P][B][2w] first w / last w importance values of every rank
+  int rank, world;
+  long long k_sel;           // kCand: M
+  unsigned long long* cand;  // kCand: [B][M] candidate keys out
+  const unsigned long long* cand_in;   // kMerge: [P][B][M] candidate keys
+};
 
 struct ScanSmem {
   int warp_tot[NW];
@@ -72,52 +112,90 @@ __device__ __forceinline__ int block_excl_scan(int v, ScanSmem& sm, int* total) 
   return res;
 }
 
-// Nrow: row length of the [B][Nrow] arrays; seq_lens (optional, row f3): the
-// request's own prompt length n_b (clamped to [1, Nrow]), else Nrow.  K_c is
-// computed per request from the keep rate in parts per million (Z9's integer rule).
-__global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all, long long Nrow,
-                                               const int* __restrict__ seq_lens, int pool_k, int chunk,
-                                               int pos0, long long ppm, int* __restrict__ ids_all,
-                                               int* __restrict__ pos_all, int* __restrict__ n_kept,
-                                               float* __restrict__ cs_all, const int* __restrict__ tokens_all,
-                                               int* __restrict__ out_all, int mode, int segcap, long long cpb) {
+// Segment length starting at chunk-aligned token `base`: whole chunks when a
+// chunk fits the segment, else the rest of the chunk up to segcap tokens.
+__device__ __forceinline__ long long seg_len(long long base, long long t_hi, int chunk, int segcap) {
+  long long next;
+  if (chunk <= segcap) {
+    next = base + (long long)(segcap / chunk) * chunk;
+  } else {
+    const long long cend = (base / chunk + 1) * chunk;
+    next = base + segcap < cend ? base + segcap : cend;
+  }
+  return (next < t_hi ? next : t_hi) - base;
+}
+
+template <int V>
+__global__ void __launch_bounds__(ST) k_select(SelArgs a) {
   extern __shared__ float seg[];                  // [segcap + 2w] staged importance, then [segcap] pooled
   __shared__ unsigned hist[256];
   __shared__ unsigned s_digit, s_remaining;
   __shared__ ScanSmem scan;
   __shared__ int kept_c[ST];                      // kept chunk ids of one scan tile, in order
   __shared__ int kept_off[ST];
+  const int mode = a.mode, chunk = a.chunk, pool_k = a.pool_k;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long N = seq_lens ? std::min<long long>(std::max(seq_lens[b], 1), Nrow) : Nrow;
-  const long long n_c = (N + chunk - 1) / chunk;
-  const long long n_c_row = (Nrow + chunk - 1) / chunk;
-  const long long K_c = std::min(n_c, std::max(1LL, (ppm * n_c + 999999) / 1000000));
-  const float* imp = imp_all + (long long)b * Nrow;
-  const long long w_ = (pool_k - 1) / 2;
+  const long long Nrow = a.row;
+  // N: the prompt length the pooling edges and chunk sizes refer to (global when sharded)
+  long long N;
+  if (V == kPlain) N = a.seq_lens ? std::min<long long>(std::max(a.seq_lens[b], 1), Nrow) : Nrow;
+  else N = a.n_glob;
+  const long long i0 = V == kCand ? a.i0 : 0;                    // global index of imp[b][0]
+  const long long n_loc = V == kCand ? Nrow : N;                 // tokens held in imp rows
+  const long long c_base = i0 / chunk;                           // global id of local chunk 0
+  const long long n_c_all = (N + chunk - 1) / chunk;             // chunks of the prompt
+  const long long n_c = V == kCand ? n_loc / chunk : n_c_all;    // chunks this selection ranks
+  const long long n_c_row = V == kPlain ? (Nrow + chunk - 1) / chunk : n_c;   // workspace row
+  long long K_sel;
+  if (V == kCand) K_sel = a.k_sel;
+  else K_sel = std::min(n_c_all, std::max(1LL, (a.ppm * n_c_all + 999999) / 1000000));
+  const float* imp = a.imp + (long long)b * Nrow;
+  const long long w = (pool_k - 1) / 2;
   // chunk scores: SMEM when this CTA runs phases B-C and n_c fits, else the workspace
   // (decided on the row's chunk count, as the launch sized the SMEM: a ragged request may have fewer)
   const bool cs_smem = mode != kModeA && n_c_row <= kSmemChunks;
-  float* cs = cs_smem ? seg + 2 * segcap + 2 * w_ : cs_all + (long long)b * n_c_row;
-  int* ids = ids_all + (long long)b * Nrow;
-  int* pos = pos_all + (long long)b * Nrow;
-  const long long w = (pool_k - 1) / 2;
+  float* cs = cs_smem ? seg + 2 * a.segcap + 2 * w : a.cs_ws + (long long)b * n_c_row;
 
-  if (mode == kModeBC) {
+  if (V == kMerge) {
+    // ---- scatter the P ranks' candidates into the dense chunk array
+    unsigned* csu = reinterpret_cast<unsigned*>(cs);
+    for (long long c = tid; c < n_c; c += ST) csu[c] = kInvalid;
+    __syncthreads();
+    const long long M = a.k_sel;
+    for (int p = 0; p < a.world; ++p) {
+      const unsigned long long* src = a.cand_in + ((long long)p * gridDim.x + b) * M;
+      for (long long m = tid; m < M; m += ST) {
+        const unsigned long long key = src[m];
+        const unsigned c = ~(unsigned)(key & 0xFFFFFFFFull);
+        if (c < (unsigned long long)n_c) csu[c] = (unsigned)(key >> 32);
+      }
+    }
+    __syncthreads();
+  } else if (mode == kModeBC) {
     if (cs_smem)
-      for (long long c = tid; c < n_c; c += ST) cs[c] = cs_all[(long long)b * n_c_row + c];
+      for (long long c = tid; c < n_c; c += ST) cs[c] = a.cs_ws[(long long)b * n_c_row + c];
     __syncthreads();
   } else {
   // ---- A. pooled scores (centred window, shrinking edges) -> chunk sums of
-  //      chunks [c_lo, c_hi) (all of them unless kModeA)
-  const long long c_lo = mode == kModeA ? std::min(n_c, (long long)blockIdx.y * cpb) : 0;
-  const long long c_hi = mode == kModeA ? std::min(n_c, c_lo + cpb) : n_c;
+  //      chunks [c_lo, c_hi) (global ids; all of the CTA's range unless kModeA)
+  const long long c_lo = c_base + (mode == kModeA ? std::min(n_c, (long long)blockIdx.y * a.cpb) : 0);
+  const long long c_hi = c_base + (mode == kModeA ? std::min(n_c, (long long)blockIdx.y * a.cpb + a.cpb) : n_c);
   const long long t_lo = c_lo * chunk, t_hi = std::min(N, c_hi * chunk);
+  const int segcap = a.segcap;
   float* pooled = seg + segcap + 2 * w;             // [segcap]
   const int wi = (int)w;
   const float inv_k = 1.f / (float)pool_k;
   const bool warp_chunks = chunk <= 32 && (chunk & (chunk - 1)) == 0;   // power of two <= 32
-  for (long long base = t_lo; base < t_hi; base += segcap) {
-    const int len = (int)((base + segcap < t_hi) ? segcap : t_hi - base);  // tokens in this segment
+  // kCand: importance of global token t in [i0 - w, i0 + n_loc + w): own shard, or a neighbour's edge
+  const float* halo_l = nullptr;
+  const float* halo_r = nullptr;
+  if (V == kCand) {
+    const long long eb = 2 * w;                       // edges row: first w, then last w values
+    if (a.rank > 0) halo_l = a.edges + ((long long)(a.rank - 1) * gridDim.x + b) * eb + w;
+    if (a.rank + 1 < a.world) halo_r = a.edges + ((long long)(a.rank + 1) * gridDim.x + b) * eb;
+  }
+  for (long long base = t_lo; base < t_hi;) {
+    const int len = (int)seg_len(base, t_hi, chunk, segcap);             // tokens in this segment
     const long long lo = base - w < 0 ? 0 : base - w, hi = base + len + w > N ? N : base + len + w;
     const int off = (int)(base - lo);                                     // seg index of token `base`
     {
@@ -125,17 +203,34 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
       constexpr int PER = SEG / ST;
       const int n = (int)(hi - lo);
       float r[PER];
+      if (V == kCand) {
 #pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        const int i = tid + k * ST;
-        r[k] = i < n ? __ldg(imp + lo + i) : 0.f;
+        for (int k = 0; k < PER; ++k) {
+          const int i = tid + k * ST;
+          const long long t = lo + i;
+          r[k] = i >= n ? 0.f
+                        : (t < i0 ? __ldg(halo_l + (t - (i0 - w)))
+                                  : (t >= i0 + n_loc ? __ldg(halo_r + (t - i0 - n_loc)) : __ldg(imp + (t - i0))));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int i = tid + k * ST;
+          r[k] = i < n ? __ldg(imp + lo + i) : 0.f;
+        }
       }
 #pragma unroll
       for (int k = 0; k < PER; ++k) {
         const int i = tid + k * ST;
         if (i < n) seg[i] = r[k];
       }
-      for (int i = PER * ST + tid; i < n; i += ST) seg[i] = imp[lo + i];   // halo beyond SEG
+      for (int i = PER * ST + tid; i < n; i += ST) {                    // halo beyond SEG
+        const long long t = lo + i;
+        if (V == kCand)
+          seg[i] = t < i0 ? halo_l[t - (i0 - w)] : (t >= i0 + n_loc ? halo_r[t - i0 - n_loc] : imp[t - i0]);
+        else
+          seg[i] = imp[t];
+      }
     }
     __syncthreads();
     // interior tokens [i_lo, i_hi) have the full window inside the sequence
@@ -150,23 +245,23 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
         pooled[i] = ws * inv_k;
       } else {                                                            // sequence edges: shrink
         const long long t = base + i;
-        const long long a = t - w < 0 ? 0 : t - w, e = t + w > N - 1 ? N - 1 : t + w;
-        for (long long j = a; j <= e; ++j) ws += seg[j - lo];
-        pooled[i] = ws / (float)(e - a + 1);
+        const long long e0 = t - w < 0 ? 0 : t - w, e1 = t + w > N - 1 ? N - 1 : t + w;
+        for (long long j = e0; j <= e1; ++j) ws += seg[j - lo];
+        pooled[i] = ws / (float)(e1 - e0 + 1);
       }
     }
     __syncthreads();
     const long long c_first = base / chunk, c_last = (base + len - 1) / chunk;
-    if (warp_chunks && base % chunk == 0) {
+    if (warp_chunks) {
       // a warp sums 32 consecutive pooled values in groups of `chunk` lanes (tree
-      // order); segcap is a multiple of 32 so every chunk starts inside its segment
+      // order); segments start on chunk boundaries and hold whole chunks
       const int lg = __ffs(chunk) - 1;
-      const int cbase = (int)(base >> lg);
+      const long long cb = (base >> lg) - c_base;
 #pragma unroll 4
       for (int g0 = warp * 32; g0 < len; g0 += ST) {
         float v = g0 + lane < len ? pooled[g0 + lane] : 0.f;
         for (int o = chunk >> 1; o >= 1; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, chunk);
-        if ((lane & (chunk - 1)) == 0 && g0 + lane < len) cs[cbase + ((g0 + lane) >> lg)] = v;
+        if ((lane & (chunk - 1)) == 0 && g0 + lane < len) cs[cb + ((g0 + lane) >> lg)] = v;
       }
     } else {
       // the owner thread walks its chunk's tokens in a rotated (fixed, hence
@@ -174,36 +269,38 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
       for (long long c = c_first + tid; c <= c_last; c += ST) {
         const long long t0 = c * chunk > base ? c * chunk : base;
         const long long t1 = (c + 1) * chunk < base + len ? (c + 1) * chunk : base + len;
-        const int n = (int)(t1 - t0), i0 = (int)(t0 - base);
-        float sacc = (t0 == c * chunk) ? 0.f : cs[c];                    // chunk continued from the previous segment
+        const int n = (int)(t1 - t0), ii = (int)(t0 - base);
+        float sacc = (t0 == c * chunk) ? 0.f : cs[c - c_base];          // chunk continued from the previous segment
         const int rot = (int)(c % n);
         for (int j = 0; j < n; ++j) {
           int k = j + rot;
           if (k >= n) k -= n;
-          sacc += pooled[i0 + k];
+          sacc += pooled[ii + k];
         }
-        cs[c] = sacc;
+        cs[c - c_base] = sacc;
       }
     }
     __syncthreads();
+    base += len;
   }
   for (long long c = c_lo + tid; c < c_hi; c += ST) {
     const long long sz = ((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk;
-    cs[c] = cs[c] / (float)sz;
+    cs[c - c_base] = cs[c - c_base] / (float)sz;
   }
   __syncthreads();
   }
   if (mode == kModeA) return;
 
-  // ---- B. radix select: threshold bit pattern T of the K_c-th largest score.
+  // ---- B. radix select: threshold bit pattern T of the K_sel-th largest score.
   //      Up to kRankMax chunks the rank is counted directly instead:
   //      rank(c) = #{c' : cs[c'] > cs[c], or cs[c'] == cs[c] and c' < c} (the
-  //      (score desc, index asc) order), kept iff rank < K_c -- one pass, no
+  //      (score desc, index asc) order), kept iff rank < K_sel -- one pass, no
   //      barrier rounds (measured: 2 us faster at 128 chunks, 29 us slower at 1024).
+  //      kMerge: invalid entries (bit pattern kInvalid, a NaN) never count.
   constexpr int kRankMax = 256;
   const bool by_rank = n_c <= kRankMax;
   unsigned prefix = 0, pmask = 0;
-  unsigned remaining = (unsigned)K_c;
+  unsigned remaining = (unsigned)K_sel;
   int rank_keep = 0;
   if (by_rank) {
     if (tid < n_c) {
@@ -214,7 +311,8 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
         const float o = cs[c2];                      // same address in every lane: broadcast
         rank += (o > mine || (o == mine && c2 < tid)) ? 1 : 0;
       }
-      rank_keep = rank < K_c ? 1 : 0;
+      rank_keep = rank < K_sel ? 1 : 0;
+      if (V == kMerge && __float_as_uint(mine) == kInvalid) rank_keep = 0;
     }
   }
   for (int shift = 24; shift >= 0 && !by_rank; shift -= 8) {
@@ -225,7 +323,8 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
     for (long long c0 = (long long)warp * 32; c0 < n_c; c0 += ST) {
       const long long c = c0 + lane;
       const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
-      const unsigned digit = (c < n_c && (key & pmask) == prefix) ? (key >> shift) & 255u : 256u;
+      const bool in = c < n_c && (V != kMerge || key != kInvalid);
+      const unsigned digit = (in && (key & pmask) == prefix) ? (key >> shift) & 255u : 256u;
       const unsigned peers = __match_any_sync(0xffffffffu, digit);
       if (digit < 256u && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], (unsigned)__popc(peers));
     }
@@ -266,21 +365,32 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
   const unsigned T = prefix;
   const int need_eq = (int)remaining;            // chunks equal to T to keep (lowest indices first)
 
-  // ---- C. keep flags in chunk order, compaction (+ gather) of the kept token ranges
-  int carry_eq = 0, carry_tok = 0;
-  const int* tokens = tokens_all ? tokens_all + (long long)b * Nrow : nullptr;
-  int* out = out_all ? out_all + (long long)b * Nrow : nullptr;
+  // ---- C. keep flags in chunk order, compaction (+ gather) of the kept token
+  //      ranges, or (kCand) the kept chunks' candidate keys
+  int carry_eq = 0, carry_tok = 0, carry_k = 0;
+  const int* tokens = a.tokens ? a.tokens + (long long)b * Nrow : nullptr;
+  int* out = a.out ? a.out + (long long)b * Nrow : nullptr;
+  int* ids = a.ids + (long long)b * Nrow;
+  int* pos = a.pos + (long long)b * Nrow;
   for (long long base = 0; base < n_c; base += ST) {
     const long long c = base + tid;
     const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
-    const int eq = (c < n_c && key == T) ? 1 : 0;
-    const int gt = (c < n_c && key > T) ? 1 : 0;
+    const bool in = c < n_c && (V != kMerge || key != kInvalid);
+    const int eq = (in && key == T) ? 1 : 0;
+    const int gt = (in && key > T) ? 1 : 0;
     int tot;
     const int eq_rank = block_excl_scan(eq, scan, &tot) + carry_eq;
     carry_eq += tot;
     const int keep = by_rank ? rank_keep : (gt | (eq & (eq_rank < need_eq ? 1 : 0)));
     const int slot = block_excl_scan(keep, scan, &tot);          // index among kept chunks of this tile
     const int nk = tot;
+    if (V == kCand) {
+      if (keep)
+        a.cand[(long long)b * K_sel + carry_k + slot] =
+            ((unsigned long long)key << 32) | (unsigned long long)(~(unsigned)(c + c_base));
+      carry_k += nk;
+      continue;
+    }
     int sz = 0;
     if (keep) sz = (int)(((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk);
     int tot2;
@@ -298,14 +408,70 @@ __global__ void __launch_bounds__(ST) k_select(const float* __restrict__ imp_all
       const int o = kept_off[k];
       for (int j = lane; j < csz; j += 32) {
         ids[o + j] = t0 + j;
-        pos[o + j] = t0 + j + pos0;
+        pos[o + j] = t0 + j + a.pos0;
         if (out) out[o + j] = tokens[t0 + j];
       }
     }
     carry_tok += tot2;
     __syncthreads();
   }
-  if (tid == 0) n_kept[b] = carry_tok;
+  if (V != kCand && tid == 0) a.n_kept[b] = carry_tok;
+}
+
+__global__ void k_seq_edges(const float* __restrict__ imp, long long n, int w, float* __restrict__ edges) {
+  const int b = blockIdx.x;
+  for (int j = threadIdx.x; j < 2 * w; j += blockDim.x)
+    edges[(long long)b * 2 * w + j] = imp[(long long)b * n + (j < w ? j : n - 2 * w + j)];
+}
+
+constexpr size_t kSmemMax = (size_t)(2 * SEG + 2 * ((kMaxPool - 1) / 2) + kSmemChunks) * sizeof(float);
+
+// The >48 KiB dynamic-SMEM opt-in is a per-device function attribute: set it
+// once per (device, variant).
+template <int V>
+cudaError_t configure() {
+  static bool done[64][1] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!done[dev][0]) {
+    e = cudaFuncSetAttribute(k_select<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+    if (e != cudaSuccess) return e;
+    done[dev][0] = true;
+  }
+  return cudaSuccess;
+}
+
+// Phase A over `nblk` blocks of cpb chunks of each request (kModeA) then B-C
+// (kModeBC) for long ranges; one kModeAll launch otherwise.
+template <int V>
+cudaError_t launch_select(SelArgs a, int B, long long n_tok, long long n_chunks, cudaStream_t st) {
+  cudaError_t e = configure<V>();
+  if (e != cudaSuccess) return e;
+  const long long w = (a.pool_k - 1) / 2;
+  const int chunk = a.chunk;
+  constexpr long long kTokPerCta = 2048;
+  const long long cpb = std::max(1LL, kTokPerCta / chunk);
+  const long long nblk = (n_chunks + cpb - 1) / cpb;
+  if (V != kMerge && nblk >= 4 && nblk <= 65535) {
+    const long long span = std::min(n_tok, cpb * chunk);
+    a.segcap = chunk > SEG ? SEG : (int)std::min<long long>(SEG, (span + 31) / 32 * 32);
+    a.cpb = cpb;
+    a.mode = kModeA;
+    const size_t needA = (size_t)(2 * a.segcap + 2 * w) * sizeof(float);
+    k_select<V><<<dim3(B, (unsigned)nblk), ST, needA, st>>>(a);
+    a.mode = kModeBC;
+    const size_t needBC = (size_t)(2 * a.segcap + 2 * w + (n_chunks <= kSmemChunks ? n_chunks : 0)) * sizeof(float);
+    k_select<V><<<B, ST, needBC, st>>>(a);
+    return cudaGetLastError();
+  }
+  a.segcap = SEG;
+  a.cpb = n_chunks;
+  a.mode = kModeAll;
+  const size_t need = (size_t)(2 * SEG + 2 * w + (n_chunks <= kSmemChunks ? n_chunks : 0)) * sizeof(float);
+  k_select<V><<<B, ST, need, st>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -320,36 +486,53 @@ bool select_supported(int pool_k) { return pool_k <= kMaxPool; }
 cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int chunk, int pos0, long long ppm,
                           int* ids, int* pos, int* n_kept, void* ws, cudaStream_t st, const int* tokens, int* out,
                           const int* seq_lens) {
-  static bool configured = false;
-  const size_t smem_max = (size_t)(2 * SEG + 2 * ((kMaxPool - 1) / 2) + kSmemChunks) * sizeof(float);
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  SelArgs a{};
+  a.imp = imp; a.row = N; a.seq_lens = seq_lens; a.pool_k = pool_k; a.chunk = chunk; a.pos0 = pos0; a.ppm = ppm;
+  a.ids = ids; a.pos = pos; a.n_kept = n_kept; a.cs_ws = reinterpret_cast<float*>(ws); a.tokens = tokens; a.out = out;
+  a.n_glob = N;
+  return launch_select<kPlain>(a, B, N, (N + chunk - 1) / chunk, st);
+}
+
+long long seq_candidate_count(long long N, int world, int chunk, long long ppm) {
   const long long n_c = (N + chunk - 1) / chunk;
-  const long long w = (pool_k - 1) / 2;
-  float* cs = reinterpret_cast<float*>(ws);
-  // Long prompts: phase A (pooling + chunk sums, the bulk of the work) on
-  // ~kTokPerCta-token blocks of chunks spread over the SMs, then B-C per request.
-  constexpr long long kTokPerCta = 2048;
-  const long long cpb = std::max(1LL, kTokPerCta / chunk);
-  const long long nblk = (n_c + cpb - 1) / cpb;
-  if (nblk >= 4 && nblk <= 65535) {
-    const long long span = std::min(N, cpb * chunk);
-    const int segcap = (int)std::min<long long>(SEG, (span + 31) / 32 * 32);
-    const size_t needA = (size_t)(2 * segcap + 2 * w) * sizeof(float);
-    k_select<<<dim3(B, (unsigned)nblk), ST, needA, st>>>(imp, N, seq_lens, pool_k, chunk, pos0, ppm, ids, pos, n_kept, cs, tokens,
-                                                        out, kModeA, segcap, cpb);
-    const size_t needBC = (size_t)(2 * segcap + 2 * w + (n_c <= kSmemChunks ? n_c : 0)) * sizeof(float);
-    k_select<<<B, ST, needBC, st>>>(imp, N, seq_lens, pool_k, chunk, pos0, ppm, ids, pos, n_kept, cs, tokens, out, kModeBC,
-                                    segcap, cpb);
-    return cudaGetLastError();
-  }
-  const size_t need = (size_t)(2 * SEG + 2 * w + (n_c <= kSmemChunks ? n_c : 0)) * sizeof(float);
-  k_select<<<B, ST, need, st>>>(imp, N, seq_lens, pool_k, chunk, pos0, ppm, ids, pos, n_kept, cs, tokens, out, kModeAll, SEG,
-                                n_c);
+  const long long K_c = std::min(n_c, std::max(1LL, (ppm * n_c + 999999) / 1000000));
+  return std::min(K_c, n_c / world);
+}
+
+size_t seq_select_ws_bytes(int B, long long N, int world, int chunk) {
+  // kCand: the shard's chunk scores; kMerge: the prompt's (when above the SMEM limit)
+  (void)world;
+  return select_ws_bytes(B, N, chunk);
+}
+
+cudaError_t seq_edges_launch(const float* imp_local, int B, long long n_local, int pool_k, float* edges,
+                             cudaStream_t st) {
+  const int w = (pool_k - 1) / 2;
+  if (w == 0) return cudaSuccess;
+  k_seq_edges<<<B, 256, 0, st>>>(imp_local, n_local, w, edges);
   return cudaGetLastError();
+}
+
+cudaError_t seq_candidates_launch(const float* imp_local, const float* edges, int rank, int world, int B,
+                                  long long N, int pool_k, int chunk, long long M, unsigned long long* cand, void* ws,
+                                  cudaStream_t st) {
+  const long long n_local = N / world;
+  SelArgs a{};
+  a.imp = imp_local; a.row = n_local; a.pool_k = pool_k; a.chunk = chunk;
+  a.ids = nullptr; a.pos = nullptr; a.cs_ws = reinterpret_cast<float*>(ws);
+  a.i0 = (long long)rank * n_local; a.n_glob = N; a.edges = edges; a.rank = rank; a.world = world;
+  a.k_sel = M; a.cand = cand;
+  return launch_select<kCand>(a, B, n_local, n_local / chunk, st);
+}
+
+cudaError_t seq_merge_launch(const unsigned long long* cand_all, int world, int B, long long N, int pool_k, int chunk,
+                             int pos0, long long ppm, long long M, const int* tokens, int* ids, int* pos, int* n_kept,
+                             int* out, void* ws, cudaStream_t st) {
+  SelArgs a{};
+  a.row = N; a.pool_k = pool_k; a.chunk = chunk; a.pos0 = pos0; a.ppm = ppm;
+  a.ids = ids; a.pos = pos; a.n_kept = n_kept; a.cs_ws = reinterpret_cast<float*>(ws); a.tokens = tokens; a.out = out;
+  a.n_glob = N; a.world = world; a.k_sel = M; a.cand_in = cand_all;
+  return launch_select<kMerge>(a, B, N, (N + chunk - 1) / chunk, st);
 }
 
 }  // namespace sp

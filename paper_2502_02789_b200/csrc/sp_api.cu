@@ -68,6 +68,7 @@ sp_status check_layout(const sp_geom* g, const sp_layout* l, const void* Q, cons
     if (ks[i] < 0 || qs[i] < 0) return SP_EINVAL;
     if (kn[i] > 1 && (ks[i] * esz) % 16 != 0) return SP_EINVAL;   // TMA: strides multiple of 16 B
     if (qn[i] > 1 && (qs[i] * esz) % 16 != 0) return SP_EINVAL;
+    if ((kn[i] > 1 && ks[i] == 0) || (qn[i] > 1 && qs[i] == 0)) return SP_EINVAL;   // no broadcast (stride-0) dims
   }
   if (l->k_i < g->d && g->N > 1) return SP_EINVAL;               // rows of one head may not overlap
   if (!aligned16(Q) || !aligned16(K)) return SP_EINVAL;
@@ -360,8 +361,10 @@ static sp_status score_paged_impl(const void* Q, const sp_paged_k* K, const sp_g
   }
   // Q strides: reuse the contiguous-layout check with a dummy K view of the same geometry
   sp_layout ql = *lay;
-  ql.k_b = ql.k_l = ql.k_g = 0;
   ql.k_i = g->d;
+  ql.k_g = ql.k_i * g->N;
+  ql.k_l = ql.k_g * g->Hkv;
+  ql.k_b = ql.k_l * g->L;
   if ((s = check_layout(g, &ql, Q, K->cache, esz)) != SP_OK) return s;
   if ((s = check_device()) != SP_OK) return s;
   const Layout Lay = to_layout(*lay);
@@ -542,6 +545,67 @@ sp_status sp_select_ragged(const float* importance, const int32_t* seq_lens, con
   if (ws == nullptr || ws_bytes < select_ws_bytes(B, N, p->chunk)) return SP_EWORKSPACE;
   return from_cuda(select_launch(importance, B, N, p->pool_k, p->chunk, p->pos0, keep_ppm(p->keep_rate), ids, pos,
                                  n_kept, ws, reinterpret_cast<cudaStream_t>(stream), tokens, out_tokens, seq_lens));
+}
+
+namespace {
+sp_status check_seq(int32_t B, int64_t N, int32_t world, const sp_select_params* p) {
+  sp_status s = check_select(B, N, p);
+  if (s != SP_OK) return s;
+  if (world < 1 || N % world != 0) return SP_EINVAL;
+  const int64_t n = N / world;
+  if (n % p->chunk != 0 || (p->pool_k - 1) / 2 > n) return SP_EINVAL;
+  return SP_OK;
+}
+}  // namespace
+
+int64_t sp_seq_candidate_count(int64_t N, int32_t world, const sp_select_params* p) {
+  if (check_seq(1, N, world, p) != SP_OK) return -1;
+  return seq_candidate_count(N, world, p->chunk, keep_ppm(p->keep_rate));
+}
+
+size_t sp_seq_select_workspace_bytes(int32_t B, int64_t N, int32_t world, const sp_select_params* p) {
+  if (check_seq(B, N, world, p) != SP_OK) return 0;
+  return seq_select_ws_bytes(B, N, world, p->chunk);
+}
+
+sp_status sp_seq_edges(const float* imp_local, int32_t B, int64_t N, int32_t world, const sp_select_params* p,
+                       float* edges, sp_stream stream) {
+  sp_status s = check_seq(B, N, world, p);
+  if (s != SP_OK) return s;
+  if (imp_local == nullptr || (edges == nullptr && p->pool_k > 1)) return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
+  return from_cuda(seq_edges_launch(imp_local, B, N / world, p->pool_k, edges, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sp_status sp_seq_candidates(const float* imp_local, const float* edges_all, int32_t rank, int32_t world, int32_t B,
+                            int64_t N, const sp_select_params* p, uint64_t* cand, void* ws, size_t ws_bytes,
+                            sp_stream stream) {
+  sp_status s = check_seq(B, N, world, p);
+  if (s != SP_OK) return s;
+  if (rank < 0 || rank >= world || imp_local == nullptr || cand == nullptr) return SP_EINVAL;
+  if (edges_all == nullptr && p->pool_k > 1 && world > 1) return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
+  if (ws == nullptr || ws_bytes < seq_select_ws_bytes(B, N, world, p->chunk)) return SP_EWORKSPACE;
+  const long long M = seq_candidate_count(N, world, p->chunk, keep_ppm(p->keep_rate));
+  return from_cuda(seq_candidates_launch(imp_local, edges_all, rank, world, B, N, p->pool_k, p->chunk, M,
+                                         reinterpret_cast<unsigned long long*>(cand), ws,
+                                         reinterpret_cast<cudaStream_t>(stream)));
+}
+
+sp_status sp_seq_merge(const uint64_t* cand_all, int32_t world, int32_t B, int64_t N, const sp_select_params* p,
+                       const int32_t* tokens, int32_t* ids, int32_t* pos, int32_t* n_kept, int32_t* out_tokens,
+                       void* ws, size_t ws_bytes, sp_stream stream) {
+  sp_status s = check_seq(B, N, world, p);
+  if (s != SP_OK) return s;
+  if (cand_all == nullptr || ids == nullptr || pos == nullptr || n_kept == nullptr) return SP_EINVAL;
+  if ((tokens == nullptr) != (out_tokens == nullptr)) return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
+  if (ws == nullptr || ws_bytes < seq_select_ws_bytes(B, N, world, p->chunk)) return SP_EWORKSPACE;
+  const long long ppm = keep_ppm(p->keep_rate);
+  const long long M = seq_candidate_count(N, world, p->chunk, ppm);
+  return from_cuda(seq_merge_launch(reinterpret_cast<const unsigned long long*>(cand_all), world, B, N, p->pool_k,
+                                    p->chunk, p->pos0, ppm, M, tokens, ids, pos, n_kept, out_tokens, ws,
+                                    reinterpret_cast<cudaStream_t>(stream)));
 }
 
 sp_status sp_gather(const int32_t* tokens, const int32_t* ids, const int32_t* n_kept, int32_t B, int64_t N,

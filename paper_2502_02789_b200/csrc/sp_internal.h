@@ -115,6 +115,17 @@ bool select_supported(int pool_k);
 cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int chunk, int pos0,
                           long long ppm, int* ids, int* pos, int* n_kept, void* ws, cudaStream_t st,
                           const int* tokens = nullptr, int* out = nullptr, const int* seq_lens = nullptr);
+// sequence-sharded selection (row e)
+long long seq_candidate_count(long long N, int world, int chunk, long long ppm);
+size_t seq_select_ws_bytes(int B, long long N, int world, int chunk);
+cudaError_t seq_edges_launch(const float* imp_local, int B, long long n_local, int pool_k, float* edges,
+                             cudaStream_t st);
+cudaError_t seq_candidates_launch(const float* imp_local, const float* edges, int rank, int world, int B,
+                                  long long N, int pool_k, int chunk, long long M, unsigned long long* cand, void* ws,
+                                  cudaStream_t st);
+cudaError_t seq_merge_launch(const unsigned long long* cand_all, int world, int B, long long N, int pool_k, int chunk,
+                             int pos0, long long ppm, long long M, const int* tokens, int* ids, int* pos, int* n_kept,
+                             int* out, void* ws, cudaStream_t st);
 cudaError_t gather_launch(const int* tokens, const int* ids, const int* n_kept, int B, long long N, int* out,
                           cudaStream_t st);
 

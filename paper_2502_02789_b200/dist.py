@@ -12,16 +12,22 @@
 * Sequence sharding, single pass (seq_sharded_fused_specprefill) -- the fused
   kernel exchanges the per-unit softmax statistics itself over peer memory
   (torch symmetric memory buffers, NVLink stores; sp_score_peer), so each rank
-  reads its K shard once; then the importance all-gather and the selection.
+  reads its K shard once; then the sharded selection below.
 * Sequence sharding, split (seq_sharded_specprefill) -- one request's prompt split along tokens.  The only real
   exchange is the softmax statistics (the lse of every (layer, head, row) needs
   all N keys):
     1. local statistics (m2, l) per row            (sp_score_stats)
     2. all-gather, merged in rank order -> lse2     (sp_stats_combine; identical on every rank)
     3. local importance with the global lse2        (sp_score_finish)
-    4. all-gather of the importance shards (4 B/token) and the selection over
-       the whole prompt (sp_select_gather), so ids/positions are bit-identical
-       to the single-GPU path's for the same importance.
+    4. the sharded selection below.
+* Sequence-sharded selection (seq_sharded_select): the
+  importance vector is never gathered.  Each rank pools its own chunks (the
+  pooling windows reach (pool_k-1)/2 tokens into the neighbours: an all-gather
+  of every rank's edge values), takes its local top-min(K_c, n_c/P) chunks as
+  (score, chunk id) candidates, all-gathers them (8 B each) and every rank runs
+  the same global top-K_c merge (sp_seq_edges -> all_gather -> sp_seq_candidates
+  -> all_gather -> sp_seq_merge).  The ids/positions are bit-identical to
+  sp_select_gather on the concatenated importance.
 """
 from __future__ import annotations
 
@@ -72,13 +78,53 @@ class CudaBackend:
     def select(imp, keep, pool_k, chunk, pos0, tokens):
         return api.select(imp, keep, pool_k, chunk, pos0, tokens=tokens)
 
+    @staticmethod
+    def seq_edges(imp_local, world, N, keep, pool_k, chunk):
+        return api.seq_edges(imp_local, world, N, keep, pool_k, chunk)
+
+    @staticmethod
+    def seq_candidates(imp_local, edges_all, rank, world, N, keep, pool_k, chunk):
+        return api.seq_candidates(imp_local, edges_all, rank, world, N, keep, pool_k, chunk)
+
+    @staticmethod
+    def seq_merge(cand_all, world, N, keep, pool_k, chunk, pos0, tokens):
+        return api.seq_merge(cand_all, world, N, keep, pool_k, chunk, pos0, tokens=tokens)
+
+
+def _all_gather(x: torch.Tensor, group) -> torch.Tensor:
+    """[world][*x.shape] in rank order."""
+    world = dist.get_world_size(group)
+    out = torch.empty((world,) + tuple(x.shape), dtype=x.dtype, device=x.device)
+    if x.numel():
+        dist.all_gather_into_tensor(out.view(-1), x.contiguous().view(-1), group=group)
+    return out
+
+
+def seq_sharded_select(imp_local, N_total: int, keep: float, pool_k: int, chunk: int, pos0: int = 0, tokens=None,
+                       group=None, backend=None):
+    """Selection over a sequence-sharded importance vector (imp_local [B][N/P]
+    holds this rank's tokens, rank order = token order): edges all-gather,
+    local candidates, candidate all-gather, global merge.  Returns (ids, pos,
+    n_kept, out_tokens) for the whole prompt, identical on every rank; tokens
+    [B][N_total] replicated (or None)."""
+    be = backend or CudaBackend
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    edges = be.seq_edges(imp_local, world, N_total, keep, pool_k, chunk)              # [B][2w]
+    edges_all = _all_gather(edges, group)                                               # [P][B][2w]
+    cand = be.seq_candidates(imp_local, edges_all, rank, world, N_total, keep, pool_k, chunk)   # [B][M]
+    cand_all = _all_gather(cand, group)                                                 # [P][B][M]
+    r = be.seq_merge(cand_all, world, N_total, keep, pool_k, chunk, pos0, tokens)
+    return r if tokens is not None else (*r, None)
+
 
 def seq_sharded_specprefill(Q, K_local, tokens, N_total: int, keep: float, pool_k: int, chunk: int,
                             R_valid=None, scale=None, pos0: int = 0, group=None, backend=None) -> dict:
     """Sequence-sharded path for one request (B = 1).  Q [1][L][R][H][d] is
     replicated; K_local [1][L][Hkv][N_total/P][d] holds this rank's tokens
     (rank order = token order); tokens [1][N_total] int32 replicated.
-    Returns importance [1][N_total], ids, pos, n_kept, out_tokens (replicated)."""
+    Returns importance_local [1][N_total/P] and ids, pos, n_kept, out_tokens
+    for the whole prompt (identical on every rank)."""
     be = backend or CudaBackend
     world = dist.get_world_size(group)
     n_local = K_local.shape[3]
@@ -89,11 +135,9 @@ def seq_sharded_specprefill(Q, K_local, tokens, N_total: int, keep: float, pool_
     dist.all_gather_into_tensor(parts, stats.contiguous(), group=group)      # concatenated in rank order
     lse2 = be.stats_combine(parts.view(world, -1, 2))                        # [rows]
     imp_local = be.score_finish(Q, K_local, lse2, R_valid, scale)            # [1][n_local]
-    imp = torch.empty((world * n_local,), dtype=imp_local.dtype, device=imp_local.device)
-    dist.all_gather_into_tensor(imp, imp_local.reshape(-1).contiguous(), group=group)
-    imp = imp.view(1, N_total)                                               # rank order = token order
-    ids, pos, n_kept, out = be.select(imp, keep, pool_k, chunk, pos0, tokens)
-    return dict(importance=imp, ids=ids, pos=pos, n_kept=n_kept, out_tokens=out, first_decode=N_total + pos0)
+    ids, pos, n_kept, out = seq_sharded_select(imp_local, N_total, keep, pool_k, chunk, pos0, tokens, group, be)
+    return dict(importance_local=imp_local, ids=ids, pos=pos, n_kept=n_kept, out_tokens=out,
+                first_decode=N_total + pos0)
 
 
 def head_range(Hkv: int, world: int, rank: int) -> tuple[int, int]:
@@ -124,41 +168,46 @@ _PEER_CACHE: dict = {}
 
 
 def _peer_buffers(Q, K_local, R_valid, group):
-    """This rank's partial buffer in torch symmetric memory and every rank's
-    address of it (cached per geometry)."""
+    """This rank's partial buffer in torch symmetric memory, every rank's
+    address of it, and the launch workspace that goes with it (cached per
+    geometry, never evicted).  The workspace's launch epoch picks the half of
+    the partial buffers a launch writes, so both are created zeroed together
+    and live together: a fresh epoch never meets stale partials."""
     import torch.distributed._symmetric_memory as symm_mem
     world = dist.get_world_size(group)
-    key = (tuple(K_local.shape), tuple(Q.shape), R_valid, world, id(group))
+    key = (tuple(K_local.shape), tuple(Q.shape), R_valid, world, id(group), K_local.device.index)
     if key not in _PEER_CACHE:
         nbytes = api.score_peer_buffer_bytes(Q, K_local, world, 0, R_valid)
         buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=K_local.device)
         buf.zero_()
         pg = group if group is not None else dist.group.WORLD
         hdl = symm_mem.rendezvous(buf, pg.group_name)
+        ws = torch.zeros(max(256, api.score_peer_workspace_bytes(Q, K_local, 0, R_valid)), dtype=torch.uint8,
+                         device=K_local.device)
         torch.cuda.synchronize()
         dist.barrier(group)
-        _PEER_CACHE[key] = (buf, hdl, [int(x) for x in hdl.buffer_ptrs])
-    return _PEER_CACHE[key][2]
+        _PEER_CACHE[key] = (buf, hdl, [int(x) for x in hdl.buffer_ptrs], ws)
+    _, _, ptrs, ws = _PEER_CACHE[key]
+    return ptrs, ws
 
 
 def seq_sharded_fused_specprefill(Q, K_local, tokens, N_total: int, keep: float, pool_k: int, chunk: int,
                                   R_valid=None, scale=None, pos0: int = 0, group=None) -> dict:
     """Sequence-sharded single pass for one request (B = 1): the statistics
     exchange runs inside the fused kernel over peer memory (one K read per
-    rank); the importance all-gather that follows also separates consecutive
-    calls (sp_score_peer's barrier requirement)."""
+    rank); the edge all-gather of the sharded selection that follows also
+    separates consecutive calls (sp_score_peer's barrier requirement: no rank
+    starts the next launch before every rank's kernel finished)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     n_local = K_local.shape[3]
     if n_local * world != N_total or Q.shape[0] != 1:
         raise ValueError("K_local must hold N_total / world tokens of a single request")
-    ptrs = _peer_buffers(Q, K_local, R_valid, group)
-    imp_local = api.score_peer(Q, K_local, rank, world, ptrs, 0, R_valid, scale)
-    imp = torch.empty((world * n_local,), dtype=imp_local.dtype, device=imp_local.device)
-    dist.all_gather_into_tensor(imp, imp_local.reshape(-1).contiguous(), group=group)
-    imp = imp.view(1, N_total)
-    ids, pos, n_kept, out = api.select(imp, keep, pool_k, chunk, pos0, tokens=tokens)
-    return dict(importance=imp, ids=ids, pos=pos, n_kept=n_kept, out_tokens=out, first_decode=N_total + pos0)
+    ptrs, ws = _peer_buffers(Q, K_local, R_valid, group)
+    imp_local = api.score_peer(Q, K_local, rank, world, ptrs, 0, R_valid, scale, ws=ws)
+    ids, pos, n_kept, out = seq_sharded_select(imp_local, N_total, keep, pool_k, chunk, pos0, tokens, group)
+    return dict(importance_local=imp_local, ids=ids, pos=pos, n_kept=n_kept, out_tokens=out,
+                first_decode=N_total + pos0)
 
 
 def batch_sharded_specprefill(Q, K, tokens, keep, pool_k, chunk, R_valid=None, scale=None, pos0=0) -> dict:

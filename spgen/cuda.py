@@ -24,7 +24,8 @@ def _lib():
         h.spgen_fill_K.argtypes = [V, L, L, L, L, I, I, I, I, L, L, L, U, V, I, V, I, I, V]
         h.spgen_fill_Q.argtypes = [V, L, L, L, L, I, I, I, I, I, I, U, I, V]
         h.spgen_fill_tokens.argtypes = [V, I, L, U, V]
-        for f in (h.spgen_fill_K, h.spgen_fill_Q, h.spgen_fill_tokens):
+        h.spgen_read_stream.argtypes = [V, L, I, V, V]
+        for f in (h.spgen_fill_K, h.spgen_fill_Q, h.spgen_fill_tokens, h.spgen_read_stream):
             f.restype = C.c_int
         _h = h
     return _h
@@ -86,3 +87,27 @@ def make_inputs(w: gen.Workload, device="cuda", i0: int = 0, n_local: int | None
     fill_K(K, w, i0)
     fill_tokens(tok, w)
     return Q, K, tok
+
+
+def read_stream_gbs(device, nbytes: int = 2 << 30, reps: int = 10) -> dict:
+    """Measured HBM read-only streaming rate (bench's second roofline
+    denominator): the best of `reps` passes over an nbytes buffer, for the TMA
+    bulk-copy probe and the 128-bit load probe (spgen/probe.cu)."""
+    buf = torch.ones(nbytes // 4, dtype=torch.int32, device=device)
+    sink = torch.zeros(1, dtype=torch.int32, device=device)
+    out = {}
+    for mode, name in ((0, "tma_bulk"), (1, "ld_v4")):
+        best = None
+        for _ in range(reps + 2):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            rc = _lib().spgen_read_stream(buf.data_ptr(), nbytes, mode, sink.data_ptr(), _stream())
+            b.record()
+            b.synchronize()
+            if rc:
+                raise RuntimeError(f"spgen_read_stream failed ({rc})")
+            ms = a.elapsed_time(b)
+            best = ms if best is None else min(best, ms)
+        out[name] = nbytes / (best / 1000.0) / 1e9
+    del buf
+    return out

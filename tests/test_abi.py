@@ -92,6 +92,45 @@ def test_score_layout_validation():
     assert sp.lib().sp_score(FAKE, FAKE, None, C.byref(lay), FAKE, FAKE, 1 << 20, None) == _lib.SP_EINVAL
 
 
+@pytest.mark.parametrize("field", ["k_b", "k_l", "k_g", "q_b", "q_l", "q_r", "q_h"])
+def test_broadcast_strides_rejected(field):
+    """A stride-0 (broadcast, e.g. K.expand(B, ...)) dimension of size > 1 is
+    rejected on the host for every algorithm (the TMA tensor maps cannot
+    express it); stride 0 on a size-1 dimension is irrelevant and accepted."""
+    g = _geom(B=2)
+    lay = _layout(g)
+    setattr(lay, field, 0)
+    for algo in (_lib.SP_SCORE_FUSED, _lib.SP_SCORE_SIMT, _lib.SP_SCORE_AUTO):
+        assert sp.lib().sp_score_ex(FAKE, FAKE, C.byref(g), C.byref(lay), FAKE, FAKE, 1 << 20, algo, None) \
+            == _lib.SP_EINVAL
+    g1 = _geom(B=1)
+    lay1 = _layout(g1)
+    lay1.k_b = lay1.q_b = 0
+    rc = sp.lib().sp_score_ex(FAKE, FAKE, C.byref(g1), C.byref(lay1), FAKE, FAKE, 1 << 20, _lib.SP_SCORE_SIMT, None)
+    assert rc != _lib.SP_EINVAL
+
+
+def test_seq_select_validation():
+    """Sequence-sharded select: N divisible by the ranks, shards made of whole
+    chunks, pooling half-window within one shard; M = min(K_c, n_c / P)."""
+    L = sp.lib()
+    p = _lib.sp_select_params(keep_rate=0.1, pool_k=5, chunk=32, pos0=0)
+    assert L.sp_seq_candidate_count(131072, 8, C.byref(p)) == 410
+    assert L.sp_seq_candidate_count(32768, 8, C.byref(p)) == 103
+    p9 = _lib.sp_select_params(keep_rate=0.9, pool_k=5, chunk=32, pos0=0)
+    assert L.sp_seq_candidate_count(131072, 8, C.byref(p9)) == 512          # keep >= 1/P: every chunk
+    assert L.sp_seq_candidate_count(1000, 3, C.byref(p)) == -1                # N % P != 0
+    assert L.sp_seq_candidate_count(3000, 3, C.byref(p)) == -1                # shard not whole chunks
+    pw = _lib.sp_select_params(keep_rate=0.1, pool_k=41, chunk=1, pos0=0)
+    assert L.sp_seq_candidate_count(128, 8, C.byref(pw)) == -1                # w = 20 > 16 tokens per shard
+    assert L.sp_seq_select_workspace_bytes(1, 1000, 3, C.byref(p)) == 0
+    assert L.sp_seq_select_workspace_bytes(2, 131072, 8, C.byref(p)) >= 2 * 4096 * 4
+    assert L.sp_seq_candidates(FAKE, FAKE, 8, 8, 1, 131072, C.byref(p), FAKE, FAKE, 1 << 20, None) == _lib.SP_EINVAL
+    assert L.sp_seq_merge(None, 8, 1, 131072, C.byref(p), None, FAKE, FAKE, FAKE, None, FAKE, 1 << 20, None) \
+        == _lib.SP_EINVAL
+    assert L.sp_seq_edges(FAKE, 1, 1000, 3, C.byref(p), FAKE, None) == _lib.SP_EINVAL
+
+
 @pytest.mark.parametrize("keep,pool,chunk,code", [
     (0.0, 3, 4, _lib.SP_EINVAL), (1.01, 3, 4, _lib.SP_EINVAL), (float("nan"), 3, 4, _lib.SP_EINVAL),
     (0.5, 2, 4, _lib.SP_EINVAL), (0.5, 0, 4, _lib.SP_EINVAL), (0.5, 3, 0, _lib.SP_EINVAL),

@@ -74,6 +74,55 @@ class OracleBackend:
         ids = torch.tensor(r["ids"])[None]
         return ids, ids + pos0, torch.tensor([r["n_kept"]]), torch.tensor(ref.gather(tokens[0].numpy(), r["ids"]))[None]
 
+    # sequence-sharded selection, restated with the oracle's O5-O9 on one shard
+    @staticmethod
+    def seq_edges(imp_local, world, N, keep, pool_k, chunk):
+        w = (pool_k - 1) // 2
+        n = imp_local.shape[1]
+        return torch.cat([imp_local[:, :w], imp_local[:, n - w:]], dim=1)
+
+    @staticmethod
+    def seq_candidates(imp_local, edges_all, rank, world, N, keep, pool_k, chunk):
+        """Local pooled chunk scores (windows completed with the neighbours'
+        edges) and the local top-min(K_c, n_c/P) chunks as (global id, score)."""
+        w = (pool_k - 1) // 2
+        n = imp_local.shape[1]
+        K_c = ref.kept_chunk_count(-(-N // chunk), keep)
+        M = min(K_c, n // chunk)
+        out = []
+        for b in range(imp_local.shape[0]):
+            parts = [imp_local[b].numpy()]
+            if rank > 0:
+                parts.insert(0, edges_all[rank - 1, b, w:].numpy())
+            if rank + 1 < world:
+                parts.append(edges_all[rank + 1, b, :w].numpy())
+            ext = np.concatenate(parts)                                 # the array's ends are true sequence ends
+            off = w if rank > 0 else 0
+            cs = ref.chunk_scores(ref.smooth_scores(ext, pool_k)[off:off + n], chunk)
+            kept = ref.select_chunks(cs, M)
+            out.append(np.stack([kept + rank * (n // chunk), cs[kept]], axis=1))
+        return torch.tensor(np.stack(out))                              # [B][M][2]
+
+    @staticmethod
+    def seq_merge(cand_all, world, N, keep, pool_k, chunk, pos0, tokens):
+        n_c = -(-N // chunk)
+        K_c = ref.kept_chunk_count(n_c, keep)
+        B = cand_all.shape[1]
+        ids_all = torch.zeros((B, N), dtype=torch.int64)
+        nk = torch.zeros(B, dtype=torch.int64)
+        outs = torch.zeros((B, N), dtype=torch.int64)
+        for b in range(B):
+            cs = np.full(n_c, -np.inf)
+            c = cand_all[:, b].reshape(-1, 2).numpy()
+            cs[c[:, 0].astype(np.int64)] = c[:, 1]
+            kept = ref.select_chunks(cs, K_c)
+            ids, _, _ = ref.restore_position_ids(kept, chunk, N, pos0)
+            ids_all[b, :len(ids)] = torch.tensor(ids)
+            nk[b] = len(ids)
+            if tokens is not None:
+                outs[b, :len(ids)] = torch.tensor(ref.gather(tokens[b].numpy(), ids))
+        return ids_all, ids_all + pos0, nk, outs
+
 
 def _free_port():
     s = socket.socket()
@@ -103,7 +152,8 @@ def _worker(rank, world, port, w, outq, mode="seq"):
             K = torch.tensor(ref.bf16_to_f64(Kb[:, :, g0:g1]))
             r = spd.head_sharded_specprefill(Q, K, torch.tensor(tok), w.keep, w.pool_k, w.chunk, w.Rv, w.scale,
                                              w.pos0, backend=OracleBackend)
-        outq.put((rank, r["importance"].numpy(), r["ids"].numpy(), int(r["n_kept"][0]), r["out_tokens"].numpy()))
+        imp = r["importance_local"] if mode == "seq" else r["importance"]
+        outq.put((rank, imp.numpy(), r["ids"].numpy(), int(r["n_kept"][0]), r["out_tokens"].numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -132,10 +182,79 @@ def test_sharded_choreography_gloo(world, mode):
     Qb, Kb, tok = gen.gen_batch(w)
     o = ref.specprefill(Qb[0], Kb[0], tok[0], w.scale, w.keep, w.pool_k, w.chunk, w.Rv, w.pos0)
     for rank, imp, ids, n, out in res:
-        np.testing.assert_allclose(imp[0], o["imp"], rtol=1e-12)
+        i0, i1 = (rank * w.N // world, (rank + 1) * w.N // world) if mode == "seq" else (0, w.N)
+        np.testing.assert_allclose(imp[0], o["imp"][i0:i1], rtol=1e-12)
         assert n == o["n_kept"]
         np.testing.assert_array_equal(ids[0][:n], o["ids"])
         np.testing.assert_array_equal(out[0][:n], o["out_tokens"])
+
+
+def _select_worker(rank, world, port, N, cases, outq):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ.setdefault("GLOO_SOCKET_IFNAME", "lo")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2502_02789_b200 import dist as spd
+        res = []
+        for (imp, keep, pool_k, chunk, pos0) in cases:
+            i0, i1 = spd.token_range(N, world, rank)
+            tok = torch.tensor(np.arange(N, dtype=np.int64) * 7 + 3)[None]
+            ids, pos, nk, out = spd.seq_sharded_select(torch.tensor(imp[None, i0:i1]), N, keep, pool_k, chunk, pos0,
+                                                       tok, backend=OracleBackend)
+            n = int(nk[0])
+            res.append((ids[0, :n].numpy(), pos[0, :n].numpy(), out[0, :n].numpy()))
+        outq.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def _seq_select_cases(N, world):
+    """Importance vectors whose chunk scores tie across ranks (dyadic values:
+    float64 sums are exact), over keep rates below and above 1/P."""
+    rng = np.random.default_rng(5)
+    cases = []
+    for chunk, pool_k in [(8, 5), (4, 1), (16, 9), (1, 3)]:
+        n_c = N // chunk
+        per = rng.integers(1, 6, size=n_c // world)                      # chunk level pattern, repeated per rank
+        lev = np.tile(per, world).astype(np.float64)
+        imp = np.repeat(lev, chunk) / 8.0                                 # constant chunks: ties across ranks
+        for keep in (0.1, 1.0 / world, 0.5, 0.9):
+            cases.append((imp, keep, pool_k, chunk, 11))
+        noisy = imp + rng.integers(0, 3, size=N) / 64.0                   # near-ties, still dyadic
+        cases.append((noisy, 0.3, pool_k, chunk, 0))
+    return cases
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_seq_sharded_select_gloo(world):
+    """Row e: edges all-gather -> local top-min(K_c,
+    n_c/P) candidates -> candidate all-gather -> global merge gives exactly the
+    oracle's whole-prompt selection on every rank, including chunk-score ties
+    across ranks (lowest index wins) and keep rates >= 1/P."""
+    N = 256
+    cases = _seq_select_cases(N, world)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_select_worker, args=(r, world, port, N, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        res = dict(q.get(timeout=240) for _ in range(world))    # drain before join (large queue items)
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    assert [p.exitcode for p in procs] == [0] * world
+    for k, (imp, keep, pool_k, chunk, pos0) in enumerate(cases):
+        o = ref.select(imp, keep, pool_k, chunk, pos0)
+        for rank in range(world):
+            ids, pos, out = res[rank][k]
+            np.testing.assert_array_equal(ids, o["ids"], err_msg=f"case {k} rank {rank}")
+            np.testing.assert_array_equal(pos, o["pos"])
+            np.testing.assert_array_equal(out, o["ids"] * 7 + 3)
 
 
 def test_ranges():
