@@ -142,24 +142,26 @@ sp_status sp_score_ex(const void* Q, const void* K, const sp_geom* g, const sp_l
                       float* importance, void* ws, size_t ws_bytes, int algo, sp_stream stream);
 
 /* Launch plan of the fused kernel for g on the current device (for reports
- * and tests): out[0..8] = grid, jobs per request, token groups, unit groups,
+ * and tests): out[0..9] = grid, jobs per request, token groups, unit groups,
  * tiles per job, units per job, TMEM unit slots, SMEM pipeline stages,
- * dynamic SMEM bytes.  Returns SP_EUNSUPPORTED if the fused kernel cannot run g. */
-sp_status sp_score_plan(const sp_geom* g, int64_t out[9]);
+ * dynamic SMEM bytes, hierarchical exchange (0: every CTA of a unit polls the
+ * unit's n_tg partial words; 1: the unit's last CTA merges them and the others
+ * poll one word).  Returns SP_EUNSUPPORTED if the fused kernel cannot run g. */
+sp_status sp_score_plan(const sp_geom* g, int64_t out[10]);
 
 /* Measured plan choice.  sp_score_tune times the fused kernel's best model
  * candidates (token groups x unit groups; at most 6, within 1.3x of the model's
  * best) on this device with private workspaces (allocated and freed inside the
  * call: not for the hot path; synchronises `stream`) and registers the fastest
- * for g: every later sp_score / plan / workspace query of g uses it.  out[0..1]
- * = (token groups, unit groups); *ms_per_launch = its mean launch time.
- * sp_score_set_plan registers a plan explicitly (n_tg = 0 clears; an invalid
- * plan is ignored at plan time).  After either call, re-query
+ * for g: every later sp_score / plan / workspace query of g uses it.  out[0..2]
+ * = (token groups, unit groups, hierarchical); *ms_per_launch = its mean launch
+ * time.  sp_score_set_plan registers a plan explicitly (n_tg = 0 clears; an
+ * invalid plan is ignored at plan time).  After either call, re-query
  * sp_score_workspace_bytes(g) and use a freshly zero-filled workspace: the
  * partial-statistics layout depends on the plan. */
-sp_status sp_score_tune(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, int64_t out[2],
+sp_status sp_score_tune(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, int64_t out[3],
                         float* ms_per_launch, sp_stream stream);
-sp_status sp_score_set_plan(const sp_geom* g, int32_t n_tg, int32_t n_ug);
+sp_status sp_score_set_plan(const sp_geom* g, int32_t n_tg, int32_t n_ug, int32_t hier);
 
 /* Debug tracing of the fused kernel (not for production runs): while enabled,
  * every sp_score launch writes globaltimer stamps (ns) into device_buffer laid
@@ -208,26 +210,32 @@ sp_status sp_acc_importance(const float* acc2, int32_t B, int32_t R_valid, int64
 /* ------------------------------------------------------------------ score, sequence-sharded single pass
  * The prompt split along tokens over `world` ranks (<= 8), one launch per rank,
  * K read once: the fused kernel's per-unit softmax-statistics exchange runs
- * over peer memory.  Each CTA stores its 64-bit (max2, sum) partial words into
- * EVERY rank's partial buffer (NVLink stores, st.relaxed.sys) and gathers the
- * unit's world*n_tg partials from its own buffer in fixed (rank, token group)
- * order, so every rank computes the same lse2 bit for bit; the importance of
- * the rank's own tokens is written to importance [B][N_local].
+ * over peer memory, hierarchically.  Each CTA publishes its 64-bit (max2, sum)
+ * partial words into its own rank's workspace; the last CTA of a unit on rank
+ * r to publish merges the rank's n_tg partials in token-group order and stores
+ * the rank's word into row r of EVERY rank's rank-word buffer (NVLink stores,
+ * st.relaxed.sys); every CTA polls the unit's `world` rank words from its own
+ * buffer and merges them in rank order, so every rank computes the same lse2
+ * bit for bit.  The importance of the rank's own tokens is written to
+ * importance [B][N_local].
  * peer_buffers: host array of `world` device pointers (256-B aligned), entry r =
- * rank r's partial buffer of sp_score_peer_buffer_bytes(g, world, sm_budget)
+ * rank r's rank-word buffer of sp_score_peer_buffer_bytes(g, world, sm_budget)
  * bytes, mapped into this process (e.g. torch symmetric memory), zero-filled
- * once before first use (the kernel leaves it re-zeroed).  All ranks pass the
- * same geometry (equal shards), world and sm_budget, and their launches of one
- * call must be co-resident (they wait for each other inside the kernel; a
- * missing rank ends in a device timeout).  Consecutive calls must be separated
- * by a cross-rank barrier (the importance all-gather that follows is one).
- * sm_budget > 0 caps the CTAs per launch (0 = every SM), so several "ranks"
- * can share one GPU (the virtual-rank tests).  ws: a private workspace of
- * sp_score_peer_workspace_bytes(g, sm_budget) bytes, zero-filled once.
- * sp_score_peer_plan reports the plan (as sp_score_plan) under sm_budget. */
+ * once before first use (the kernel keeps it so).  All ranks pass the same
+ * geometry (equal shards), world and sm_budget, and their launches of one call
+ * must be co-resident (they wait for each other inside the kernel; a missing
+ * rank ends in a device timeout, SP_ETIMEOUT from sp_check_device_error).
+ * Consecutive calls must be separated by a cross-rank barrier (the sequence-
+ * sharded selection's edge all-gather that follows is one).  sm_budget > 0 caps
+ * the CTAs per launch (0 = every SM), so several "ranks" can share one GPU (the
+ * virtual-rank tests).  ws: a private workspace of
+ * sp_score_peer_workspace_bytes(g, world, sm_budget) bytes, zero-filled once and
+ * kept with the peer buffers (its launch epoch selects the buffers' half).
+ * sp_score_peer_plan reports the plan (as sp_score_plan) for world ranks under
+ * sm_budget. */
 size_t sp_score_peer_buffer_bytes(const sp_geom* g, int32_t world, int32_t sm_budget);
-size_t sp_score_peer_workspace_bytes(const sp_geom* g, int32_t sm_budget);
-sp_status sp_score_peer_plan(const sp_geom* g, int32_t sm_budget, int64_t out[9]);
+size_t sp_score_peer_workspace_bytes(const sp_geom* g, int32_t world, int32_t sm_budget);
+sp_status sp_score_peer_plan(const sp_geom* g, int32_t world, int32_t sm_budget, int64_t out[10]);
 sp_status sp_score_peer(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, int32_t rank,
                         int32_t world, void* const* peer_buffers, int32_t sm_budget, float* importance, void* ws,
                         size_t ws_bytes, sp_stream stream);
@@ -246,12 +254,12 @@ sp_status sp_score_peer(const void* Q, const void* K, const sp_geom* g, const sp
  * d % 32 == 0 (else SP_EUNSUPPORTED).  q_scale, k_scale finite and > 0.
  * Workspace: sp_score_e4m3_workspace_bytes(g) bytes, same rules as sp_score. */
 size_t sp_score_e4m3_workspace_bytes(const sp_geom* g);
-sp_status sp_score_e4m3_plan(const sp_geom* g, int64_t out[9]);
+sp_status sp_score_e4m3_plan(const sp_geom* g, int64_t out[10]);
 sp_status sp_score_e4m3(const void* Q8, const void* K8, float q_scale, float k_scale, const sp_geom* g,
                         const sp_layout* lay, float* importance, void* ws, size_t ws_bytes, sp_stream stream);
 /* sp_score_tune for the e4m3 path (its plans are registered separately from bf16's). */
 sp_status sp_score_e4m3_tune(const void* Q8, const void* K8, float q_scale, float k_scale, const sp_geom* g,
-                             const sp_layout* lay, int64_t out[2], float* ms_per_launch, sp_stream stream);
+                             const sp_layout* lay, int64_t out[3], float* ms_per_launch, sp_stream stream);
 
 /* ------------------------------------------------------------------ score, look-ahead-key denominator
  * SURVEY 8(f) row f4, reading Z2': each look-ahead

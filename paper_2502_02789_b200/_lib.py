@@ -16,6 +16,9 @@ if os.environ.get("SP_LIB_AB"):
 
 SP_OK, SP_EINVAL, SP_EUNSUPPORTED, SP_ECUDA, SP_ENONFINITE, SP_EEMPTY, SP_EWORKSPACE, SP_ETIMEOUT = 0, 1, 2, 3, 5, 6, 7, 8
 SP_SCORE_AUTO, SP_SCORE_FUSED, SP_SCORE_SIMT = 0, 1, 2
+PLAN_INFO = 10          # entries of sp_score_plan's out array
+PLAN_KEYS = ("grid", "jobs_per_request", "token_groups", "unit_groups", "tiles_per_job", "units_per_job",
+             "tmem_slots", "stages", "smem_bytes", "hier")
 ABI_VERSION = 1
 
 
@@ -75,7 +78,7 @@ SIGNATURES = {
     "sp_score_tune": (C.c_int, [_P, _P, _G, _L, C.POINTER(C.c_int64), C.POINTER(C.c_float), _P]),
     "sp_score_e4m3_tune": (C.c_int, [_P, _P, C.c_float, C.c_float, _G, _L, C.POINTER(C.c_int64),
                                      C.POINTER(C.c_float), _P]),
-    "sp_score_set_plan": (C.c_int, [_G, C.c_int32, C.c_int32]),
+    "sp_score_set_plan": (C.c_int, [_G, C.c_int32, C.c_int32, C.c_int32]),
     "sp_trace_enable": (C.c_int, [_P, C.c_int64]),
     "sp_score_split_workspace_bytes": (C.c_size_t, [_G]),
     "sp_score_stats": (C.c_int, [_P, _P, _G, _L, _P, _P, C.c_size_t, _P]),
@@ -84,8 +87,8 @@ SIGNATURES = {
     "sp_score_acc": (C.c_int, [_P, _P, _G, _L, _P, _P, C.c_size_t, _P]),
     "sp_acc_importance": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int64, _P, _P]),
     "sp_score_peer_buffer_bytes": (C.c_size_t, [_G, C.c_int32, C.c_int32]),
-    "sp_score_peer_workspace_bytes": (C.c_size_t, [_G, C.c_int32]),
-    "sp_score_peer_plan": (C.c_int, [_G, C.c_int32, C.POINTER(C.c_int64)]),
+    "sp_score_peer_workspace_bytes": (C.c_size_t, [_G, C.c_int32, C.c_int32]),
+    "sp_score_peer_plan": (C.c_int, [_G, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
     "sp_score_peer": (C.c_int, [_P, _P, _G, _L, C.c_int32, C.c_int32, C.POINTER(C.c_void_p), C.c_int32, _P, _P,
                                 C.c_size_t, _P]),
     "sp_score_e4m3_workspace_bytes": (C.c_size_t, [_G]),

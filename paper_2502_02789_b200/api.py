@@ -61,8 +61,8 @@ def _geom_key(g) -> tuple:
     """Workspace cache key: the geometry and the fused plan it runs with (the
     partial-statistics layout depends on the plan: env override, sp_score_tune)."""
     import os
-    out = (C.c_int64 * 9)()
-    plan = tuple(out)[2:4] if lib().sp_score_plan(C.byref(g), out) == _lib.SP_OK else None
+    out = (C.c_int64 * _lib.PLAN_INFO)()
+    plan = (out[2], out[3], out[9]) if lib().sp_score_plan(C.byref(g), out) == _lib.SP_OK else None
     return (g.B, g.L, g.H, g.Hkv, g.d, g.R, g.R_valid, g.N, os.environ.get("SP_FUSED_PLAN"), plan)
 
 
@@ -114,9 +114,9 @@ def score_e4m3(Q8, K8, q_scale: float = 1.0, k_scale: float = 1.0, R_valid=None,
     nbytes = lib().sp_score_e4m3_workspace_bytes(C.byref(g))
     if nbytes == 0:
         check(_lib.SP_EUNSUPPORTED, "sp_score_e4m3")
-    pl = (C.c_int64 * 9)()
+    pl = (C.c_int64 * _lib.PLAN_INFO)()
     lib().sp_score_e4m3_plan(C.byref(g), pl)
-    ws = workspace(("score_e4m3", _geom_key(g), tuple(pl)[2:4]), nbytes, K8.device, stream)
+    ws = workspace(("score_e4m3", _geom_key(g), (pl[2], pl[3], pl[9])), nbytes, K8.device, stream)
     check(lib().sp_score_e4m3(Q8.data_ptr(), K8.data_ptr(), float(q_scale), float(k_scale), C.byref(g), C.byref(lay),
                               out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_score_e4m3")
     return out
@@ -124,11 +124,9 @@ def score_e4m3(Q8, K8, q_scale: float = 1.0, k_scale: float = 1.0, R_valid=None,
 
 def score_e4m3_plan(Q8, K8, R_valid=None) -> dict:
     g, _ = make_geom(Q8, K8, R_valid, e4m3=True)
-    out = (C.c_int64 * 9)()
+    out = (C.c_int64 * _lib.PLAN_INFO)()
     check(lib().sp_score_e4m3_plan(C.byref(g), out), "sp_score_e4m3_plan")
-    keys = ("grid", "jobs_per_request", "token_groups", "unit_groups", "tiles_per_job", "units_per_job",
-            "tmem_slots", "stages", "smem_bytes")
-    return dict(zip(keys, list(out)))
+    return dict(zip(_lib.PLAN_KEYS, list(out)))
 
 
 def score_lookahead(Q, K, K_la, la_shift: int = 0, R_valid=None, scale=None, out=None, stream=None) -> torch.Tensor:
@@ -190,9 +188,9 @@ def score_paged(Q, K_cache, block_table, seq_lens=None, N=None, R_valid=None, sc
         nbytes = lib().sp_score_e4m3_workspace_bytes(C.byref(g))
         if nbytes == 0:
             check(_lib.SP_EUNSUPPORTED, "sp_score_paged_e4m3")
-        pl = (C.c_int64 * 9)()
+        pl = (C.c_int64 * _lib.PLAN_INFO)()
         lib().sp_score_e4m3_plan(C.byref(g), pl)
-        ws = workspace(("score_paged_e4m3", _geom_key(g), tuple(pl)[2:4]), nbytes, K_cache.device, stream)
+        ws = workspace(("score_paged_e4m3", _geom_key(g), (pl[2], pl[3], pl[9])), nbytes, K_cache.device, stream)
         check(lib().sp_score_paged_e4m3(Q.data_ptr(), C.byref(pk), float(q_scale), float(k_scale), C.byref(g),
                                         C.byref(lay), out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
               "sp_score_paged_e4m3")
@@ -358,31 +356,29 @@ def score_tune(Q, K, R_valid=None, scale=None, stream=None) -> dict:
     """Time the fused kernel's best plan candidates on these inputs and register
     the fastest for this geometry (sp_score_tune; synchronises, allocates)."""
     g, lay = make_geom(Q, K, R_valid, scale)
-    out = (C.c_int64 * 2)()
+    out = (C.c_int64 * 3)()
     ms = C.c_float()
     check(lib().sp_score_tune(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), out, C.byref(ms),
                               _stream_ptr(stream)), "sp_score_tune")
-    return {"token_groups": out[0], "unit_groups": out[1], "ms_per_launch": ms.value}
+    return {"token_groups": out[0], "unit_groups": out[1], "hier": out[2], "ms_per_launch": ms.value}
 
 
 def score_e4m3_tune(Q8, K8, q_scale: float = 1.0, k_scale: float = 1.0, R_valid=None, scale=None,
                     stream=None) -> dict:
     g, lay = make_geom(Q8, K8, R_valid, scale, e4m3=True)
-    out = (C.c_int64 * 2)()
+    out = (C.c_int64 * 3)()
     ms = C.c_float()
     check(lib().sp_score_e4m3_tune(Q8.data_ptr(), K8.data_ptr(), float(q_scale), float(k_scale), C.byref(g),
                                    C.byref(lay), out, C.byref(ms), _stream_ptr(stream)), "sp_score_e4m3_tune")
-    return {"token_groups": out[0], "unit_groups": out[1], "ms_per_launch": ms.value}
+    return {"token_groups": out[0], "unit_groups": out[1], "hier": out[2], "ms_per_launch": ms.value}
 
 
 def score_plan(Q, K, R_valid=None) -> dict:
     """The fused kernel's launch plan for this geometry on the current device."""
     g, _ = make_geom(Q, K, R_valid)
-    out = (C.c_int64 * 9)()
+    out = (C.c_int64 * _lib.PLAN_INFO)()
     check(lib().sp_score_plan(C.byref(g), out), "sp_score_plan")
-    keys = ("grid", "jobs_per_request", "token_groups", "unit_groups", "tiles_per_job", "units_per_job",
-            "tmem_slots", "stages", "smem_bytes")
-    return dict(zip(keys, list(out)))
+    return dict(zip(_lib.PLAN_KEYS, list(out)))
 
 
 def score_stats(Q, K, R_valid=None, scale=None, out=None, stream=None) -> torch.Tensor:
@@ -449,18 +445,16 @@ def score_peer_buffer_bytes(Q, K, world: int, sm_budget: int = 0, R_valid=None) 
     return int(lib().sp_score_peer_buffer_bytes(C.byref(g), world, sm_budget))
 
 
-def score_peer_plan(Q, K, sm_budget: int = 0, R_valid=None) -> dict:
+def score_peer_plan(Q, K, world: int, sm_budget: int = 0, R_valid=None) -> dict:
     g, _ = make_geom(Q, K, R_valid)
-    out = (C.c_int64 * 9)()
-    check(lib().sp_score_peer_plan(C.byref(g), sm_budget, out), "sp_score_peer_plan")
-    keys = ("grid", "jobs_per_request", "token_groups", "unit_groups", "tiles_per_job", "units_per_job",
-            "tmem_slots", "stages", "smem_bytes")
-    return dict(zip(keys, list(out)))
+    out = (C.c_int64 * _lib.PLAN_INFO)()
+    check(lib().sp_score_peer_plan(C.byref(g), int(world), sm_budget, out), "sp_score_peer_plan")
+    return dict(zip(_lib.PLAN_KEYS, list(out)))
 
 
-def score_peer_workspace_bytes(Q, K, sm_budget: int = 0, R_valid=None) -> int:
+def score_peer_workspace_bytes(Q, K, world: int, sm_budget: int = 0, R_valid=None) -> int:
     g, _ = make_geom(Q, K, R_valid)
-    return int(lib().sp_score_peer_workspace_bytes(C.byref(g), sm_budget))
+    return int(lib().sp_score_peer_workspace_bytes(C.byref(g), int(world), sm_budget))
 
 
 def score_peer(Q, K, rank: int, world: int, peer_ptrs, sm_budget: int = 0, R_valid=None, scale=None, out=None,
@@ -473,9 +467,12 @@ def score_peer(Q, K, rank: int, world: int, peer_ptrs, sm_budget: int = 0, R_val
     together); by default one from the cache."""
     g, lay = make_geom(Q, K, R_valid, scale)
     out = torch.empty((g.B, g.N), dtype=torch.float32, device=K.device) if out is None else out
-    nbytes = lib().sp_score_peer_workspace_bytes(C.byref(g), sm_budget)
+    nbytes = lib().sp_score_peer_workspace_bytes(C.byref(g), int(world), sm_budget)
+    if nbytes == 0:
+        check(_lib.SP_EUNSUPPORTED, "sp_score_peer")
     if ws is None:
-        ws = workspace(("peer", _geom_key(g), sm_budget, rank if ws_tag is None else ws_tag), nbytes, K.device, stream)
+        ws = workspace(("peer", _geom_key(g), world, sm_budget, rank if ws_tag is None else ws_tag), nbytes, K.device,
+                       stream)
     elif ws.numel() < nbytes:
         raise ValueError("peer workspace too small")
     ptrs = (C.c_void_p * world)(*[int(x) for x in peer_ptrs])

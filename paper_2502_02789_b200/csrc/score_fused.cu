@@ -99,6 +99,8 @@ struct FusedParams {
   // workspace
   unsigned long long* part;            // [2][B][U][n_tg][NCP] CTA partials, one buffer per launch parity:
                                        // (max2, sum) packed in one 64-bit word; 0 = "not yet written"
+  int hier;                            // hierarchical exchange: the unit's last CTA merges, the rest poll one word
+  unsigned* hcnt;                      // [B][U] hier: CTA partials published so far (reset by the merging CTA)
   unsigned* epoch;                     // [2] launch epoch (parity selects the partial buffer), CTAs done
   float* accpart;                      // [B][n_ug][Rv][N]
   unsigned* fin_cnt;                   // [B][n_tg]    finalize counters (self-cleaning)
@@ -110,11 +112,14 @@ struct FusedParams {
   unsigned long long* tile_trace;      // optional [1000][8] per-tile MMA stamps of CTA 0 (debug)
   int mode;                            // kModeFull / kModeStats (publish partials only) / kModeFinish (lse2 given)
   const float* lse_in;                 // kModeFinish: lse2 per row ((b*L + l)*H + h)*Rv + r
-  // peer-memory exchange (sequence-sharded single pass): world ranks each score
-  // their own tokens; a CTA publishes its partial into every rank's buffer and
-  // gathers the unit's world*n_tg partials from its own.  world = 1: local only.
-  int rank, world, ntg_all;            // ntg_all = world * n_tg partials per unit
-  unsigned long long* peer[kMaxPeers]; // every rank's partial buffer base ([2][B][U][ntg_all][NCP])
+  // hierarchical exchange and its peer-memory form (sequence-sharded single pass):
+  // world ranks each score their own tokens; the last CTA of a unit on rank r to
+  // publish merges the rank's n_tg partials (token-group order) and stores the
+  // rank's word into row r of every rank's rank-word buffer; every CTA then
+  // polls the unit's `world` rank words and merges them in rank order (the same
+  // lse2 bits on every rank).  world = 1 with hier: one word, local.
+  int rank, world;
+  unsigned long long* peer[kMaxPeers]; // every rank's rank-word buffer base ([2][B][U][world][NCP])
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -310,12 +315,20 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 __device__ __forceinline__ void set_err(int* err, int code) { atomicCAS(err, 0, code); }
 
 // Spin (one thread) until *p >= target; bounded so a broken exchange can never hang the GPU.
+// (deadline 2 s of globaltimer: before mbar_wait_slow's 4 s trap)
 __device__ __forceinline__ void spin_geq(const unsigned* p, unsigned target, int* err) {
   long long it = 0;
+  unsigned long long t_dead = 0;
   while (ld_acquire(p) < target) {
-    if (++it > (1LL << 25)) {
-      set_err(err, kDevTimeout);
-      return;
+    ++it;
+    if ((it & 1023) == 0) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+      if (t_dead == 0) t_dead = now + 2000000000ull;
+      else if (now > t_dead) {
+        set_err(err, kDevTimeout);
+        return;
+      }
     }
     if (it > 8) __nanosleep(it < 64 ? 32 : 100);
   }
@@ -540,6 +553,59 @@ __device__ __forceinline__ float transpose_add32(float (&s)[32], int lane) {
   return s[0];
 }
 
+// Bounded spin deadline: every in-kernel wait gives up (SP_ETIMEOUT) after
+// kSpinNs of globaltimer, well before mbar_wait_slow's 4 s trap.
+constexpr unsigned long long kSpinNs = 2000000000ull;
+
+// Hierarchical exchange, exchange warp (whole warp): after publishing this CTA's
+// partial words of unit ubase, count the arrival; the CTA that completes the
+// count merges the unit's n_tg partials in token-group order (all are visible:
+// each writer fenced before counting) into the rank word, stores it into row
+// `rank` of every rank's rank-word buffer (this launch's parity half), re-zeroes
+// the same row of the other half (read by nobody now; zero = "not yet written"
+// for the launch after next) and resets the counter.  Out of line: executed
+// once per unit.
+__device__ __noinline__ void hier_merge(const FusedParams& p, long long ubase, const unsigned long long* part_cur,
+                                        uint32_t parity, int NCP, int lane) {
+  unsigned old = 0;
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();                                           // release this CTA's partial words
+    old = atomicAdd(p.hcnt + ubase, 1u);
+  }
+  old = __shfl_sync(0xffffffffu, old, 0);
+  if (old + 1u != (unsigned)p.n_tg) return;
+  __threadfence();                                             // acquire the other CTAs' words
+  const unsigned long long* src = part_cur + ubase * p.n_tg * NCP;
+  const long long fin_half = (long long)p.B * p.U * p.world * NCP;
+  const long long row = (ubase * p.world + p.rank) * NCP;
+  for (int c = lane; c < NCP; c += 32) {
+    float M = -CUDART_INF_F, S = 0.f;
+    for (int s0 = 0; s0 < p.n_tg; s0 += 16) {
+      unsigned long long v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = s0 + j < p.n_tg ? ld_relaxed_u64(src + (long long)(s0 + j) * NCP + c) : 0ull;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float2 w = unpack_ms(v[j]);
+        if (s0 + j < p.n_tg && w.y > 0.f) merge2(M, S, w.x, w.y);
+      }
+    }
+    const unsigned long long word = S > 0.f ? pack_ms(M, S) : pack_ms(-CUDART_INF_F, -1.f);   // never 0
+    if (p.world == 1) {
+      st_relaxed_u64(p.peer[0] + parity * fin_half + row + c, word);
+      p.peer[0][(parity ^ 1u) * fin_half + row + c] = 0ull;
+    } else {
+      for (int r = 0; r < p.world; ++r) {                      // NVLink stores to the peers
+        st_relaxed_sys_u64(p.peer[r] + parity * fin_half + row + c, word);
+        p.peer[r][(parity ^ 1u) * fin_half + row + c] = 0ull;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) atomicExch(p.hcnt + ubase, 0u);
+}
+
 // kG: compile-time GQA group size (1, 2, 4, 8) or 0 for any G.  One
 // instantiation per group size keeps the kernel's hot code small: the warp
 // roles run different code concurrently on each SMSP and share the
@@ -610,7 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   // this launch publishes into part[parity]; part[parity ^ 1] (the previous
   // launch's) is re-zeroed off the critical path, for the launch after next
   const uint32_t parity = ld_acquire(p.epoch) & 1u;
-  const long long part_half = (long long)p.B * p.U * p.ntg_all * NCP;
+  const long long part_half = (long long)p.B * p.U * p.n_tg * NCP;
   unsigned long long* const part_cur = p.part + parity * part_half;
   unsigned long long* const part_old = p.part + (parity ^ 1u) * part_half;
 
@@ -837,7 +903,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const long long ubase = (long long)jb.b * p.U + u;
         mbar_wait(bar_rfull + 8 * (ui & 1), (ui >> 1) & 1);
         const float2* rb = red + (ui & 1) * 4 * NCP;
-        const long long row = (ubase * p.ntg_all + p.rank * p.n_tg + jb.tg) * NCP;
+        const long long row = (ubase * p.n_tg + jb.tg) * NCP;
         for (int c = lane; c < NCP; c += 32) {
           float mm = -CUDART_INF_F, ss = 0.f;
           if (c < p.NC) {
@@ -849,27 +915,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           }
           if (!(ss > 0.f) || jb.t_lo == jb.t_hi) { mm = -CUDART_INF_F; ss = -1.f; }   // written, but empty
                                                                         // (an empty job of a ragged batch)
-          if (p.world == 1) {
-            st_relaxed_u64(part_cur + row + c, pack_ms(mm, ss));
-          } else {
-            for (int r = 0; r < p.world; ++r)                               // NVLink stores to the peers
-              st_relaxed_sys_u64(p.peer[r] + parity * part_half + row + c, pack_ms(mm, ss));
-          }
+          st_relaxed_u64(part_cur + row + c, pack_ms(mm, ss));
         }
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(bar_rempty + 8 * (ui & 1));
           trace_stamp(p, ui, 3);
         }
+        if (p.hier && p.mode == kModeFull) hier_merge(p, ubase, part_cur, parity, NCP, lane);
       }
     }
     // re-zero this CTA's rows of the previous launch's buffer (read by nobody now)
-    for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
+    for (long long job = blockIdx.x; job < p.total_jobs && !p.hier; job += gridDim.x) {
       const Job jb = decode_job(p, job);
       for (int u = jb.u_lo; u < jb.u_hi; ++u) {
-        const long long row = (((long long)jb.b * p.U + u) * p.ntg_all + p.rank * p.n_tg + jb.tg) * NCP;
-        for (int r = 0; r < p.world; ++r)
-          for (int c = lane; c < NCP; c += 32) p.peer[r][(parity ^ 1u) * part_half + row + c] = 0ull;
+        const long long row = (((long long)jb.b * p.U + u) * p.n_tg + jb.tg) * NCP;
+        for (int c = lane; c < NCP; c += 32) part_old[row + c] = 0ull;
       }
     }
   } else if (warp == 3 && p.mode != kModeStats) {
@@ -887,8 +948,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const long long ubase = (long long)jb.b * p.U + u;
         mbar_wait(bar_lempty + 8 * par, ((ui / kLseRing) & 1) ^ 1);    // aggregation done with ls[par]
         float* ls = lse_s + par * NCP;
-        const unsigned long long* src = part_cur + ubase * p.ntg_all * NCP;
-        const int ntg = p.ntg_all;
+        // flat: the unit's n_tg CTA partials; hierarchical: its `world` rank words
+        const unsigned long long* src = p.hier ? p.peer[p.rank] + parity * ((long long)p.B * p.U * p.world * NCP)
+                                                     + ubase * p.world * NCP
+                                               : part_cur + ubase * p.n_tg * NCP;
+        const int ntg = p.hier ? p.world : p.n_tg;
         for (int c = lane; c < NCP && p.mode == kModeFinish; c += 32) {
           // lse2 supplied by the caller (sequence-sharded split: globally combined statistics)
           float l2 = 0.f;
@@ -909,6 +973,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
               missing |= (v[j] == 0ull ? 1ull : 0ull) << j;
             }
             long long it = 0;
+            unsigned long long t_dead = 0;
             while (__any_sync(0xffffffffu, missing != 0)) {
               __nanosleep(it < 8 ? 64 : 200);
 #pragma unroll
@@ -918,7 +983,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
                   if (v[j] != 0ull) missing &= ~(1ull << j);
                 }
               }
-              if (++it > (1LL << 22)) {
+              if ((++it & 1023) == 0 && t_dead == 0) t_dead = globaltimer_ns() + kSpinNs;
+              if (t_dead != 0 && (it & 1023) == 0 && globaltimer_ns() > t_dead) {
                 set_err(p.err, kDevTimeout);
 #pragma unroll
                 for (int j = 0; j < kMaxLseBatch; ++j)
@@ -1129,8 +1195,9 @@ struct Plan {
   uint32_t off_k = 0, off_q = 0, off_acc = 0, off_red = 0, off_lse = 0, off_comb = 0, off_bar = 0, off_bt = 0, smem = 0;
   uint32_t k_stage_bytes = 0, q_slot_bytes = 0;
   int nq = 2;
-  size_t ws_part = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0;
-  size_t ws_total() const { return ws_part + ws_cnt + ws_acc + ws_fin; }
+  int hier = 0, world = 1;                            // hierarchical exchange; ranks of a peer exchange
+  size_t ws_part = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0, ws_hcnt = 0, ws_rank = 0;
+  size_t ws_total() const { return ws_part + ws_cnt + ws_acc + ws_fin + ws_hcnt + ws_rank; }
   bool ok = false;
 };
 
@@ -1167,10 +1234,12 @@ uint32_t carve(Plan& pl, int Rv, int stages) {
   return o + 1024;                                   // slack for the manual 1024-byte alignment
 }
 
-// Measured plan choices (sp_score_tune / sp_score_set_plan), per geometry.
+// Measured plan choices (sp_score_tune / sp_score_set_plan), per geometry:
+// (n_tg, n_ug, hier).
 using PlanKey = std::tuple<int, int, int, int, int, int, int, long long, int, int>;
-std::map<PlanKey, std::pair<int, int>>& plan_registry() {
-  static std::map<PlanKey, std::pair<int, int>> m;
+using PlanChoice = std::tuple<int, int, int>;
+std::map<PlanKey, PlanChoice>& plan_registry() {
+  static std::map<PlanKey, PlanChoice> m;
   return m;
 }
 std::mutex& plan_registry_mu() {
@@ -1182,9 +1251,10 @@ PlanKey plan_key(const Geom& g, int sm_budget) {
 }
 
 // sm_budget > 0: plan for at most that many CTAs (co-scheduled peer launches on one GPU, tests).
-// cands (optional): every valid (model cost, n_tg, n_ug), for the tuner.
+// cands (optional): every valid (model cost, n_tg, n_ug, hier), for the tuner.
+// world > 1: a peer-memory exchange over that many ranks (always hierarchical).
 Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
-               std::vector<std::tuple<double, int, int>>* cands = nullptr) {
+               std::vector<std::tuple<double, int, int, int>>* cands = nullptr, int world = 1) {
   Plan pl;
   pl.NC = g.G * g.Rv;
   pl.NCP = ((pl.NC + 31) / 32) * 32;                  // TMEM column groups of 32 (one tcgen05.ld.x32)
@@ -1207,16 +1277,20 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   // model below.
   pl.nslots = std::min(kMaxSlots, kTmemCols / pl.NCP);
   double best = 1e300;
-  // test/tuning override: SP_FUSED_PLAN="n_tg,n_ug" (ignored unless valid for g)
-  int force_tg = 0, force_ug = 0;
+  // test/tuning override: SP_FUSED_PLAN="n_tg,n_ug[,hier]" (ignored unless valid for g)
+  int force_tg = 0, force_ug = 0, force_h = -1;
   if (const char* env = allow_override ? std::getenv("SP_FUSED_PLAN") : nullptr) {
-    if (std::sscanf(env, "%d,%d", &force_tg, &force_ug) != 2) force_tg = force_ug = 0;
+    const int n = std::sscanf(env, "%d,%d,%d", &force_tg, &force_ug, &force_h);
+    if (n < 2) force_tg = force_ug = 0;
+    if (n < 3) force_h = -1;
   }
-  if (allow_override && force_tg == 0) {                  // a measured choice for this geometry
+  if (allow_override && force_tg == 0 && world == 1) {   // a measured choice for this geometry
     std::lock_guard<std::mutex> lk(plan_registry_mu());
     auto it = plan_registry().find(plan_key(g, sm_budget));
-    if (it != plan_registry().end()) { force_tg = it->second.first; force_ug = it->second.second; }
+    if (it != plan_registry().end()) std::tie(force_tg, force_ug, force_h) = it->second;
   }
+  if (world > 1) force_h = 1;
+  pl.world = world;
   for (int J = 1; J <= pl.P; ++J) {
     if ((long long)g.B * J > pl.P && pl.P % J) continue;
     for (int n_tg = 1; n_tg <= J; ++n_tg) {
@@ -1237,24 +1311,32 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
       // (per-tile costs measured for bf16 hold for e4m3 too: the statistics,
       // aggregation and exchange work per tile does not depend on the K bytes)
       const double tile_us = (double)kTileM * g.d * 2 / kSmHbmBytesPerUs;
-      const int batches = (n_tg + kMaxLseBatch - 1) / kMaxLseBatch;
-      const double L_us = 5.0 + 0.8 * batches;
-      const int W = std::max(1, pl.nslots / tpc);
-      const double exposed = std::max(0.0, L_us - (W - 1) * tpc * tile_us);
-      // (+0.4 us fixed per unit: Q load, statistics merge and publish)
-      const double per_unit = std::max(tpc * tile_us + exposed / W + 0.4, 1.6 * batches);
-      double cost = upc * per_unit + L_us;                                   // + pipeline fill
-      if (n_ug > 1)                                                          // cross-group max + its sync
-        cost += 2.0 * g.Rv * tpc * kTileM * 4.0 / kSmHbmBytesPerUs + 5.0 + 0.25 * n_ug;
-      cost *= (double)waves;
-      if (cands != nullptr) cands->emplace_back(cost, n_tg, n_ug);
-      if (cost < best * 0.999) {
-        best = cost;
-        pl.J = J; pl.n_tg = n_tg; pl.n_ug = n_ug; pl.tpc = tpc; pl.upc = upc;
+      for (int hier = 0; hier < 2; ++hier) {
+        if (force_h >= 0 && hier != force_h) continue;
+        if (world > 1 && hier == 0) continue;
+        // flat: every CTA polls the unit's n_tg partials (batches of kMaxLseBatch);
+        // hierarchical: the unit's last CTA merges them (one more L2 hop, + an
+        // NVLink hop when world > 1) and every CTA polls `world` rank words
+        const int batches = hier ? (world + kMaxLseBatch - 1) / kMaxLseBatch : (n_tg + kMaxLseBatch - 1) / kMaxLseBatch;
+        const double L_us = 5.0 + 0.8 * batches + (hier ? 1.5 + 0.25 * ((n_tg + 15) / 16) : 0.0) +
+                            (world > 1 ? 2.0 : 0.0);
+        const int W = std::max(1, pl.nslots / tpc);
+        const double exposed = std::max(0.0, L_us - (W - 1) * tpc * tile_us);
+        // (+0.4 us fixed per unit: Q load, statistics merge and publish)
+        const double per_unit = std::max(tpc * tile_us + exposed / W + 0.4, 1.6 * batches);
+        double cost = upc * per_unit + L_us;                                   // + pipeline fill
+        if (n_ug > 1)                                                          // cross-group max + its sync
+          cost += 2.0 * g.Rv * tpc * kTileM * 4.0 / kSmHbmBytesPerUs + 5.0 + 0.25 * n_ug;
+        cost *= (double)waves;
+        if (cands != nullptr) cands->emplace_back(cost, n_tg, n_ug, hier);
+        if (cost < best * 0.999) {
+          best = cost;
+          pl.J = J; pl.n_tg = n_tg; pl.n_ug = n_ug; pl.tpc = tpc; pl.upc = upc; pl.hier = hier;
+        }
       }
     }
   }
-  if (pl.J == 0 && force_tg > 0) return make_plan(g, false, sm_budget);   // invalid override: plan normally
+  if (pl.J == 0 && force_tg > 0) return make_plan(g, false, sm_budget, nullptr, world);   // invalid override
   if (pl.J == 0) return pl;
   pl.total_jobs = (long long)g.B * pl.J;
   // 4 query slots (Q loads issued 3 units ahead) unless that costs a K stage on long units
@@ -1274,6 +1356,8 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   pl.ws_cnt = 256;                                   // launch epoch + CTAs-done counter
   pl.ws_acc = pl.n_ug > 1 ? align256((size_t)g.B * pl.n_ug * g.Rv * g.N * sizeof(float)) : 0;
   pl.ws_fin = align256((size_t)g.B * pl.n_tg * sizeof(unsigned));
+  pl.ws_hcnt = align256((size_t)g.B * pl.U * sizeof(unsigned));
+  pl.ws_rank = world == 1 ? align256(2 * (size_t)g.B * pl.U * pl.NCP * sizeof(unsigned long long)) : 0;
   pl.ok = true;
   return pl;
 }
@@ -1336,11 +1420,11 @@ bool fused_supported(const Geom& g, const Layout&, const void*, const void*) {
   return make_plan(g).ok;
 }
 
-bool fused_plan_info(const Geom& g, long long out[9]) {
+bool fused_plan_info(const Geom& g, long long out[kPlanInfo]) {
   Plan pl = make_plan(g);
   if (!pl.ok) return false;
   out[0] = std::min<long long>(pl.P, pl.total_jobs); out[1] = pl.J; out[2] = pl.n_tg; out[3] = pl.n_ug;
-  out[4] = pl.tpc; out[5] = pl.upc; out[6] = pl.nslots; out[7] = pl.stages; out[8] = pl.smem;
+  out[4] = pl.tpc; out[5] = pl.upc; out[6] = pl.nslots; out[7] = pl.stages; out[8] = pl.smem; out[9] = pl.hier;
   return true;
 }
 
@@ -1445,10 +1529,10 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
                          const float* lse_in, float* importance, void* ws, size_t ws_bytes, cudaStream_t st,
                          float* acc_out = nullptr, const PeerArgs& peer = PeerArgs(), const PagedK* pk = nullptr,
                          const float2* la = nullptr) {
-  Plan pl = make_plan(g, true, peer.sm_budget);
-  if (!pl.ok || ws_bytes < pl.ws_total()) return cudaErrorInvalidValue;
   if (peer.world < 1 || peer.world > kMaxPeers || peer.rank < 0 || peer.rank >= peer.world) return cudaErrorInvalidValue;
-  if (peer.world > 1 && (peer.bufs == nullptr || pl.n_tg * peer.world > kMaxLseBatch * 64)) return cudaErrorInvalidValue;
+  Plan pl = make_plan(g, true, peer.sm_budget, nullptr, peer.world);
+  if (!pl.ok || ws_bytes < pl.ws_total()) return cudaErrorInvalidValue;
+  if (peer.world > 1 && (peer.bufs == nullptr || !pl.hier)) return cudaErrorInvalidValue;
   static FusedParams p;                               // large (two tensor maps); host-side scratch
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
@@ -1493,14 +1577,16 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   p.part = reinterpret_cast<unsigned long long*>(w);
   w += pl.ws_part;
   p.accpart = pl.ws_acc ? reinterpret_cast<float*>(w) : nullptr;
+  w += pl.ws_acc;
+  p.hcnt = reinterpret_cast<unsigned*>(w);
+  w += pl.ws_hcnt;
+  p.hier = pl.hier;
   p.rank = peer.rank;
   p.world = peer.world;
-  p.ntg_all = pl.n_tg * peer.world;
   if (peer.world > 1) {
     for (int r = 0; r < peer.world; ++r) p.peer[r] = reinterpret_cast<unsigned long long*>(peer.bufs[r]);
-    p.part = p.peer[peer.rank];
   } else {
-    p.peer[0] = p.part;
+    p.peer[0] = reinterpret_cast<unsigned long long*>(w);          // rank words (hierarchical, local)
   }
   p.imp = importance;
   p.acc_out = acc_out;
@@ -1531,15 +1617,18 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
       {{k_fused<1, 0, true>, k_fused<1, 32, true>}, {k_fused<2, 0, true>, k_fused<2, 32, true>},
        {k_fused<4, 0, true>, k_fused<4, 32, true>}, {k_fused<8, 0, true>, k_fused<8, 32, true>},
        {k_fused<0, 0, true>, k_fused<0, 32, true>}}};
-  static bool configured[2][5][2] = {};
+  // the >48 KiB dynamic-SMEM opt-in is per device: set once per (device, instantiation)
+  static bool configured[64][2][5][2] = {};
   const int kt = g.esz == 1 ? 1 : 0;
   const int ki = g.G == 1 ? 0 : g.G == 2 ? 1 : g.G == 4 ? 2 : g.G == 8 ? 3 : 4;
   const int kj = pl.NCP == 32 ? 1 : 0;
   KernFn kern = table[kt][ki][kj];
-  if (!configured[kt][ki][kj]) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!configured[dev][kt][ki][kj]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (e != cudaSuccess) return e;
-    configured[kt][ki][kj] = true;
+    configured[dev][kt][ki][kj] = true;
   }
   const int grid = (int)std::min<long long>(pl.P, pl.total_jobs);
   cudaLaunchConfig_t cfg = {};
@@ -1632,8 +1721,8 @@ cudaError_t fused_score_paged(const __nv_bfloat16* Q, const PagedK& K, const Geo
 constexpr int kTuneMax = SP_TUNE_MAX;        // candidates timed
 constexpr double kTuneSpan = SP_TUNE_SPAN;   // ... within this factor of the model's best cost
 cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
-                       cudaStream_t st, int* tg_out, int* ug_out, float* ms_out) {
-  std::vector<std::tuple<double, int, int>> cands;
+                       cudaStream_t st, int* tg_out, int* ug_out, int* hier_out, float* ms_out) {
+  std::vector<std::tuple<double, int, int, int>> cands;
   {
     std::lock_guard<std::mutex> lk(plan_registry_mu());
     plan_registry().erase(plan_key(g, 0));
@@ -1643,20 +1732,20 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
   std::sort(cands.begin(), cands.end());
   const double best_cost = std::get<0>(cands.front());
   float best_ms = 1e30f;
-  int best_tg = base.n_tg, best_ug = base.n_ug;
+  int best_tg = base.n_tg, best_ug = base.n_ug, best_h = base.hier;
   cudaEvent_t e0, e1;
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return cudaGetLastError();
   float* imp = nullptr;
   cudaError_t err = cudaMalloc(&imp, (size_t)g.B * g.N * sizeof(float));
   for (size_t i = 0; err == cudaSuccess && i < cands.size() && i < (size_t)kTuneMax; ++i) {
     if (std::get<0>(cands[i]) > kTuneSpan * best_cost) break;
-    const int tg = std::get<1>(cands[i]), ug = std::get<2>(cands[i]);
+    const int tg = std::get<1>(cands[i]), ug = std::get<2>(cands[i]), h = std::get<3>(cands[i]);
     {
       std::lock_guard<std::mutex> lk(plan_registry_mu());
-      plan_registry()[plan_key(g, 0)] = {tg, ug};
+      plan_registry()[plan_key(g, 0)] = PlanChoice(tg, ug, h);
     }
     Plan pl = make_plan(g);
-    if (!pl.ok || pl.n_tg != tg || pl.n_ug != ug) continue;
+    if (!pl.ok || pl.n_tg != tg || pl.n_ug != ug || pl.hier != h) continue;
     void* ws = nullptr;
     if ((err = cudaMalloc(&ws, pl.ws_total())) != cudaSuccess) break;
     cudaMemsetAsync(ws, 0, pl.ws_total(), st);
@@ -1668,25 +1757,26 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
     float ms = 0.f;
     if (err == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
     cudaFree(ws);
-    if (err == cudaSuccess && ms < best_ms) { best_ms = ms; best_tg = tg; best_ug = ug; }
+    if (err == cudaSuccess && ms < best_ms) { best_ms = ms; best_tg = tg; best_ug = ug; best_h = h; }
   }
   cudaFree(imp);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   {
     std::lock_guard<std::mutex> lk(plan_registry_mu());
-    plan_registry()[plan_key(g, 0)] = {best_tg, best_ug};
+    plan_registry()[plan_key(g, 0)] = PlanChoice(best_tg, best_ug, best_h);
   }
   *tg_out = best_tg;
   *ug_out = best_ug;
+  *hier_out = best_h;
   *ms_out = best_ms / 5.f;
   return err;
 }
 
-bool fused_set_plan(const Geom& g, int n_tg, int n_ug) {
+bool fused_set_plan(const Geom& g, int n_tg, int n_ug, int hier) {
   std::lock_guard<std::mutex> lk(plan_registry_mu());
   if (n_tg <= 0) { plan_registry().erase(plan_key(g, 0)); return true; }
-  plan_registry()[plan_key(g, 0)] = {n_tg, n_ug};
+  plan_registry()[plan_key(g, 0)] = PlanChoice(n_tg, n_ug, hier);
   return true;
 }
 
@@ -1715,21 +1805,21 @@ cudaError_t fused_score_acc(const __nv_bfloat16* Q, const __nv_bfloat16* K, cons
 }
 
 size_t fused_peer_buffer_bytes(const Geom& g, int world, int sm_budget) {
-  Plan pl = make_plan(g, true, sm_budget);
+  Plan pl = make_plan(g, true, sm_budget, nullptr, world);
   if (!pl.ok) return 0;
-  return align256(2 * (size_t)g.B * pl.U * pl.NCP * pl.n_tg * world * sizeof(unsigned long long));
+  return align256(2 * (size_t)g.B * pl.U * pl.NCP * world * sizeof(unsigned long long));   // rank words
 }
 
-size_t fused_peer_ws_bytes(const Geom& g, int sm_budget) {
-  Plan pl = make_plan(g, true, sm_budget);
+size_t fused_peer_ws_bytes(const Geom& g, int world, int sm_budget) {
+  Plan pl = make_plan(g, true, sm_budget, nullptr, world);
   return pl.ok ? pl.ws_total() : 0;
 }
 
-bool fused_peer_plan_info(const Geom& g, int sm_budget, long long out[9]) {
-  Plan pl = make_plan(g, true, sm_budget);
+bool fused_peer_plan_info(const Geom& g, int world, int sm_budget, long long out[kPlanInfo]) {
+  Plan pl = make_plan(g, true, sm_budget, nullptr, world);
   if (!pl.ok) return false;
   out[0] = std::min<long long>(pl.P, pl.total_jobs); out[1] = pl.J; out[2] = pl.n_tg; out[3] = pl.n_ug;
-  out[4] = pl.tpc; out[5] = pl.upc; out[6] = pl.nslots; out[7] = pl.stages; out[8] = pl.smem;
+  out[4] = pl.tpc; out[5] = pl.upc; out[6] = pl.nslots; out[7] = pl.stages; out[8] = pl.smem; out[9] = pl.hier;
   return true;
 }
 

@@ -215,18 +215,19 @@ size_t sp_score_peer_buffer_bytes(const sp_geom* g, int32_t world, int32_t sm_bu
   return fused_peer_buffer_bytes(to_geom(*g), world, sm_budget);
 }
 
-size_t sp_score_peer_workspace_bytes(const sp_geom* g, int32_t sm_budget) {
+size_t sp_score_peer_workspace_bytes(const sp_geom* g, int32_t world, int32_t sm_budget) {
   if (check_geom(g) != SP_OK) return 0;
-  return fused_peer_ws_bytes(to_geom(*g), sm_budget);
+  if (world < 1 || world > 8) return 0;
+  return fused_peer_ws_bytes(to_geom(*g), world, sm_budget);
 }
 
-sp_status sp_score_peer_plan(const sp_geom* g, int32_t sm_budget, int64_t out[9]) {
+sp_status sp_score_peer_plan(const sp_geom* g, int32_t world, int32_t sm_budget, int64_t out[10]) {
   sp_status s = check_geom(g);
   if (s != SP_OK) return s;
-  if (out == nullptr) return SP_EINVAL;
-  long long o[9];
-  if (!fused_peer_plan_info(to_geom(*g), sm_budget, o)) return SP_EUNSUPPORTED;
-  for (int i = 0; i < 9; ++i) out[i] = o[i];
+  if (out == nullptr || world < 1 || world > 8) return SP_EINVAL;
+  long long o[kPlanInfo];
+  if (!fused_peer_plan_info(to_geom(*g), world, sm_budget, o)) return SP_EUNSUPPORTED;
+  for (int i = 0; i < kPlanInfo; ++i) out[i] = o[i];
   return SP_OK;
 }
 
@@ -245,7 +246,7 @@ sp_status sp_score_peer(const void* Q, const void* K, const sp_geom* g, const sp
   const Geom G = to_geom(*g);
   const Layout Lay = to_layout(*lay);
   if (!fused_supported(G, Lay, Q, K)) return SP_EUNSUPPORTED;
-  const size_t need = fused_peer_ws_bytes(G, sm_budget);
+  const size_t need = fused_peer_ws_bytes(G, world, sm_budget);
   if (need == 0) return SP_EUNSUPPORTED;
   if (ws == nullptr || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return SP_EWORKSPACE;
   return from_cuda(fused_score_peer(reinterpret_cast<const __nv_bfloat16*>(Q),
@@ -274,14 +275,14 @@ size_t sp_score_e4m3_workspace_bytes(const sp_geom* g) {
   return fused_supported(G, Layout{}, nullptr, nullptr) ? fused_score_ws_bytes(G) : 0;
 }
 
-sp_status sp_score_e4m3_plan(const sp_geom* g, int64_t out[9]) {
+sp_status sp_score_e4m3_plan(const sp_geom* g, int64_t out[10]) {
   Geom G;
   sp_status s = e4m3_geom(g, 1.f, 1.f, &G);
   if (s != SP_OK) return s;
   if (out == nullptr) return SP_EINVAL;
-  long long o[9];
+  long long o[kPlanInfo];
   if (!fused_plan_info(G, o)) return SP_EUNSUPPORTED;
-  for (int i = 0; i < 9; ++i) out[i] = o[i];
+  for (int i = 0; i < kPlanInfo; ++i) out[i] = o[i];
   return SP_OK;
 }
 
@@ -390,7 +391,7 @@ sp_status sp_score_paged_e4m3(const void* Q8, const sp_paged_k* K, float q_scale
   return score_paged_impl(Q8, K, g, lay, importance, ws, ws_bytes, stream, 1, q_scale, k_scale);
 }
 
-sp_status sp_score_tune(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, int64_t out[2],
+sp_status sp_score_tune(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, int64_t out[3],
                         float* ms_per_launch, sp_stream stream) {
   sp_status s = check_geom(g);
   if (s != SP_OK) return s;
@@ -399,17 +400,17 @@ sp_status sp_score_tune(const void* Q, const void* K, const sp_geom* g, const sp
   const Geom G = to_geom(*g);
   const Layout Lay = to_layout(*lay);
   if (!fused_supported(G, Lay, Q, K)) return SP_EUNSUPPORTED;
-  int tg = 0, ug = 0;
+  int tg = 0, ug = 0, h = 0;
   float ms = 0.f;
   s = from_cuda(fused_tune(reinterpret_cast<const __nv_bfloat16*>(Q), reinterpret_cast<const __nv_bfloat16*>(K), G,
-                           Lay, reinterpret_cast<cudaStream_t>(stream), &tg, &ug, &ms));
-  if (out != nullptr) { out[0] = tg; out[1] = ug; }
+                           Lay, reinterpret_cast<cudaStream_t>(stream), &tg, &ug, &h, &ms));
+  if (out != nullptr) { out[0] = tg; out[1] = ug; out[2] = h; }
   if (ms_per_launch != nullptr) *ms_per_launch = ms;
   return s;
 }
 
 sp_status sp_score_e4m3_tune(const void* Q8, const void* K8, float q_scale, float k_scale, const sp_geom* g,
-                             const sp_layout* lay, int64_t out[2], float* ms_per_launch, sp_stream stream) {
+                             const sp_layout* lay, int64_t out[3], float* ms_per_launch, sp_stream stream) {
   Geom G;
   sp_status s = e4m3_geom(g, q_scale, k_scale, &G);
   if (s != SP_OK) return s;
@@ -417,30 +418,30 @@ sp_status sp_score_e4m3_tune(const void* Q8, const void* K8, float q_scale, floa
   if ((s = check_device()) != SP_OK) return s;
   const Layout Lay = to_layout(*lay);
   if (!fused_supported(G, Lay, Q8, K8)) return SP_EUNSUPPORTED;
-  int tg = 0, ug = 0;
+  int tg = 0, ug = 0, h = 0;
   float ms = 0.f;
   s = from_cuda(fused_tune(reinterpret_cast<const __nv_bfloat16*>(Q8), reinterpret_cast<const __nv_bfloat16*>(K8), G,
-                           Lay, reinterpret_cast<cudaStream_t>(stream), &tg, &ug, &ms));
-  if (out != nullptr) { out[0] = tg; out[1] = ug; }
+                           Lay, reinterpret_cast<cudaStream_t>(stream), &tg, &ug, &h, &ms));
+  if (out != nullptr) { out[0] = tg; out[1] = ug; out[2] = h; }
   if (ms_per_launch != nullptr) *ms_per_launch = ms;
   return s;
 }
 
-sp_status sp_score_set_plan(const sp_geom* g, int32_t n_tg, int32_t n_ug) {
+sp_status sp_score_set_plan(const sp_geom* g, int32_t n_tg, int32_t n_ug, int32_t hier) {
   sp_status s = check_geom(g);
   if (s != SP_OK) return s;
-  if (n_tg > 0 && n_ug < 1) return SP_EINVAL;
-  fused_set_plan(to_geom(*g), n_tg, n_ug);
+  if (n_tg > 0 && (n_ug < 1 || hier < 0 || hier > 1)) return SP_EINVAL;
+  fused_set_plan(to_geom(*g), n_tg, n_ug, hier);
   return SP_OK;
 }
 
-sp_status sp_score_plan(const sp_geom* g, int64_t out[9]) {
+sp_status sp_score_plan(const sp_geom* g, int64_t out[10]) {
   sp_status s = check_geom(g);
   if (s != SP_OK) return s;
   if (out == nullptr) return SP_EINVAL;
-  long long o[9];
+  long long o[kPlanInfo];
   if (!fused_plan_info(to_geom(*g), o)) return SP_EUNSUPPORTED;
-  for (int i = 0; i < 9; ++i) out[i] = o[i];
+  for (int i = 0; i < kPlanInfo; ++i) out[i] = o[i];
   return SP_OK;
 }
 

@@ -80,8 +80,10 @@ cudaError_t simt_score_finish(const __nv_bfloat16* Q, const __nv_bfloat16* K, co
 
 // ---------------------------------------------------------------- fused tcgen05 score (score_fused.cu)
 bool fused_supported(const Geom& g, const Layout& lay, const void* Q, const void* K);
+// plan summary: grid, jobs/request, n_tg, n_ug, tiles/job, units/job, TMEM slots, stages, SMEM bytes, hier
+constexpr int kPlanInfo = 10;
 size_t fused_score_ws_bytes(const Geom& g);
-bool fused_plan_info(const Geom& g, long long out[9]);
+bool fused_plan_info(const Geom& g, long long out[kPlanInfo]);
 void fused_set_trace(unsigned long long* buf, long long records);
 cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                         float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
@@ -97,12 +99,12 @@ size_t fused_la_ws_bytes(const Geom& g);
 cudaError_t fused_score_la(const __nv_bfloat16* Q, const __nv_bfloat16* K, const LookaheadK& la, const Geom& g,
                            const Layout& lay, float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
-                       cudaStream_t st, int* tg_out, int* ug_out, float* ms_out);
-bool fused_set_plan(const Geom& g, int n_tg, int n_ug);
+                       cudaStream_t st, int* tg_out, int* ug_out, int* hier_out, float* ms_out);
+bool fused_set_plan(const Geom& g, int n_tg, int n_ug, int hier);
 cudaError_t acc_importance(const float* acc2, int B, int Rv, long long N, float* importance, cudaStream_t st);
 size_t fused_peer_buffer_bytes(const Geom& g, int world, int sm_budget);
-size_t fused_peer_ws_bytes(const Geom& g, int sm_budget);
-bool fused_peer_plan_info(const Geom& g, int sm_budget, long long out[9]);
+size_t fused_peer_ws_bytes(const Geom& g, int world, int sm_budget);
+bool fused_peer_plan_info(const Geom& g, int world, int sm_budget, long long out[kPlanInfo]);
 cudaError_t fused_score_peer(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                              int rank, int world, void* const* bufs, int sm_budget, float* importance, void* ws,
                              size_t ws_bytes, cudaStream_t st);

@@ -182,7 +182,7 @@ def _peer_buffers(Q, K_local, R_valid, group):
         buf.zero_()
         pg = group if group is not None else dist.group.WORLD
         hdl = symm_mem.rendezvous(buf, pg.group_name)
-        ws = torch.zeros(max(256, api.score_peer_workspace_bytes(Q, K_local, 0, R_valid)), dtype=torch.uint8,
+        ws = torch.zeros(max(256, api.score_peer_workspace_bytes(Q, K_local, world, 0, R_valid)), dtype=torch.uint8,
                          device=K_local.device)
         torch.cuda.synchronize()
         dist.barrier(group)

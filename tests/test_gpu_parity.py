@@ -471,6 +471,6 @@ def test_tune_registers_a_valid_plan():
     g, _ = sp.make_geom(Q, K, w.Rv)
     import ctypes as C
     g = C.byref(g)
-    assert sp.lib().sp_score_set_plan(g, 0, 0) == 0
+    assert sp.lib().sp_score_set_plan(g, 0, 0, 0) == 0
     cleared = sp.score_plan(Q, K, w.Rv)
     assert (cleared["token_groups"], cleared["unit_groups"]) == (before["token_groups"], before["unit_groups"])

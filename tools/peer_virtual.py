@@ -21,7 +21,7 @@ def run(w, P, iters=3, check=None):
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     budget = sms // P
     shards = [K[:, :, :, p * n:(p + 1) * n] for p in range(P)]
-    plan = sp.score_peer_plan(Q, shards[0], budget, w.Rv)
+    plan = sp.score_peer_plan(Q, shards[0], P, budget, w.Rv)
     nb = sp.score_peer_buffer_bytes(Q, shards[0], P, budget, w.Rv)
     bufs = [torch.zeros(nb, dtype=torch.uint8, device="cuda") for _ in range(P)]
     ptrs = [b.data_ptr() for b in bufs]
