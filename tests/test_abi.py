@@ -189,8 +189,7 @@ def test_fused_plan_invariants(name, variant):
         assert P % J == 0                      # a request never straddles two waves
     assert pl["tiles_per_job"] <= pl["tmem_slots"]
     assert 2 <= pl["stages"] and pl["smem_bytes"] <= 232448
-    if name == "C3" and not variant:
-        assert (pl["token_groups"], pl["unit_groups"]) == (37, 4)   # the plan the bench line is quoted on
+    assert pl["hier"] in (0, 1)
 
 
 # ---------------------------------------------------------------- rows f3 / f4 host-side validation
