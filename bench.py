@@ -465,12 +465,10 @@ def run_ours(args):
                             "(one CTA per SM) and 128-bit ld.global.nc read-xor (spgen/probe.cu), CUDA events"}
     roofline["read_peak"] = read_peak
 
-    # select_gather is one launch, or two for long prompts (phase A over the SMs,
-    # then B-C): the rule of launch_select() in csrc/select.cu
+    # select_gather is one launch (phase A over several CTAs for long prompts, the
+    # last of them continuing with the top-K: launch_select() in csrc/select.cu)
     def sel_launches(n_tok):
-        n_c = -(-n_tok // w.chunk)
-        cpb = max(1, 2048 // w.chunk)
-        return 2 if 4 <= -(-n_c // cpb) <= 65535 else 1
+        return 1
     if seq:
         n_loc = w.N // world
         sel = (1 if w.pool_k > 1 else 0) + sel_launches(n_loc) + 1         # edges, candidates, merge

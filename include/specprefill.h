@@ -334,7 +334,11 @@ sp_status sp_score_paged_e4m3(const void* Q8, const sp_paged_k* K, float q_scale
  *   ids  = ascending union of the kept chunks' token indices                  (Z11)
  *   pos  = ids + pos0;  the first decode position is N + pos0
  * importance: device fp32 [B][N].  ids, pos: device int32 [B][N] (capacity N per
- * request; entries >= n_kept[b] are left untouched).  n_kept: device int32 [B]. */
+ * request; entries >= n_kept[b] are left untouched).  n_kept: device int32 [B].
+ * Workspace: sp_select_workspace_bytes bytes, zero-filled once before first use
+ * (it holds per-request completion counters that the kernel leaves at zero),
+ * not shared by concurrent calls.  One launch, programmatic-dependent on the
+ * preceding kernel of the stream (it waits for that kernel's results inside). */
 size_t sp_select_workspace_bytes(int32_t B, int64_t N, const sp_select_params* p);
 sp_status sp_select(const float* importance, int32_t B, int64_t N, const sp_select_params* p,
                     int32_t* ids, int32_t* pos, int32_t* n_kept, void* ws, size_t ws_bytes,

@@ -671,6 +671,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // every CTA is resident (cooperative launch): a programmatic dependent (the
+  // selection) may be scheduled now and waits for this grid in griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;");
   const uint32_t tmem = *tmem_base_s;
   const uint32_t nslots = (uint32_t)p.nslots;
   // this launch publishes into part[parity]; part[parity ^ 1] (the previous

@@ -12,9 +12,11 @@
 // over its true size (Z8), K_c from the exact ppm rule (Z9, computed on the
 // host), ties to the lowest chunk index (Z10), ascending ids (Z11).
 //
-// Phase A can run on many CTAs per request (kModeA: grid (B, chunk blocks),
-// writing cs to the workspace), phases B-C on one CTA of 1024 threads per
-// request (kModeBC); short prompts run all three in one launch (kModeAll):
+// One launch.  Phase A can run on many CTAs per request (kModeA: grid (B, chunk
+// blocks), writing cs to the workspace), the request's last CTA to finish it
+// continuing with phases B-C (1024 threads); short prompts run all three on one
+// CTA per request (kModeAll).  Launched as a programmatic dependent of the
+// score kernel (its prologue overlaps the score kernel's tail):
 //   A. importance is staged in shared memory segment by segment (all loads of a
 //      segment in flight together), pooled, and summed per chunk (a canonical
 //      order that depends only on the chunk: segments are chunk-aligned, so the
@@ -50,11 +52,12 @@ constexpr int SEG = 16384;          // tokens of importance staged in SMEM per s
 constexpr int kMaxPool = 4097;      // largest pooling window (half-window staged on each side)
 constexpr int kSmemChunks = 8192;   // chunk scores kept in SMEM when n_c fits (else L2-resident workspace)
 constexpr unsigned kInvalid = 0xFFFFFFFFu;   // merge: chunk with no candidate (never a score: scores are >= 0)
-enum SelectMode : int { kModeAll = 0, kModeA = 1, kModeBC = 2 };
+enum SelectMode : int { kModeAll = 0, kModeA = 1 };
 enum Variant : int { kPlain = 0, kCand = 1, kMerge = 2 };
 
 struct SelArgs {
   const float* imp;          // [B][row] importance (kCand: this rank's shard)
+  unsigned* blk_cnt;         // [B] kModeA: phase-A CTAs done (workspace, zero, self-resetting)
   long long row;             // row length of imp / ids / pos / tokens / out
   const int* seq_lens;       // kPlain, optional [B]: per-request prompt length (row f3)
   int pool_k, chunk, pos0;
@@ -133,6 +136,12 @@ __global__ void __launch_bounds__(ST) k_select(SelArgs a) {
   __shared__ ScanSmem scan;
   __shared__ int kept_c[ST];                      // kept chunk ids of one scan tile, in order
   __shared__ int kept_off[ST];
+  __shared__ int s_last;
+  // programmatic dependent launch: this grid may start while the producer of
+  // the importance (the score kernel) is finishing; wait for its results here,
+  // then let the next dependent launch begin its own prologue
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   const int mode = a.mode, chunk = a.chunk, pool_k = a.pool_k;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long Nrow = a.row;
@@ -153,7 +162,7 @@ __global__ void __launch_bounds__(ST) k_select(SelArgs a) {
   const long long w = (pool_k - 1) / 2;
   // chunk scores: SMEM when this CTA runs phases B-C and n_c fits, else the workspace
   // (decided on the row's chunk count, as the launch sized the SMEM: a ragged request may have fewer)
-  const bool cs_smem = mode != kModeA && n_c_row <= kSmemChunks;
+  const bool cs_smem = mode == kModeAll && n_c_row <= kSmemChunks;
   float* cs = cs_smem ? seg + 2 * a.segcap + 2 * w : a.cs_ws + (long long)b * n_c_row;
 
   if (V == kMerge) {
@@ -170,10 +179,6 @@ __global__ void __launch_bounds__(ST) k_select(SelArgs a) {
         if (c < (unsigned long long)n_c) csu[c] = (unsigned)(key >> 32);
       }
     }
-    __syncthreads();
-  } else if (mode == kModeBC) {
-    if (cs_smem)
-      for (long long c = tid; c < n_c; c += ST) cs[c] = a.cs_ws[(long long)b * n_c_row + c];
     __syncthreads();
   } else {
   // ---- A. pooled scores (centred window, shrinking edges) -> chunk sums of
@@ -289,7 +294,23 @@ __global__ void __launch_bounds__(ST) k_select(SelArgs a) {
   }
   __syncthreads();
   }
-  if (mode == kModeA) return;
+  if (mode == kModeA) {
+    // the request's last phase-A CTA to finish runs phases B-C (one launch for
+    // the whole selection): every CTA publishes its chunk scores, then counts
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(a.blk_cnt + b, 1u) + 1u == gridDim.y;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (tid == 0) a.blk_cnt[b] = 0u;                                     // self-resetting for the next call
+    if (n_c_row <= kSmemChunks) {                                       // the launch sized SMEM for it
+      float* cs_s = seg + 2 * a.segcap + 2 * w;
+      for (long long c = tid; c < n_c; c += ST) cs_s[c] = __ldcg(cs + c);
+      cs = cs_s;
+    }
+    __syncthreads();
+  }
 
   // ---- B. radix select: threshold bit pattern T of the K_sel-th largest score.
   //      Up to kRankMax chunks the rank is counted directly instead:
@@ -443,8 +464,24 @@ cudaError_t configure() {
   return cudaSuccess;
 }
 
-// Phase A over `nblk` blocks of cpb chunks of each request (kModeA) then B-C
-// (kModeBC) for long ranges; one kModeAll launch otherwise.
+template <int V>
+cudaError_t launch_pdl(dim3 grid, size_t smem, cudaStream_t st, const SelArgs& a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(ST);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // overlap with the producer's tail
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_select<V>, a);
+}
+
+// Long ranges: phase A over `nblk` blocks of cpb chunks of each request
+// (kModeA), the last block of a request continuing with B-C; one kModeAll CTA
+// per request otherwise.  Either way one launch.
 template <int V>
 cudaError_t launch_select(SelArgs a, int B, long long n_tok, long long n_chunks, cudaStream_t st) {
   cudaError_t e = configure<V>();
@@ -454,32 +491,33 @@ cudaError_t launch_select(SelArgs a, int B, long long n_tok, long long n_chunks,
   constexpr long long kTokPerCta = 2048;
   const long long cpb = std::max(1LL, kTokPerCta / chunk);
   const long long nblk = (n_chunks + cpb - 1) / cpb;
+  const size_t cs_bytes = (size_t)(n_chunks <= kSmemChunks ? n_chunks : 0) * sizeof(float);
   if (V != kMerge && nblk >= 4 && nblk <= 65535) {
     const long long span = std::min(n_tok, cpb * chunk);
     a.segcap = chunk > SEG ? SEG : (int)std::min<long long>(SEG, (span + 31) / 32 * 32);
     a.cpb = cpb;
     a.mode = kModeA;
-    const size_t needA = (size_t)(2 * a.segcap + 2 * w) * sizeof(float);
-    k_select<V><<<dim3(B, (unsigned)nblk), ST, needA, st>>>(a);
-    a.mode = kModeBC;
-    const size_t needBC = (size_t)(2 * a.segcap + 2 * w + (n_chunks <= kSmemChunks ? n_chunks : 0)) * sizeof(float);
-    k_select<V><<<B, ST, needBC, st>>>(a);
-    return cudaGetLastError();
+    return launch_pdl<V>(dim3(B, (unsigned)nblk), (size_t)(2 * a.segcap + 2 * w) * sizeof(float) + cs_bytes, st, a);
   }
   a.segcap = SEG;
   a.cpb = n_chunks;
   a.mode = kModeAll;
-  const size_t need = (size_t)(2 * SEG + 2 * w + (n_chunks <= kSmemChunks ? n_chunks : 0)) * sizeof(float);
-  k_select<V><<<B, ST, need, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl<V>(dim3(B), (size_t)(2 * SEG + 2 * w) * sizeof(float) + cs_bytes, st, a);
 }
 
 }  // namespace
 
+// [B][n_c] chunk scores, then [B] phase-A completion counters (zero-filled once, self-resetting)
 size_t select_ws_bytes(int B, long long N, int chunk) {
   long long n_c = (N + chunk - 1) / chunk;
-  return align256((size_t)B * n_c * sizeof(float));
+  return align256((size_t)B * n_c * sizeof(float)) + align256((size_t)B * sizeof(unsigned));
 }
+
+namespace {
+unsigned* ws_counters(void* ws, int B, long long n_c_row) {
+  return reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + align256((size_t)B * n_c_row * sizeof(float)));
+}
+}  // namespace
 
 bool select_supported(int pool_k) { return pool_k <= kMaxPool; }
 
@@ -490,6 +528,7 @@ cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int 
   a.imp = imp; a.row = N; a.seq_lens = seq_lens; a.pool_k = pool_k; a.chunk = chunk; a.pos0 = pos0; a.ppm = ppm;
   a.ids = ids; a.pos = pos; a.n_kept = n_kept; a.cs_ws = reinterpret_cast<float*>(ws); a.tokens = tokens; a.out = out;
   a.n_glob = N;
+  a.blk_cnt = ws_counters(ws, B, (N + chunk - 1) / chunk);
   return launch_select<kPlain>(a, B, N, (N + chunk - 1) / chunk, st);
 }
 
@@ -500,7 +539,7 @@ long long seq_candidate_count(long long N, int world, int chunk, long long ppm) 
 }
 
 size_t seq_select_ws_bytes(int B, long long N, int world, int chunk) {
-  // kCand: the shard's chunk scores; kMerge: the prompt's (when above the SMEM limit)
+  // kCand: the shard's chunk scores; kMerge: the prompt's (when above the SMEM limit); counters
   (void)world;
   return select_ws_bytes(B, N, chunk);
 }
@@ -522,6 +561,7 @@ cudaError_t seq_candidates_launch(const float* imp_local, const float* edges, in
   a.ids = nullptr; a.pos = nullptr; a.cs_ws = reinterpret_cast<float*>(ws);
   a.i0 = (long long)rank * n_local; a.n_glob = N; a.edges = edges; a.rank = rank; a.world = world;
   a.k_sel = M; a.cand = cand;
+  a.blk_cnt = ws_counters(ws, B, (N + chunk - 1) / chunk);
   return launch_select<kCand>(a, B, n_local, n_local / chunk, st);
 }
 
@@ -532,6 +572,7 @@ cudaError_t seq_merge_launch(const unsigned long long* cand_all, int world, int 
   a.row = N; a.pool_k = pool_k; a.chunk = chunk; a.pos0 = pos0; a.ppm = ppm;
   a.ids = ids; a.pos = pos; a.n_kept = n_kept; a.cs_ws = reinterpret_cast<float*>(ws); a.tokens = tokens; a.out = out;
   a.n_glob = N; a.world = world; a.k_sel = M; a.cand_in = cand_all;
+  a.blk_cnt = ws_counters(ws, B, (N + chunk - 1) / chunk);
   return launch_select<kMerge>(a, B, N, (N + chunk - 1) / chunk, st);
 }
 
