@@ -99,8 +99,7 @@ struct FusedParams {
   // workspace
   unsigned long long* part;            // [2][B][U][n_tg][NCP] CTA partials, one buffer per launch parity:
                                        // (max2, sum) packed in one 64-bit word; 0 = "not yet written"
-  int hier;                            // hierarchical exchange: the unit's last CTA merges, the rest poll one word
-  unsigned* hcnt;                      // [B][U] hier: CTA partials published so far (reset by the merging CTA)
+  int hier;                            // hierarchical exchange: one CTA per unit merges, the rest poll one word
   unsigned* epoch;                     // [2] launch epoch (parity selects the partial buffer), CTAs done
   float* accpart;                      // [B][n_ug][Rv][N]
   unsigned* fin_cnt;                   // [B][n_tg]    finalize counters (self-cleaning)
@@ -113,11 +112,12 @@ struct FusedParams {
   int mode;                            // kModeFull / kModeStats (publish partials only) / kModeFinish (lse2 given)
   const float* lse_in;                 // kModeFinish: lse2 per row ((b*L + l)*H + h)*Rv + r
   // hierarchical exchange and its peer-memory form (sequence-sharded single pass):
-  // world ranks each score their own tokens; the last CTA of a unit on rank r to
-  // publish merges the rank's n_tg partials (token-group order) and stores the
-  // rank's word into row r of every rank's rank-word buffer; every CTA then
-  // polls the unit's `world` rank words and merges them in rank order (the same
-  // lse2 bits on every rank).  world = 1 with hier: one word, local.
+  // world ranks each score their own tokens; on rank r the unit's designated
+  // CTA (token group u mod n_tg: the merges are spread evenly over the CTAs)
+  // gathers the rank's n_tg partials (token-group order) and stores the rank's
+  // word into row r of every rank's rank-word buffer; every CTA then polls the
+  // unit's `world` rank words and merges them in rank order (the same lse2 bits
+  // on every rank).  world = 1 with hier: one word, local.
   int rank, world;
   unsigned long long* peer[kMaxPeers]; // every rank's rank-word buffer base ([2][B][U][world][NCP])
 };
@@ -557,53 +557,72 @@ __device__ __forceinline__ float transpose_add32(float (&s)[32], int lane) {
 // kSpinNs of globaltimer, well before mbar_wait_slow's 4 s trap.
 constexpr unsigned long long kSpinNs = 2000000000ull;
 
-// Hierarchical exchange, exchange warp (whole warp): after publishing this CTA's
-// partial words of unit ubase, count the arrival; the CTA that completes the
-// count merges the unit's n_tg partials in token-group order (all are visible:
-// each writer fenced before counting) into the rank word, stores it into row
-// `rank` of every rank's rank-word buffer (this launch's parity half), re-zeroes
-// the same row of the other half (read by nobody now; zero = "not yet written"
-// for the launch after next) and resets the counter.  Out of line: executed
-// once per unit.
-__device__ __noinline__ void hier_merge(const FusedParams& p, long long ubase, const unsigned long long* part_cur,
-                                        uint32_t parity, int NCP, int lane) {
-  unsigned old = 0;
-  __syncwarp();
-  if (lane == 0) {
-    __threadfence();                                           // release this CTA's partial words
-    old = atomicAdd(p.hcnt + ubase, 1u);
+// Poll `count` 64-bit partial words (stride NCP) of column c until all are
+// written (non-zero), merging them in index order.  Bounded: after kSpinNs the
+// missing words are merged as empty and SP_ETIMEOUT is flagged.
+__device__ __noinline__ float2 poll_merge(const FusedParams& p, const unsigned long long* src, int count, int NCP,
+                                          int c) {
+  float M = -CUDART_INF_F, S = 0.f;
+  for (int s0 = 0; s0 < count; s0 += kMaxLseBatch) {
+    unsigned long long v[kMaxLseBatch];
+    unsigned long long missing = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxLseBatch; ++j) {
+      v[j] = (s0 + j < count) ? ld_relaxed_sys_u64(src + (long long)(s0 + j) * NCP + c) : pack_ms(0.f, -1.f);
+      missing |= (v[j] == 0ull ? 1ull : 0ull) << j;
+    }
+    long long it = 0;
+    unsigned long long t_dead = 0;
+    while (__any_sync(0xffffffffu, missing != 0)) {
+      __nanosleep(it < 8 ? 64 : 200);
+#pragma unroll
+      for (int j = 0; j < kMaxLseBatch; ++j) {
+        if (missing & (1ull << j)) {
+          v[j] = ld_relaxed_sys_u64(src + (long long)(s0 + j) * NCP + c);
+          if (v[j] != 0ull) missing &= ~(1ull << j);
+        }
+      }
+      if ((++it & 1023) == 0 && t_dead == 0) t_dead = globaltimer_ns() + kSpinNs;
+      if (t_dead != 0 && (it & 1023) == 0 && globaltimer_ns() > t_dead) {
+        set_err(p.err, kDevTimeout);
+#pragma unroll
+        for (int j = 0; j < kMaxLseBatch; ++j)
+          if (missing & (1ull << j)) v[j] = pack_ms(0.f, -1.f);
+        missing = 0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxLseBatch; ++j) {
+      const float2 w = unpack_ms(v[j]);
+      if (w.y > 0.f) merge2(M, S, w.x, w.y);
+    }
   }
-  old = __shfl_sync(0xffffffffu, old, 0);
-  if (old + 1u != (unsigned)p.n_tg) return;
-  __threadfence();                                             // acquire the other CTAs' words
-  const unsigned long long* src = part_cur + ubase * p.n_tg * NCP;
+  return make_float2(M, S);
+}
+
+// Hierarchical exchange, gather warp (whole warp), unit ubase: the designated
+// CTA merges the rank's n_tg partials and publishes the rank word (row `rank`
+// of every rank's buffer, this launch's parity half; the same row of the other
+// half is re-zeroed for the launch after next); then every CTA merges the
+// `world` rank words in rank order into (max2, sum) per column, staged in ms.
+// Out of line: once per unit.
+__device__ __noinline__ void hier_gather(const FusedParams& p, long long ubase, bool designated,
+                                         const unsigned long long* part_cur, uint32_t parity, int NCP, int lane,
+                                         float2* ms) {
   const long long fin_half = (long long)p.B * p.U * p.world * NCP;
-  const long long row = (ubase * p.world + p.rank) * NCP;
+  const long long row = ubase * p.world * NCP;
   for (int c = lane; c < NCP; c += 32) {
-    float M = -CUDART_INF_F, S = 0.f;
-    for (int s0 = 0; s0 < p.n_tg; s0 += 16) {
-      unsigned long long v[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = s0 + j < p.n_tg ? ld_relaxed_u64(src + (long long)(s0 + j) * NCP + c) : 0ull;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float2 w = unpack_ms(v[j]);
-        if (s0 + j < p.n_tg && w.y > 0.f) merge2(M, S, w.x, w.y);
+    float2 mine = make_float2(-CUDART_INF_F, 0.f);
+    if (designated) {
+      mine = poll_merge(p, part_cur + ubase * p.n_tg * NCP, p.n_tg, NCP, c);
+      const unsigned long long word = mine.y > 0.f ? pack_ms(mine.x, mine.y) : pack_ms(-CUDART_INF_F, -1.f);
+      for (int r = 0; r < p.world; ++r) {                     // NVLink stores to the peers (world > 1)
+        st_relaxed_sys_u64(p.peer[r] + parity * fin_half + row + (long long)p.rank * NCP + c, word);
+        p.peer[r][(parity ^ 1u) * fin_half + row + (long long)p.rank * NCP + c] = 0ull;
       }
     }
-    const unsigned long long word = S > 0.f ? pack_ms(M, S) : pack_ms(-CUDART_INF_F, -1.f);   // never 0
-    if (p.world == 1) {
-      st_relaxed_u64(p.peer[0] + parity * fin_half + row + c, word);
-      p.peer[0][(parity ^ 1u) * fin_half + row + c] = 0ull;
-    } else {
-      for (int r = 0; r < p.world; ++r) {                      // NVLink stores to the peers
-        st_relaxed_sys_u64(p.peer[r] + parity * fin_half + row + c, word);
-        p.peer[r][(parity ^ 1u) * fin_half + row + c] = 0ull;
-      }
-    }
+    ms[c] = (p.world == 1 && designated) ? mine : poll_merge(p, p.peer[p.rank] + parity * fin_half + row, p.world, NCP, c);
   }
-  __syncwarp();
-  if (lane == 0) atomicExch(p.hcnt + ubase, 0u);
 }
 
 // kG: compile-time GQA group size (1, 2, 4, 8) or 0 for any G.  One
@@ -925,7 +944,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           mbar_arrive(bar_rempty + 8 * (ui & 1));
           trace_stamp(p, ui, 3);
         }
-        if (p.hier && p.mode == kModeFull) hier_merge(p, ubase, part_cur, parity, NCP, lane);
       }
     }
     // re-zero this CTA's rows of the previous launch's buffer (read by nobody now)
@@ -951,21 +969,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const long long ubase = (long long)jb.b * p.U + u;
         mbar_wait(bar_lempty + 8 * par, ((ui / kLseRing) & 1) ^ 1);    // aggregation done with ls[par]
         float* ls = lse_s + par * NCP;
-        // flat: the unit's n_tg CTA partials; hierarchical: its `world` rank words
-        const unsigned long long* src = p.hier ? p.peer[p.rank] + parity * ((long long)p.B * p.U * p.world * NCP)
-                                                     + ubase * p.world * NCP
-                                               : part_cur + ubase * p.n_tg * NCP;
-        const int ntg = p.hier ? p.world : p.n_tg;
-        for (int c = lane; c < NCP && p.mode == kModeFinish; c += 32) {
-          // lse2 supplied by the caller (sequence-sharded split: globally combined statistics)
-          float l2 = 0.f;
-          if (c < p.NC) {
-            const int l = u / p.Hkv, g = u % p.Hkv;
-            l2 = p.lse_in[(((long long)jb.b * p.L + l) * p.Hkv * p.G + g * p.G + c % p.G) * p.Rv + c / p.G];
+        const unsigned long long* src = part_cur + ubase * p.n_tg * NCP;
+        const int ntg = p.n_tg;
+        if (p.hier && p.mode == kModeFull) {
+          float2* ms = reinterpret_cast<float2*>(smem + p.off_comb);              // [NCP] (max2, sum)
+          hier_gather(p, ubase, (int)(u % p.n_tg) == jb.tg, part_cur, parity, NCP, lane, ms);
+          __syncwarp();
+          for (int c = lane; c < NCP; c += 32) {
+            float M = ms[c].x, S = ms[c].y;
+            if (p.la != nullptr && c < p.NC) {
+              const float2 v = p.la[ubase * NCP + c];
+              if (v.y > 0.f) merge2(M, S, v.x, v.y);
+            }
+            float l2 = 0.f;
+            if (c < p.NC) {
+              l2 = M + log2f(S);
+              if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
+            }
+            ls[c] = l2;
           }
-          ls[c] = l2;
         }
-        for (int c = lane; c < NCP && p.mode == kModeFull; c += 32) {
+        for (int c = lane; c < NCP && p.mode == kModeFull && !p.hier; c += 32) {
           float M = -CUDART_INF_F, S = 0.f;
           for (int s0 = 0; s0 < ntg; s0 += kMaxLseBatch) {
             unsigned long long v[kMaxLseBatch];
@@ -1199,8 +1223,8 @@ struct Plan {
   uint32_t k_stage_bytes = 0, q_slot_bytes = 0;
   int nq = 2;
   int hier = 0, world = 1;                            // hierarchical exchange; ranks of a peer exchange
-  size_t ws_part = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0, ws_hcnt = 0, ws_rank = 0;
-  size_t ws_total() const { return ws_part + ws_cnt + ws_acc + ws_fin + ws_hcnt + ws_rank; }
+  size_t ws_part = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0, ws_rank = 0;
+  size_t ws_total() const { return ws_part + ws_cnt + ws_acc + ws_fin + ws_rank; }
   bool ok = false;
 };
 
@@ -1318,15 +1342,16 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
         if (force_h >= 0 && hier != force_h) continue;
         if (world > 1 && hier == 0) continue;
         // flat: every CTA polls the unit's n_tg partials (batches of kMaxLseBatch);
-        // hierarchical: the unit's last CTA merges them (one more L2 hop, + an
-        // NVLink hop when world > 1) and every CTA polls `world` rank words
-        const int batches = hier ? (world + kMaxLseBatch - 1) / kMaxLseBatch : (n_tg + kMaxLseBatch - 1) / kMaxLseBatch;
-        const double L_us = 5.0 + 0.8 * batches + (hier ? 1.5 + 0.25 * ((n_tg + 15) / 16) : 0.0) +
-                            (world > 1 ? 2.0 : 0.0);
+        // hierarchical: one CTA per unit (round robin) polls them and publishes
+        // the rank word (one more hop, + an NVLink hop when world > 1), every CTA
+        // polls the unit's `world` rank words
+        const int bf = (n_tg + kMaxLseBatch - 1) / kMaxLseBatch, br = (world + kMaxLseBatch - 1) / kMaxLseBatch;
+        const double L_us = 5.0 + 0.8 * (hier ? bf + br : bf) + (hier ? 1.0 : 0.0) + (world > 1 ? 2.0 : 0.0);
+        const double gather_us = 1.6 * (hier ? (double)bf / n_tg + br : bf);
         const int W = std::max(1, pl.nslots / tpc);
         const double exposed = std::max(0.0, L_us - (W - 1) * tpc * tile_us);
         // (+0.4 us fixed per unit: Q load, statistics merge and publish)
-        const double per_unit = std::max(tpc * tile_us + exposed / W + 0.4, 1.6 * batches);
+        const double per_unit = std::max(tpc * tile_us + exposed / W + 0.4, gather_us);
         double cost = upc * per_unit + L_us;                                   // + pipeline fill
         if (n_ug > 1)                                                          // cross-group max + its sync
           cost += 2.0 * g.Rv * tpc * kTileM * 4.0 / kSmHbmBytesPerUs + 5.0 + 0.25 * n_ug;
@@ -1359,7 +1384,6 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   pl.ws_cnt = 256;                                   // launch epoch + CTAs-done counter
   pl.ws_acc = pl.n_ug > 1 ? align256((size_t)g.B * pl.n_ug * g.Rv * g.N * sizeof(float)) : 0;
   pl.ws_fin = align256((size_t)g.B * pl.n_tg * sizeof(unsigned));
-  pl.ws_hcnt = align256((size_t)g.B * pl.U * sizeof(unsigned));
   pl.ws_rank = world == 1 ? align256(2 * (size_t)g.B * pl.U * pl.NCP * sizeof(unsigned long long)) : 0;
   pl.ok = true;
   return pl;
@@ -1581,8 +1605,6 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   w += pl.ws_part;
   p.accpart = pl.ws_acc ? reinterpret_cast<float*>(w) : nullptr;
   w += pl.ws_acc;
-  p.hcnt = reinterpret_cast<unsigned*>(w);
-  w += pl.ws_hcnt;
   p.hier = pl.hier;
   p.rank = peer.rank;
   p.world = peer.world;

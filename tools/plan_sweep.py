@@ -45,10 +45,16 @@ def sweep(name, plans, kv="bf16"):
             continue
         for _ in range(4):
             run()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()                     # 20 launches in one graph: no host overhead
+        with torch.cuda.graph(g):
+            for _ in range(20):
+                run()
+        g.replay()
+        torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        for _ in range(20):
-            run()
+        g.replay()
         b.record()
         torch.cuda.synchronize()
         sp.check_device_error()
