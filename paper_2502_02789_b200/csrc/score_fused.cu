@@ -1309,7 +1309,7 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   if (const char* env = allow_override ? std::getenv("SP_FUSED_PLAN") : nullptr) {
     const int n = std::sscanf(env, "%d,%d,%d", &force_tg, &force_ug, &force_h);
     if (n < 2) force_tg = force_ug = 0;
-    if (n < 3) force_h = -1;
+    if (n == 2) force_h = 0;                               // "n_tg,n_ug": the flat exchange
   }
   if (allow_override && force_tg == 0 && world == 1) {   // a measured choice for this geometry
     std::lock_guard<std::mutex> lk(plan_registry_mu());

@@ -42,6 +42,7 @@
 #include "sp_internal.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace sp {
 namespace {
@@ -464,6 +465,13 @@ cudaError_t configure() {
   return cudaSuccess;
 }
 
+// Development A/B knobs (timing only): SP_SELECT_NO_PDL=1 launches without the
+// programmatic-dependent attribute.
+bool select_pdl() {
+  static const bool on = std::getenv("SP_SELECT_NO_PDL") == nullptr;
+  return on;
+}
+
 template <int V>
 cudaError_t launch_pdl(dim3 grid, size_t smem, cudaStream_t st, const SelArgs& a) {
   cudaLaunchConfig_t cfg = {};
@@ -475,7 +483,7 @@ cudaError_t launch_pdl(dim3 grid, size_t smem, cudaStream_t st, const SelArgs& a
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // overlap with the producer's tail
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = select_pdl() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k_select<V>, a);
 }
 
