@@ -13,9 +13,10 @@
 //   job = (request, token group, unit group).  All jobs of one request run in
 //   the same wave of CTAs, so every CTA that shares a unit is co-resident.
 // * Warp roles (384 threads): warp 0 TMA producer, warp 1 tcgen05.mma issuer
-//   (+TMEM owner), warp 2 statistics exchange, warp 3 lse2 gather, warps 4-7
-//   softmax statistics, warps 8-11 max-aggregation.  The TMA/MMA warps run
-//   warp-uniform loops and issue from one elected lane.
+//   (+TMEM owner), warp 2 statistics exchange (+ the rank merges of the
+//   hierarchical exchange), warp 3 lse2 gather, warps 4-7 softmax statistics,
+//   warps 8-11 max-aggregation.  The TMA/MMA warps run warp-uniform loops and
+//   issue from one elected lane.
 // * K tiles [128 tokens x d] bf16 stream HBM -> SMEM by TMA (swizzled); the
 //   unit's query block [G*Rv x d] is the MMA B operand; each tile's logits
 //   D[128 x NCP] fp32 go to the next slot of a 16-slot TMEM ring and stay
@@ -600,28 +601,92 @@ __device__ __noinline__ float2 poll_merge(const FusedParams& p, const unsigned l
   return make_float2(M, S);
 }
 
-// Hierarchical exchange, gather warp (whole warp), unit ubase: the designated
-// CTA merges the rank's n_tg partials and publishes the rank word (row `rank`
-// of every rank's buffer, this launch's parity half; the same row of the other
-// half is re-zeroed for the launch after next); then every CTA merges the
-// `world` rank words in rank order into (max2, sum) per column, staged in ms.
-// Out of line: once per unit.
-__device__ __noinline__ void hier_gather(const FusedParams& p, long long ubase, bool designated,
-                                         const unsigned long long* part_cur, uint32_t parity, int NCP, int lane,
-                                         float2* ms) {
-  const long long fin_half = (long long)p.B * p.U * p.world * NCP;
-  const long long row = ubase * p.world * NCP;
-  for (int c = lane; c < NCP; c += 32) {
-    float2 mine = make_float2(-CUDART_INF_F, 0.f);
-    if (designated) {
-      mine = poll_merge(p, part_cur + ubase * p.n_tg * NCP, p.n_tg, NCP, c);
-      const unsigned long long word = mine.y > 0.f ? pack_ms(mine.x, mine.y) : pack_ms(-CUDART_INF_F, -1.f);
-      for (int r = 0; r < p.world; ++r) {                     // NVLink stores to the peers (world > 1)
-        st_relaxed_sys_u64(p.peer[r] + parity * fin_half + row + (long long)p.rank * NCP + c, word);
-        p.peer[r][(parity ^ 1u) * fin_half + row + (long long)p.rank * NCP + c] = 0ull;
-      }
+// Hierarchical exchange: the rank merges, serviced by the exchange warp.  The
+// designated merger of unit u is the CTA of token group u mod n_tg (the merges
+// are spread evenly).  It gathers the rank's n_tg CTA partials (token-group
+// order) and publishes the rank word into row `rank` of every rank's rank-word
+// buffer (this launch's parity half; the same row of the other half is
+// re-zeroed for the launch after next).  The exchange warp never waits on an
+// lse, so it tries its pending merges (non-blocking) while it waits for the
+// next unit's statistics: no merge waits behind another CTA's gather.
+struct MergeCursor {
+  long long job;                 // job of the next designated unit (>= total_jobs: none left)
+  int u, u_hi, tg, b;
+  uint32_t ui;                   // its index in this CTA's unit sequence
+};
+
+// Advance to the first designated unit at or after (cur.job, u_from); ui_from
+// is the unit-sequence index of (cur.job, u_from).
+__device__ __noinline__ void cursor_seek(const FusedParams& p, MergeCursor& cur, int u_from, uint32_t ui_from) {
+  for (; cur.job < p.total_jobs; cur.job += gridDim.x) {
+    const Job jb = decode_job(p, cur.job);
+    if (u_from < jb.u_lo) u_from = jb.u_lo;
+    const int first = u_from + ((jb.tg - u_from) % p.n_tg + p.n_tg) % p.n_tg;
+    if (first < jb.u_hi) {
+      cur.u = first; cur.u_hi = jb.u_hi; cur.tg = jb.tg; cur.b = jb.b;
+      cur.ui = ui_from + (uint32_t)(first - u_from);
+      return;
     }
-    ms[c] = (p.world == 1 && designated) ? mine : poll_merge(p, p.peer[p.rank] + parity * fin_half + row, p.world, NCP, c);
+    ui_from += (uint32_t)(jb.u_hi - u_from);
+    u_from = 0;
+  }
+}
+
+// One non-blocking attempt at the cursor's merge (whole warp): true (and the
+// cursor advanced) if every partial was there.
+__device__ __noinline__ bool try_rank_merge(const FusedParams& p, MergeCursor& cur, const unsigned long long* part_cur,
+                                            uint32_t parity, int NCP, int lane) {
+  const long long ubase = (long long)cur.b * p.U + cur.u;
+  const unsigned long long* src = part_cur + ubase * p.n_tg * NCP;
+  bool ok = true;
+  for (int c = lane; c < NCP && ok; c += 32)
+    for (int s0 = 0; s0 < p.n_tg; ++s0)
+      ok &= ld_relaxed_u64(src + (long long)s0 * NCP + c) != 0ull;
+  if (!__all_sync(0xffffffffu, ok)) return false;
+  const long long fin_half = (long long)p.B * p.U * p.world * NCP;
+  const long long row = (ubase * p.world + p.rank) * NCP;
+  for (int c = lane; c < NCP; c += 32) {
+    float M = -CUDART_INF_F, S = 0.f;
+    for (int s0 = 0; s0 < p.n_tg; ++s0) {
+      const float2 w = unpack_ms(ld_relaxed_u64(src + (long long)s0 * NCP + c));
+      if (w.y > 0.f) merge2(M, S, w.x, w.y);
+    }
+    const unsigned long long word = S > 0.f ? pack_ms(M, S) : pack_ms(-CUDART_INF_F, -1.f);
+    for (int r = 0; r < p.world; ++r) {                       // NVLink stores to the peers (world > 1)
+      st_relaxed_sys_u64(p.peer[r] + parity * fin_half + row + c, word);
+      p.peer[r][(parity ^ 1u) * fin_half + row + c] = 0ull;
+    }
+  }
+  __syncwarp();
+  const int u_next = cur.u + p.n_tg;
+  const uint32_t ui_next = cur.ui + (uint32_t)p.n_tg;
+  if (u_next < cur.u_hi) {
+    cur.u = u_next;
+    cur.ui = ui_next;
+  } else {
+    const uint32_t ui_end = cur.ui + (uint32_t)(cur.u_hi - cur.u);   // first unit index of the next job
+    cur.job += gridDim.x;
+    cursor_seek(p, cur, 0, ui_end);
+  }
+  return true;
+}
+
+// Wait for the statistics of unit ui (mbarrier phase) while servicing the rank
+// merges of units already published (cursor ui < ui_pub).  Bounded like mbar_wait.
+__device__ __noinline__ void wait_servicing(const FusedParams& p, uint32_t bar, uint32_t parity, MergeCursor& cur,
+                                            uint32_t ui_pub, const unsigned long long* part_cur, uint32_t ppar,
+                                            int NCP, int lane) {
+  uint64_t t0 = 0;
+  for (uint32_t i = 1;; ++i) {
+    if (mbar_test_wait(bar, parity)) return;
+    bool merged = false;
+    if (cur.job < p.total_jobs && cur.ui < ui_pub) merged = try_rank_merge(p, cur, part_cur, ppar, NCP, lane);
+    if (!merged) __nanosleep(64);
+    if ((i & 1023) == 0) {
+      const uint64_t now = globaltimer_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 4000000000ull) asm volatile("trap;");
+    }
   }
 }
 
@@ -918,12 +983,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     // 64-bit word (max2, sum) per column, single-copy atomic, so a reader sees
     // either 0 (not yet written) or the complete pair -- no flag, no fence.
     const float2* red = reinterpret_cast<const float2*>(smem + p.off_red);   // [2][4][NCP]
+    const bool merges = p.hier && p.mode == kModeFull;
+    MergeCursor cur;
+    cur.job = merges ? blockIdx.x : p.total_jobs;
+    if (merges) cursor_seek(p, cur, 0, 0);
     uint32_t ui = 0;
     for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
       const Job jb = decode_job(p, job);
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
         const long long ubase = (long long)jb.b * p.U + u;
-        mbar_wait(bar_rfull + 8 * (ui & 1), (ui >> 1) & 1);
+        if (merges) wait_servicing(p, bar_rfull + 8 * (ui & 1), (ui >> 1) & 1, cur, ui, part_cur, parity, NCP, lane);
+        else mbar_wait(bar_rfull + 8 * (ui & 1), (ui >> 1) & 1);
         const float2* rb = red + (ui & 1) * 4 * NCP;
         const long long row = (ubase * p.n_tg + jb.tg) * NCP;
         for (int c = lane; c < NCP; c += 32) {
@@ -944,10 +1014,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           mbar_arrive(bar_rempty + 8 * (ui & 1));
           trace_stamp(p, ui, 3);
         }
+        if (merges && cur.job < p.total_jobs && cur.ui <= ui) try_rank_merge(p, cur, part_cur, parity, NCP, lane);
+      }
+    }
+    // the remaining rank merges (all of this CTA's partials are published)
+    for (uint64_t t0 = 0, i = 1; merges && cur.job < p.total_jobs; ++i) {
+      if (!try_rank_merge(p, cur, part_cur, parity, NCP, lane)) __nanosleep(100);
+      if ((i & 1023) == 0) {
+        const uint64_t now = globaltimer_ns();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > kSpinNs) { set_err(p.err, kDevTimeout); break; }
       }
     }
     // re-zero this CTA's rows of the previous launch's buffer (read by nobody now)
-    for (long long job = blockIdx.x; job < p.total_jobs && !p.hier; job += gridDim.x) {
+    for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
       const Job jb = decode_job(p, job);
       for (int u = jb.u_lo; u < jb.u_hi; ++u) {
         const long long row = (((long long)jb.b * p.U + u) * p.n_tg + jb.tg) * NCP;
@@ -972,11 +1052,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const unsigned long long* src = part_cur + ubase * p.n_tg * NCP;
         const int ntg = p.n_tg;
         if (p.hier && p.mode == kModeFull) {
-          float2* ms = reinterpret_cast<float2*>(smem + p.off_comb);              // [NCP] (max2, sum)
-          hier_gather(p, ubase, (int)(u % p.n_tg) == jb.tg, part_cur, parity, NCP, lane, ms);
-          __syncwarp();
+          // the unit's `world` rank words, merged in rank order
+          const unsigned long long* rw = p.peer[p.rank] + parity * ((long long)p.B * p.U * p.world * NCP) +
+                                         ubase * p.world * NCP;
           for (int c = lane; c < NCP; c += 32) {
-            float M = ms[c].x, S = ms[c].y;
+            const float2 ms = poll_merge(p, rw, p.world, NCP, c);
+            float M = ms.x, S = ms.y;
             if (p.la != nullptr && c < p.NC) {
               const float2 v = p.la[ubase * NCP + c];
               if (v.y > 0.f) merge2(M, S, v.x, v.y);
@@ -1342,12 +1423,12 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
         if (force_h >= 0 && hier != force_h) continue;
         if (world > 1 && hier == 0) continue;
         // flat: every CTA polls the unit's n_tg partials (batches of kMaxLseBatch);
-        // hierarchical: one CTA per unit (round robin) polls them and publishes
-        // the rank word (one more hop, + an NVLink hop when world > 1), every CTA
-        // polls the unit's `world` rank words
+        // hierarchical: one CTA per unit (round robin) polls them in its merge
+        // warp and publishes the rank word (one more hop, + an NVLink hop when
+        // world > 1), every CTA's gather warp polls the unit's `world` rank words
         const int bf = (n_tg + kMaxLseBatch - 1) / kMaxLseBatch, br = (world + kMaxLseBatch - 1) / kMaxLseBatch;
         const double L_us = 5.0 + 0.8 * (hier ? bf + br : bf) + (hier ? 1.0 : 0.0) + (world > 1 ? 2.0 : 0.0);
-        const double gather_us = 1.6 * (hier ? (double)bf / n_tg + br : bf);
+        const double gather_us = 1.6 * (hier ? br : bf);
         const int W = std::max(1, pl.nslots / tpc);
         const double exposed = std::max(0.0, L_us - (W - 1) * tpc * tile_us);
         // (+0.4 us fixed per unit: Q load, statistics merge and publish)
