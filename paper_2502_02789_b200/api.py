@@ -222,7 +222,7 @@ def select_ragged(importance: torch.Tensor, seq_lens: torch.Tensor, keep: float,
     nbytes = lib().sp_select_workspace_bytes(B, N, C.byref(p))
     if nbytes == 0:
         check(_lib.SP_EINVAL, "sp_select_ragged")
-    ws = workspace("select", nbytes, dev, stream)
+    ws = workspace(("select", B, N, int(chunk)), nbytes, dev, stream)
     check(lib().sp_select_ragged(importance.data_ptr(), seq_lens.data_ptr(),
                                  None if tokens is None else tokens.data_ptr(), B, N, C.byref(p), ids.data_ptr(),
                                  pos.data_ptr(), n_kept.data_ptr(), None if out is None else out.data_ptr(),
@@ -247,7 +247,7 @@ def select(importance: torch.Tensor, keep: float, pool_k: int, chunk: int, pos0:
     nbytes = lib().sp_select_workspace_bytes(B, N, C.byref(p))
     if nbytes == 0:
         check(_lib.SP_EINVAL, "sp_select")
-    ws = workspace("select", nbytes, dev, stream)
+    ws = workspace(("select", B, N, int(chunk)), nbytes, dev, stream)
     if tokens is None:
         check(lib().sp_select(importance.data_ptr(), B, N, C.byref(p), ids.data_ptr(), pos.data_ptr(),
                               n_kept.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_select")
@@ -303,7 +303,7 @@ def seq_candidates(imp_local: torch.Tensor, edges_all, rank: int, world: int, N:
     nbytes = lib().sp_seq_select_workspace_bytes(B, int(N), int(world), C.byref(p))
     if nbytes == 0:
         check(_lib.SP_EINVAL, "sp_seq_candidates")
-    ws = workspace("seq_sel", nbytes, imp_local.device, stream)
+    ws = workspace(("seq_sel", B, int(N), int(world), int(chunk)), nbytes, imp_local.device, stream)
     if edges_all is not None and (edges_all.dtype != torch.float32 or not edges_all.is_contiguous()):
         raise ValueError("edges_all must be contiguous fp32 [world][B][2w]")
     check(lib().sp_seq_candidates(imp_local.data_ptr(), None if edges_all is None or edges_all.numel() == 0
@@ -333,7 +333,7 @@ def seq_merge(cand_all: torch.Tensor, world: int, N: int, keep: float, pool_k: i
     nbytes = lib().sp_seq_select_workspace_bytes(B, int(N), int(world), C.byref(p))
     if nbytes == 0:
         check(_lib.SP_EINVAL, "sp_seq_merge")
-    ws = workspace("seq_sel", nbytes, dev, stream)
+    ws = workspace(("seq_sel", B, int(N), int(world), int(chunk)), nbytes, dev, stream)
     check(lib().sp_seq_merge(cand_all.data_ptr(), int(world), B, int(N), C.byref(p),
                              None if tokens is None else tokens.data_ptr(), ids.data_ptr(), pos.data_ptr(),
                              n_kept.data_ptr(), None if out is None else out.data_ptr(), ws.data_ptr(), ws.numel(),

@@ -13,9 +13,9 @@
 //   job = (request, token group, unit group).  All jobs of one request run in
 //   the same wave of CTAs, so every CTA that shares a unit is co-resident.
 // * Warp roles (384 threads): warp 0 TMA producer, warp 1 tcgen05.mma issuer
-//   (+TMEM owner), warp 2 statistics exchange (+ the rank merges of the
-//   hierarchical exchange), warp 3 lse2 gather, warps 4-7 softmax statistics,
-//   warps 8-11 max-aggregation.  The TMA/MMA warps run warp-uniform loops and
+//   (+TMEM owner), warp 2 statistics exchange, warp 3 lse2 gather (and, when
+//   the prompt is sequence-sharded over GPUs, the cross-rank merge), warps 4-7
+//   softmax statistics, warps 8-11 max-aggregation.  The TMA/MMA warps run warp-uniform loops and
 //   issue from one elected lane.
 // * K tiles [128 tokens x d] bf16 stream HBM -> SMEM by TMA (swizzled); the
 //   unit's query block [G*Rv x d] is the MMA B operand; each tile's logits
@@ -100,7 +100,7 @@ struct FusedParams {
   // workspace
   unsigned long long* part;            // [2][B][U][n_tg][NCP] CTA partials, one buffer per launch parity:
                                        // (max2, sum) packed in one 64-bit word; 0 = "not yet written"
-  int hier;                            // hierarchical exchange: one CTA per unit merges, the rest poll one word
+  int hier;                            // cross-rank (peer) exchange: world > 1
   unsigned* epoch;                     // [2] launch epoch (parity selects the partial buffer), CTAs done
   float* accpart;                      // [B][n_ug][Rv][N]
   unsigned* fin_cnt;                   // [B][n_tg]    finalize counters (self-cleaning)
@@ -112,13 +112,12 @@ struct FusedParams {
   unsigned long long* tile_trace;      // optional [1000][8] per-tile MMA stamps of CTA 0 (debug)
   int mode;                            // kModeFull / kModeStats (publish partials only) / kModeFinish (lse2 given)
   const float* lse_in;                 // kModeFinish: lse2 per row ((b*L + l)*H + h)*Rv + r
-  // hierarchical exchange and its peer-memory form (sequence-sharded single pass):
-  // world ranks each score their own tokens; on rank r the unit's designated
-  // CTA (token group u mod n_tg: the merges are spread evenly over the CTAs)
-  // gathers the rank's n_tg partials (token-group order) and stores the rank's
-  // word into row r of every rank's rank-word buffer; every CTA then polls the
-  // unit's `world` rank words and merges them in rank order (the same lse2 bits
-  // on every rank).  world = 1 with hier: one word, local.
+  // peer-memory exchange (sequence-sharded single pass, world > 1): world ranks
+  // each score their own tokens; every CTA merges its rank's n_tg partials into
+  // the rank word, the unit's designated CTA (token group u mod n_tg) stores it
+  // into row `rank` of every rank's rank-word buffer, and every CTA merges the
+  // unit's `world` rank words in rank order (the same lse2 bits on every rank;
+  // peer_gather).
   int rank, world;
   unsigned long long* peer[kMaxPeers]; // every rank's rank-word buffer base ([2][B][U][world][NCP])
 };
@@ -601,93 +600,76 @@ __device__ __noinline__ float2 poll_merge(const FusedParams& p, const unsigned l
   return make_float2(M, S);
 }
 
-// Hierarchical exchange: the rank merges, serviced by the exchange warp.  The
-// designated merger of unit u is the CTA of token group u mod n_tg (the merges
-// are spread evenly).  It gathers the rank's n_tg CTA partials (token-group
-// order) and publishes the rank word into row `rank` of every rank's rank-word
-// buffer (this launch's parity half; the same row of the other half is
-// re-zeroed for the launch after next).  The exchange warp never waits on an
-// lse, so it tries its pending merges (non-blocking) while it waits for the
-// next unit's statistics: no merge waits behind another CTA's gather.
-struct MergeCursor {
-  long long job;                 // job of the next designated unit (>= total_jobs: none left)
-  int u, u_hi, tg, b;
-  uint32_t ui;                   // its index in this CTA's unit sequence
-};
-
-// Advance to the first designated unit at or after (cur.job, u_from); ui_from
-// is the unit-sequence index of (cur.job, u_from).
-__device__ __noinline__ void cursor_seek(const FusedParams& p, MergeCursor& cur, int u_from, uint32_t ui_from) {
-  for (; cur.job < p.total_jobs; cur.job += gridDim.x) {
-    const Job jb = decode_job(p, cur.job);
-    if (u_from < jb.u_lo) u_from = jb.u_lo;
-    const int first = u_from + ((jb.tg - u_from) % p.n_tg + p.n_tg) % p.n_tg;
-    if (first < jb.u_hi) {
-      cur.u = first; cur.u_hi = jb.u_hi; cur.tg = jb.tg; cur.b = jb.b;
-      cur.ui = ui_from + (uint32_t)(first - u_from);
-      return;
-    }
-    ui_from += (uint32_t)(jb.u_hi - u_from);
-    u_from = 0;
-  }
-}
-
-// One non-blocking attempt at the cursor's merge (whole warp): true (and the
-// cursor advanced) if every partial was there.
-__device__ __noinline__ bool try_rank_merge(const FusedParams& p, MergeCursor& cur, const unsigned long long* part_cur,
-                                            uint32_t parity, int NCP, int lane) {
-  const long long ubase = (long long)cur.b * p.U + cur.u;
-  const unsigned long long* src = part_cur + ubase * p.n_tg * NCP;
-  bool ok = true;
-  for (int c = lane; c < NCP && ok; c += 32)
-    for (int s0 = 0; s0 < p.n_tg; ++s0)
-      ok &= ld_relaxed_u64(src + (long long)s0 * NCP + c) != 0ull;
-  if (!__all_sync(0xffffffffu, ok)) return false;
+// Sequence-sharded peer exchange (world > 1), gather warp (whole warp).  Per
+// unit: every CTA merges its own rank's n_tg CTA partials (token-group order,
+// local memory) into the rank word; the unit's designated CTA (token group u
+// mod n_tg) also stores it into row `rank` of every rank's rank-word buffer
+// (NVLink stores; the same row of the other parity half is re-zeroed for the
+// launch after next); then the world rank words are merged in rank order (the
+// own one from registers, bit-identical to what the peers read) -- the same
+// lse2 bits on every rank.  The local merge runs one unit ahead of the
+// cross-rank merge, so a rank publishes unit u's word before it waits for the
+// peers' words of unit u-1: the ranks' progress is not chained unit by unit
+// (the plan keeps two units resident in TMEM, so the look-ahead cannot block).
+// Out of line: the single-GPU gather's code stays as it was.
+__device__ __noinline__ void peer_gather(const FusedParams& p, const unsigned long long* part_cur, uint32_t parity,
+                                         int NCP, int lane, float* lse_s, uint32_t bar_lfull, uint32_t bar_lempty,
+                                         float2* lw) {
   const long long fin_half = (long long)p.B * p.U * p.world * NCP;
-  const long long row = (ubase * p.world + p.rank) * NCP;
-  for (int c = lane; c < NCP; c += 32) {
-    float M = -CUDART_INF_F, S = 0.f;
-    for (int s0 = 0; s0 < p.n_tg; ++s0) {
-      const float2 w = unpack_ms(ld_relaxed_u64(src + (long long)s0 * NCP + c));
-      if (w.y > 0.f) merge2(M, S, w.x, w.y);
+  uint32_t ui = 0;
+  long long prev_ubase = -1;
+  const long long n_units = p.total_jobs;                     // (loop bound only)
+  (void)n_units;
+  auto finish = [&](long long ubase, uint32_t pui) {          // cross-rank merge of unit ubase -> lse2
+    const uint32_t par = pui % kLseRing;
+    mbar_wait(bar_lempty + 8 * par, ((pui / kLseRing) & 1) ^ 1);
+    float* ls = lse_s + par * NCP;
+    const unsigned long long* rw = p.peer[p.rank] + parity * fin_half + ubase * p.world * NCP;
+    const float2* mine = lw + (pui & 1) * NCP;
+    for (int c = lane; c < NCP; c += 32) {
+      float M = -CUDART_INF_F, S = 0.f;
+      for (int r = 0; r < p.world; ++r) {
+        float2 w;
+        if (r == p.rank) {
+          w = mine[c];
+        } else {
+          w = poll_merge(p, rw + (long long)r * NCP, 1, NCP, c);   // one word: (max2, sum) or empty
+        }
+        if (w.y > 0.f) merge2(M, S, w.x, w.y);
+      }
+      float l2 = 0.f;
+      if (c < p.NC) {
+        l2 = M + log2f(S);
+        if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
+      }
+      ls[c] = l2;
     }
-    const unsigned long long word = S > 0.f ? pack_ms(M, S) : pack_ms(-CUDART_INF_F, -1.f);
-    for (int r = 0; r < p.world; ++r) {                       // NVLink stores to the peers (world > 1)
-      st_relaxed_sys_u64(p.peer[r] + parity * fin_half + row + c, word);
-      p.peer[r][(parity ^ 1u) * fin_half + row + c] = 0ull;
+    mbar_arrive(bar_lfull + 8 * par);
+  };
+  for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
+    const Job jb = decode_job(p, job);
+    for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
+      const long long ubase = (long long)jb.b * p.U + u;
+      const bool designated = (u % p.n_tg) == jb.tg;
+      float2* mine = lw + (ui & 1) * NCP;
+      for (int c = lane; c < NCP; c += 32) {
+        const float2 m = poll_merge(p, part_cur + ubase * p.n_tg * NCP, p.n_tg, NCP, c);
+        mine[c] = m;
+        if (designated) {
+          const unsigned long long word = m.y > 0.f ? pack_ms(m.x, m.y) : pack_ms(-CUDART_INF_F, -1.f);
+          const long long row = (ubase * p.world + p.rank) * NCP + c;
+          for (int r = 0; r < p.world; ++r) {
+            if (r != p.rank) st_relaxed_sys_u64(p.peer[r] + parity * fin_half + row, word);
+            p.peer[r][(parity ^ 1u) * fin_half + row] = 0ull;
+          }
+        }
+      }
+      __syncwarp();
+      if (prev_ubase >= 0) finish(prev_ubase, ui - 1);
+      prev_ubase = ubase;
     }
   }
-  __syncwarp();
-  const int u_next = cur.u + p.n_tg;
-  const uint32_t ui_next = cur.ui + (uint32_t)p.n_tg;
-  if (u_next < cur.u_hi) {
-    cur.u = u_next;
-    cur.ui = ui_next;
-  } else {
-    const uint32_t ui_end = cur.ui + (uint32_t)(cur.u_hi - cur.u);   // first unit index of the next job
-    cur.job += gridDim.x;
-    cursor_seek(p, cur, 0, ui_end);
-  }
-  return true;
-}
-
-// Wait for the statistics of unit ui (mbarrier phase) while servicing the rank
-// merges of units already published (cursor ui < ui_pub).  Bounded like mbar_wait.
-__device__ __noinline__ void wait_servicing(const FusedParams& p, uint32_t bar, uint32_t parity, MergeCursor& cur,
-                                            uint32_t ui_pub, const unsigned long long* part_cur, uint32_t ppar,
-                                            int NCP, int lane) {
-  uint64_t t0 = 0;
-  for (uint32_t i = 1;; ++i) {
-    if (mbar_test_wait(bar, parity)) return;
-    bool merged = false;
-    if (cur.job < p.total_jobs && cur.ui < ui_pub) merged = try_rank_merge(p, cur, part_cur, ppar, NCP, lane);
-    if (!merged) __nanosleep(64);
-    if ((i & 1023) == 0) {
-      const uint64_t now = globaltimer_ns();
-      if (t0 == 0) t0 = now;
-      else if (now - t0 > 4000000000ull) asm volatile("trap;");
-    }
-  }
+  if (prev_ubase >= 0) finish(prev_ubase, ui - 1);
 }
 
 // kG: compile-time GQA group size (1, 2, 4, 8) or 0 for any G.  One
@@ -983,17 +965,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     // 64-bit word (max2, sum) per column, single-copy atomic, so a reader sees
     // either 0 (not yet written) or the complete pair -- no flag, no fence.
     const float2* red = reinterpret_cast<const float2*>(smem + p.off_red);   // [2][4][NCP]
-    const bool merges = p.hier && p.mode == kModeFull;
-    MergeCursor cur;
-    cur.job = merges ? blockIdx.x : p.total_jobs;
-    if (merges) cursor_seek(p, cur, 0, 0);
     uint32_t ui = 0;
     for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
       const Job jb = decode_job(p, job);
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
         const long long ubase = (long long)jb.b * p.U + u;
-        if (merges) wait_servicing(p, bar_rfull + 8 * (ui & 1), (ui >> 1) & 1, cur, ui, part_cur, parity, NCP, lane);
-        else mbar_wait(bar_rfull + 8 * (ui & 1), (ui >> 1) & 1);
+        mbar_wait(bar_rfull + 8 * (ui & 1), (ui >> 1) & 1);
         const float2* rb = red + (ui & 1) * 4 * NCP;
         const long long row = (ubase * p.n_tg + jb.tg) * NCP;
         for (int c = lane; c < NCP; c += 32) {
@@ -1014,16 +991,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           mbar_arrive(bar_rempty + 8 * (ui & 1));
           trace_stamp(p, ui, 3);
         }
-        if (merges && cur.job < p.total_jobs && cur.ui <= ui) try_rank_merge(p, cur, part_cur, parity, NCP, lane);
-      }
-    }
-    // the remaining rank merges (all of this CTA's partials are published)
-    for (uint64_t t0 = 0, i = 1; merges && cur.job < p.total_jobs; ++i) {
-      if (!try_rank_merge(p, cur, part_cur, parity, NCP, lane)) __nanosleep(100);
-      if ((i & 1023) == 0) {
-        const uint64_t now = globaltimer_ns();
-        if (t0 == 0) t0 = now;
-        else if (now - t0 > kSpinNs) { set_err(p.err, kDevTimeout); break; }
       }
     }
     // re-zero this CTA's rows of the previous launch's buffer (read by nobody now)
@@ -1042,7 +1009,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     // stages lse2 in SMEM for the aggregation warps.
     float* lse_s = reinterpret_cast<float*>(smem + p.off_lse);    // [kLseRing][NCP]
     uint32_t ui = 0;
-    for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
+    if (p.world > 1 && p.mode == kModeFull)                          // sequence-sharded peer exchange
+      peer_gather(p, part_cur, parity, NCP, lane, lse_s, bar_lfull, bar_lempty,
+                  reinterpret_cast<float2*>(smem + p.off_comb));
+    for (long long job = blockIdx.x; job < p.total_jobs && !(p.world > 1 && p.mode == kModeFull);
+         job += gridDim.x) {
       const Job jb = decode_job(p, job);
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
         const uint32_t par = ui % kLseRing;
@@ -1051,26 +1022,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         float* ls = lse_s + par * NCP;
         const unsigned long long* src = part_cur + ubase * p.n_tg * NCP;
         const int ntg = p.n_tg;
-        if (p.hier && p.mode == kModeFull) {
-          // the unit's `world` rank words, merged in rank order
-          const unsigned long long* rw = p.peer[p.rank] + parity * ((long long)p.B * p.U * p.world * NCP) +
-                                         ubase * p.world * NCP;
-          for (int c = lane; c < NCP; c += 32) {
-            const float2 ms = poll_merge(p, rw, p.world, NCP, c);
-            float M = ms.x, S = ms.y;
-            if (p.la != nullptr && c < p.NC) {
-              const float2 v = p.la[ubase * NCP + c];
-              if (v.y > 0.f) merge2(M, S, v.x, v.y);
-            }
-            float l2 = 0.f;
-            if (c < p.NC) {
-              l2 = M + log2f(S);
-              if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
-            }
-            ls[c] = l2;
-          }
-        }
-        for (int c = lane; c < NCP && p.mode == kModeFull && !p.hier; c += 32) {
+        for (int c = lane; c < NCP && p.mode == kModeFull; c += 32) {
           float M = -CUDART_INF_F, S = 0.f;
           for (int s0 = 0; s0 < ntg; s0 += kMaxLseBatch) {
             unsigned long long v[kMaxLseBatch];
@@ -1303,7 +1255,7 @@ struct Plan {
   uint32_t off_k = 0, off_q = 0, off_acc = 0, off_red = 0, off_lse = 0, off_comb = 0, off_bar = 0, off_bt = 0, smem = 0;
   uint32_t k_stage_bytes = 0, q_slot_bytes = 0;
   int nq = 2;
-  int hier = 0, world = 1;                            // hierarchical exchange; ranks of a peer exchange
+  int hier = 0, world = 1;                            // peer exchange (world > 1); ranks
   size_t ws_part = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0, ws_rank = 0;
   size_t ws_total() const { return ws_part + ws_cnt + ws_acc + ws_fin + ws_rank; }
   bool ok = false;
@@ -1360,7 +1312,7 @@ PlanKey plan_key(const Geom& g, int sm_budget) {
 
 // sm_budget > 0: plan for at most that many CTAs (co-scheduled peer launches on one GPU, tests).
 // cands (optional): every valid (model cost, n_tg, n_ug, hier), for the tuner.
-// world > 1: a peer-memory exchange over that many ranks (always hierarchical).
+// world > 1: a peer-memory exchange over that many ranks (hier = 1).
 Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
                std::vector<std::tuple<double, int, int, int>>* cands = nullptr, int world = 1) {
   Plan pl;
@@ -1397,7 +1349,6 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
     auto it = plan_registry().find(plan_key(g, sm_budget));
     if (it != plan_registry().end()) std::tie(force_tg, force_ug, force_h) = it->second;
   }
-  if (world > 1) force_h = 1;
   pl.world = world;
   for (int J = 1; J <= pl.P; ++J) {
     if ((long long)g.B * J > pl.P && pl.P % J) continue;
@@ -1419,16 +1370,15 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
       // (per-tile costs measured for bf16 hold for e4m3 too: the statistics,
       // aggregation and exchange work per tile does not depend on the K bytes)
       const double tile_us = (double)kTileM * g.d * 2 / kSmHbmBytesPerUs;
-      for (int hier = 0; hier < 2; ++hier) {
-        if (force_h >= 0 && hier != force_h) continue;
-        if (world > 1 && hier == 0) continue;
-        // flat: every CTA polls the unit's n_tg partials (batches of kMaxLseBatch);
-        // hierarchical: one CTA per unit (round robin) polls them in its merge
-        // warp and publishes the rank word (one more hop, + an NVLink hop when
-        // world > 1), every CTA's gather warp polls the unit's `world` rank words
-        const int bf = (n_tg + kMaxLseBatch - 1) / kMaxLseBatch, br = (world + kMaxLseBatch - 1) / kMaxLseBatch;
-        const double L_us = 5.0 + 0.8 * (hier ? bf + br : bf) + (hier ? 1.0 : 0.0) + (world > 1 ? 2.0 : 0.0);
-        const double gather_us = 1.6 * (hier ? br : bf);
+      {
+        const int hier = world > 1 ? 1 : 0;
+        if (hier && pl.nslots / tpc < 2) continue;       // peer_gather's look-ahead needs 2 resident units
+        // single GPU: every CTA polls the unit's n_tg partials (batches of
+        // kMaxLseBatch); peer: its rank's n_tg partials, then the other ranks'
+        // words (+ an NVLink hop)
+        const int bf = (n_tg + kMaxLseBatch - 1) / kMaxLseBatch;
+        const double L_us = 5.0 + 0.8 * bf + (hier ? 2.8 : 0.0);
+        const double gather_us = 1.6 * bf + (hier ? 0.4 * (world - 1) : 0.0);
         const int W = std::max(1, pl.nslots / tpc);
         const double exposed = std::max(0.0, L_us - (W - 1) * tpc * tile_us);
         // (+0.4 us fixed per unit: Q load, statistics merge and publish)
@@ -1465,7 +1415,7 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   pl.ws_cnt = 256;                                   // launch epoch + CTAs-done counter
   pl.ws_acc = pl.n_ug > 1 ? align256((size_t)g.B * pl.n_ug * g.Rv * g.N * sizeof(float)) : 0;
   pl.ws_fin = align256((size_t)g.B * pl.n_tg * sizeof(unsigned));
-  pl.ws_rank = world == 1 ? align256(2 * (size_t)g.B * pl.U * pl.NCP * sizeof(unsigned long long)) : 0;
+  pl.ws_rank = 0;
   pl.ok = true;
   return pl;
 }
@@ -1691,8 +1641,6 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   p.world = peer.world;
   if (peer.world > 1) {
     for (int r = 0; r < peer.world; ++r) p.peer[r] = reinterpret_cast<unsigned long long*>(peer.bufs[r]);
-  } else {
-    p.peer[0] = reinterpret_cast<unsigned long long*>(w);          // rank words (hierarchical, local)
   }
   p.imp = importance;
   p.acc_out = acc_out;

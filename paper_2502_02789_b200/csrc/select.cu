@@ -515,15 +515,17 @@ cudaError_t launch_select(SelArgs a, int B, long long n_tok, long long n_chunks,
 
 }  // namespace
 
-// [B][n_c] chunk scores, then [B] phase-A completion counters (zero-filled once, self-resetting)
+// [B] phase-A completion counters (zero-filled once, self-resetting; first, so
+// their place does not depend on N or chunk), then [B][n_c] chunk scores
 size_t select_ws_bytes(int B, long long N, int chunk) {
   long long n_c = (N + chunk - 1) / chunk;
-  return align256((size_t)B * n_c * sizeof(float)) + align256((size_t)B * sizeof(unsigned));
+  return align256((size_t)B * sizeof(unsigned)) + align256((size_t)B * n_c * sizeof(float));
 }
 
 namespace {
-unsigned* ws_counters(void* ws, int B, long long n_c_row) {
-  return reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ws) + align256((size_t)B * n_c_row * sizeof(float)));
+unsigned* ws_counters(void* ws) { return reinterpret_cast<unsigned*>(ws); }
+float* ws_scores(void* ws, int B) {
+  return reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align256((size_t)B * sizeof(unsigned)));
 }
 }  // namespace
 
@@ -534,9 +536,9 @@ cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int 
                           const int* seq_lens) {
   SelArgs a{};
   a.imp = imp; a.row = N; a.seq_lens = seq_lens; a.pool_k = pool_k; a.chunk = chunk; a.pos0 = pos0; a.ppm = ppm;
-  a.ids = ids; a.pos = pos; a.n_kept = n_kept; a.cs_ws = reinterpret_cast<float*>(ws); a.tokens = tokens; a.out = out;
+  a.ids = ids; a.pos = pos; a.n_kept = n_kept; a.cs_ws = ws_scores(ws, B); a.tokens = tokens; a.out = out;
   a.n_glob = N;
-  a.blk_cnt = ws_counters(ws, B, (N + chunk - 1) / chunk);
+  a.blk_cnt = ws_counters(ws);
   return launch_select<kPlain>(a, B, N, (N + chunk - 1) / chunk, st);
 }
 
@@ -566,10 +568,10 @@ cudaError_t seq_candidates_launch(const float* imp_local, const float* edges, in
   const long long n_local = N / world;
   SelArgs a{};
   a.imp = imp_local; a.row = n_local; a.pool_k = pool_k; a.chunk = chunk;
-  a.ids = nullptr; a.pos = nullptr; a.cs_ws = reinterpret_cast<float*>(ws);
+  a.ids = nullptr; a.pos = nullptr; a.cs_ws = ws_scores(ws, B);
   a.i0 = (long long)rank * n_local; a.n_glob = N; a.edges = edges; a.rank = rank; a.world = world;
   a.k_sel = M; a.cand = cand;
-  a.blk_cnt = ws_counters(ws, B, (N + chunk - 1) / chunk);
+  a.blk_cnt = ws_counters(ws);
   return launch_select<kCand>(a, B, n_local, n_local / chunk, st);
 }
 
@@ -578,9 +580,9 @@ cudaError_t seq_merge_launch(const unsigned long long* cand_all, int world, int 
                              int* out, void* ws, cudaStream_t st) {
   SelArgs a{};
   a.row = N; a.pool_k = pool_k; a.chunk = chunk; a.pos0 = pos0; a.ppm = ppm;
-  a.ids = ids; a.pos = pos; a.n_kept = n_kept; a.cs_ws = reinterpret_cast<float*>(ws); a.tokens = tokens; a.out = out;
+  a.ids = ids; a.pos = pos; a.n_kept = n_kept; a.cs_ws = ws_scores(ws, B); a.tokens = tokens; a.out = out;
   a.n_glob = N; a.world = world; a.k_sel = M; a.cand_in = cand_all;
-  a.blk_cnt = ws_counters(ws, B, (N + chunk - 1) / chunk);
+  a.blk_cnt = ws_counters(ws);
   return launch_select<kMerge>(a, B, N, (N + chunk - 1) / chunk, st);
 }
 
