@@ -113,11 +113,11 @@ struct FusedParams {
   int mode;                            // kModeFull / kModeStats (publish partials only) / kModeFinish (lse2 given)
   const float* lse_in;                 // kModeFinish: lse2 per row ((b*L + l)*H + h)*Rv + r
   // peer-memory exchange (sequence-sharded single pass, world > 1): world ranks
-  // each score their own tokens; every CTA merges its rank's n_tg partials into
-  // the rank word, the unit's designated CTA (token group u mod n_tg) stores it
-  // into row `rank` of every rank's rank-word buffer, and every CTA merges the
-  // unit's `world` rank words in rank order (the same lse2 bits on every rank;
-  // peer_gather).
+  // each score their own tokens; the unit's designated CTA (token group u mod
+  // n_tg) merges its rank's n_tg partials into the rank word and stores it into
+  // row `rank` of every rank's rank-word buffer, and every CTA merges the unit's
+  // `world` rank words in rank order (the same lse2 bits on every rank;
+  // peer_publish).
   int rank, world;
   unsigned long long* peer[kMaxPeers]; // every rank's rank-word buffer base ([2][B][U][world][NCP])
 };
@@ -600,76 +600,28 @@ __device__ __noinline__ float2 poll_merge(const FusedParams& p, const unsigned l
   return make_float2(M, S);
 }
 
-// Sequence-sharded peer exchange (world > 1), gather warp (whole warp).  Per
-// unit: every CTA merges its own rank's n_tg CTA partials (token-group order,
-// local memory) into the rank word; the unit's designated CTA (token group u
-// mod n_tg) also stores it into row `rank` of every rank's rank-word buffer
-// (NVLink stores; the same row of the other parity half is re-zeroed for the
-// launch after next); then the world rank words are merged in rank order (the
-// own one from registers, bit-identical to what the peers read) -- the same
-// lse2 bits on every rank.  The local merge runs one unit ahead of the
-// cross-rank merge, so a rank publishes unit u's word before it waits for the
-// peers' words of unit u-1: the ranks' progress is not chained unit by unit
-// (the plan keeps two units resident in TMEM, so the look-ahead cannot block).
-// Out of line: the single-GPU gather's code stays as it was.
-__device__ __noinline__ void peer_gather(const FusedParams& p, const unsigned long long* part_cur, uint32_t parity,
-                                         int NCP, int lane, float* lse_s, uint32_t bar_lfull, uint32_t bar_lempty,
-                                         float2* lw) {
+// Sequence-sharded peer exchange (world > 1).  Exchange warp, after publishing
+// this CTA's partial of unit ubase: if this CTA is the unit's designated merger
+// (token group u mod n_tg: spread evenly), wait for the rank's n_tg CTA
+// partials (local memory), merge them in token-group order into the rank word
+// and store it into row `rank` of every rank's rank-word buffer (NVLink stores,
+// this launch's parity half; the same row of the other half is re-zeroed for
+// the launch after next).  The exchange warps never wait on an lse, so this
+// wait is paced by the statistics of the rank's slowest CTA only; the gather
+// warps then merge the unit's `world` rank words in rank order (the same lse2
+// bits on every rank).  Out of line: once per designated unit.
+__device__ __noinline__ void peer_publish(const FusedParams& p, long long ubase, const unsigned long long* part_cur,
+                                          uint32_t parity, int NCP, int lane) {
   const long long fin_half = (long long)p.B * p.U * p.world * NCP;
-  uint32_t ui = 0;
-  long long prev_ubase = -1;
-  const long long n_units = p.total_jobs;                     // (loop bound only)
-  (void)n_units;
-  auto finish = [&](long long ubase, uint32_t pui) {          // cross-rank merge of unit ubase -> lse2
-    const uint32_t par = pui % kLseRing;
-    mbar_wait(bar_lempty + 8 * par, ((pui / kLseRing) & 1) ^ 1);
-    float* ls = lse_s + par * NCP;
-    const unsigned long long* rw = p.peer[p.rank] + parity * fin_half + ubase * p.world * NCP;
-    const float2* mine = lw + (pui & 1) * NCP;
-    for (int c = lane; c < NCP; c += 32) {
-      float M = -CUDART_INF_F, S = 0.f;
-      for (int r = 0; r < p.world; ++r) {
-        float2 w;
-        if (r == p.rank) {
-          w = mine[c];
-        } else {
-          w = poll_merge(p, rw + (long long)r * NCP, 1, NCP, c);   // one word: (max2, sum) or empty
-        }
-        if (w.y > 0.f) merge2(M, S, w.x, w.y);
-      }
-      float l2 = 0.f;
-      if (c < p.NC) {
-        l2 = M + log2f(S);
-        if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
-      }
-      ls[c] = l2;
-    }
-    mbar_arrive(bar_lfull + 8 * par);
-  };
-  for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
-    const Job jb = decode_job(p, job);
-    for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
-      const long long ubase = (long long)jb.b * p.U + u;
-      const bool designated = (u % p.n_tg) == jb.tg;
-      float2* mine = lw + (ui & 1) * NCP;
-      for (int c = lane; c < NCP; c += 32) {
-        const float2 m = poll_merge(p, part_cur + ubase * p.n_tg * NCP, p.n_tg, NCP, c);
-        mine[c] = m;
-        if (designated) {
-          const unsigned long long word = m.y > 0.f ? pack_ms(m.x, m.y) : pack_ms(-CUDART_INF_F, -1.f);
-          const long long row = (ubase * p.world + p.rank) * NCP + c;
-          for (int r = 0; r < p.world; ++r) {
-            if (r != p.rank) st_relaxed_sys_u64(p.peer[r] + parity * fin_half + row, word);
-            p.peer[r][(parity ^ 1u) * fin_half + row] = 0ull;
-          }
-        }
-      }
-      __syncwarp();
-      if (prev_ubase >= 0) finish(prev_ubase, ui - 1);
-      prev_ubase = ubase;
+  const long long row = (ubase * p.world + p.rank) * NCP;
+  for (int c = lane; c < NCP; c += 32) {
+    const float2 m = poll_merge(p, part_cur + ubase * p.n_tg * NCP, p.n_tg, NCP, c);
+    const unsigned long long word = m.y > 0.f ? pack_ms(m.x, m.y) : pack_ms(-CUDART_INF_F, -1.f);   // never 0
+    for (int r = 0; r < p.world; ++r) {
+      st_relaxed_sys_u64(p.peer[r] + parity * fin_half + row + c, word);
+      p.peer[r][(parity ^ 1u) * fin_half + row + c] = 0ull;
     }
   }
-  if (prev_ubase >= 0) finish(prev_ubase, ui - 1);
 }
 
 // kG: compile-time GQA group size (1, 2, 4, 8) or 0 for any G.  One
@@ -991,6 +943,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           mbar_arrive(bar_rempty + 8 * (ui & 1));
           trace_stamp(p, ui, 3);
         }
+        if (p.world > 1 && p.mode == kModeFull && (u % p.n_tg) == jb.tg) {
+          __threadfence();                                     // own partial before the peers' words
+          peer_publish(p, ubase, part_cur, parity, NCP, lane);
+        }
       }
     }
     // re-zero this CTA's rows of the previous launch's buffer (read by nobody now)
@@ -1009,19 +965,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     // stages lse2 in SMEM for the aggregation warps.
     float* lse_s = reinterpret_cast<float*>(smem + p.off_lse);    // [kLseRing][NCP]
     uint32_t ui = 0;
-    if (p.world > 1 && p.mode == kModeFull)                          // sequence-sharded peer exchange
-      peer_gather(p, part_cur, parity, NCP, lane, lse_s, bar_lfull, bar_lempty,
-                  reinterpret_cast<float2*>(smem + p.off_comb));
-    for (long long job = blockIdx.x; job < p.total_jobs && !(p.world > 1 && p.mode == kModeFull);
-         job += gridDim.x) {
+    for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
       const Job jb = decode_job(p, job);
       for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
         const uint32_t par = ui % kLseRing;
         const long long ubase = (long long)jb.b * p.U + u;
         mbar_wait(bar_lempty + 8 * par, ((ui / kLseRing) & 1) ^ 1);    // aggregation done with ls[par]
         float* ls = lse_s + par * NCP;
-        const unsigned long long* src = part_cur + ubase * p.n_tg * NCP;
-        const int ntg = p.n_tg;
+        // single GPU: the unit's n_tg CTA partials; sequence-sharded over world
+        // GPUs: the unit's world rank words (peer_publish)
+        const bool peer = p.world > 1;
+        const unsigned long long* src = peer ? p.peer[p.rank] + parity * ((long long)p.B * p.U * p.world * NCP) +
+                                                   ubase * p.world * NCP
+                                             : part_cur + ubase * p.n_tg * NCP;
+        const int ntg = peer ? p.world : p.n_tg;
         for (int c = lane; c < NCP && p.mode == kModeFull; c += 32) {
           float M = -CUDART_INF_F, S = 0.f;
           for (int s0 = 0; s0 < ntg; s0 += kMaxLseBatch) {
@@ -1372,13 +1329,13 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
       const double tile_us = (double)kTileM * g.d * 2 / kSmHbmBytesPerUs;
       {
         const int hier = world > 1 ? 1 : 0;
-        if (hier && pl.nslots / tpc < 2) continue;       // peer_gather's look-ahead needs 2 resident units
         // single GPU: every CTA polls the unit's n_tg partials (batches of
-        // kMaxLseBatch); peer: its rank's n_tg partials, then the other ranks'
-        // words (+ an NVLink hop)
+        // kMaxLseBatch); peer: the designated CTA's exchange warp merges the
+        // rank's n_tg partials (one more hop + an NVLink hop), every gather polls
+        // the unit's `world` rank words
         const int bf = (n_tg + kMaxLseBatch - 1) / kMaxLseBatch;
-        const double L_us = 5.0 + 0.8 * bf + (hier ? 2.8 : 0.0);
-        const double gather_us = 1.6 * bf + (hier ? 0.4 * (world - 1) : 0.0);
+        const double L_us = 5.0 + 0.8 * bf + (hier ? 0.8 + 2.0 : 0.0);
+        const double gather_us = 1.6 * (hier ? (world + kMaxLseBatch - 1) / kMaxLseBatch : bf);
         const int W = std::max(1, pl.nslots / tpc);
         const double exposed = std::max(0.0, L_us - (W - 1) * tpc * tile_us);
         // (+0.4 us fixed per unit: Q load, statistics merge and publish)
