@@ -979,6 +979,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
                                                    ubase * p.world * NCP
                                              : part_cur + ubase * p.n_tg * NCP;
         const int ntg = peer ? p.world : p.n_tg;
+        for (int c = lane; c < NCP && p.mode == kModeFinish; c += 32) {
+          // lse2 supplied by the caller (sequence-sharded split: globally combined statistics)
+          float l2 = 0.f;
+          if (c < p.NC) {
+            const int l = u / p.Hkv, g = u % p.Hkv;
+            l2 = p.lse_in[(((long long)jb.b * p.L + l) * p.Hkv * p.G + g * p.G + c % p.G) * p.Rv + c / p.G];
+          }
+          ls[c] = l2;
+        }
         for (int c = lane; c < NCP && p.mode == kModeFull; c += 32) {
           float M = -CUDART_INF_F, S = 0.f;
           for (int s0 = 0; s0 < ntg; s0 += kMaxLseBatch) {
