@@ -113,11 +113,11 @@ struct FusedParams {
   int mode;                            // kModeFull / kModeStats (publish partials only) / kModeFinish (lse2 given)
   const float* lse_in;                 // kModeFinish: lse2 per row ((b*L + l)*H + h)*Rv + r
   // peer-memory exchange (sequence-sharded single pass, world > 1): world ranks
-  // each score their own tokens; the unit's designated CTA (token group u mod
-  // n_tg) merges its rank's n_tg partials into the rank word and stores it into
-  // row `rank` of every rank's rank-word buffer, and every CTA merges the unit's
-  // `world` rank words in rank order (the same lse2 bits on every rank;
-  // peer_publish).
+  // each score their own tokens; every CTA merges its rank's n_tg partials into
+  // the rank word, the unit's designated CTA (token group u mod n_tg) stores it
+  // into row `rank` of every peer's rank-word buffer, and every CTA merges the
+  // unit's `world` rank words in rank order (the same lse2 bits on every rank;
+  // peer_gather_unit).
   int rank, world;
   unsigned long long* peer[kMaxPeers]; // every rank's rank-word buffer base ([2][B][U][world][NCP])
 };
@@ -600,27 +600,47 @@ __device__ __noinline__ float2 poll_merge(const FusedParams& p, const unsigned l
   return make_float2(M, S);
 }
 
-// Sequence-sharded peer exchange (world > 1).  Exchange warp, after publishing
-// this CTA's partial of unit ubase: if this CTA is the unit's designated merger
-// (token group u mod n_tg: spread evenly), wait for the rank's n_tg CTA
-// partials (local memory), merge them in token-group order into the rank word
-// and store it into row `rank` of every rank's rank-word buffer (NVLink stores,
-// this launch's parity half; the same row of the other half is re-zeroed for
-// the launch after next).  The exchange warps never wait on an lse, so this
-// wait is paced by the statistics of the rank's slowest CTA only; the gather
-// warps then merge the unit's `world` rank words in rank order (the same lse2
-// bits on every rank).  Out of line: once per designated unit.
-__device__ __noinline__ void peer_publish(const FusedParams& p, long long ubase, const unsigned long long* part_cur,
-                                          uint32_t parity, int NCP, int lane) {
+// Sequence-sharded peer exchange (world > 1), gather warp (whole warp), unit
+// ubase: every CTA merges its own rank's n_tg CTA partials (token-group order,
+// local memory -- the single-GPU gather); the unit's designated CTA (token
+// group u mod n_tg: spread evenly) also stores that rank word into row `rank`
+// of every peer's rank-word buffer (NVLink stores, this launch's parity half;
+// the same row of the other half is re-zeroed for the launch after next); then
+// the world rank words are merged in rank order -- the own one from registers,
+// bit-identical to what the peers read -- so every rank computes the same lse2
+// bits.  Writes lse2 (+ the look-ahead keys' share, Z2') into ls.  Out of line:
+// the single-GPU gather's code stays as it was.
+__device__ __noinline__ void peer_gather_unit(const FusedParams& p, long long ubase, bool designated,
+                                              const unsigned long long* part_cur, uint32_t parity, int NCP, int lane,
+                                              float* ls) {
   const long long fin_half = (long long)p.B * p.U * p.world * NCP;
-  const long long row = (ubase * p.world + p.rank) * NCP;
+  const long long rows = ubase * p.world * NCP;
   for (int c = lane; c < NCP; c += 32) {
-    const float2 m = poll_merge(p, part_cur + ubase * p.n_tg * NCP, p.n_tg, NCP, c);
-    const unsigned long long word = m.y > 0.f ? pack_ms(m.x, m.y) : pack_ms(-CUDART_INF_F, -1.f);   // never 0
-    for (int r = 0; r < p.world; ++r) {
-      st_relaxed_sys_u64(p.peer[r] + parity * fin_half + row + c, word);
-      p.peer[r][(parity ^ 1u) * fin_half + row + c] = 0ull;
+    const float2 mine = poll_merge(p, part_cur + ubase * p.n_tg * NCP, p.n_tg, NCP, c);
+    if (designated) {
+      const unsigned long long word = mine.y > 0.f ? pack_ms(mine.x, mine.y) : pack_ms(-CUDART_INF_F, -1.f);
+      for (int r = 0; r < p.world; ++r) {
+        if (r == p.rank) continue;
+        st_relaxed_sys_u64(p.peer[r] + parity * fin_half + rows + (long long)p.rank * NCP + c, word);
+        p.peer[r][(parity ^ 1u) * fin_half + rows + (long long)p.rank * NCP + c] = 0ull;
+      }
     }
+    float M = -CUDART_INF_F, S = 0.f;
+    for (int r = 0; r < p.world; ++r) {
+      const float2 w = r == p.rank ? mine : poll_merge(p, p.peer[p.rank] + parity * fin_half + rows + (long long)r * NCP,
+                                                       1, NCP, c);
+      if (w.y > 0.f) merge2(M, S, w.x, w.y);
+    }
+    if (p.la != nullptr && c < p.NC) {                           // the look-ahead keys' share (Z2')
+      const float2 v = p.la[ubase * NCP + c];
+      if (v.y > 0.f) merge2(M, S, v.x, v.y);
+    }
+    float l2 = 0.f;
+    if (c < p.NC) {
+      l2 = M + log2f(S);
+      if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
+    }
+    ls[c] = l2;
   }
 }
 
@@ -943,10 +963,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           mbar_arrive(bar_rempty + 8 * (ui & 1));
           trace_stamp(p, ui, 3);
         }
-        if (p.world > 1 && p.mode == kModeFull && (u % p.n_tg) == jb.tg) {
-          __threadfence();                                     // own partial before the peers' words
-          peer_publish(p, ubase, part_cur, parity, NCP, lane);
-        }
       }
     }
     // re-zero this CTA's rows of the previous launch's buffer (read by nobody now)
@@ -972,13 +988,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const long long ubase = (long long)jb.b * p.U + u;
         mbar_wait(bar_lempty + 8 * par, ((ui / kLseRing) & 1) ^ 1);    // aggregation done with ls[par]
         float* ls = lse_s + par * NCP;
-        // single GPU: the unit's n_tg CTA partials; sequence-sharded over world
-        // GPUs: the unit's world rank words (peer_publish)
-        const bool peer = p.world > 1;
-        const unsigned long long* src = peer ? p.peer[p.rank] + parity * ((long long)p.B * p.U * p.world * NCP) +
-                                                   ubase * p.world * NCP
-                                             : part_cur + ubase * p.n_tg * NCP;
-        const int ntg = peer ? p.world : p.n_tg;
+        const unsigned long long* src = part_cur + ubase * p.n_tg * NCP;
+        const int ntg = p.n_tg;
+        if (p.world > 1 && p.mode == kModeFull)                        // sequence-sharded over GPUs
+          peer_gather_unit(p, ubase, (u % p.n_tg) == jb.tg, part_cur, parity, NCP, lane, ls);
         for (int c = lane; c < NCP && p.mode == kModeFinish; c += 32) {
           // lse2 supplied by the caller (sequence-sharded split: globally combined statistics)
           float l2 = 0.f;
@@ -988,7 +1001,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           }
           ls[c] = l2;
         }
-        for (int c = lane; c < NCP && p.mode == kModeFull; c += 32) {
+        for (int c = lane; c < NCP && p.mode == kModeFull && p.world == 1; c += 32) {
           float M = -CUDART_INF_F, S = 0.f;
           for (int s0 = 0; s0 < ntg; s0 += kMaxLseBatch) {
             unsigned long long v[kMaxLseBatch];
@@ -1339,12 +1352,10 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
       {
         const int hier = world > 1 ? 1 : 0;
         // single GPU: every CTA polls the unit's n_tg partials (batches of
-        // kMaxLseBatch); peer: the designated CTA's exchange warp merges the
-        // rank's n_tg partials (one more hop + an NVLink hop), every gather polls
-        // the unit's `world` rank words
+        // kMaxLseBatch); peer: then the other ranks' words (an NVLink hop)
         const int bf = (n_tg + kMaxLseBatch - 1) / kMaxLseBatch;
-        const double L_us = 5.0 + 0.8 * bf + (hier ? 0.8 + 2.0 : 0.0);
-        const double gather_us = 1.6 * (hier ? (world + kMaxLseBatch - 1) / kMaxLseBatch : bf);
+        const double L_us = 5.0 + 0.8 * bf + (hier ? 2.5 : 0.0);
+        const double gather_us = 1.6 * bf + (hier ? 0.2 * (world - 1) : 0.0);
         const int W = std::max(1, pl.nslots / tpc);
         const double exposed = std::max(0.0, L_us - (W - 1) * tpc * tile_us);
         // (+0.4 us fixed per unit: Q load, statistics merge and publish)
