@@ -625,10 +625,35 @@ __device__ __noinline__ void peer_gather_unit(const FusedParams& p, long long ub
         p.peer[r][(parity ^ 1u) * fin_half + rows + (long long)p.rank * NCP + c] = 0ull;
       }
     }
+    // the peers' words of this unit, all loads in flight together (one round trip)
+    const unsigned long long* rw = p.peer[p.rank] + parity * fin_half + rows + c;
+    unsigned long long v[kMaxPeers];
+    unsigned missing = 0;
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r) {
+      v[r] = (r < p.world && r != p.rank) ? ld_relaxed_sys_u64(rw + (long long)r * NCP) : 1ull;
+      missing |= (v[r] == 0ull ? 1u : 0u) << r;
+    }
+    unsigned long long t_dead = 0;
+    for (long long it = 0; __any_sync(0xffffffffu, missing != 0); ++it) {
+      __nanosleep(64);
+#pragma unroll
+      for (int r = 0; r < kMaxPeers; ++r)
+        if (missing & (1u << r)) {
+          v[r] = ld_relaxed_sys_u64(rw + (long long)r * NCP);
+          if (v[r] != 0ull) missing &= ~(1u << r);
+        }
+      if ((it & 1023) == 1023) {
+        const unsigned long long now = globaltimer_ns();
+        if (t_dead == 0) t_dead = now + kSpinNs;
+        else if (now > t_dead) { set_err(p.err, kDevTimeout); missing = 0; }
+      }
+    }
     float M = -CUDART_INF_F, S = 0.f;
-    for (int r = 0; r < p.world; ++r) {
-      const float2 w = r == p.rank ? mine : poll_merge(p, p.peer[p.rank] + parity * fin_half + rows + (long long)r * NCP,
-                                                       1, NCP, c);
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r) {
+      if (r >= p.world) break;
+      const float2 w = r == p.rank ? mine : (v[r] == 0ull ? make_float2(0.f, -1.f) : unpack_ms(v[r]));
       if (w.y > 0.f) merge2(M, S, w.x, w.y);
     }
     if (p.la != nullptr && c < p.NC) {                           // the look-ahead keys' share (Z2')
