@@ -117,7 +117,7 @@ struct FusedParams {
   // the rank word, the unit's designated CTA (token group u mod n_tg) stores it
   // into row `rank` of every peer's rank-word buffer, and every CTA merges the
   // unit's `world` rank words in rank order (the same lse2 bits on every rank;
-  // peer_gather_unit).
+  // peer_merge_col).
   int rank, world;
   unsigned long long* peer[kMaxPeers]; // every rank's rank-word buffer base ([2][B][U][world][NCP])
 };
@@ -557,115 +557,58 @@ __device__ __forceinline__ float transpose_add32(float (&s)[32], int lane) {
 // kSpinNs of globaltimer, well before mbar_wait_slow's 4 s trap.
 constexpr unsigned long long kSpinNs = 2000000000ull;
 
-// Poll `count` 64-bit partial words (stride NCP) of column c until all are
-// written (non-zero), merging them in index order.  Bounded: after kSpinNs the
-// missing words are merged as empty and SP_ETIMEOUT is flagged.
-__device__ __noinline__ float2 poll_merge(const FusedParams& p, const unsigned long long* src, int count, int NCP,
-                                          int c) {
-  float M = -CUDART_INF_F, S = 0.f;
-  for (int s0 = 0; s0 < count; s0 += kMaxLseBatch) {
-    unsigned long long v[kMaxLseBatch];
-    unsigned long long missing = 0;
-#pragma unroll
-    for (int j = 0; j < kMaxLseBatch; ++j) {
-      v[j] = (s0 + j < count) ? ld_relaxed_sys_u64(src + (long long)(s0 + j) * NCP + c) : pack_ms(0.f, -1.f);
-      missing |= (v[j] == 0ull ? 1ull : 0ull) << j;
-    }
-    long long it = 0;
-    unsigned long long t_dead = 0;
-    while (__any_sync(0xffffffffu, missing != 0)) {
-      __nanosleep(it < 8 ? 64 : 200);
-#pragma unroll
-      for (int j = 0; j < kMaxLseBatch; ++j) {
-        if (missing & (1ull << j)) {
-          v[j] = ld_relaxed_sys_u64(src + (long long)(s0 + j) * NCP + c);
-          if (v[j] != 0ull) missing &= ~(1ull << j);
-        }
-      }
-      if ((++it & 1023) == 0 && t_dead == 0) t_dead = globaltimer_ns() + kSpinNs;
-      if (t_dead != 0 && (it & 1023) == 0 && globaltimer_ns() > t_dead) {
-        set_err(p.err, kDevTimeout);
-#pragma unroll
-        for (int j = 0; j < kMaxLseBatch; ++j)
-          if (missing & (1ull << j)) v[j] = pack_ms(0.f, -1.f);
-        missing = 0;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kMaxLseBatch; ++j) {
-      const float2 w = unpack_ms(v[j]);
-      if (w.y > 0.f) merge2(M, S, w.x, w.y);
+// Sequence-sharded peer exchange (world > 1), gather warp, one column, after
+// the rank's n_tg CTA partials were merged into (M, S) (the single-GPU
+// gather): the unit's designated CTA (token group u mod n_tg: spread evenly)
+// stores that rank word into row `rank` of every peer's rank-word buffer
+// (NVLink stores, this launch's parity half; the same row of the other half is
+// re-zeroed for the launch after next); then the world rank words are merged
+// in rank order -- the own one from registers, bit-identical to what the peers
+// read -- so every rank computes the same lse2 bits.  The peers' words are
+// polled together (one round trip).  Inline: the gather's code stays in one
+// place (instruction cache).
+__device__ __forceinline__ void peer_merge_col(const FusedParams& p, const unsigned long long* rw, bool designated,
+                                               uint32_t parity, long long fin_half, int NCP, float& M, float& S) {
+  const unsigned long long own = S > 0.f ? pack_ms(M, S) : pack_ms(-CUDART_INF_F, -1.f);   // never 0
+  if (designated) {
+    for (int r = 0; r < p.world; ++r) {
+      if (r == p.rank) continue;
+      unsigned long long* dst = p.peer[r] + (rw - p.peer[p.rank]) + (long long)p.rank * NCP;
+      st_relaxed_sys_u64(dst + parity * fin_half, own);
+      dst[(parity ^ 1u) * fin_half] = 0ull;
     }
   }
-  return make_float2(M, S);
-}
-
-// Sequence-sharded peer exchange (world > 1), gather warp (whole warp), unit
-// ubase: every CTA merges its own rank's n_tg CTA partials (token-group order,
-// local memory -- the single-GPU gather); the unit's designated CTA (token
-// group u mod n_tg: spread evenly) also stores that rank word into row `rank`
-// of every peer's rank-word buffer (NVLink stores, this launch's parity half;
-// the same row of the other half is re-zeroed for the launch after next); then
-// the world rank words are merged in rank order -- the own one from registers,
-// bit-identical to what the peers read -- so every rank computes the same lse2
-// bits.  Writes lse2 (+ the look-ahead keys' share, Z2') into ls.  Out of line:
-// the single-GPU gather's code stays as it was.
-__device__ __noinline__ void peer_gather_unit(const FusedParams& p, long long ubase, bool designated,
-                                              const unsigned long long* part_cur, uint32_t parity, int NCP, int lane,
-                                              float* ls) {
-  const long long fin_half = (long long)p.B * p.U * p.world * NCP;
-  const long long rows = ubase * p.world * NCP;
-  for (int c = lane; c < NCP; c += 32) {
-    const float2 mine = poll_merge(p, part_cur + ubase * p.n_tg * NCP, p.n_tg, NCP, c);
-    if (designated) {
-      const unsigned long long word = mine.y > 0.f ? pack_ms(mine.x, mine.y) : pack_ms(-CUDART_INF_F, -1.f);
-      for (int r = 0; r < p.world; ++r) {
-        if (r == p.rank) continue;
-        st_relaxed_sys_u64(p.peer[r] + parity * fin_half + rows + (long long)p.rank * NCP + c, word);
-        p.peer[r][(parity ^ 1u) * fin_half + rows + (long long)p.rank * NCP + c] = 0ull;
+  const unsigned long long* cur = rw + parity * fin_half;
+  unsigned long long v[kMaxPeers];
+  unsigned missing = 0;
+#pragma unroll
+  for (int r = 0; r < kMaxPeers; ++r) {
+    v[r] = (r < p.world && r != p.rank) ? ld_relaxed_sys_u64(cur + (long long)r * NCP) : own;
+    missing |= (v[r] == 0ull ? 1u : 0u) << r;
+  }
+  unsigned long long t_dead = 0;
+  for (long long it = 0; __any_sync(0xffffffffu, missing != 0); ++it) {
+    __nanosleep(64);
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r)
+      if (missing & (1u << r)) {
+        v[r] = ld_relaxed_sys_u64(cur + (long long)r * NCP);
+        if (v[r] != 0ull) missing &= ~(1u << r);
       }
+    if ((it & 1023) == 1023) {
+      const unsigned long long now = globaltimer_ns();
+      if (t_dead == 0) t_dead = now + kSpinNs;
+      else if (now > t_dead) { set_err(p.err, kDevTimeout); missing = 0; }
     }
-    // the peers' words of this unit, all loads in flight together (one round trip)
-    const unsigned long long* rw = p.peer[p.rank] + parity * fin_half + rows + c;
-    unsigned long long v[kMaxPeers];
-    unsigned missing = 0;
+  }
+  M = -CUDART_INF_F;
+  S = 0.f;
 #pragma unroll
-    for (int r = 0; r < kMaxPeers; ++r) {
-      v[r] = (r < p.world && r != p.rank) ? ld_relaxed_sys_u64(rw + (long long)r * NCP) : 1ull;
-      missing |= (v[r] == 0ull ? 1u : 0u) << r;
-    }
-    unsigned long long t_dead = 0;
-    for (long long it = 0; __any_sync(0xffffffffu, missing != 0); ++it) {
-      __nanosleep(64);
-#pragma unroll
-      for (int r = 0; r < kMaxPeers; ++r)
-        if (missing & (1u << r)) {
-          v[r] = ld_relaxed_sys_u64(rw + (long long)r * NCP);
-          if (v[r] != 0ull) missing &= ~(1u << r);
-        }
-      if ((it & 1023) == 1023) {
-        const unsigned long long now = globaltimer_ns();
-        if (t_dead == 0) t_dead = now + kSpinNs;
-        else if (now > t_dead) { set_err(p.err, kDevTimeout); missing = 0; }
-      }
-    }
-    float M = -CUDART_INF_F, S = 0.f;
-#pragma unroll
-    for (int r = 0; r < kMaxPeers; ++r) {
-      if (r >= p.world) break;
-      const float2 w = r == p.rank ? mine : (v[r] == 0ull ? make_float2(0.f, -1.f) : unpack_ms(v[r]));
+  for (int r = 0; r < kMaxPeers; ++r) {
+    if (r < p.world && v[r] != 0ull) {
+      const float2 w = unpack_ms(v[r]);
       if (w.y > 0.f) merge2(M, S, w.x, w.y);
     }
-    if (p.la != nullptr && c < p.NC) {                           // the look-ahead keys' share (Z2')
-      const float2 v = p.la[ubase * NCP + c];
-      if (v.y > 0.f) merge2(M, S, v.x, v.y);
-    }
-    float l2 = 0.f;
-    if (c < p.NC) {
-      l2 = M + log2f(S);
-      if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
-    }
-    ls[c] = l2;
   }
 }
 
@@ -1015,8 +958,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         float* ls = lse_s + par * NCP;
         const unsigned long long* src = part_cur + ubase * p.n_tg * NCP;
         const int ntg = p.n_tg;
-        if (p.world > 1 && p.mode == kModeFull)                        // sequence-sharded over GPUs
-          peer_gather_unit(p, ubase, (u % p.n_tg) == jb.tg, part_cur, parity, NCP, lane, ls);
         for (int c = lane; c < NCP && p.mode == kModeFinish; c += 32) {
           // lse2 supplied by the caller (sequence-sharded split: globally combined statistics)
           float l2 = 0.f;
@@ -1026,7 +967,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           }
           ls[c] = l2;
         }
-        for (int c = lane; c < NCP && p.mode == kModeFull && p.world == 1; c += 32) {
+        for (int c = lane; c < NCP && p.mode == kModeFull; c += 32) {
           float M = -CUDART_INF_F, S = 0.f;
           for (int s0 = 0; s0 < ntg; s0 += kMaxLseBatch) {
             unsigned long long v[kMaxLseBatch];
@@ -1061,6 +1002,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
               const float2 w = unpack_ms(v[j]);
               if (w.y > 0.f) merge2(M, S, w.x, w.y);
             }
+          }
+          if (p.world > 1) {                                         // sequence-sharded over GPUs
+            const long long fin_half = (long long)p.B * p.U * p.world * NCP;
+            peer_merge_col(p, p.peer[p.rank] + ubase * p.world * NCP + c, (u % p.n_tg) == jb.tg, parity, fin_half,
+                           NCP, M, S);
           }
           if (p.la != nullptr && c < p.NC) {                         // the look-ahead keys' share (Z2')
             const float2 v = p.la[ubase * NCP + c];

@@ -4,11 +4,10 @@ one rank of a P-GPU run, measured on one GPU (dev tool).
 The P ranks are first run once as co-scheduled virtual ranks (SMs/P CTAs each)
 so that every rank word of every unit exists.  Rank 0's kernel is then
 launched alone with the whole GPU (sm_budget 0, the plan a real rank uses),
-after its rank-word buffer's current half has been filled with the other
-ranks' words (its own row zeroed: its designated CTAs write it): the launch
-streams its 1/P shard and merges the world rank words exactly as on a real
-rank, minus the wait for the slowest peer.  Timed with CUDA events around the
-launch alone.
+with both halves of its rank-word buffer holding the other ranks' words (rank
+0 never writes its own buffer's rows): each launch streams its 1/P shard and
+merges the world rank words exactly as on a real rank, minus the wait for the
+slowest peer.  20 back-to-back launches in a CUDA graph, timed with events.
 
   python tools/peer_replay.py C4 8 [C3 8 ...]
 """
@@ -25,7 +24,7 @@ from spgen import cuda as spgen_cuda  # noqa: E402
 from spgen import gen  # noqa: E402
 
 
-def replay(w, P, iters=12):
+def replay(w, P, iters=5):
     Q, K, T = spgen_cuda.make_inputs(w)
     n = w.N // P
     shards = [K[:, :, :, p * n:(p + 1) * n] for p in range(P)]
@@ -43,33 +42,36 @@ def replay(w, P, iters=12):
         sp.score_peer(Q, shards[p], p, P, ptrs, budget, w.Rv, w.scale, stream=streams[p], ws=wsv[p])
     torch.cuda.synchronize()
     sp.check_device_error()
-    B, U = w.B, w.L * w.Hkv
     words = bufs[0].view(torch.int64)
     half = words.numel() // 2
-    NCP = half // (B * U * P)
-    saved = words[:half].clone().view(B * U, P, NCP)
-    saved[:, 0, :] = 0
-    saved = saved.reshape(-1)
+    saved = words[:half].clone()
+    words[half:].copy_(saved)                         # both parity halves: the peers' words of every unit
     # 2. rank 0 alone on the whole GPU
     ws0 = torch.zeros(sp.score_peer_workspace_bytes(Q, shards[0], P, 0, w.Rv), dtype=torch.uint8, device="cuda")
     out = torch.empty((w.B, n), dtype=torch.float32, device="cuda")
     plan = sp.score_peer_plan(Q, shards[0], P, 0, w.Rv)
+
+    def run():
+        sp.score_peer(Q, shards[0], 0, P, ptrs, 0, w.Rv, w.scale, out=out, ws=ws0)
+
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    ref = out.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(20):
+            run()
     ms = []
-    ref = None
-    for it in range(iters):
-        par = int(ws0.view(torch.int32)[0].item()) & 1
-        words[par * half:(par + 1) * half].copy_(saved)
-        words[(1 - par) * half:(2 - par) * half].zero_()
+    for _ in range(iters):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        sp.score_peer(Q, shards[0], 0, P, ptrs, 0, w.Rv, w.scale, out=out, ws=ws0)
+        g.replay()
         b.record()
         torch.cuda.synchronize()
-        sp.check_device_error()
-        ms.append(a.elapsed_time(b))
-        if ref is None:
-            ref = out.clone()
-        assert torch.equal(out, ref)
+        ms.append(a.elapsed_time(b) / 20)
+    sp.check_device_error()
+    assert torch.equal(out, ref)
     full = sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")[:, :n]
     err = ((out - full).abs() / full.abs().clamp_min(1e-30)).max().item()
     return plan, ms, err, n
@@ -81,9 +83,9 @@ if __name__ == "__main__":
         name, P = args[i], int(args[i + 1])
         w = gen.CONFIGS[name]
         plan, ms, err, n = replay(w, P)
-        best = float(np.min(ms[2:]))
+        best = float(np.min(ms))
         kb = w.k_bytes / P
-        print(f"{name} P={P}: rank-0 kernel {best:.4f} ms (min; median {np.median(ms[2:]):.4f}), "
+        print(f"{name} P={P}: rank-0 kernel {best:.4f} ms (min; median {np.median(ms):.4f}), "
               f"{kb / best / 1e6:.0f} GB/s of its {kb / 2**30:.2f} GiB shard, rel diff vs sp_score {err:.1e}; "
               f"plan n_tg {plan['token_groups']} n_ug {plan['unit_groups']} hier {plan['hier']} "
               f"tiles/job {plan['tiles_per_job']} grid {plan['grid']}", flush=True)
