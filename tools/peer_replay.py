@@ -9,7 +9,7 @@ with both halves of its rank-word buffer holding the other ranks' words (rank
 merges the world rank words exactly as on a real rank, minus the wait for the
 slowest peer.  20 back-to-back launches in a CUDA graph, timed with events.
 
-  python tools/peer_replay.py C4 8 [C3 8 ...]
+  python tools/peer_replay.py C4 8 [C3 8 ...]      (C4 8:16,9 forces the plan n_tg,n_ug)
 """
 import os
 import sys
@@ -24,7 +24,7 @@ from spgen import cuda as spgen_cuda  # noqa: E402
 from spgen import gen  # noqa: E402
 
 
-def replay(w, P, iters=5):
+def replay(w, P, iters=5, plan_env=None):
     Q, K, T = spgen_cuda.make_inputs(w)
     n = w.N // P
     shards = [K[:, :, :, p * n:(p + 1) * n] for p in range(P)]
@@ -46,7 +46,9 @@ def replay(w, P, iters=5):
     half = words.numel() // 2
     saved = words[:half].clone()
     words[half:].copy_(saved)                         # both parity halves: the peers' words of every unit
-    # 2. rank 0 alone on the whole GPU
+    # 2. rank 0 alone on the whole GPU (optionally under a forced plan)
+    if plan_env:
+        os.environ["SP_FUSED_PLAN"] = plan_env
     ws0 = torch.zeros(sp.score_peer_workspace_bytes(Q, shards[0], P, 0, w.Rv), dtype=torch.uint8, device="cuda")
     out = torch.empty((w.B, n), dtype=torch.float32, device="cuda")
     plan = sp.score_peer_plan(Q, shards[0], P, 0, w.Rv)
@@ -72,6 +74,7 @@ def replay(w, P, iters=5):
         ms.append(a.elapsed_time(b) / 20)
     sp.check_device_error()
     assert torch.equal(out, ref)
+    os.environ.pop("SP_FUSED_PLAN", None)
     full = sp.score(Q, K, R_valid=w.Rv, scale=w.scale, algo="fused")[:, :n]
     err = ((out - full).abs() / full.abs().clamp_min(1e-30)).max().item()
     return plan, ms, err, n
@@ -80,9 +83,10 @@ def replay(w, P, iters=5):
 if __name__ == "__main__":
     args = sys.argv[1:]
     for i in range(0, len(args), 2):
-        name, P = args[i], int(args[i + 1])
+        name, Ps = args[i], args[i + 1]
+        P, plan_env = (int(Ps.split(":")[0]), Ps.split(":")[1]) if ":" in Ps else (int(Ps), None)
         w = gen.CONFIGS[name]
-        plan, ms, err, n = replay(w, P)
+        plan, ms, err, n = replay(w, P, plan_env=plan_env)
         best = float(np.min(ms))
         kb = w.k_bytes / P
         print(f"{name} P={P}: rank-0 kernel {best:.4f} ms (min; median {np.median(ms):.4f}), "
