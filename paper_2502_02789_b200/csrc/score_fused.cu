@@ -566,7 +566,7 @@ constexpr unsigned long long kSpinNs = 2000000000ull;
 // in rank order -- the own one from registers, bit-identical to what the peers
 // read -- so every rank computes the same lse2 bits.  The peers' words are
 // polled together (one round trip).  Inline: the gather's code stays in one
-// place (instruction cache).
+// place: it runs inside peer_gather_unit.
 __device__ __forceinline__ void peer_merge_col(const FusedParams& p, const unsigned long long* rw, bool designated,
                                                uint32_t parity, long long fin_half, int NCP, float& M, float& S) {
   const unsigned long long own = S > 0.f ? pack_ms(M, S) : pack_ms(-CUDART_INF_F, -1.f);   // never 0
@@ -609,6 +609,67 @@ __device__ __forceinline__ void peer_merge_col(const FusedParams& p, const unsig
       const float2 w = unpack_ms(v[r]);
       if (w.y > 0.f) merge2(M, S, w.x, w.y);
     }
+  }
+}
+
+// Sequence-sharded gather of one unit (whole warp): the rank's n_tg partials
+// (the single-GPU gather's loop), then peer_merge_col, then lse2 (+ the
+// look-ahead keys' share, Z2') into ls.  Out of line, once per unit: the
+// single-GPU gather's code stays exactly as it is (measured: inlining this
+// path into the gather loop cost the single-GPU kernel 3 %).
+__device__ __noinline__ void peer_gather_unit(const FusedParams& p, long long ubase, bool designated,
+                                              const unsigned long long* part_cur, uint32_t parity, int NCP, int lane,
+                                              float* ls) {
+  const unsigned long long* src = part_cur + ubase * p.n_tg * NCP;
+  const int ntg = p.n_tg;
+  const long long fin_half = (long long)p.B * p.U * p.world * NCP;
+  for (int c = lane; c < NCP; c += 32) {
+    float M = -CUDART_INF_F, S = 0.f;
+    for (int s0 = 0; s0 < ntg; s0 += kMaxLseBatch) {
+      unsigned long long v[kMaxLseBatch];
+      unsigned long long missing = 0;
+#pragma unroll
+      for (int j = 0; j < kMaxLseBatch; ++j) {
+        v[j] = (s0 + j < ntg) ? ld_relaxed_sys_u64(src + (long long)(s0 + j) * NCP + c) : pack_ms(0.f, -1.f);
+        missing |= (v[j] == 0ull ? 1ull : 0ull) << j;
+      }
+      long long it = 0;
+      unsigned long long t_dead = 0;
+      while (__any_sync(0xffffffffu, missing != 0)) {
+        __nanosleep(it < 8 ? 64 : 200);
+#pragma unroll
+        for (int j = 0; j < kMaxLseBatch; ++j) {
+          if (missing & (1ull << j)) {
+            v[j] = ld_relaxed_sys_u64(src + (long long)(s0 + j) * NCP + c);
+            if (v[j] != 0ull) missing &= ~(1ull << j);
+          }
+        }
+        if ((++it & 1023) == 0 && t_dead == 0) t_dead = globaltimer_ns() + kSpinNs;
+        if (t_dead != 0 && (it & 1023) == 0 && globaltimer_ns() > t_dead) {
+          set_err(p.err, kDevTimeout);
+#pragma unroll
+          for (int j = 0; j < kMaxLseBatch; ++j)
+            if (missing & (1ull << j)) v[j] = pack_ms(0.f, -1.f);
+          missing = 0;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kMaxLseBatch; ++j) {
+        const float2 w = unpack_ms(v[j]);
+        if (w.y > 0.f) merge2(M, S, w.x, w.y);
+      }
+    }
+    peer_merge_col(p, p.peer[p.rank] + ubase * p.world * NCP + c, designated, parity, fin_half, NCP, M, S);
+    if (p.la != nullptr && c < p.NC) {                           // the look-ahead keys' share (Z2')
+      const float2 v = p.la[ubase * NCP + c];
+      if (v.y > 0.f) merge2(M, S, v.x, v.y);
+    }
+    float l2 = 0.f;
+    if (c < p.NC) {
+      l2 = M + log2f(S);
+      if (!isfinite(l2)) set_err(p.err, kDevNonFinite);
+    }
+    ls[c] = l2;
   }
 }
 
@@ -967,7 +1028,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           }
           ls[c] = l2;
         }
-        for (int c = lane; c < NCP && p.mode == kModeFull; c += 32) {
+        if (p.world > 1 && p.mode == kModeFull)                        // sequence-sharded over GPUs
+          peer_gather_unit(p, ubase, (u % p.n_tg) == jb.tg, part_cur, parity, NCP, lane, ls);
+        for (int c = lane; c < NCP && p.mode == kModeFull && p.world == 1; c += 32) {
           float M = -CUDART_INF_F, S = 0.f;
           for (int s0 = 0; s0 < ntg; s0 += kMaxLseBatch) {
             unsigned long long v[kMaxLseBatch];
@@ -1002,11 +1065,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
               const float2 w = unpack_ms(v[j]);
               if (w.y > 0.f) merge2(M, S, w.x, w.y);
             }
-          }
-          if (p.world > 1) {                                         // sequence-sharded over GPUs
-            const long long fin_half = (long long)p.B * p.U * p.world * NCP;
-            peer_merge_col(p, p.peer[p.rank] + ubase * p.world * NCP + c, (u % p.n_tg) == jb.tg, parity, fin_half,
-                           NCP, M, S);
           }
           if (p.la != nullptr && c < p.NC) {                         // the look-ahead keys' share (Z2')
             const float2 v = p.la[ubase * NCP + c];
