@@ -192,12 +192,15 @@ def _peer_buffers(Q, K_local, R_valid, group):
 
 
 def seq_sharded_fused_specprefill(Q, K_local, tokens, N_total: int, keep: float, pool_k: int, chunk: int,
-                                  R_valid=None, scale=None, pos0: int = 0, group=None) -> dict:
+                                  R_valid=None, scale=None, pos0: int = 0, group=None, check: bool = True) -> dict:
     """Sequence-sharded single pass for one request (B = 1): the statistics
     exchange runs inside the fused kernel over peer memory (one K read per
     rank); the edge all-gather of the sharded selection that follows also
     separates consecutive calls (sp_score_peer's barrier requirement: no rank
-    starts the next launch before every rank's kernel finished)."""
+    starts the next launch before every rank's kernel finished).  check: read
+    the device error flag at the end (synchronises the stream) so a peer that
+    never arrived (SP_ETIMEOUT: its words merged as empty) raises instead of
+    returning a silently wrong selection."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     n_local = K_local.shape[3]
@@ -206,6 +209,8 @@ def seq_sharded_fused_specprefill(Q, K_local, tokens, N_total: int, keep: float,
     ptrs, ws = _peer_buffers(Q, K_local, R_valid, group)
     imp_local = api.score_peer(Q, K_local, rank, world, ptrs, 0, R_valid, scale, ws=ws)
     ids, pos, n_kept, out = seq_sharded_select(imp_local, N_total, keep, pool_k, chunk, pos0, tokens, group)
+    if check:
+        api.check_device_error()
     return dict(importance_local=imp_local, ids=ids, pos=pos, n_kept=n_kept, out_tokens=out,
                 first_decode=N_total + pos0)
 
