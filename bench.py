@@ -404,18 +404,33 @@ def run_ours(args):
         run_step()
     t_end.record(stream)
     barrier()
-    # the dominant kernel alone, same launch configuration, same stream
-    s_start = torch.cuda.Event(enable_timing=True)
-    s_end = torch.cuda.Event(enable_timing=True)
-    s_start.record(stream)
-    for _ in range(args.steps):
-        run_score()
-    s_end.record(stream)
-    barrier()
+    # the dominant kernel alone, same launch configuration, same stream.  The
+    # sequence-sharded peer kernel needs a cross-rank barrier between launches
+    # (its rank-word buffers alternate halves): each launch is bracketed by its
+    # own events and the barrier sits outside them.
+    if seq_peer:
+        score_ms = 0.0
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run_score()
+            e1.record(stream)
+            barrier()
+            score_ms += e0.elapsed_time(e1)
+        score_ms /= args.steps
+    else:
+        s_start = torch.cuda.Event(enable_timing=True)
+        s_end = torch.cuda.Event(enable_timing=True)
+        s_start.record(stream)
+        for _ in range(args.steps):
+            run_score()
+        s_end.record(stream)
+        barrier()
     clk = clocks.stop()
     sp.check_device_error()
     ms_total = t_start.elapsed_time(t_end)
-    score_ms = s_start.elapsed_time(s_end) / args.steps
+    if not seq_peer:
+        score_ms = s_start.elapsed_time(s_end) / args.steps
     if dist is not None:
         tt = torch.tensor([ms_total, score_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
