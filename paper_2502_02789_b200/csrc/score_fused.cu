@@ -1292,9 +1292,7 @@ uint32_t carve(Plan& pl, int Rv, int stages) {
   pl.off_lse = o;
   o += kLseRing * pl.NCP * 4;
   o = (o + 15) & ~15u;
-  pl.off_comb = o;
-  o += 16 + 4 * pl.NCP * 8;
-  o = (o + 15) & ~15u;
+  pl.off_comb = o;                                   // (unused)
   pl.off_bt = o;                                     // paged K: the job's block-table slice
   o += (kMaxSlots * kTileM / 8 + 8) * 4;
   pl.off_bar = o;
@@ -1414,6 +1412,13 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   const int s2 = max_stages(2), s4 = max_stages(4);
   pl.nq = (s4 >= 2 && (s4 >= s2 || pl.tpc <= 8)) ? 4 : 2;
   int stages = pl.nq == 4 ? s4 : s2;
+  // development A/B knobs (timing only): SP_FUSED_NQ=2|4, SP_FUSED_MAXSTAGES=n
+  if (const char* e = allow_override ? std::getenv("SP_FUSED_NQ") : nullptr) {
+    const int nq = std::atoi(e);
+    if ((nq == 2 && s2 >= 2) || (nq == 4 && s4 >= 2)) { pl.nq = nq; stages = nq == 4 ? s4 : s2; }
+  }
+  if (const char* e = allow_override ? std::getenv("SP_FUSED_MAXSTAGES") : nullptr)
+    stages = std::max(2, std::min(stages, std::atoi(e)));
   if (stages < 2) return pl;
   pl.stages = stages;
   pl.smem = carve(pl, g.Rv, stages);
