@@ -63,6 +63,10 @@ constexpr int kTileM = 128;
 constexpr int kStatsWarp0 = 4;
 constexpr int kFinalWarp0 = 8;
 constexpr int kMaxStages = 8;
+// Stage cap of the plans (measured, r2 tools/gpu_r2_stages.sh): more TMA tiles in
+// flight than 4 slow the bf16 kernel down (C3 37x4: 4 stages 0.3405 ms, 5: 0.3442;
+// C1 8x16: 0.0720 vs 0.0745); the e4m3 kernel is indifferent (3..8 stages within 0.5 %).
+constexpr int kStageCap = 4;
 constexpr int kMaxChunks = 8;          // NCP <= 128 columns (16-column chunks)
 constexpr int kMaxSlots = 16;          // TMEM tile slots (512 columns / 32)
 constexpr int kLseRing = 8;            // lse2 buffers in SMEM (gather may run ahead of aggregation)
@@ -1405,7 +1409,7 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   // 4 query slots (Q loads issued 3 units ahead) unless that costs a K stage on long units
   auto max_stages = [&](int nq) {
     pl.nq = nq;
-    int s = kMaxStages;
+    int s = kStageCap;
     while (s >= 2 && carve(pl, g.Rv, s) > (uint32_t)kSmemLimit) --s;
     return s;
   };
