@@ -39,7 +39,7 @@
 //             array (absent chunks marked invalid), B-C with K = K_c over the
 //             whole prompt: the global top-K_c is a subset of the union of the
 //             local top-M lists because every rank ranks by the same total order.
-#include "sp_internal.h"
+#include "select_body.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -47,397 +47,19 @@
 namespace sp {
 namespace {
 
+using namespace sel;
 constexpr int ST = 1024;
-constexpr int NW = ST / 32;
-constexpr int SEG = 16384;          // tokens of importance staged in SMEM per segment (64 KiB)
-constexpr int kMaxPool = 4097;      // largest pooling window (half-window staged on each side)
-constexpr int kSmemChunks = 8192;   // chunk scores kept in SMEM when n_c fits (else L2-resident workspace)
-constexpr unsigned kInvalid = 0xFFFFFFFFu;   // merge: chunk with no candidate (never a score: scores are >= 0)
-enum SelectMode : int { kModeAll = 0, kModeA = 1 };
-enum Variant : int { kPlain = 0, kCand = 1, kMerge = 2 };
-
-struct SelArgs {
-  const float* imp;          // [B][row] importance (kCand: this rank's shard)
-  unsigned* blk_cnt;         // [B] kModeA: phase-A CTAs done (workspace, zero, self-resetting)
-  long long row;             // row length of imp / ids / pos / tokens / out
-  const int* seq_lens;       // kPlain, optional [B]: per-request prompt length (row f3)
-  int pool_k, chunk, pos0;
-  long long ppm;             // keep rate in parts per million (K_c, Z9)
-  int* ids;
-  int* pos;
-  int* n_kept;
-  float* cs_ws;              // [B][n_c_row] chunk scores (workspace)
-  const int* tokens;         // optional gather source [B][row]
-  int* out;                  // optional gathered tokens [B][row]
-  int mode, segcap;
-  long long cpb;             // chunks per CTA in kModeA
-  // sequence sharding
-  long long i0;              // kCand: global index of this shard's first token
-  long long n_glob;          // kCand / kMerge: prompt length N (kPlain: row / seq_lens)
-  const float* edges;        // kCand: [P][B][2w] first w / last w importance values of every rank
-  int rank, world;
-  long long k_sel;           // kCand: M
-  unsigned long long* cand;  // kCand: [B][M] candidate keys out
-  const unsigned long long* cand_in;   // kMerge: [P][B][M] candidate keys
-};
-
-struct ScanSmem {
-  int warp_tot[NW];
-  int total;
-};
-
-// Block-wide exclusive scan of v (all ST threads participate); returns the
-// exclusive prefix, writes the block total to *total.
-__device__ __forceinline__ int block_excl_scan(int v, ScanSmem& sm, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) sm.warp_tot[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int t = lane < NW ? sm.warp_tot[lane] : 0;
-    int u = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, u, o);
-      if (lane >= o) u += y;
-    }
-    if (lane < NW) sm.warp_tot[lane] = u - t;    // exclusive warp offsets
-    if (lane == 31) sm.total = u;
-  }
-  __syncthreads();
-  int res = sm.warp_tot[warp] + x - v;
-  *total = sm.total;
-  __syncthreads();                                 // sm reusable after return
-  return res;
-}
-
-// Segment length starting at chunk-aligned token `base`: whole chunks when a
-// chunk fits the segment, else the rest of the chunk up to segcap tokens.
-__device__ __forceinline__ long long seg_len(long long base, long long t_hi, int chunk, int segcap) {
-  long long next;
-  if (chunk <= segcap) {
-    next = base + (long long)(segcap / chunk) * chunk;
-  } else {
-    const long long cend = (base / chunk + 1) * chunk;
-    next = base + segcap < cend ? base + segcap : cend;
-  }
-  return (next < t_hi ? next : t_hi) - base;
-}
 
 template <int V>
 __global__ void __launch_bounds__(ST) k_select(SelArgs a) {
-  extern __shared__ float seg[];                  // [segcap + 2w] staged importance, then [segcap] pooled
-  __shared__ unsigned hist[256];
-  __shared__ unsigned s_digit, s_remaining;
-  __shared__ ScanSmem scan;
-  __shared__ int kept_c[ST];                      // kept chunk ids of one scan tile, in order
-  __shared__ int kept_off[ST];
-  __shared__ int s_last;
+  extern __shared__ __align__(16) float dyn[];    // [segcap + 2w] staged importance, [segcap] pooled, [n_c] scores
   // programmatic dependent launch: this grid may start while the producer of
   // the importance (the score kernel) is finishing; wait for its results here,
   // then let the next dependent launch begin its own prologue
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
-  const int mode = a.mode, chunk = a.chunk, pool_k = a.pool_k;
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long Nrow = a.row;
-  // N: the prompt length the pooling edges and chunk sizes refer to (global when sharded)
-  long long N;
-  if (V == kPlain) N = a.seq_lens ? std::min<long long>(std::max(a.seq_lens[b], 1), Nrow) : Nrow;
-  else N = a.n_glob;
-  const long long i0 = V == kCand ? a.i0 : 0;                    // global index of imp[b][0]
-  const long long n_loc = V == kCand ? Nrow : N;                 // tokens held in imp rows
-  const long long c_base = i0 / chunk;                           // global id of local chunk 0
-  const long long n_c_all = (N + chunk - 1) / chunk;             // chunks of the prompt
-  const long long n_c = V == kCand ? n_loc / chunk : n_c_all;    // chunks this selection ranks
-  const long long n_c_row = V == kPlain ? (Nrow + chunk - 1) / chunk : n_c;   // workspace row
-  long long K_sel;
-  if (V == kCand) K_sel = a.k_sel;
-  else K_sel = std::min(n_c_all, std::max(1LL, (a.ppm * n_c_all + 999999) / 1000000));
-  const float* imp = a.imp + (long long)b * Nrow;
-  const long long w = (pool_k - 1) / 2;
-  // chunk scores: SMEM when this CTA runs phases B-C and n_c fits, else the workspace
-  // (decided on the row's chunk count, as the launch sized the SMEM: a ragged request may have fewer)
-  const bool cs_smem = mode == kModeAll && n_c_row <= kSmemChunks;
-  float* cs = cs_smem ? seg + 2 * a.segcap + 2 * w : a.cs_ws + (long long)b * n_c_row;
-
-  if (V == kMerge) {
-    // ---- scatter the P ranks' candidates into the dense chunk array
-    unsigned* csu = reinterpret_cast<unsigned*>(cs);
-    for (long long c = tid; c < n_c; c += ST) csu[c] = kInvalid;
-    __syncthreads();
-    const long long M = a.k_sel;
-    for (int p = 0; p < a.world; ++p) {
-      const unsigned long long* src = a.cand_in + ((long long)p * gridDim.x + b) * M;
-      for (long long m = tid; m < M; m += ST) {
-        const unsigned long long key = src[m];
-        const unsigned c = ~(unsigned)(key & 0xFFFFFFFFull);
-        if (c < (unsigned long long)n_c) csu[c] = (unsigned)(key >> 32);
-      }
-    }
-    __syncthreads();
-  } else {
-  // ---- A. pooled scores (centred window, shrinking edges) -> chunk sums of
-  //      chunks [c_lo, c_hi) (global ids; all of the CTA's range unless kModeA)
-  const long long c_lo = c_base + (mode == kModeA ? std::min(n_c, (long long)blockIdx.y * a.cpb) : 0);
-  const long long c_hi = c_base + (mode == kModeA ? std::min(n_c, (long long)blockIdx.y * a.cpb + a.cpb) : n_c);
-  const long long t_lo = c_lo * chunk, t_hi = std::min(N, c_hi * chunk);
-  const int segcap = a.segcap;
-  float* pooled = seg + segcap + 2 * w;             // [segcap]
-  const int wi = (int)w;
-  const float inv_k = 1.f / (float)pool_k;
-  const bool warp_chunks = chunk <= 32 && (chunk & (chunk - 1)) == 0;   // power of two <= 32
-  // kCand: importance of global token t in [i0 - w, i0 + n_loc + w): own shard, or a neighbour's edge
-  const float* halo_l = nullptr;
-  const float* halo_r = nullptr;
-  if (V == kCand) {
-    const long long eb = 2 * w;                       // edges row: first w, then last w values
-    if (a.rank > 0) halo_l = a.edges + ((long long)(a.rank - 1) * gridDim.x + b) * eb + w;
-    if (a.rank + 1 < a.world) halo_r = a.edges + ((long long)(a.rank + 1) * gridDim.x + b) * eb;
-  }
-  for (long long base = t_lo; base < t_hi;) {
-    const int len = (int)seg_len(base, t_hi, chunk, segcap);             // tokens in this segment
-    const long long lo = base - w < 0 ? 0 : base - w, hi = base + len + w > N ? N : base + len + w;
-    const int off = (int)(base - lo);                                     // seg index of token `base`
-    {
-      // all loads of the segment in flight before any store (latency-bound otherwise)
-      constexpr int PER = SEG / ST;
-      const int n = (int)(hi - lo);
-      float r[PER];
-      if (V == kCand) {
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-          const int i = tid + k * ST;
-          const long long t = lo + i;
-          r[k] = i >= n ? 0.f
-                        : (t < i0 ? __ldg(halo_l + (t - (i0 - w)))
-                                  : (t >= i0 + n_loc ? __ldg(halo_r + (t - i0 - n_loc)) : __ldg(imp + (t - i0))));
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-          const int i = tid + k * ST;
-          r[k] = i < n ? __ldg(imp + lo + i) : 0.f;
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        const int i = tid + k * ST;
-        if (i < n) seg[i] = r[k];
-      }
-      for (int i = PER * ST + tid; i < n; i += ST) {                    // halo beyond SEG
-        const long long t = lo + i;
-        if (V == kCand)
-          seg[i] = t < i0 ? halo_l[t - (i0 - w)] : (t >= i0 + n_loc ? halo_r[t - i0 - n_loc] : imp[t - i0]);
-        else
-          seg[i] = imp[t];
-      }
-    }
-    __syncthreads();
-    // interior tokens [i_lo, i_hi) have the full window inside the sequence
-    const int i_lo = (int)(w - base > 0 ? w - base : 0);
-    const int i_hi = (int)(N - 1 - w - base + 1 < len ? N - 1 - w - base + 1 : len);
-#pragma unroll 4
-    for (int i = tid; i < len; i += ST) {                               // coalesced, conflict-free
-      float ws = 0.f;
-      if (i >= i_lo && i < i_hi) {                                      // interior: full window
-        const float* p0 = seg + off + i - wi;
-        for (int k = 0; k < pool_k; ++k) ws += p0[k];
-        pooled[i] = ws * inv_k;
-      } else {                                                            // sequence edges: shrink
-        const long long t = base + i;
-        const long long e0 = t - w < 0 ? 0 : t - w, e1 = t + w > N - 1 ? N - 1 : t + w;
-        for (long long j = e0; j <= e1; ++j) ws += seg[j - lo];
-        pooled[i] = ws / (float)(e1 - e0 + 1);
-      }
-    }
-    __syncthreads();
-    const long long c_first = base / chunk, c_last = (base + len - 1) / chunk;
-    if (warp_chunks) {
-      // a warp sums 32 consecutive pooled values in groups of `chunk` lanes (tree
-      // order); segments start on chunk boundaries and hold whole chunks
-      const int lg = __ffs(chunk) - 1;
-      const long long cb = (base >> lg) - c_base;
-#pragma unroll 4
-      for (int g0 = warp * 32; g0 < len; g0 += ST) {
-        float v = g0 + lane < len ? pooled[g0 + lane] : 0.f;
-        for (int o = chunk >> 1; o >= 1; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, chunk);
-        if ((lane & (chunk - 1)) == 0 && g0 + lane < len) cs[cb + ((g0 + lane) >> lg)] = v;
-      }
-    } else {
-      // the owner thread walks its chunk's tokens in a rotated (fixed, hence
-      // deterministic) order so a warp's reads hit distinct banks
-      for (long long c = c_first + tid; c <= c_last; c += ST) {
-        const long long t0 = c * chunk > base ? c * chunk : base;
-        const long long t1 = (c + 1) * chunk < base + len ? (c + 1) * chunk : base + len;
-        const int n = (int)(t1 - t0), ii = (int)(t0 - base);
-        float sacc = (t0 == c * chunk) ? 0.f : cs[c - c_base];          // chunk continued from the previous segment
-        const int rot = (int)(c % n);
-        for (int j = 0; j < n; ++j) {
-          int k = j + rot;
-          if (k >= n) k -= n;
-          sacc += pooled[ii + k];
-        }
-        cs[c - c_base] = sacc;
-      }
-    }
-    __syncthreads();
-    base += len;
-  }
-  for (long long c = c_lo + tid; c < c_hi; c += ST) {
-    const long long sz = ((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk;
-    cs[c - c_base] = cs[c - c_base] / (float)sz;
-  }
-  __syncthreads();
-  }
-  if (mode == kModeA) {
-    // the request's last phase-A CTA to finish runs phases B-C (one launch for
-    // the whole selection): every CTA publishes its chunk scores, then counts
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(a.blk_cnt + b, 1u) + 1u == gridDim.y;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (tid == 0) a.blk_cnt[b] = 0u;                                     // self-resetting for the next call
-    if (n_c_row <= kSmemChunks) {                                       // the launch sized SMEM for it
-      float* cs_s = seg + 2 * a.segcap + 2 * w;
-      for (long long c = tid; c < n_c; c += ST) cs_s[c] = __ldcg(cs + c);
-      cs = cs_s;
-    }
-    __syncthreads();
-  }
-
-  // ---- B. radix select: threshold bit pattern T of the K_sel-th largest score.
-  //      Up to kRankMax chunks the rank is counted directly instead:
-  //      rank(c) = #{c' : cs[c'] > cs[c], or cs[c'] == cs[c] and c' < c} (the
-  //      (score desc, index asc) order), kept iff rank < K_sel -- one pass, no
-  //      barrier rounds (measured: 2 us faster at 128 chunks, 29 us slower at 1024).
-  //      kMerge: invalid entries (bit pattern kInvalid, a NaN) never count.
-  constexpr int kRankMax = 256;
-  const bool by_rank = n_c <= kRankMax;
-  unsigned prefix = 0, pmask = 0;
-  unsigned remaining = (unsigned)K_sel;
-  int rank_keep = 0;
-  if (by_rank) {
-    if (tid < n_c) {
-      const float mine = cs[tid];
-      int rank = 0;
-#pragma unroll 8
-      for (int c2 = 0; c2 < (int)n_c; ++c2) {
-        const float o = cs[c2];                      // same address in every lane: broadcast
-        rank += (o > mine || (o == mine && c2 < tid)) ? 1 : 0;
-      }
-      rank_keep = rank < K_sel ? 1 : 0;
-      if (V == kMerge && __float_as_uint(mine) == kInvalid) rank_keep = 0;
-    }
-  }
-  for (int shift = 24; shift >= 0 && !by_rank; shift -= 8) {
-    if (tid < 256) hist[tid] = 0;
-    __syncthreads();
-    // warp-aggregated: lanes with the same digit add once (the top digits of
-    // near-equal scores collide, and SMEM atomics on one address serialise)
-    for (long long c0 = (long long)warp * 32; c0 < n_c; c0 += ST) {
-      const long long c = c0 + lane;
-      const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
-      const bool in = c < n_c && (V != kMerge || key != kInvalid);
-      const unsigned digit = (in && (key & pmask) == prefix) ? (key >> shift) & 255u : 256u;
-      const unsigned peers = __match_any_sync(0xffffffffu, digit);
-      if (digit < 256u && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], (unsigned)__popc(peers));
-    }
-    __syncthreads();
-    // digit D: count(digits > D) < remaining <= count(digits >= D); warps 0-7 scan 256 bins
-    if (tid < 256) {
-      // suffix sums over bins (high digit first): bin d handled by thread 255 - d
-      const int d = 255 - tid;
-      unsigned v = hist[d];
-      unsigned x = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (lane == 31) scan.warp_tot[warp] = (int)x;
-      __syncwarp();
-      // (warps 0..7 only) combine warp totals below
-      kept_off[tid] = (int)x;                      // inclusive within warp
-    }
-    __syncthreads();
-    if (tid < 256) {
-      unsigned before = 0;
-      for (int ww = 0; ww < warp; ++ww) before += (unsigned)scan.warp_tot[ww];
-      const unsigned incl = before + (unsigned)kept_off[tid];   // count of digits >= d
-      const unsigned excl = incl - hist[255 - tid];             // count of digits > d
-      if (excl < remaining && incl >= remaining) {
-        s_digit = (unsigned)(255 - tid);
-        s_remaining = remaining - excl;
-      }
-    }
-    __syncthreads();
-    prefix |= s_digit << shift;
-    pmask |= 255u << shift;
-    remaining = s_remaining;
-    __syncthreads();
-  }
-  const unsigned T = prefix;
-  const int need_eq = (int)remaining;            // chunks equal to T to keep (lowest indices first)
-
-  // ---- C. keep flags in chunk order, compaction (+ gather) of the kept token
-  //      ranges, or (kCand) the kept chunks' candidate keys
-  int carry_eq = 0, carry_tok = 0, carry_k = 0;
-  const int* tokens = a.tokens ? a.tokens + (long long)b * Nrow : nullptr;
-  int* out = a.out ? a.out + (long long)b * Nrow : nullptr;
-  int* ids = a.ids + (long long)b * Nrow;
-  int* pos = a.pos + (long long)b * Nrow;
-  for (long long base = 0; base < n_c; base += ST) {
-    const long long c = base + tid;
-    const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
-    const bool in = c < n_c && (V != kMerge || key != kInvalid);
-    const int eq = (in && key == T) ? 1 : 0;
-    const int gt = (in && key > T) ? 1 : 0;
-    int tot;
-    const int eq_rank = block_excl_scan(eq, scan, &tot) + carry_eq;
-    carry_eq += tot;
-    const int keep = by_rank ? rank_keep : (gt | (eq & (eq_rank < need_eq ? 1 : 0)));
-    const int slot = block_excl_scan(keep, scan, &tot);          // index among kept chunks of this tile
-    const int nk = tot;
-    if (V == kCand) {
-      if (keep)
-        a.cand[(long long)b * K_sel + carry_k + slot] =
-            ((unsigned long long)key << 32) | (unsigned long long)(~(unsigned)(c + c_base));
-      carry_k += nk;
-      continue;
-    }
-    int sz = 0;
-    if (keep) sz = (int)(((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk);
-    int tot2;
-    const int off = block_excl_scan(sz, scan, &tot2) + carry_tok;
-    if (keep) {
-      kept_c[slot] = (int)c;
-      kept_off[slot] = off;
-    }
-    __syncthreads();
-    // one warp per kept chunk: coalesced ids / pos (/ gathered tokens)
-    for (int k = warp; k < nk; k += NW) {
-      const long long cc = kept_c[k];
-      const int t0 = (int)(cc * chunk);
-      const int csz = (int)(((cc + 1) * chunk < N ? (cc + 1) * chunk : N) - cc * chunk);
-      const int o = kept_off[k];
-      for (int j = lane; j < csz; j += 32) {
-        ids[o + j] = t0 + j;
-        pos[o + j] = t0 + j + a.pos0;
-        if (out) out[o + j] = tokens[t0 + j];
-      }
-    }
-    carry_tok += tot2;
-    __syncthreads();
-  }
-  if (V != kCand && tid == 0) a.n_kept[b] = carry_tok;
+  SelShared<ST>& sh = *reinterpret_cast<SelShared<ST>*>(dyn + a.sh_off);
+  select_body<V, ST>(a, blockIdx.x, blockIdx.y, dyn, sh);
 }
 
 __global__ void k_seq_edges(const float* __restrict__ imp, long long n, int w, float* __restrict__ edges) {
@@ -446,7 +68,8 @@ __global__ void k_seq_edges(const float* __restrict__ imp, long long n, int w, f
     edges[(long long)b * 2 * w + j] = imp[(long long)b * n + (j < w ? j : n - 2 * w + j)];
 }
 
-constexpr size_t kSmemMax = (size_t)(2 * SEG + 2 * ((kMaxPool - 1) / 2) + kSmemChunks) * sizeof(float);
+constexpr size_t kSmemMax = (size_t)(2 * SEG + 2 * ((kMaxPool - 1) / 2) + kSmemChunks + 4) * sizeof(float) +
+                            sizeof(SelShared<ST>);
 
 // The >48 KiB dynamic-SMEM opt-in is a per-device function attribute: set it
 // once per (device, variant).
@@ -496,21 +119,30 @@ cudaError_t launch_select(SelArgs a, int B, long long n_tok, long long n_chunks,
   if (e != cudaSuccess) return e;
   const long long w = (a.pool_k - 1) / 2;
   const int chunk = a.chunk;
-  constexpr long long kTokPerCta = 2048;
+  static const long long kTokPerCta = std::getenv("SP_SELECT_TPC") ? std::atoll(std::getenv("SP_SELECT_TPC")) : 2048;
   const long long cpb = std::max(1LL, kTokPerCta / chunk);
   const long long nblk = (n_chunks + cpb - 1) / cpb;
-  const size_t cs_bytes = (size_t)(n_chunks <= kSmemChunks ? n_chunks : 0) * sizeof(float);
+  const long long cs_floats = n_chunks <= kSmemChunks ? n_chunks : 0;
+  a.nreq = B;
+  auto smem_for = [&](int segcap) {                 // staged region (16-byte aligned), then the scratch
+    a.sh_off = (int)((2 * segcap + 2 * w + cs_floats + 3) / 4 * 4);
+    return (size_t)a.sh_off * sizeof(float) + sizeof(SelShared<ST>);
+  };
   if (V != kMerge && nblk >= 4 && nblk <= 65535) {
     const long long span = std::min(n_tok, cpb * chunk);
     a.segcap = chunk > SEG ? SEG : (int)std::min<long long>(SEG, (span + 31) / 32 * 32);
     a.cpb = cpb;
+    a.nblk = (int)nblk;
     a.mode = kModeA;
-    return launch_pdl<V>(dim3(B, (unsigned)nblk), (size_t)(2 * a.segcap + 2 * w) * sizeof(float) + cs_bytes, st, a);
+    const size_t smem = smem_for(a.segcap);
+    return launch_pdl<V>(dim3(B, (unsigned)nblk), smem, st, a);
   }
   a.segcap = SEG;
   a.cpb = n_chunks;
+  a.nblk = 1;
   a.mode = kModeAll;
-  return launch_pdl<V>(dim3(B), (size_t)(2 * SEG + 2 * w) * sizeof(float) + cs_bytes, st, a);
+  const size_t smem = smem_for(SEG);
+  return launch_pdl<V>(dim3(B), smem, st, a);
 }
 
 }  // namespace

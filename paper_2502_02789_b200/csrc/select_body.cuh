@@ -1,0 +1,417 @@
+// The selection kernel's body (select.cu), as a device function over NT
+// threads, so that the standalone kernel (NT = 1024) and the score kernel's
+// fused tail (NT = 384, score_fused.cu) run the same code and give the same
+// bits.  See select.cu for the method and its citations.  Internal header.
+#pragma once
+
+#include <algorithm>
+
+#include "sp_internal.h"
+
+namespace sp {
+namespace sel {
+
+constexpr int SEG = 16384;          // tokens of importance staged in SMEM per segment (64 KiB)
+constexpr int kMaxPool = 4097;      // largest pooling window (half-window staged on each side)
+constexpr int kSmemChunks = 8192;   // chunk scores kept in SMEM when n_c fits (else L2-resident workspace)
+constexpr unsigned kInvalid = 0xFFFFFFFFu;   // merge: chunk with no candidate (never a score: scores are >= 0)
+enum SelectMode : int { kModeAll = 0, kModeA = 1 };
+enum Variant : int { kPlain = 0, kCand = 1, kMerge = 2 };
+
+struct SelArgs {
+  const float* imp;          // [B][row] importance (kCand: this rank's shard)
+  int nreq;                  // B (rows of every [B][...] array)
+  int nblk;                  // kModeA: phase-A blocks per request
+  int sh_off;                // floats from the dynamic SMEM base to the SelShared scratch
+  unsigned* blk_cnt;         // [B] kModeA: phase-A CTAs done (workspace, zero, self-resetting)
+  long long row;             // row length of imp / ids / pos / tokens / out
+  const int* seq_lens;       // kPlain, optional [B]: per-request prompt length (row f3)
+  int pool_k, chunk, pos0;
+  long long ppm;             // keep rate in parts per million (K_c, Z9)
+  int* ids;
+  int* pos;
+  int* n_kept;
+  float* cs_ws;              // [B][n_c_row] chunk scores (workspace)
+  const int* tokens;         // optional gather source [B][row]
+  int* out;                  // optional gathered tokens [B][row]
+  int mode, segcap;
+  long long cpb;             // chunks per CTA in kModeA
+  // sequence sharding
+  long long i0;              // kCand: global index of this shard's first token
+  long long n_glob;          // kCand / kMerge: prompt length N (kPlain: row / seq_lens)
+  const float* edges;        // kCand: [P][B][2w] first w / last w importance values of every rank
+  int rank, world;
+  long long k_sel;           // kCand: M
+  unsigned long long* cand;  // kCand: [B][M] candidate keys out
+  const unsigned long long* cand_in;   // kMerge: [P][B][M] candidate keys
+};
+
+template <int NT>
+struct ScanSmem {
+  int warp_tot[NT / 32];
+  int total;
+};
+
+// The selection's shared scratch (besides the staged importance / chunk scores),
+// for NT threads: placed in dynamic shared memory by the caller.
+template <int NT>
+struct SelShared {
+  unsigned hist[256];
+  unsigned s_digit, s_remaining;
+  int s_last;
+  ScanSmem<NT> scan;
+  int kept_c[NT];                   // kept chunk ids of one scan tile, in order
+  int kept_off[NT];
+};
+
+// Block-wide exclusive scan of v (all NT threads participate); returns the
+// exclusive prefix, writes the block total to *total.
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, ScanSmem<NT>& sm, int* total) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm.warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int t = lane < NW ? sm.warp_tot[lane] : 0;
+    int u = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, u, o);
+      if (lane >= o) u += y;
+    }
+    if (lane < NW) sm.warp_tot[lane] = u - t;    // exclusive warp offsets
+    if (lane == 31) sm.total = u;
+  }
+  __syncthreads();
+  int res = sm.warp_tot[warp] + x - v;
+  *total = sm.total;
+  __syncthreads();                                 // sm reusable after return
+  return res;
+}
+
+// Segment length starting at chunk-aligned token `base`: whole chunks when a
+// chunk fits the segment, else the rest of the chunk up to segcap tokens.
+__device__ __forceinline__ long long seg_len(long long base, long long t_hi, int chunk, int segcap) {
+  long long next;
+  if (chunk <= segcap) {
+    next = base + (long long)(segcap / chunk) * chunk;
+  } else {
+    const long long cend = (base / chunk + 1) * chunk;
+    next = base + segcap < cend ? base + segcap : cend;
+  }
+  return (next < t_hi ? next : t_hi) - base;
+}
+
+
+// One CTA's share of the selection of request b: phase A over chunk block blk
+// (kModeA) or all three phases (kModeAll); in kModeA the request's last block
+// to finish continues with B-C.  seg: dynamic shared memory of
+// (2 segcap + 2w + (n_c if it fits)) floats; sh: the shared scratch.
+template <int V, int NT>
+__device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, float* seg, SelShared<NT>& sh) {
+  const int mode = a.mode, chunk = a.chunk, pool_k = a.pool_k;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long Nrow = a.row;
+  // N: the prompt length the pooling edges and chunk sizes refer to (global when sharded)
+  long long N;
+  if (V == kPlain) N = a.seq_lens ? std::min<long long>(std::max(a.seq_lens[b], 1), Nrow) : Nrow;
+  else N = a.n_glob;
+  const long long i0 = V == kCand ? a.i0 : 0;                    // global index of imp[b][0]
+  const long long n_loc = V == kCand ? Nrow : N;                 // tokens held in imp rows
+  const long long c_base = i0 / chunk;                           // global id of local chunk 0
+  const long long n_c_all = (N + chunk - 1) / chunk;             // chunks of the prompt
+  const long long n_c = V == kCand ? n_loc / chunk : n_c_all;    // chunks this selection ranks
+  const long long n_c_row = V == kPlain ? (Nrow + chunk - 1) / chunk : n_c;   // workspace row
+  long long K_sel;
+  if (V == kCand) K_sel = a.k_sel;
+  else K_sel = std::min(n_c_all, std::max(1LL, (a.ppm * n_c_all + 999999) / 1000000));
+  const float* imp = a.imp + (long long)b * Nrow;
+  const long long w = (pool_k - 1) / 2;
+  // chunk scores: SMEM when this CTA runs phases B-C and n_c fits, else the workspace
+  // (decided on the row's chunk count, as the launch sized the SMEM: a ragged request may have fewer)
+  const bool cs_smem = mode == kModeAll && n_c_row <= kSmemChunks;
+  float* cs = cs_smem ? seg + 2 * a.segcap + 2 * w : a.cs_ws + (long long)b * n_c_row;
+
+  if (V == kMerge) {
+    // ---- scatter the P ranks' candidates into the dense chunk array
+    unsigned* csu = reinterpret_cast<unsigned*>(cs);
+    for (long long c = tid; c < n_c; c += NT) csu[c] = kInvalid;
+    __syncthreads();
+    const long long M = a.k_sel;
+    for (int p = 0; p < a.world; ++p) {
+      const unsigned long long* src = a.cand_in + ((long long)p * a.nreq + b) * M;
+      for (long long m = tid; m < M; m += NT) {
+        const unsigned long long key = src[m];
+        const unsigned c = ~(unsigned)(key & 0xFFFFFFFFull);
+        if (c < (unsigned long long)n_c) csu[c] = (unsigned)(key >> 32);
+      }
+    }
+    __syncthreads();
+  } else {
+  // ---- A. pooled scores (centred window, shrinking edges) -> chunk sums of
+  //      chunks [c_lo, c_hi) (global ids; all of the CTA's range unless kModeA)
+  const long long c_lo = c_base + (mode == kModeA ? std::min(n_c, (long long)blk * a.cpb) : 0);
+  const long long c_hi = c_base + (mode == kModeA ? std::min(n_c, (long long)blk * a.cpb + a.cpb) : n_c);
+  const long long t_lo = c_lo * chunk, t_hi = std::min(N, c_hi * chunk);
+  const int segcap = a.segcap;
+  float* pooled = seg + segcap + 2 * w;             // [segcap]
+  const int wi = (int)w;
+  const float inv_k = 1.f / (float)pool_k;
+  const bool warp_chunks = chunk <= 32 && (chunk & (chunk - 1)) == 0;   // power of two <= 32
+  // kCand: importance of global token t in [i0 - w, i0 + n_loc + w): own shard, or a neighbour's edge
+  const float* halo_l = nullptr;
+  const float* halo_r = nullptr;
+  if (V == kCand) {
+    const long long eb = 2 * w;                       // edges row: first w, then last w values
+    if (a.rank > 0) halo_l = a.edges + ((long long)(a.rank - 1) * a.nreq + b) * eb + w;
+    if (a.rank + 1 < a.world) halo_r = a.edges + ((long long)(a.rank + 1) * a.nreq + b) * eb;
+  }
+  for (long long base = t_lo; base < t_hi;) {
+    const int len = (int)seg_len(base, t_hi, chunk, segcap);             // tokens in this segment
+    const long long lo = base - w < 0 ? 0 : base - w, hi = base + len + w > N ? N : base + len + w;
+    const int off = (int)(base - lo);                                     // seg index of token `base`
+    {
+      // all loads of the segment in flight before any store (latency-bound otherwise)
+      constexpr int PER = (SEG / NT) < 16 ? (SEG / NT) : 16;
+      const int n = (int)(hi - lo);
+      float r[PER];
+      if (V == kCand) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int i = tid + k * NT;
+          const long long t = lo + i;
+          r[k] = i >= n ? 0.f
+                        : (t < i0 ? __ldcg(halo_l + (t - (i0 - w)))
+                                  : (t >= i0 + n_loc ? __ldcg(halo_r + (t - i0 - n_loc)) : __ldcg(imp + (t - i0))));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int i = tid + k * NT;
+          r[k] = i < n ? __ldcg(imp + lo + i) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int i = tid + k * NT;
+        if (i < n) seg[i] = r[k];
+      }
+      for (int i = PER * NT + tid; i < n; i += NT) {                    // halo beyond SEG
+        const long long t = lo + i;
+        if (V == kCand)
+          seg[i] = t < i0 ? halo_l[t - (i0 - w)] : (t >= i0 + n_loc ? halo_r[t - i0 - n_loc] : imp[t - i0]);
+        else
+          seg[i] = imp[t];
+      }
+    }
+    __syncthreads();
+    // interior tokens [i_lo, i_hi) have the full window inside the sequence
+    const int i_lo = (int)(w - base > 0 ? w - base : 0);
+    const int i_hi = (int)(N - 1 - w - base + 1 < len ? N - 1 - w - base + 1 : len);
+#pragma unroll 4
+    for (int i = tid; i < len; i += NT) {                               // coalesced, conflict-free
+      float ws = 0.f;
+      if (i >= i_lo && i < i_hi) {                                      // interior: full window
+        const float* p0 = seg + off + i - wi;
+        for (int k = 0; k < pool_k; ++k) ws += p0[k];
+        pooled[i] = ws * inv_k;
+      } else {                                                            // sequence edges: shrink
+        const long long t = base + i;
+        const long long e0 = t - w < 0 ? 0 : t - w, e1 = t + w > N - 1 ? N - 1 : t + w;
+        for (long long j = e0; j <= e1; ++j) ws += seg[j - lo];
+        pooled[i] = ws / (float)(e1 - e0 + 1);
+      }
+    }
+    __syncthreads();
+    const long long c_first = base / chunk, c_last = (base + len - 1) / chunk;
+    if (warp_chunks) {
+      // a warp sums 32 consecutive pooled values in groups of `chunk` lanes (tree
+      // order); segments start on chunk boundaries and hold whole chunks
+      const int lg = __ffs(chunk) - 1;
+      const long long cb = (base >> lg) - c_base;
+#pragma unroll 4
+      for (int g0 = warp * 32; g0 < len; g0 += NT) {
+        float v = g0 + lane < len ? pooled[g0 + lane] : 0.f;
+        for (int o = chunk >> 1; o >= 1; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, chunk);
+        if ((lane & (chunk - 1)) == 0 && g0 + lane < len) cs[cb + ((g0 + lane) >> lg)] = v;
+      }
+    } else {
+      // the owner thread walks its chunk's tokens in a rotated (fixed, hence
+      // deterministic) order so a warp's reads hit distinct banks
+      for (long long c = c_first + tid; c <= c_last; c += NT) {
+        const long long t0 = c * chunk > base ? c * chunk : base;
+        const long long t1 = (c + 1) * chunk < base + len ? (c + 1) * chunk : base + len;
+        const int n = (int)(t1 - t0), ii = (int)(t0 - base);
+        float sacc = (t0 == c * chunk) ? 0.f : cs[c - c_base];          // chunk continued from the previous segment
+        const int rot = (int)(c % n);
+        for (int j = 0; j < n; ++j) {
+          int k = j + rot;
+          if (k >= n) k -= n;
+          sacc += pooled[ii + k];
+        }
+        cs[c - c_base] = sacc;
+      }
+    }
+    __syncthreads();
+    base += len;
+  }
+  for (long long c = c_lo + tid; c < c_hi; c += NT) {
+    const long long sz = ((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk;
+    cs[c - c_base] = cs[c - c_base] / (float)sz;
+  }
+  __syncthreads();
+  }
+  if (mode == kModeA) {
+    // the request's last phase-A CTA to finish runs phases B-C (one launch for
+    // the whole selection): every CTA publishes its chunk scores, then counts
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) sh.s_last = atomicAdd(a.blk_cnt + b, 1u) + 1u == a.nblk;
+    __syncthreads();
+    if (!sh.s_last) return;
+    __threadfence();
+    if (tid == 0) a.blk_cnt[b] = 0u;                                     // self-resetting for the next call
+    if (n_c_row <= kSmemChunks) {                                       // the launch sized SMEM for it
+      float* cs_s = seg + 2 * a.segcap + 2 * w;
+      for (long long c = tid; c < n_c; c += NT) cs_s[c] = __ldcg(cs + c);
+      cs = cs_s;
+    }
+    __syncthreads();
+  }
+
+  // ---- B. radix select: threshold bit pattern T of the K_sel-th largest score.
+  //      Up to kRankMax chunks the rank is counted directly instead:
+  //      rank(c) = #{c' : cs[c'] > cs[c], or cs[c'] == cs[c] and c' < c} (the
+  //      (score desc, index asc) order), kept iff rank < K_sel -- one pass, no
+  //      barrier rounds (measured: 2 us faster at 128 chunks, 29 us slower at 1024).
+  //      kMerge: invalid entries (bit pattern kInvalid, a NaN) never count.
+  constexpr int kRankMax = 256;
+  const bool by_rank = n_c <= kRankMax;
+  unsigned prefix = 0, pmask = 0;
+  unsigned remaining = (unsigned)K_sel;
+  int rank_keep = 0;
+  if (by_rank) {
+    if (tid < n_c) {
+      const float mine = cs[tid];
+      int rank = 0;
+#pragma unroll 8
+      for (int c2 = 0; c2 < (int)n_c; ++c2) {
+        const float o = cs[c2];                      // same address in every lane: broadcast
+        rank += (o > mine || (o == mine && c2 < tid)) ? 1 : 0;
+      }
+      rank_keep = rank < K_sel ? 1 : 0;
+      if (V == kMerge && __float_as_uint(mine) == kInvalid) rank_keep = 0;
+    }
+  }
+  for (int shift = 24; shift >= 0 && !by_rank; shift -= 8) {
+    if (tid < 256) sh.hist[tid] = 0;
+    __syncthreads();
+    // warp-aggregated: lanes with the same digit add once (the top digits of
+    // near-equal scores collide, and SMEM atomics on one address serialise)
+    for (long long c0 = (long long)warp * 32; c0 < n_c; c0 += NT) {
+      const long long c = c0 + lane;
+      const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
+      const bool in = c < n_c && (V != kMerge || key != kInvalid);
+      const unsigned digit = (in && (key & pmask) == prefix) ? (key >> shift) & 255u : 256u;
+      const unsigned peers = __match_any_sync(0xffffffffu, digit);
+      if (digit < 256u && lane == __ffs(peers) - 1) atomicAdd(&sh.hist[digit], (unsigned)__popc(peers));
+    }
+    __syncthreads();
+    // digit D: count(digits > D) < remaining <= count(digits >= D); warps 0-7 scan 256 bins
+    if (tid < 256) {
+      // suffix sums over bins (high digit first): bin d handled by thread 255 - d
+      const int d = 255 - tid;
+      unsigned v = sh.hist[d];
+      unsigned x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) sh.scan.warp_tot[warp] = (int)x;
+      __syncwarp();
+      // (warps 0..7 only) combine warp totals below
+      sh.kept_off[tid] = (int)x;                      // inclusive within warp
+    }
+    __syncthreads();
+    if (tid < 256) {
+      unsigned before = 0;
+      for (int ww = 0; ww < warp; ++ww) before += (unsigned)sh.scan.warp_tot[ww];
+      const unsigned incl = before + (unsigned)sh.kept_off[tid];   // count of digits >= d
+      const unsigned excl = incl - sh.hist[255 - tid];             // count of digits > d
+      if (excl < remaining && incl >= remaining) {
+        sh.s_digit = (unsigned)(255 - tid);
+        sh.s_remaining = remaining - excl;
+      }
+    }
+    __syncthreads();
+    prefix |= sh.s_digit << shift;
+    pmask |= 255u << shift;
+    remaining = sh.s_remaining;
+    __syncthreads();
+  }
+  const unsigned T = prefix;
+  const int need_eq = (int)remaining;            // chunks equal to T to keep (lowest indices first)
+
+  // ---- C. keep flags in chunk order, compaction (+ gather) of the kept token
+  //      ranges, or (kCand) the kept chunks' candidate keys
+  int carry_eq = 0, carry_tok = 0, carry_k = 0;
+  const int* tokens = a.tokens ? a.tokens + (long long)b * Nrow : nullptr;
+  int* out = a.out ? a.out + (long long)b * Nrow : nullptr;
+  int* ids = a.ids + (long long)b * Nrow;
+  int* pos = a.pos + (long long)b * Nrow;
+  for (long long base = 0; base < n_c; base += NT) {
+    const long long c = base + tid;
+    const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
+    const bool in = c < n_c && (V != kMerge || key != kInvalid);
+    const int eq = (in && key == T) ? 1 : 0;
+    const int gt = (in && key > T) ? 1 : 0;
+    int tot;
+    const int eq_rank = block_excl_scan<NT>(eq, sh.scan, &tot) + carry_eq;
+    carry_eq += tot;
+    const int keep = by_rank ? rank_keep : (gt | (eq & (eq_rank < need_eq ? 1 : 0)));
+    const int slot = block_excl_scan<NT>(keep, sh.scan, &tot);          // index among kept chunks of this tile
+    const int nk = tot;
+    if (V == kCand) {
+      if (keep)
+        a.cand[(long long)b * K_sel + carry_k + slot] =
+            ((unsigned long long)key << 32) | (unsigned long long)(~(unsigned)(c + c_base));
+      carry_k += nk;
+      continue;
+    }
+    int sz = 0;
+    if (keep) sz = (int)(((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk);
+    int tot2;
+    const int off = block_excl_scan<NT>(sz, sh.scan, &tot2) + carry_tok;
+    if (keep) {
+      sh.kept_c[slot] = (int)c;
+      sh.kept_off[slot] = off;
+    }
+    __syncthreads();
+    // one warp per kept chunk: coalesced ids / pos (/ gathered tokens)
+    for (int k = warp; k < nk; k += NT / 32) {
+      const long long cc = sh.kept_c[k];
+      const int t0 = (int)(cc * chunk);
+      const int csz = (int)(((cc + 1) * chunk < N ? (cc + 1) * chunk : N) - cc * chunk);
+      const int o = sh.kept_off[k];
+      for (int j = lane; j < csz; j += 32) {
+        ids[o + j] = t0 + j;
+        pos[o + j] = t0 + j + a.pos0;
+        if (out) out[o + j] = tokens[t0 + j];
+      }
+    }
+    carry_tok += tot2;
+    __syncthreads();
+  }
+  if (V != kCand && tid == 0) a.n_kept[b] = carry_tok;
+}
+
+}  // namespace sel
+}  // namespace sp
