@@ -8,5 +8,5 @@ from .api import (gather, kept_chunks, make_geom, score, score_e4m3, score_e4m3_
                   check_device_error, run_host, run_workspace_bytes, score_plan, workspace,
                   score_stats, stats_combine, score_finish, score_acc, acc_importance,
                   score_peer, score_peer_buffer_bytes, score_peer_plan, score_peer_workspace_bytes,
-                  seq_candidate_count, seq_edges, seq_candidates, seq_merge)
+                  seq_candidate_count, seq_edges, seq_candidates, seq_merge, score_select)
 from ._lib import LIB_PATH, SIGNATURES, SpError, lib  # noqa: F401

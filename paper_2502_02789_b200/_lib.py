@@ -110,6 +110,8 @@ SIGNATURES = {
     "sp_seq_edges": (C.c_int, [_P, C.c_int32, C.c_int64, C.c_int32, _S, _P, _P]),
     "sp_seq_candidates": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int64, _S, _P, _P, C.c_size_t, _P]),
     "sp_seq_merge": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int64, _S, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
+    "sp_score_select_workspace_bytes": (C.c_size_t, [_G, _S]),
+    "sp_score_select": (C.c_int, [_P, _P, _G, _L, _S, _P, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "sp_run_workspace_bytes": (C.c_size_t, [_G, _S]),
     "sp_run_host": (C.c_int, [C.POINTER(sp_host_io), C.POINTER(sp_device_bufs), _G, _L, _S, _P]),
 }

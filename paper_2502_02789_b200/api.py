@@ -341,6 +341,37 @@ def seq_merge(cand_all: torch.Tensor, world: int, N: int, keep: float, pool_k: i
     return (ids, pos, n_kept) if tokens is None else (ids, pos, n_kept, out)
 
 
+def score_select(Q, K, keep: float, pool_k: int, chunk: int, pos0: int = 0, tokens=None, R_valid=None, scale=None,
+                 out=None, stream=None):
+    """sp_score + sp_select_gather in one call (one launch for a single request
+    on the fused kernel: the selection runs as the score kernel's tail).
+    Returns (importance, ids, pos, n_kept[, gathered tokens]); ``out`` may hold
+    preallocated tensors with those keys."""
+    g, lay = make_geom(Q, K, R_valid, scale)
+    p = _lib.sp_select_params(keep_rate=float(keep), pool_k=int(pool_k), chunk=int(chunk), pos0=int(pos0))
+    dev = K.device
+    o = dict(out or {})
+    imp = o.get("importance") if o.get("importance") is not None else torch.empty((g.B, g.N), dtype=torch.float32,
+                                                                                  device=dev)
+    ids = o.get("ids") if o.get("ids") is not None else torch.empty((g.B, g.N), dtype=torch.int32, device=dev)
+    pos = o.get("pos") if o.get("pos") is not None else torch.empty((g.B, g.N), dtype=torch.int32, device=dev)
+    nk = o.get("n_kept") if o.get("n_kept") is not None else torch.empty((g.B,), dtype=torch.int32, device=dev)
+    outt = None
+    if tokens is not None:
+        if tokens.dtype != torch.int32 or not tokens.is_contiguous() or tuple(tokens.shape) != (g.B, g.N):
+            raise ValueError("tokens must be contiguous int32 [B][N]")
+        outt = o.get("out_tokens") if o.get("out_tokens") is not None else torch.empty_like(tokens)
+    nbytes = lib().sp_score_select_workspace_bytes(C.byref(g), C.byref(p))
+    if nbytes == 0:
+        check(_lib.SP_EINVAL, "sp_score_select")
+    ws = workspace(("score_select", _geom_key(g), int(chunk), int(pool_k), float(keep)), nbytes, dev, stream)
+    check(lib().sp_score_select(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), C.byref(p),
+                                None if tokens is None else tokens.data_ptr(), imp.data_ptr(), ids.data_ptr(),
+                                pos.data_ptr(), nk.data_ptr(), None if outt is None else outt.data_ptr(),
+                                ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_score_select")
+    return (imp, ids, pos, nk) if tokens is None else (imp, ids, pos, nk, outt)
+
+
 def gather(tokens: torch.Tensor, ids: torch.Tensor, n_kept: torch.Tensor, out=None, stream=None) -> torch.Tensor:
     """out[b][j] = tokens[b][ids[b][j]] for j < n_kept[b] (bit-exact)."""
     if tokens.dtype != torch.int32 or not tokens.is_contiguous():

@@ -2,6 +2,7 @@
 //
 // Host-side argument validation, workspace carving and kernel dispatch.  No
 // exception crosses this boundary; every entry point returns an sp_status.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -617,6 +618,44 @@ sp_status sp_gather(const int32_t* tokens, const int32_t* ids, const int32_t* n_
   sp_status s = check_device();
   if (s != SP_OK) return s;
   return from_cuda(gather_launch(tokens, ids, n_kept, B, N, out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+size_t sp_score_select_workspace_bytes(const sp_geom* g, const sp_select_params* p) {
+  if (check_geom(g) != SP_OK || check_select(g->B, g->N, p) != SP_OK) return 0;
+  const Geom G = to_geom(*g);
+  const size_t two = align256(score_ws(G, SP_SCORE_AUTO)) + select_ws_bytes(g->B, g->N, p->chunk);
+  const size_t fused = G.B == 1 && fused_supported(G, Layout{}, nullptr, nullptr) ? fused_select_ws_bytes(G, p->chunk) : 0;
+  return std::max(two, fused);
+}
+
+sp_status sp_score_select(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay,
+                          const sp_select_params* p, const int32_t* tokens, float* importance, int32_t* ids,
+                          int32_t* pos, int32_t* n_kept, int32_t* out_tokens, void* ws, size_t ws_bytes,
+                          sp_stream stream) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if ((s = check_layout(g, lay, Q, K)) != SP_OK) return s;
+  if ((s = check_select(g->B, g->N, p)) != SP_OK) return s;
+  if (importance == nullptr || ids == nullptr || pos == nullptr || n_kept == nullptr) return SP_EINVAL;
+  if ((tokens == nullptr) != (out_tokens == nullptr)) return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
+  if (ws == nullptr || ws_bytes < sp_score_select_workspace_bytes(g, p) || (reinterpret_cast<uintptr_t>(ws) & 255u) != 0)
+    return SP_EWORKSPACE;
+  const Geom G = to_geom(*g);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (G.B == 1 && fused_supported(G, to_layout(*lay), Q, K)) {
+    const cudaError_t e = fused_score_select(reinterpret_cast<const __nv_bfloat16*>(Q),
+                                             reinterpret_cast<const __nv_bfloat16*>(K), G, to_layout(*lay), p->pool_k,
+                                             p->chunk, p->pos0, keep_ppm(p->keep_rate), tokens, importance, ids, pos,
+                                             n_kept, out_tokens, ws, ws_bytes, st);
+    if (e != cudaErrorNotSupported) return from_cuda(e);
+    cudaGetLastError();
+  }
+  // two launches: the score, then the selection (+ gather)
+  const size_t sb = align256(score_ws(G, SP_SCORE_AUTO));
+  if ((s = sp_score(Q, K, g, lay, importance, ws, sb, stream)) != SP_OK) return s;
+  return sp_select_gather(importance, tokens, g->B, g->N, p, ids, pos, n_kept, out_tokens,
+                          reinterpret_cast<char*>(ws) + sb, ws_bytes - sb, stream);
 }
 
 size_t sp_run_workspace_bytes(const sp_geom* g, const sp_select_params* p) {
