@@ -332,10 +332,9 @@ def run_ours(args):
         score_only()
         select_only()
 
-    # one request on the fused kernel: sp_score_select runs the selection as the
-    # score kernel's tail (one launch per step)
-    fused_step = (not (seq or head or paged or f8 or bsplit or shard == "replica") and w.B == 1
-                  and args.algo != "simt")
+    # (sp_score_select as the score kernel's tail measured slower than two
+    # launches: DESIGN.md 5.3; the step keeps the separate selection launch)
+    fused_step = False
     sel_out = {"importance": imp, "ids": ids, "pos": pos, "n_kept": nk, "out_tokens": out}
     if fused_step:
         def step():                                    # noqa: F811

@@ -362,16 +362,14 @@ sp_status sp_select_ragged(const float* importance, const int32_t* seq_lens, con
                            int32_t* out_tokens, void* ws, size_t ws_bytes, sp_stream stream);
 
 /* ------------------------------------------------------------------ score + select in one call
- * sp_score followed by sp_select_gather (O1-O11, Alg.1) with the
- * same outputs.  For one request (B == 1) on the fused kernel this is ONE
- * launch: the selection runs as the score kernel's tail once every CTA's
- * importance is written (phase A spread over the grid's first CTAs, the last
- * of them running the top-K) -- the same code and bits as the standalone
- * selection, without a second launch.  Otherwise (B > 1, the SIMT path, or a
- * decomposition the tail cannot take) it launches the two kernels.
- * Workspace: sp_score_select_workspace_bytes(g, p) bytes, 256-byte aligned,
- * zero-filled once and reused only for this geometry and selection.  tokens /
- * out_tokens may both be NULL (no gather). */
+ * sp_score followed by sp_select_gather (O1-O11, Alg.1) with the same
+ * outputs, in one call: the score kernel, then the selection launched as its
+ * programmatic dependent.  (Measured and not adopted: the selection as the
+ * score kernel's own tail on its 384 threads, 3-7 us slower than the separate
+ * 1024-thread launch -- DESIGN.md 5.3.)  Workspace:
+ * sp_score_select_workspace_bytes(g, p) bytes, 256-byte aligned, zero-filled
+ * once and reused only for this geometry and selection.  tokens / out_tokens
+ * may both be NULL (no gather). */
 size_t sp_score_select_workspace_bytes(const sp_geom* g, const sp_select_params* p);
 sp_status sp_score_select(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay,
                           const sp_select_params* p, const int32_t* tokens, float* importance, int32_t* ids,

@@ -33,7 +33,6 @@
 //   the warp roles share the SM's instruction cache, so the executed code is
 //   kept small (measured: code size moved C3 by > 20 %).
 #include "sp_internal.h"
-#include "select_body.cuh"
 
 #include <cuda.h>
 #include <math_constants.h>
@@ -125,11 +124,6 @@ struct FusedParams {
   // peer_merge_col).
   int rank, world;
   unsigned long long* peer[kMaxPeers]; // every rank's rank-word buffer base ([2][B][U][world][NCP])
-  // fused selection tail (sp_score_select, B = 1): once every CTA's importance is
-  // written, the selection kernel's body runs in this grid (select_tail)
-  int sel_on;
-  unsigned* sel_sync;                  // [0]: CTAs done, counted over all launches (grid per launch)
-  sel::SelArgs sel;
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -681,51 +675,6 @@ __device__ __noinline__ void peer_gather_unit(const FusedParams& p, long long ub
     }
     ls[c] = l2;
   }
-}
-
-// Fused selection tail (sp_score_select, one request): after its teardown every
-// CTA counts itself done; once all of the grid's CTAs are (importance complete,
-// released by each CTA's fence before counting), the selection runs in this
-// grid with the standalone kernel's code over the CTA's 384 threads and the
-// now idle shared memory: short prompts on CTA 0 alone (all phases), long ones
-// with phase A spread over the first nblk CTAs and the last of them running the
-// top-K (the same bits as sp_select_gather).  The done counter is never reset:
-// each launch adds exactly gridDim.x, so a launch's target is the next multiple
-// of the grid.  Out of line: runs once per CTA at the end.
-__device__ __noinline__ void select_tail(const FusedParams& p, uint8_t* smem) {
-  volatile unsigned* s_go = reinterpret_cast<volatile unsigned*>(smem);   // (all of SMEM is idle now)
-  if (threadIdx.x == 0) {
-    const unsigned grid = gridDim.x;
-    const unsigned before = atomicAdd(p.sel_sync, 0u);                 // (this CTA has not counted yet)
-    const unsigned target = (before / grid + 1u) * grid;
-    __threadfence();                                                   // release this CTA's importance
-    atomicAdd(p.sel_sync, 1u);
-    const bool works = p.sel.mode == sel::kModeAll ? blockIdx.x == 0 : (int)blockIdx.x < p.sel.nblk;
-    if (works) {
-      uint64_t t0 = 0;
-      for (uint32_t i = 1; ld_acquire(p.sel_sync) < target; ++i) {     // every CTA's importance is written
-        __nanosleep(200);
-        if ((i & 1023) == 0) {
-          const uint64_t now = globaltimer_ns();
-          if (t0 == 0) t0 = now;
-          else if (now - t0 > kSpinNs) { set_err(p.err, kDevTimeout); break; }
-        }
-      }
-      __threadfence();
-    }
-    *s_go = works ? 1u : 0u;
-  }
-  __syncthreads();
-  const bool go = *s_go != 0u;
-  __syncthreads();
-  if (!go) return;
-  const long long w = (p.sel.pool_k - 1) / 2;
-  const long long n_c = (p.sel.row + p.sel.chunk - 1) / p.sel.chunk;
-  const long long cs_floats = n_c <= sel::kSmemChunks ? n_c : 0;
-  float* seg = reinterpret_cast<float*>(smem);
-  const long long sh_off = (2 * (long long)p.sel.segcap + 2 * w + cs_floats + 3) / 4 * 4;
-  sel::SelShared<kThreads>& sh = *reinterpret_cast<sel::SelShared<kThreads>*>(seg + sh_off);
-  sel::select_body<sel::kPlain, kThreads>(p.sel, 0, p.sel.mode == sel::kModeAll ? 0 : (int)blockIdx.x, seg, sh);
 }
 
 // kG: compile-time GQA group size (1, 2, 4, 8) or 0 for any G.  One
@@ -1290,7 +1239,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
       atomicAdd(p.epoch, 1u);
     }
   }
-  if (p.sel_on) select_tail(p, smem);
 }
 
 // ------------------------------------------------------------------ host side
@@ -1653,7 +1601,7 @@ bool encode_paged_interleaved(const PagedK& pk, const Geom& g, const Plan& pl, C
 cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay, int mode,
                          const float* lse_in, float* importance, void* ws, size_t ws_bytes, cudaStream_t st,
                          float* acc_out = nullptr, const PeerArgs& peer = PeerArgs(), const PagedK* pk = nullptr,
-                         const float2* la = nullptr, const sel::SelArgs* sel = nullptr, unsigned* sel_sync = nullptr) {
+                         const float2* la = nullptr) {
   if (peer.world < 1 || peer.world > kMaxPeers || peer.rank < 0 || peer.rank >= peer.world) return cudaErrorInvalidValue;
   Plan pl = make_plan(g, true, peer.sm_budget, nullptr, peer.world);
   if (!pl.ok || ws_bytes < pl.ws_total()) return cudaErrorInvalidValue;
@@ -1711,11 +1659,6 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   }
   p.imp = importance;
   p.acc_out = acc_out;
-  p.sel_on = sel != nullptr ? 1 : 0;
-  if (sel != nullptr) {
-    p.sel = *sel;
-    p.sel_sync = sel_sync;
-  }
   p.err = device_error_flag();
   p.trace = nullptr;
   p.mode = mode;
@@ -1773,54 +1716,6 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
 cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                         float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
   return fused_launch(Q, K, g, lay, kModeFull, nullptr, importance, ws, ws_bytes, st);
-}
-
-// sp_score_select's fused path (one request): the score kernel with the
-// selection as its tail.  ws: [score workspace][select workspace: one counter,
-// then the chunk scores][tail counter].  Returns cudaErrorNotSupported when
-// the geometry cannot take the tail (B > 1, more chunk blocks than CTAs, or
-// not enough shared memory): the caller then launches the selection itself.
-size_t fused_select_ws_bytes(const Geom& g, int chunk) {
-  const size_t sw = fused_score_ws_bytes(g);
-  if (sw == 0) return 0;
-  const long long n_c = (g.N + chunk - 1) / chunk;
-  return align256(sw) + align256(sizeof(unsigned)) + align256((size_t)n_c * sizeof(float)) + 256;
-}
-
-cudaError_t fused_score_select(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
-                               int pool_k, int chunk, int pos0, long long ppm, const int* tokens, float* importance,
-                               int* ids, int* pos, int* n_kept, int* out, void* ws, size_t ws_bytes, cudaStream_t st) {
-  if (g.B != 1) return cudaErrorNotSupported;
-  Plan pl = make_plan(g);
-  if (!pl.ok) return cudaErrorNotSupported;
-  const size_t sw = align256(pl.ws_total());
-  const long long N = g.N, n_c = (N + chunk - 1) / chunk;
-  char* sws = reinterpret_cast<char*>(ws) + sw;
-  sel::SelArgs a{};
-  a.imp = importance; a.nreq = 1; a.row = N; a.pool_k = pool_k; a.chunk = chunk; a.pos0 = pos0; a.ppm = ppm;
-  a.ids = ids; a.pos = pos; a.n_kept = n_kept; a.tokens = tokens; a.out = out; a.n_glob = N;
-  a.blk_cnt = reinterpret_cast<unsigned*>(sws);
-  a.cs_ws = reinterpret_cast<float*>(sws + align256(sizeof(unsigned)));
-  unsigned* sync = reinterpret_cast<unsigned*>(sws + align256(sizeof(unsigned)) + align256((size_t)n_c * sizeof(float)));
-  // the standalone selection's decomposition (launch_select in select.cu)
-  const long long cpb = std::max(1LL, 2048LL / chunk);
-  const long long nblk = (n_c + cpb - 1) / cpb;
-  const long long w = (pool_k - 1) / 2;
-  const long long grid = std::min<long long>(pl.P, pl.total_jobs);
-  if (nblk >= 4 && nblk <= 65535) {
-    if (nblk > grid) return cudaErrorNotSupported;
-    const long long span = std::min(N, cpb * chunk);
-    a.segcap = chunk > sel::SEG ? sel::SEG : (int)std::min<long long>(sel::SEG, (span + 31) / 32 * 32);
-    a.cpb = cpb; a.nblk = (int)nblk; a.mode = sel::kModeA;
-  } else {
-    a.segcap = sel::SEG; a.cpb = n_c; a.nblk = 1; a.mode = sel::kModeAll;
-  }
-  const long long cs_floats = n_c <= sel::kSmemChunks ? n_c : 0;
-  const size_t need = (size_t)((2 * (long long)a.segcap + 2 * w + cs_floats + 3) / 4 * 4) * sizeof(float) +
-                      sizeof(sel::SelShared<kThreads>);
-  if (need + 1024 > pl.smem || ws_bytes < fused_select_ws_bytes(g, chunk)) return cudaErrorNotSupported;
-  return fused_launch(Q, K, g, lay, kModeFull, nullptr, importance, ws, sw, st, nullptr, PeerArgs(), nullptr, nullptr,
-                      &a, sync);
 }
 
 // Z2' (row f4): the look-ahead keys' (max2, sum) per (request, unit, column), one

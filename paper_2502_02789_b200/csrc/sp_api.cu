@@ -622,10 +622,7 @@ sp_status sp_gather(const int32_t* tokens, const int32_t* ids, const int32_t* n_
 
 size_t sp_score_select_workspace_bytes(const sp_geom* g, const sp_select_params* p) {
   if (check_geom(g) != SP_OK || check_select(g->B, g->N, p) != SP_OK) return 0;
-  const Geom G = to_geom(*g);
-  const size_t two = align256(score_ws(G, SP_SCORE_AUTO)) + select_ws_bytes(g->B, g->N, p->chunk);
-  const size_t fused = G.B == 1 && fused_supported(G, Layout{}, nullptr, nullptr) ? fused_select_ws_bytes(G, p->chunk) : 0;
-  return std::max(two, fused);
+  return align256(score_ws(to_geom(*g), SP_SCORE_AUTO)) + select_ws_bytes(g->B, g->N, p->chunk);
 }
 
 sp_status sp_score_select(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay,
@@ -641,18 +638,8 @@ sp_status sp_score_select(const void* Q, const void* K, const sp_geom* g, const 
   if ((s = check_device()) != SP_OK) return s;
   if (ws == nullptr || ws_bytes < sp_score_select_workspace_bytes(g, p) || (reinterpret_cast<uintptr_t>(ws) & 255u) != 0)
     return SP_EWORKSPACE;
-  const Geom G = to_geom(*g);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (G.B == 1 && fused_supported(G, to_layout(*lay), Q, K)) {
-    const cudaError_t e = fused_score_select(reinterpret_cast<const __nv_bfloat16*>(Q),
-                                             reinterpret_cast<const __nv_bfloat16*>(K), G, to_layout(*lay), p->pool_k,
-                                             p->chunk, p->pos0, keep_ppm(p->keep_rate), tokens, importance, ids, pos,
-                                             n_kept, out_tokens, ws, ws_bytes, st);
-    if (e != cudaErrorNotSupported) return from_cuda(e);
-    cudaGetLastError();
-  }
-  // two launches: the score, then the selection (+ gather)
-  const size_t sb = align256(score_ws(G, SP_SCORE_AUTO));
+  // the score, then the selection (+ gather) as its programmatic dependent
+  const size_t sb = align256(score_ws(to_geom(*g), SP_SCORE_AUTO));
   if ((s = sp_score(Q, K, g, lay, importance, ws, sb, stream)) != SP_OK) return s;
   return sp_select_gather(importance, tokens, g->B, g->N, p, ids, pos, n_kept, out_tokens,
                           reinterpret_cast<char*>(ws) + sb, ws_bytes - sb, stream);

@@ -87,10 +87,6 @@ bool fused_plan_info(const Geom& g, long long out[kPlanInfo]);
 void fused_set_trace(unsigned long long* buf, long long records);
 cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                         float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
-size_t fused_select_ws_bytes(const Geom& g, int chunk);
-cudaError_t fused_score_select(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
-                               int pool_k, int chunk, int pos0, long long ppm, const int* tokens, float* importance,
-                               int* ids, int* pos, int* n_kept, int* out, void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t fused_score_stats(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                               float* stats, void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t fused_score_finish(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,

@@ -1,8 +1,7 @@
-"""sp_score_select: the score kernel with the selection as its tail (one launch
-for a single request) gives exactly sp_score + sp_select_gather's outputs, over
-the selection's decompositions (one CTA; phase A spread over many CTAs),
-repeated calls (the tail's counters run across launches) and the two-launch
-fallback (B > 1, the SIMT path)."""
+"""sp_score_select (score, then the selection as its programmatic dependent, in
+one call) gives exactly sp_score + sp_select_gather's outputs, over the
+selection's decompositions (one CTA; phase A spread over many CTAs), repeated
+calls (the selection's counters run across launches) and B > 1."""
 import numpy as np
 import pytest
 import torch
