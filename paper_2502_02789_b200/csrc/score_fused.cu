@@ -63,10 +63,14 @@ constexpr int kTileM = 128;
 constexpr int kStatsWarp0 = 4;
 constexpr int kFinalWarp0 = 8;
 constexpr int kMaxStages = 8;
-// Stage cap of the plans (measured, r2 tools/gpu_r2_stages.sh): more TMA tiles in
-// flight than 4 slow the bf16 kernel down (C3 37x4: 4 stages 0.3405 ms, 5: 0.3442;
-// C1 8x16: 0.0720 vs 0.0745); the e4m3 kernel is indifferent (3..8 stages within 0.5 %).
+// Stage cap of the plans (measured, r2 tools/gpu_r2_stages.sh, gpu_r2_pst.sh): more
+// TMA tiles in flight than 4 slow the bf16 kernel down (C3 37x4: 4 stages 0.3405 ms,
+// 5: 0.3442; C1 8x16: 0.0720 vs 0.0745); some geometries prefer 3 (a 16K prompt:
+// 0.1916 vs 0.1964 ms; the C4/8 peer shard 0.2122 vs 0.2190), others 4 (C2: 0.641
+// vs 0.672 ms), so the tuner tries both; peer plans (no tuner) take 3.  The e4m3
+// kernel is indifferent (3..8 stages within 0.5 %).
 constexpr int kStageCap = 4;
+constexpr int kStageCapPeer = 3;
 constexpr int kMaxChunks = 8;          // NCP <= 128 columns (16-column chunks)
 constexpr int kMaxSlots = 16;          // TMEM tile slots (512 columns / 32)
 constexpr int kLseRing = 8;            // lse2 buffers in SMEM (gather may run ahead of aggregation)
@@ -1307,7 +1311,7 @@ uint32_t carve(Plan& pl, int Rv, int stages) {
 // Measured plan choices (sp_score_tune / sp_score_set_plan), per geometry:
 // (n_tg, n_ug, hier).
 using PlanKey = std::tuple<int, int, int, int, int, int, int, long long, int, int>;
-using PlanChoice = std::tuple<int, int, int>;
+using PlanChoice = std::tuple<int, int, int, int>;   // (n_tg, n_ug, hier, stage cap or 0)
 std::map<PlanKey, PlanChoice>& plan_registry() {
   static std::map<PlanKey, PlanChoice> m;
   return m;
@@ -1348,7 +1352,7 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   pl.nslots = std::min(kMaxSlots, kTmemCols / pl.NCP);
   double best = 1e300;
   // test/tuning override: SP_FUSED_PLAN="n_tg,n_ug[,hier]" (ignored unless valid for g)
-  int force_tg = 0, force_ug = 0, force_h = -1;
+  int force_tg = 0, force_ug = 0, force_h = -1, reg_cap = 0;
   if (const char* env = allow_override ? std::getenv("SP_FUSED_PLAN") : nullptr) {
     const int n = std::sscanf(env, "%d,%d,%d", &force_tg, &force_ug, &force_h);
     if (n < 2) force_tg = force_ug = 0;
@@ -1357,7 +1361,7 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   if (allow_override && force_tg == 0 && world == 1) {   // a measured choice for this geometry
     std::lock_guard<std::mutex> lk(plan_registry_mu());
     auto it = plan_registry().find(plan_key(g, sm_budget));
-    if (it != plan_registry().end()) std::tie(force_tg, force_ug, force_h) = it->second;
+    if (it != plan_registry().end()) std::tie(force_tg, force_ug, force_h, reg_cap) = it->second;
   }
   pl.world = world;
   for (int J = 1; J <= pl.P; ++J) {
@@ -1409,7 +1413,7 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   // 4 query slots (Q loads issued 3 units ahead) unless that costs a K stage on long units
   auto max_stages = [&](int nq) {
     pl.nq = nq;
-    int s = kStageCap;
+    int s = reg_cap > 0 ? reg_cap : (world > 1 ? kStageCapPeer : kStageCap);
     while (s >= 2 && carve(pl, g.Rv, s) > (uint32_t)kSmemLimit) --s;
     return s;
   };
@@ -1801,7 +1805,7 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
   std::sort(cands.begin(), cands.end());
   const double best_cost = std::get<0>(cands.front());
   float best_ms = 1e30f;
-  int best_tg = base.n_tg, best_ug = base.n_ug, best_h = base.hier;
+  int best_tg = base.n_tg, best_ug = base.n_ug, best_h = base.hier, best_cap = 0;
   cudaEvent_t e0, e1;
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return cudaGetLastError();
   float* imp = nullptr;
@@ -1809,31 +1813,35 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
   for (size_t i = 0; err == cudaSuccess && i < cands.size() && i < (size_t)kTuneMax; ++i) {
     if (std::get<0>(cands[i]) > kTuneSpan * best_cost) break;
     const int tg = std::get<1>(cands[i]), ug = std::get<2>(cands[i]), h = std::get<3>(cands[i]);
-    {
-      std::lock_guard<std::mutex> lk(plan_registry_mu());
-      plan_registry()[plan_key(g, 0)] = PlanChoice(tg, ug, h);
+    int prev_stages = -1;
+    for (int cap : {kStageCap, kStageCap - 1}) {                 // (measured: 3 or 4 TMA stages win)
+      {
+        std::lock_guard<std::mutex> lk(plan_registry_mu());
+        plan_registry()[plan_key(g, 0)] = PlanChoice(tg, ug, h, cap);
+      }
+      Plan pl = make_plan(g);
+      if (!pl.ok || pl.n_tg != tg || pl.n_ug != ug || pl.hier != h || pl.stages == prev_stages) continue;
+      prev_stages = pl.stages;
+      void* ws = nullptr;
+      if ((err = cudaMalloc(&ws, pl.ws_total())) != cudaSuccess) break;
+      cudaMemsetAsync(ws, 0, pl.ws_total(), st);
+      for (int w = 0; w < 2 && err == cudaSuccess; ++w) err = fused_score(Q, K, g, lay, imp, ws, pl.ws_total(), st);
+      cudaEventRecord(e0, st);
+      for (int r = 0; r < 5 && err == cudaSuccess; ++r) err = fused_score(Q, K, g, lay, imp, ws, pl.ws_total(), st);
+      cudaEventRecord(e1, st);
+      if (err == cudaSuccess) err = cudaEventSynchronize(e1);
+      float ms = 0.f;
+      if (err == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
+      cudaFree(ws);
+      if (err == cudaSuccess && ms < best_ms) { best_ms = ms; best_tg = tg; best_ug = ug; best_h = h; best_cap = cap; }
     }
-    Plan pl = make_plan(g);
-    if (!pl.ok || pl.n_tg != tg || pl.n_ug != ug || pl.hier != h) continue;
-    void* ws = nullptr;
-    if ((err = cudaMalloc(&ws, pl.ws_total())) != cudaSuccess) break;
-    cudaMemsetAsync(ws, 0, pl.ws_total(), st);
-    for (int w = 0; w < 2 && err == cudaSuccess; ++w) err = fused_score(Q, K, g, lay, imp, ws, pl.ws_total(), st);
-    cudaEventRecord(e0, st);
-    for (int r = 0; r < 5 && err == cudaSuccess; ++r) err = fused_score(Q, K, g, lay, imp, ws, pl.ws_total(), st);
-    cudaEventRecord(e1, st);
-    if (err == cudaSuccess) err = cudaEventSynchronize(e1);
-    float ms = 0.f;
-    if (err == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
-    cudaFree(ws);
-    if (err == cudaSuccess && ms < best_ms) { best_ms = ms; best_tg = tg; best_ug = ug; best_h = h; }
   }
   cudaFree(imp);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   {
     std::lock_guard<std::mutex> lk(plan_registry_mu());
-    plan_registry()[plan_key(g, 0)] = PlanChoice(best_tg, best_ug, best_h);
+    plan_registry()[plan_key(g, 0)] = PlanChoice(best_tg, best_ug, best_h, best_cap);
   }
   *tg_out = best_tg;
   *ug_out = best_ug;
@@ -1845,7 +1853,7 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
 bool fused_set_plan(const Geom& g, int n_tg, int n_ug, int hier) {
   std::lock_guard<std::mutex> lk(plan_registry_mu());
   if (n_tg <= 0) { plan_registry().erase(plan_key(g, 0)); return true; }
-  plan_registry()[plan_key(g, 0)] = PlanChoice(n_tg, n_ug, hier);
+  plan_registry()[plan_key(g, 0)] = PlanChoice(n_tg, n_ug, hier, 0);
   return true;
 }
 
