@@ -128,6 +128,7 @@ struct FusedParams {
   // peer_merge_col).
   int rank, world;
   unsigned long long* peer[kMaxPeers]; // every rank's rank-word buffer base ([2][B][U][world][NCP])
+  int l2hint;                          // K tiles loaded with an L2 evict_first hint (plan; A/B: SP_FUSED_L2HINT)
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -206,6 +207,16 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
       "@e cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];\n\t}" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+// With an L2 cache-policy hint (createpolicy, e.g. evict_first for the K stream).
+__device__ __forceinline__ void tma_load_5d_hint(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                                 int c2, int c3, int c4, uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;\n\t}" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "l"(policy)
       : "memory");
 }
 // Per-lane variant (no election): every calling lane issues its own box.
@@ -767,6 +778,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
     {
       uint32_t stage = 0, sphase = 0, ui = 0;
       unsigned long long w_empty = 0, w_q = 0;
+      uint64_t l2pol = 0;
+      if (p.l2hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(l2pol));
       for (long long job = blockIdx.x; job < p.total_jobs; job += gridDim.x) {
         const Job jb = decode_job(p, job);
         for (int u = jb.u_lo; u < jb.u_hi; ++u, ++ui) {
@@ -783,10 +796,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             mbar_wait_acc(p, bar_empty + 8 * stage, sphase ^ 1, w_empty);
             mbar_expect_tx(bar_full + 8 * stage, p.k_stage_bytes);
             const uint32_t kdst = smem_u32(smem + p.off_k + stage * p.k_stage_bytes);
-            #pragma unroll 1
-            for (int kb = 0; kb < p.nkb; ++kb)
-              tma_load_5d(kdst + kb * (kTileM * p.swb), &p.tmK, bar_full + 8 * stage, kb * p.W, t * kTileM, g, l,
-                          jb.b);
+            if (p.l2hint) {
+              #pragma unroll 1
+              for (int kb = 0; kb < p.nkb; ++kb)
+                tma_load_5d_hint(kdst + kb * (kTileM * p.swb), &p.tmK, bar_full + 8 * stage, kb * p.W, t * kTileM, g,
+                                 l, jb.b, l2pol);
+            } else {
+              #pragma unroll 1
+              for (int kb = 0; kb < p.nkb; ++kb)
+                tma_load_5d(kdst + kb * (kTileM * p.swb), &p.tmK, bar_full + 8 * stage, kb * p.W, t * kTileM, g, l,
+                            jb.b);
+            }
             if (++stage == (uint32_t)p.stages) { stage = 0; sphase ^= 1; }
           }
         }
@@ -1272,6 +1292,7 @@ struct Plan {
   uint32_t k_stage_bytes = 0, q_slot_bytes = 0;
   int nq = 2;
   int hier = 0, world = 1;                            // peer exchange (world > 1); ranks
+  int l2hint = 1;                                     // K tiles loaded with an L2 evict_first hint
   size_t ws_part = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0, ws_rank = 0;
   size_t ws_total() const { return ws_part + ws_cnt + ws_acc + ws_fin + ws_rank; }
   bool ok = false;
@@ -1311,7 +1332,7 @@ uint32_t carve(Plan& pl, int Rv, int stages) {
 // Measured plan choices (sp_score_tune / sp_score_set_plan), per geometry:
 // (n_tg, n_ug, hier).
 using PlanKey = std::tuple<int, int, int, int, int, int, int, long long, int, int>;
-using PlanChoice = std::tuple<int, int, int, int>;   // (n_tg, n_ug, hier, stage cap or 0)
+using PlanChoice = std::tuple<int, int, int, int, int>;   // (n_tg, n_ug, hier, stage cap or 0, L2 hint or -1)
 std::map<PlanKey, PlanChoice>& plan_registry() {
   static std::map<PlanKey, PlanChoice> m;
   return m;
@@ -1352,7 +1373,7 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   pl.nslots = std::min(kMaxSlots, kTmemCols / pl.NCP);
   double best = 1e300;
   // test/tuning override: SP_FUSED_PLAN="n_tg,n_ug[,hier]" (ignored unless valid for g)
-  int force_tg = 0, force_ug = 0, force_h = -1, reg_cap = 0;
+  int force_tg = 0, force_ug = 0, force_h = -1, reg_cap = 0, reg_hint = -1;
   if (const char* env = allow_override ? std::getenv("SP_FUSED_PLAN") : nullptr) {
     const int n = std::sscanf(env, "%d,%d,%d", &force_tg, &force_ug, &force_h);
     if (n < 2) force_tg = force_ug = 0;
@@ -1361,7 +1382,7 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   if (allow_override && force_tg == 0 && world == 1) {   // a measured choice for this geometry
     std::lock_guard<std::mutex> lk(plan_registry_mu());
     auto it = plan_registry().find(plan_key(g, sm_budget));
-    if (it != plan_registry().end()) std::tie(force_tg, force_ug, force_h, reg_cap) = it->second;
+    if (it != plan_registry().end()) std::tie(force_tg, force_ug, force_h, reg_cap, reg_hint) = it->second;
   }
   pl.world = world;
   for (int J = 1; J <= pl.P; ++J) {
@@ -1430,6 +1451,8 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   if (stages < 2) return pl;
   pl.stages = stages;
   pl.smem = carve(pl, g.Rv, stages);
+  pl.l2hint = reg_hint >= 0 ? reg_hint : 1;
+  if (const char* e = allow_override ? std::getenv("SP_FUSED_L2HINT") : nullptr) pl.l2hint = std::atoi(e) != 0;
   pl.ws_part = align256(2 * (size_t)g.B * pl.U * pl.NCP * pl.n_tg * sizeof(unsigned long long));
   pl.ws_cnt = 256;                                   // launch epoch + CTAs-done counter
   pl.ws_acc = pl.n_ug > 1 ? align256((size_t)g.B * pl.n_ug * g.Rv * g.N * sizeof(float)) : 0;
@@ -1663,6 +1686,7 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   }
   p.imp = importance;
   p.acc_out = acc_out;
+  p.l2hint = pl.l2hint;
   p.err = device_error_flag();
   p.trace = nullptr;
   p.mode = mode;
@@ -1805,7 +1829,7 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
   std::sort(cands.begin(), cands.end());
   const double best_cost = std::get<0>(cands.front());
   float best_ms = 1e30f;
-  int best_tg = base.n_tg, best_ug = base.n_ug, best_h = base.hier, best_cap = 0;
+  int best_tg = base.n_tg, best_ug = base.n_ug, best_h = base.hier, best_cap = 0, best_hint = -1;
   cudaEvent_t e0, e1;
   if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return cudaGetLastError();
   float* imp = nullptr;
@@ -1813,15 +1837,17 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
   for (size_t i = 0; err == cudaSuccess && i < cands.size() && i < (size_t)kTuneMax; ++i) {
     if (std::get<0>(cands[i]) > kTuneSpan * best_cost) break;
     const int tg = std::get<1>(cands[i]), ug = std::get<2>(cands[i]), h = std::get<3>(cands[i]);
-    int prev_stages = -1;
+    int last_stages = -1;
+    for (int hint : {1, 0})                                        // L2 evict_first on the K stream, or not
     for (int cap : {kStageCap, kStageCap - 1}) {                 // (measured: 3 or 4 TMA stages win)
+      if (cap == kStageCap) last_stages = -1;
       {
         std::lock_guard<std::mutex> lk(plan_registry_mu());
-        plan_registry()[plan_key(g, 0)] = PlanChoice(tg, ug, h, cap);
+        plan_registry()[plan_key(g, 0)] = PlanChoice(tg, ug, h, cap, hint);
       }
       Plan pl = make_plan(g);
-      if (!pl.ok || pl.n_tg != tg || pl.n_ug != ug || pl.hier != h || pl.stages == prev_stages) continue;
-      prev_stages = pl.stages;
+      if (!pl.ok || pl.n_tg != tg || pl.n_ug != ug || pl.hier != h || pl.stages == last_stages) continue;
+      last_stages = pl.stages;
       void* ws = nullptr;
       if ((err = cudaMalloc(&ws, pl.ws_total())) != cudaSuccess) break;
       cudaMemsetAsync(ws, 0, pl.ws_total(), st);
@@ -1833,7 +1859,9 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
       float ms = 0.f;
       if (err == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
       cudaFree(ws);
-      if (err == cudaSuccess && ms < best_ms) { best_ms = ms; best_tg = tg; best_ug = ug; best_h = h; best_cap = cap; }
+      if (err == cudaSuccess && ms < best_ms) {
+        best_ms = ms; best_tg = tg; best_ug = ug; best_h = h; best_cap = cap; best_hint = hint;
+      }
     }
   }
   cudaFree(imp);
@@ -1841,7 +1869,7 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
   cudaEventDestroy(e1);
   {
     std::lock_guard<std::mutex> lk(plan_registry_mu());
-    plan_registry()[plan_key(g, 0)] = PlanChoice(best_tg, best_ug, best_h, best_cap);
+    plan_registry()[plan_key(g, 0)] = PlanChoice(best_tg, best_ug, best_h, best_cap, best_hint);
   }
   *tg_out = best_tg;
   *ug_out = best_ug;
@@ -1853,7 +1881,7 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
 bool fused_set_plan(const Geom& g, int n_tg, int n_ug, int hier) {
   std::lock_guard<std::mutex> lk(plan_registry_mu());
   if (n_tg <= 0) { plan_registry().erase(plan_key(g, 0)); return true; }
-  plan_registry()[plan_key(g, 0)] = PlanChoice(n_tg, n_ug, hier, 0);
+  plan_registry()[plan_key(g, 0)] = PlanChoice(n_tg, n_ug, hier, 0, -1);
   return true;
 }
 
