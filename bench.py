@@ -40,6 +40,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3", choices=["C0", "C1", "C2", "C3", "C4"])
+    ap.add_argument("--R", type=int, default=None, help="secondary point: look-ahead rows (SURVEY 8(d): R=1 'Full', R=9)")
+    ap.add_argument("--chunk", type=int, default=None, help="secondary point: chunk size (chunk=1: raw SpecPrefill)")
+    ap.add_argument("--pool", type=int, default=None, help="secondary point: pooling window (odd)")
+    ap.add_argument("--keep", type=float, default=None, help="secondary point: keep rate")
     ap.add_argument("--algo", default="fused", choices=["fused", "simt", "auto"])
     ap.add_argument("--plan", default=None, help="fused-kernel decomposition override 'n_tg,n_ug'")
     ap.add_argument("--shard", default="auto", choices=["auto", "batch", "replica", "seq", "seq-split", "head"],
@@ -138,9 +142,21 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+_SECONDARY = {}
+
+
 def workload(name):
+    """BASELINE.json config `name`, with the secondary-point overrides of SURVEY
+    8(d) (--R, --chunk, --pool, --keep) if given."""
     from spgen import gen
-    return gen.CONFIGS[name]
+    w = gen.CONFIGS[name]
+    kw = {k: v for k, v in _SECONDARY.items() if v is not None}
+    return w.with_(**kw) if kw else w
+
+
+def secondary_label() -> str:
+    kw = {k: v for k, v in _SECONDARY.items() if v is not None}
+    return (" (" + ", ".join(f"{k}={v}" for k, v in kw.items()) + ")") if kw else ""
 
 
 def kept_chunks_tokens(w) -> int:
@@ -224,7 +240,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config} {w.name}", "B": w.B, "N": w.N, "L": w.L, "H": w.H,
+            "config": {"workload": f"{args.config} {w.name}" + secondary_label(), "B": w.B, "N": w.N, "L": w.L, "H": w.H,
                        "Hkv": w.Hkv, "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk,
                        "sampled_layers": layers, "prompt_token_equiv_per_step": tok_equiv},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
@@ -539,7 +555,7 @@ def run_ours(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if (seq or head or bsplit) else "weak", "vs_baseline": None, "dtype": args.kv, "data": "synthetic",
-            "config": {"workload": f"{args.config} {w.name}" + (" e4m3 K/Q" if f8 else "")
+            "config": {"workload": f"{args.config} {w.name}" + secondary_label() + (" e4m3 K/Q" if f8 else "")
                        + (f" paged bs{args.paged} {args.paged_layout}" if paged else "") + (" ragged" if seq_lens is not None else ""),
                        "prompt_tokens_per_step": n_tokens, "B": w.B, "N": w.N, "L": w.L, "H": w.H, "Hkv": w.Hkv,
                        "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk,
@@ -605,6 +621,7 @@ def run_e2e(args, w, Q, K, T, dev, stream, dist, job_tokens):
 
 def main():
     args = parse()
+    _SECONDARY.update(R=args.R, chunk=args.chunk, pool_k=args.pool, keep=args.keep)
     if args.plan:
         os.environ["SP_FUSED_PLAN"] = args.plan
     if args.impl == "reference":

@@ -63,9 +63,10 @@ def check_selection(ids: np.ndarray, pos: np.ndarray, n_kept: int, o: dict, chun
     assert len(kept_c) == o["K_c"]
     sizes = np.minimum((kept_c + 1) * chunk, N) - kept_c * chunk
     assert n_kept == int(sizes.sum())
-    for c in kept_c:                                   # whole chunks, in order
-        lo, hi = c * chunk, min(N, (c + 1) * chunk)
-        assert np.isin(np.arange(lo, hi), ids).all()
+    # whole chunks, in order: ids are exactly the concatenated token ranges of the kept chunks
+    starts = np.repeat(kept_c * chunk, sizes)
+    offs = np.arange(n_kept) - np.repeat(np.cumsum(sizes) - sizes, sizes)
+    np.testing.assert_array_equal(ids, starts + offs)
     cs = o["cs"]
     dropped = np.setdiff1d(np.arange(len(cs)), kept_c)
     if len(dropped):

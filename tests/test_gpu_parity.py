@@ -296,6 +296,25 @@ def test_c4_keep_sweep():
     assert len(regimes) == 9
 
 
+# ---------------------------------------------------------------- secondary points at full size
+@pytest.mark.parametrize("name,kw,keeps", [
+    ("C1", dict(R=1), None),                          # "Full": no look-ahead
+    ("C3", dict(R=1), None),
+    ("C1", dict(R=9), None),                          # G*R = 36: a non-multiple-of-32 column count
+    ("C1", dict(chunk=1, pool_k=1), [0.1, 0.9]),      # raw SpecPrefill, token-level
+])
+def test_secondary_points_full(name, kw, keeps):
+    _full_config(gen.CONFIGS[name].with_(**kw), "fused", [0], keeps=keeps, where="secondary")
+
+
+@pytest.mark.slow
+def test_c4_token_level_full():
+    """C4 at chunk = 1, pool = 1 (raw SpecPrefill at 128K): up to 117,965 of
+    131,072 tokens kept at keep 0.9 -- exactly ceil(keep * N) tokens (BJ)."""
+    w = gen.CONFIGS["C4"].with_(chunk=1, pool_k=1)
+    _full_config(w, "fused", [0], keeps=[0.1, 0.9], where="secondary")
+
+
 # ---------------------------------------------------------------- full-mantissa inputs (spgen "randn")
 # Every dyadic-grid test above accumulates exactly in fp32; these run the same
 # path on full-mantissa bf16 (all 8 significand bits, wide exponent range,
