@@ -365,8 +365,61 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
   int carry_eq = 0, carry_tok = 0, carry_k = 0;
   const int* tokens = a.tokens ? a.tokens + (long long)b * Nrow : nullptr;
   int* out = a.out ? a.out + (long long)b * Nrow : nullptr;
-  int* ids = a.ids + (long long)b * Nrow;
-  int* pos = a.pos + (long long)b * Nrow;
+  int* ids = V == kCand ? nullptr : a.ids + (long long)b * Nrow;
+  int* pos = V == kCand ? nullptr : a.pos + (long long)b * Nrow;
+  if (n_c > 4 * NT && !by_rank) {
+    // many chunks (token-level selection of long prompts): every thread owns a
+    // contiguous run of chunks, so the block needs three scans in all instead
+    // of three per tile of NT chunks; the same keep rule (every chunk above T,
+    // the lowest-index chunks equal to T) and the same output order
+    const long long R = (n_c + NT - 1) / NT;
+    const long long r0 = std::min(n_c, (long long)tid * R), r1 = std::min(n_c, r0 + R);
+    int my_eq = 0;
+    for (long long c = r0; c < r1; ++c) {
+      const unsigned key = __float_as_uint(cs[c]);
+      my_eq += ((V != kMerge || key != kInvalid) && key == T) ? 1 : 0;
+    }
+    int tot;
+    const int eq_before = block_excl_scan<NT>(my_eq, sh.scan, &tot);
+    int my_k = 0, my_tok = 0;
+    for (long long c = r0, e = eq_before; c < r1; ++c) {
+      const unsigned key = __float_as_uint(cs[c]);
+      const bool in = V != kMerge || key != kInvalid;
+      const bool eq = in && key == T;
+      const bool keep = (in && key > T) || (eq && e < need_eq);
+      e += eq ? 1 : 0;
+      if (keep) {
+        ++my_k;
+        my_tok += (int)(((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk);
+      }
+    }
+    const int k_before = block_excl_scan<NT>(my_k, sh.scan, &tot);
+    int tok_total = 0;
+    const int tok_before = V == kCand ? 0 : block_excl_scan<NT>(my_tok, sh.scan, &tok_total);
+    int kk = k_before, o = tok_before;
+    for (long long c = r0, e = eq_before; c < r1; ++c) {
+      const unsigned key = __float_as_uint(cs[c]);
+      const bool in = V != kMerge || key != kInvalid;
+      const bool eq = in && key == T;
+      const bool keep = (in && key > T) || (eq && e < need_eq);
+      e += eq ? 1 : 0;
+      if (!keep) continue;
+      if (V == kCand) {
+        a.cand[(long long)b * K_sel + kk++] = ((unsigned long long)key << 32) | (unsigned long long)(~(unsigned)(c + c_base));
+        continue;
+      }
+      const int t0 = (int)(c * chunk);
+      const int csz = (int)(((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk);
+      for (int j = 0; j < csz; ++j) {
+        ids[o + j] = t0 + j;
+        pos[o + j] = t0 + j + a.pos0;
+        if (out) out[o + j] = tokens[t0 + j];
+      }
+      o += csz;
+    }
+    if (V != kCand && tid == 0) a.n_kept[b] = tok_total;
+    return;
+  }
   for (long long base = 0; base < n_c; base += NT) {
     const long long c = base + tid;
     const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
