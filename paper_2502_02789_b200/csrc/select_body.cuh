@@ -368,54 +368,80 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
   int* ids = V == kCand ? nullptr : a.ids + (long long)b * Nrow;
   int* pos = V == kCand ? nullptr : a.pos + (long long)b * Nrow;
   if (n_c > 4 * NT && !by_rank) {
-    // many chunks (token-level selection of long prompts): every thread owns a
-    // contiguous run of chunks, so the block needs three scans in all instead
-    // of three per tile of NT chunks; the same keep rule (every chunk above T,
-    // the lowest-index chunks equal to T) and the same output order
-    const long long R = (n_c + NT - 1) / NT;
-    const long long r0 = std::min(n_c, (long long)tid * R), r1 = std::min(n_c, r0 + R);
-    int my_eq = 0;
-    for (long long c = r0; c < r1; ++c) {
-      const unsigned key = __float_as_uint(cs[c]);
-      my_eq += ((V != kMerge || key != kInvalid) && key == T) ? 1 : 0;
+    // many chunks (token-level selection of long prompts): every warp owns a
+    // contiguous range of chunks and walks it in coalesced 32-chunk tiles
+    // (ballots / shuffles inside the warp), so the block needs three scans in
+    // all instead of three per NT-chunk tile; the same keep rule (every chunk
+    // above T, the lowest-index chunks equal to T) and the same output order
+    constexpr int NWP = NT / 32;
+    const long long per = ((n_c + NWP - 1) / NWP + 31) / 32 * 32;
+    const long long w0 = std::min(n_c, (long long)warp * per), w1 = std::min(n_c, w0 + per);
+    const unsigned lt = (1u << lane) - 1u;
+    auto flags = [&](long long c, unsigned* key_out, bool* eq, bool* gt) {
+      const unsigned key = c < w1 ? __float_as_uint(cs[c]) : 0u;           // (SMEM or workspace)
+      const bool in = c < w1 && (V != kMerge || key != kInvalid);
+      *key_out = key;
+      *eq = in && key == T;
+      *gt = in && key > T;
+    };
+    auto csize = [&](long long c) { return (int)(((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk); };
+    int w_eq = 0;
+    for (long long c0 = w0; c0 < w1; c0 += 32) {
+      unsigned key; bool eq, gt;
+      flags(c0 + lane, &key, &eq, &gt);
+      w_eq += __popc(__ballot_sync(0xffffffffu, eq));
     }
     int tot;
-    const int eq_before = block_excl_scan<NT>(my_eq, sh.scan, &tot);
-    int my_k = 0, my_tok = 0;
-    for (long long c = r0, e = eq_before; c < r1; ++c) {
-      const unsigned key = __float_as_uint(cs[c]);
-      const bool in = V != kMerge || key != kInvalid;
-      const bool eq = in && key == T;
-      const bool keep = (in && key > T) || (eq && e < need_eq);
-      e += eq ? 1 : 0;
-      if (keep) {
-        ++my_k;
-        my_tok += (int)(((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk);
-      }
+    const int eq_before = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? w_eq : 0, sh.scan, &tot), 0);
+    int w_k = 0, w_tok = 0;
+    for (long long c0 = w0, e = eq_before; c0 < w1; c0 += 32) {
+      unsigned key; bool eq, gt;
+      flags(c0 + lane, &key, &eq, &gt);
+      const unsigned eqm = __ballot_sync(0xffffffffu, eq);
+      const bool keep = gt || (eq && e + __popc(eqm & lt) < need_eq);
+      e += __popc(eqm);
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      w_k += __popc(km);
+      int sz = keep ? csize(c0 + lane) : 0;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, o);
+      w_tok += sz;
     }
-    const int k_before = block_excl_scan<NT>(my_k, sh.scan, &tot);
+    const int k_before = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? w_k : 0, sh.scan, &tot), 0);
     int tok_total = 0;
-    const int tok_before = V == kCand ? 0 : block_excl_scan<NT>(my_tok, sh.scan, &tok_total);
+    const int tok_before = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? w_tok : 0, sh.scan, &tok_total), 0);
     int kk = k_before, o = tok_before;
-    for (long long c = r0, e = eq_before; c < r1; ++c) {
-      const unsigned key = __float_as_uint(cs[c]);
-      const bool in = V != kMerge || key != kInvalid;
-      const bool eq = in && key == T;
-      const bool keep = (in && key > T) || (eq && e < need_eq);
-      e += eq ? 1 : 0;
-      if (!keep) continue;
+    for (long long c0 = w0, e = eq_before; c0 < w1; c0 += 32) {
+      unsigned key; bool eq, gt;
+      const long long c = c0 + lane;
+      flags(c, &key, &eq, &gt);
+      const unsigned eqm = __ballot_sync(0xffffffffu, eq);
+      const bool keep = gt || (eq && e + __popc(eqm & lt) < need_eq);
+      e += __popc(eqm);
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
       if (V == kCand) {
-        a.cand[(long long)b * K_sel + kk++] = ((unsigned long long)key << 32) | (unsigned long long)(~(unsigned)(c + c_base));
+        if (keep)
+          a.cand[(long long)b * K_sel + kk + __popc(km & lt)] =
+              ((unsigned long long)key << 32) | (unsigned long long)(~(unsigned)(c + c_base));
+        kk += __popc(km);
         continue;
       }
-      const int t0 = (int)(c * chunk);
-      const int csz = (int)(((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk);
-      for (int j = 0; j < csz; ++j) {
-        ids[o + j] = t0 + j;
-        pos[o + j] = t0 + j + a.pos0;
-        if (out) out[o + j] = tokens[t0 + j];
+      const int sz = keep ? csize(c) : 0;
+      int incl = sz;                                            // inclusive prefix of the kept sizes
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
       }
-      o += csz;
+      if (keep) {
+        const int t0 = (int)(c * chunk), oo = o + incl - sz;
+        for (int j = 0; j < sz; ++j) {
+          ids[oo + j] = t0 + j;
+          pos[oo + j] = t0 + j + a.pos0;
+          if (out) out[oo + j] = tokens[t0 + j];
+        }
+      }
+      o += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (V != kCand && tid == 0) a.n_kept[b] = tok_total;
     return;

@@ -6,7 +6,7 @@ sys.path.insert(0, ROOT)
 import paper_2502_02789_b200 as sp
 
 for (B, N, chunk, pool) in [(1, 1024, 32, 5), (1, 4096, 32, 5), (1, 32768, 32, 5), (1, 131072, 32, 5),
-                            (1, 32768, 1, 5), (1, 32768, 32, 1), (64, 1024, 32, 5)]:
+                            (1, 32768, 1, 5), (1, 32768, 32, 1), (64, 1024, 32, 5), (1, 131072, 1, 1), (1, 8192, 1, 5)]:
     imp = torch.rand((B, N), device="cuda") + 1e-3
     tok = torch.randint(0, 1000, (B, N), dtype=torch.int32, device="cuda")
     ids = torch.empty_like(tok)
