@@ -315,13 +315,22 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
     __syncthreads();
     // warp-aggregated: lanes with the same digit add once (the top digits of
     // near-equal scores collide, and SMEM atomics on one address serialise)
-    for (long long c0 = (long long)warp * 32; c0 < n_c; c0 += NT) {
-      const long long c = c0 + lane;
-      const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
-      const bool in = c < n_c && (V != kMerge || key != kInvalid);
-      const unsigned digit = (in && (key & pmask) == prefix) ? (key >> shift) & 255u : 256u;
-      const unsigned peers = __match_any_sync(0xffffffffu, digit);
-      if (digit < 256u && lane == __ffs(peers) - 1) atomicAdd(&sh.hist[digit], (unsigned)__popc(peers));
+    constexpr int U = 8;                                     // keys in flight per lane (latency-bound otherwise)
+    for (long long c0 = (long long)warp * 32; c0 < n_c; c0 += (long long)NT * U) {
+      unsigned keys[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long c = c0 + (long long)u * NT + lane;
+        keys[u] = c < n_c ? __float_as_uint(cs[c]) : kInvalid;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long c = c0 + (long long)u * NT + lane;
+        const bool in = c < n_c && (V != kMerge || keys[u] != kInvalid);
+        const unsigned digit = (in && (keys[u] & pmask) == prefix) ? (keys[u] >> shift) & 255u : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, digit);
+        if (digit < 256u && lane == __ffs(peers) - 1) atomicAdd(&sh.hist[digit], (unsigned)__popc(peers));
+      }
     }
     __syncthreads();
     // digit D: count(digits > D) < remaining <= count(digits >= D); warps 0-7 scan 256 bins
@@ -377,71 +386,96 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
     const long long per = ((n_c + NWP - 1) / NWP + 31) / 32 * 32;
     const long long w0 = std::min(n_c, (long long)warp * per), w1 = std::min(n_c, w0 + per);
     const unsigned lt = (1u << lane) - 1u;
-    auto flags = [&](long long c, unsigned* key_out, bool* eq, bool* gt) {
-      const unsigned key = c < w1 ? __float_as_uint(cs[c]) : 0u;           // (SMEM or workspace)
+    auto flags_of = [&](long long c, unsigned key, bool* eq, bool* gt) {
       const bool in = c < w1 && (V != kMerge || key != kInvalid);
-      *key_out = key;
       *eq = in && key == T;
       *gt = in && key > T;
     };
+    constexpr int TU = 4;                                    // tiles whose keys are loaded together
+    auto load4 = [&](long long c0, unsigned (&k4)[TU]) {
+#pragma unroll
+      for (int u = 0; u < TU; ++u) {
+        const long long c = c0 + 32 * u + lane;
+        k4[u] = c < w1 ? __float_as_uint(cs[c]) : 0u;                    // (SMEM or workspace)
+      }
+    };
     auto csize = [&](long long c) { return (int)(((c + 1) * chunk < N ? (c + 1) * chunk : N) - c * chunk); };
     int w_eq = 0;
-    for (long long c0 = w0; c0 < w1; c0 += 32) {
-      unsigned key; bool eq, gt;
-      flags(c0 + lane, &key, &eq, &gt);
-      w_eq += __popc(__ballot_sync(0xffffffffu, eq));
+    for (long long c1 = w0; c1 < w1; c1 += 32 * TU) {
+      unsigned k4[TU];
+      load4(c1, k4);
+#pragma unroll
+      for (int u = 0; u < TU; ++u) {
+        bool eq, gt;
+        flags_of(c1 + 32 * u + lane, k4[u], &eq, &gt);
+        w_eq += __popc(__ballot_sync(0xffffffffu, eq));
+      }
     }
     int tot;
     const int eq_before = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? w_eq : 0, sh.scan, &tot), 0);
     int w_k = 0, w_tok = 0;
-    for (long long c0 = w0, e = eq_before; c0 < w1; c0 += 32) {
-      unsigned key; bool eq, gt;
-      flags(c0 + lane, &key, &eq, &gt);
-      const unsigned eqm = __ballot_sync(0xffffffffu, eq);
-      const bool keep = gt || (eq && e + __popc(eqm & lt) < need_eq);
-      e += __popc(eqm);
-      const unsigned km = __ballot_sync(0xffffffffu, keep);
-      w_k += __popc(km);
-      int sz = keep ? csize(c0 + lane) : 0;
+    long long e2 = eq_before;
+    for (long long c1 = w0; c1 < w1; c1 += 32 * TU) {
+      unsigned k4[TU];
+      load4(c1, k4);
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, o);
-      w_tok += sz;
+      for (int u = 0; u < TU; ++u) {
+        const long long c0 = c1 + 32 * u;
+        bool eq, gt;
+        flags_of(c0 + lane, k4[u], &eq, &gt);
+        const unsigned eqm = __ballot_sync(0xffffffffu, eq);
+        const bool keep = gt || (eq && e2 + __popc(eqm & lt) < need_eq);
+        e2 += __popc(eqm);
+        const unsigned km = __ballot_sync(0xffffffffu, keep);
+        w_k += __popc(km);
+        int sz = keep ? csize(c0 + lane) : 0;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, o);
+        w_tok += sz;
+      }
     }
     const int k_before = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? w_k : 0, sh.scan, &tot), 0);
     int tok_total = 0;
     const int tok_before = __shfl_sync(0xffffffffu, block_excl_scan<NT>(lane == 0 ? w_tok : 0, sh.scan, &tok_total), 0);
     int kk = k_before, o = tok_before;
-    for (long long c0 = w0, e = eq_before; c0 < w1; c0 += 32) {
-      unsigned key; bool eq, gt;
-      const long long c = c0 + lane;
-      flags(c, &key, &eq, &gt);
-      const unsigned eqm = __ballot_sync(0xffffffffu, eq);
-      const bool keep = gt || (eq && e + __popc(eqm & lt) < need_eq);
-      e += __popc(eqm);
-      const unsigned km = __ballot_sync(0xffffffffu, keep);
-      if (V == kCand) {
-        if (keep)
-          a.cand[(long long)b * K_sel + kk + __popc(km & lt)] =
-              ((unsigned long long)key << 32) | (unsigned long long)(~(unsigned)(c + c_base));
-        kk += __popc(km);
-        continue;
-      }
-      const int sz = keep ? csize(c) : 0;
-      int incl = sz;                                            // inclusive prefix of the kept sizes
+    long long e3 = eq_before;
+    for (long long c1 = w0; c1 < w1; c1 += 32 * TU) {
+      unsigned k4[TU];
+      load4(c1, k4);
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += y;
-      }
-      if (keep) {
-        const int t0 = (int)(c * chunk), oo = o + incl - sz;
-        for (int j = 0; j < sz; ++j) {
-          ids[oo + j] = t0 + j;
-          pos[oo + j] = t0 + j + a.pos0;
-          if (out) out[oo + j] = tokens[t0 + j];
+      for (int u = 0; u < TU; ++u) {
+        const long long c = c1 + 32 * u + lane;
+        const unsigned key = k4[u];
+        bool eq, gt;
+        flags_of(c, key, &eq, &gt);
+        const unsigned eqm = __ballot_sync(0xffffffffu, eq);
+        const bool keep = gt || (eq && e3 + __popc(eqm & lt) < need_eq);
+        e3 += __popc(eqm);
+        const unsigned km = __ballot_sync(0xffffffffu, keep);
+        if (V == kCand) {
+          if (keep)
+            a.cand[(long long)b * K_sel + kk + __popc(km & lt)] =
+                ((unsigned long long)key << 32) | (unsigned long long)(~(unsigned)(c + c_base));
+          kk += __popc(km);
+          continue;
         }
+        const int sz = keep ? csize(c) : 0;
+        int incl = sz;                                          // inclusive prefix of the kept sizes
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl += y;
+        }
+        if (keep) {
+          const int t0 = (int)(c * chunk), oo = o + incl - sz;
+          for (int j = 0; j < sz; ++j) {
+            ids[oo + j] = t0 + j;
+            pos[oo + j] = t0 + j + a.pos0;
+            if (out) out[oo + j] = tokens[t0 + j];
+          }
+        }
+        o += __shfl_sync(0xffffffffu, incl, 31);
       }
-      o += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (V != kCand && tid == 0) a.n_kept[b] = tok_total;
     return;
