@@ -315,6 +315,16 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
     __syncthreads();
     // warp-aggregated: lanes with the same digit add once (the top digits of
     // near-equal scores collide, and SMEM atomics on one address serialise)
+    if (n_c <= 4 * NT) {
+      for (long long c0 = (long long)warp * 32; c0 < n_c; c0 += NT) {
+        const long long c = c0 + lane;
+        const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
+        const bool in = c < n_c && (V != kMerge || key != kInvalid);
+        const unsigned digit = (in && (key & pmask) == prefix) ? (key >> shift) & 255u : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, digit);
+        if (digit < 256u && lane == __ffs(peers) - 1) atomicAdd(&sh.hist[digit], (unsigned)__popc(peers));
+      }
+    } else {
     constexpr int U = 8;                                     // keys in flight per lane (latency-bound otherwise)
     for (long long c0 = (long long)warp * 32; c0 < n_c; c0 += (long long)NT * U) {
       unsigned keys[U];
@@ -331,6 +341,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
         const unsigned peers = __match_any_sync(0xffffffffu, digit);
         if (digit < 256u && lane == __ffs(peers) - 1) atomicAdd(&sh.hist[digit], (unsigned)__popc(peers));
       }
+    }
     }
     __syncthreads();
     // digit D: count(digits > D) < remaining <= count(digits >= D); warps 0-7 scan 256 bins
