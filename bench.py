@@ -357,9 +357,24 @@ def run_ours(args):
             sp.score_select(Q, K, w.keep, w.pool_k, w.chunk, w.pos0, tokens=T, R_valid=w.Rv, scale=w.scale,
                             out=sel_out)
 
+    peer_note = None
+
+    def all_agree_failed(failed: bool) -> bool:        # a collective decision: any rank failed
+        t = torch.tensor([1 if failed else 0], device=dev, dtype=torch.int32)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return bool(t.item())
+
     if seq_peer:
         from paper_2502_02789_b200 import dist as spd
-        peer_ptrs, peer_ws = spd._peer_buffers(Q, K, w.Rv, None)
+        err = None
+        try:
+            peer_ptrs, peer_ws = spd._peer_buffers(Q, K, w.Rv, None)
+        except Exception as e:                                      # noqa: BLE001
+            err = e
+        if all_agree_failed(err is not None):
+            # the symmetric-memory peer exchange is not available here: the NCCL-only split
+            seq_peer, shard = False, "seq-split"
+            peer_note = f"peer exchange setup failed ({type(err).__name__ if err else 'on another rank'}): seq-split"
     if seq:
         from paper_2502_02789_b200 import dist as spd
         imp_loc = torch.empty((w.B, K.shape[3]), dtype=torch.float32, device=dev)
@@ -397,6 +412,19 @@ def run_ours(args):
             tuned = sp.score_tune(Q, K, w.Rv, w.scale)     # setup, not timed; later calls use the winner
     for _ in range(args.warmup):
         step()
+    if seq_peer:
+        # a peer exchange that cannot complete (e.g. peer memory not reachable) ends in
+        # SP_ETIMEOUT: decided on every rank together, fall back to the NCCL-only split
+        failed = False
+        try:
+            sp.check_device_error()
+        except sp.SpError as e:                                     # noqa: BLE001
+            failed, peer_note = True, f"peer exchange failed in warm-up ({e}): seq-split"
+        if all_agree_failed(failed):
+            seq_peer, shard = False, "seq-split"
+            peer_note = peer_note or "peer exchange failed on another rank in warm-up: seq-split"
+            for _ in range(args.warmup):
+                step()
     sp.check_device_error()
 
     # one CUDA graph per timed unit (the step; the score kernel alone for the
@@ -560,6 +588,7 @@ def run_ours(args):
                        "prompt_tokens_per_step": n_tokens, "B": w.B, "N": w.N, "L": w.L, "H": w.H, "Hkv": w.Hkv,
                        "d": w.d, "R": w.R, "keep": w.keep, "pool_k": w.pool_k, "chunk": w.chunk,
                        "algo": args.algo, "plan": plan, "plan_tuned": tuned, "launch": graph_note, "shard": shard,
+                       "shard_note": peer_note,
                        "parallelism": (f"seq{world} (prompt split, in-kernel statistics exchange over NVLink "
                                        f"peer memory, sharded select: candidate all-gather + merge)" if seq_peer else
                                        f"seq{world} (prompt split, NCCL stats all-gather, sharded select)" if seq else
