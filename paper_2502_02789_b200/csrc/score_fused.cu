@@ -1225,21 +1225,54 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           __threadfence();
         }
         named_bar(2, 128);
-        // this CTA finalises slice ug of the token group's tokens
+        // this CTA finalises slice ug of the token group's tokens: the max over
+        // the n_ug unit groups' partial maps, every (group, row, token) value
+        // loaded with many loads in flight (coalesced over tokens) and folded into
+        // SMEM with an order-preserving unsigned max (order-free, so the same bits
+        // as a sequential max); then mean_r 2^max in row order.  (A per-token loop
+        // over the groups was a chain of dependent L2 round trips: ~0.9 us per
+        // unit group at the end of every launch.)
         const long long g_lo = (long long)jb.t_lo * kTileM;
         const long long g_hi = min((long long)jb.t_hi * kTileM, (long long)jb.n);
         const long long n = max(0LL, g_hi - g_lo);
         const long long s_lo = g_lo + n * jb.ug / p.n_ug, s_hi = g_lo + n * (jb.ug + 1) / p.n_ug;
-        for (long long i = s_lo + tok; i < s_hi; i += kTileM) {
+        const int S = (int)(s_hi - s_lo), RS = p.Rv * S;
+        unsigned* mx = reinterpret_cast<unsigned*>(acc);          // [Rv][S] (acc was copied out above)
+        for (int e = tok; e < RS; e += kTileM) mx[e] = 0u;        // below every ordered key
+        named_bar(2, 128);
+        {
+          const float* src = p.accpart + (long long)jb.b * p.n_ug * p.Rv * p.N + s_lo;
+          const int tot = p.n_ug * RS;
+          constexpr int kU = 8;
+          for (int e0 = tok; e0 < tot; e0 += kU * kTileM) {
+            float v[kU];
+            int dst[kU];
+#pragma unroll
+            for (int k = 0; k < kU; ++k) {
+              const int e = e0 + k * kTileM;
+              const int gr = e / S, i = e - gr * S;                // gr = group * Rv + r
+              dst[k] = e < tot ? (gr % p.Rv) * S + i : -1;
+              v[k] = e < tot ? __ldcg(src + (long long)gr * p.N + i) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < kU; ++k) {
+              if (dst[k] >= 0) {
+                const unsigned u = __float_as_uint(v[k]);
+                atomicMax(&mx[dst[k]], (u & 0x80000000u) ? ~u : (u | 0x80000000u));
+              }
+            }
+          }
+        }
+        named_bar(2, 128);
+        for (int i = tok; i < S; i += kTileM) {
           float s = 0.f;
           for (int r = 0; r < p.Rv; ++r) {
-            float m = -CUDART_INF_F;
-            for (int g = 0; g < p.n_ug; ++g)
-              m = fmaxf(m, __ldcg(&p.accpart[(((long long)jb.b * p.n_ug + g) * p.Rv + r) * p.N + i]));
-            if (p.acc_out != nullptr) p.acc_out[((long long)jb.b * p.Rv + r) * p.N + i] = m;
+            const unsigned k = mx[r * S + i];
+            const float m = __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+            if (p.acc_out != nullptr) p.acc_out[((long long)jb.b * p.Rv + r) * p.N + s_lo + i] = m;
             s += ex2(m);
           }
-          if (p.acc_out == nullptr) p.imp[(long long)jb.b * p.N + i] = s * inv;
+          if (p.acc_out == nullptr) p.imp[(long long)jb.b * p.N + s_lo + i] = s * inv;
         }
         named_bar(2, 128);
         if (threadIdx.x == kFinalWarp0 * 32) {

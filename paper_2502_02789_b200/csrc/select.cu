@@ -50,14 +50,32 @@ namespace {
 using namespace sel;
 constexpr int ST = 1024;
 
+}  // namespace
+#ifdef SP_SELECT_TRACE
+// [0] first CTA entry, [1] first CTA past griddepcontrol.wait, [2] phase A done
+// (last CTA), [3] B-C start, [4] B done, [5] C done
+extern "C" int sp_select_trace_read(unsigned long long* host8, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(host8, sel::g_sel_trace, sizeof(g_sel_trace)) != cudaSuccess) return 1;
+  if (reset) {
+    unsigned long long init[8] = {~0ull, ~0ull, 0, 0, 0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(sel::g_sel_trace, init, sizeof(init)) != cudaSuccess) return 1;
+  }
+  return 0;
+}
+#endif
+namespace {
+
 template <int V>
 __global__ void __launch_bounds__(ST) k_select(SelArgs a) {
   extern __shared__ __align__(16) float dyn[];    // [segcap + 2w] staged importance, [segcap] pooled, [n_c] scores
+  SEL_STAMP_MIN(0);
   // programmatic dependent launch: this grid may start while the producer of
   // the importance (the score kernel) is finishing; wait for its results here,
   // then let the next dependent launch begin its own prologue
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
+  SEL_STAMP_MIN(1);
   SelShared<ST>& sh = *reinterpret_cast<SelShared<ST>*>(dyn + a.sh_off);
   select_body<V, ST>(a, blockIdx.x, blockIdx.y, dyn, sh);
 }

@@ -18,6 +18,21 @@ constexpr unsigned kInvalid = 0xFFFFFFFFu;   // merge: chunk with no candidate (
 enum SelectMode : int { kModeAll = 0, kModeA = 1 };
 enum Variant : int { kPlain = 0, kCand = 1, kMerge = 2 };
 
+// Debug timeline (-DSP_SELECT_TRACE builds only, tools/sel_trace.py): globaltimer
+// stamps of the selection's phases in g_sel_trace (select.cu).
+#ifdef SP_SELECT_TRACE
+__device__ unsigned long long g_sel_trace[8];   // (select.cu is the only includer)
+#define SEL_STAMP(k) \
+  do { if (threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); \
+       g_sel_trace[k] = t_; } } while (0)
+#define SEL_STAMP_MIN(k) \
+  do { if (threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); \
+       atomicMin(&g_sel_trace[k], t_); } } while (0)
+#else
+#define SEL_STAMP(k) do { } while (0)
+#define SEL_STAMP_MIN(k) do { } while (0)
+#endif
+
 struct SelArgs {
   const float* imp;          // [B][row] importance (kCand: this rank's shard)
   int nreq;                  // B (rows of every [B][...] array)
@@ -268,6 +283,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
   }
   __syncthreads();
   }
+  SEL_STAMP(2);
   if (mode == kModeA) {
     // the request's last phase-A CTA to finish runs phases B-C (one launch for
     // the whole selection): every CTA publishes its chunk scores, then counts
@@ -285,6 +301,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
     }
     __syncthreads();
   }
+  SEL_STAMP(3);
 
   // ---- B. radix select: threshold bit pattern T of the K_sel-th largest score.
   //      Up to kRankMax chunks the rank is counted directly instead:
@@ -377,6 +394,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
     remaining = sh.s_remaining;
     __syncthreads();
   }
+  SEL_STAMP(4);
   const unsigned T = prefix;
   const int need_eq = (int)remaining;            // chunks equal to T to keep (lowest indices first)
 
@@ -489,6 +507,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
       }
     }
     if (V != kCand && tid == 0) a.n_kept[b] = tok_total;
+    SEL_STAMP(5);
     return;
   }
   for (long long base = 0; base < n_c; base += NT) {
@@ -535,6 +554,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
     __syncthreads();
   }
   if (V != kCand && tid == 0) a.n_kept[b] = carry_tok;
+  SEL_STAMP(5);
 }
 
 }  // namespace sel
