@@ -14,9 +14,11 @@
  *             caller-provided workspace of at least *_workspace_bytes() bytes.
  *             A score workspace must be zero-filled before its first use with a
  *             given geometry (sp_geom) and may then be reused for that geometry
- *             indefinitely: the fused kernel's exchange counters are left at zero
- *             at the end of every successful call.  Reusing it for another
- *             geometry, or after SP_ETIMEOUT, requires zero-filling it again.
+ *             indefinitely: the fused kernel's exchange counters are left at
+ *             zero at the end of every successful call.  Reusing it for another
+ *             geometry or another launch plan (sp_score_set_plan,
+ *             sp_score_tune), or after SP_ETIMEOUT, requires zero-filling it
+ *             again.
  * Streams     Every call is enqueued on `stream` (a cudaStream_t / CUstream;
  *             NULL = legacy default stream) and returns without synchronising.
  *             Outputs are valid in stream order.
@@ -363,18 +365,33 @@ sp_status sp_select_ragged(const float* importance, const int32_t* seq_lens, con
 
 /* ------------------------------------------------------------------ score + select in one call
  * sp_score followed by sp_select_gather (O1-O11, Alg.1) with the same
- * outputs, in one call: the score kernel, then the selection launched as its
- * programmatic dependent.  (Measured and not adopted: the selection as the
- * score kernel's own tail on its 384 threads, 3-7 us slower than the separate
- * 1024-thread launch -- DESIGN.md 5.3.)  Workspace:
- * sp_score_select_workspace_bytes(g, p) bytes, 256-byte aligned, zero-filled
- * once and reused only for this geometry and selection.  tokens / out_tokens
- * may both be NULL (no gather). */
+ * outputs, bit for bit, in one call.  On the fused kernel the selection's
+ * pooling and chunk means (sec:chunk_select P:121-123, Z6, Z8) run in the score
+ * kernel's epilogue -- each token group's chunks as soon as its importance and
+ * its neighbours' are written, in the selection kernel's own arithmetic order --
+ * and the selection launch, a programmatic dependent, runs only the top-K_c and
+ * the compaction (+ gather).  Where the epilogue cannot stage a token group's
+ * window (e.g. R_valid = 1, a very wide pool) it is sp_score then the whole
+ * selection.  Workspace: sp_score_select_workspace_bytes(g, p) bytes, 256-byte
+ * aligned, zero-filled once and reused only for this geometry and selection.
+ * tokens / out_tokens may both be NULL (no gather). */
 size_t sp_score_select_workspace_bytes(const sp_geom* g, const sp_select_params* p);
 sp_status sp_score_select(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay,
                           const sp_select_params* p, const int32_t* tokens, float* importance, int32_t* ids,
                           int32_t* pos, int32_t* n_kept, int32_t* out_tokens, void* ws, size_t ws_bytes,
                           sp_stream stream);
+
+/* The score kernel of sp_score_select on its own: the importance (as sp_score)
+ * plus the selection's chunk scores cs[b][c] = mean over chunk c of the pooled
+ * importance (O5-O6: centred window of pool_k with shrinking edges, Z6; the
+ * partial last chunk over its true size, Z8), c < ceil(N / chunk), the same bits
+ * as the selection computes -- for callers that rank the chunks themselves.
+ * cs: device float [B][ceil(N / chunk)].  pool_k odd, 1..4097; chunk 1..16384.
+ * Workspace: sp_score_workspace_bytes(g).  SP_EUNSUPPORTED when the geometry's
+ * plan cannot stage a token group's window in the epilogue (then sp_score +
+ * sp_select). */
+sp_status sp_score_chunks(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, int32_t pool_k,
+                          int32_t chunk, float* importance, float* cs, void* ws, size_t ws_bytes, sp_stream stream);
 
 /* ------------------------------------------------------------------ sequence-sharded select
  * Row e: one request's prompt split along tokens over

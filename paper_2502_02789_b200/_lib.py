@@ -112,6 +112,7 @@ SIGNATURES = {
     "sp_seq_merge": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int64, _S, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "sp_score_select_workspace_bytes": (C.c_size_t, [_G, _S]),
     "sp_score_select": (C.c_int, [_P, _P, _G, _L, _S, _P, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
+    "sp_score_chunks": (C.c_int, [_P, _P, _G, _L, C.c_int32, C.c_int32, _P, _P, _P, C.c_size_t, _P]),
     "sp_run_workspace_bytes": (C.c_size_t, [_G, _S]),
     "sp_run_host": (C.c_int, [C.POINTER(sp_host_io), C.POINTER(sp_device_bufs), _G, _L, _S, _P]),
 }

@@ -343,8 +343,9 @@ def seq_merge(cand_all: torch.Tensor, world: int, N: int, keep: float, pool_k: i
 
 def score_select(Q, K, keep: float, pool_k: int, chunk: int, pos0: int = 0, tokens=None, R_valid=None, scale=None,
                  out=None, stream=None):
-    """sp_score + sp_select_gather in one call (one launch for a single request
-    on the fused kernel: the selection runs as the score kernel's tail).
+    """sp_score + sp_select_gather in one call: the fused score kernel computes the
+    selection's chunk scores in its epilogue and the dependent selection launch
+    runs the top-K_c and the compaction (same bits as the two calls).
     Returns (importance, ids, pos, n_kept[, gathered tokens]); ``out`` may hold
     preallocated tensors with those keys."""
     g, lay = make_geom(Q, K, R_valid, scale)
@@ -370,6 +371,24 @@ def score_select(Q, K, keep: float, pool_k: int, chunk: int, pos0: int = 0, toke
                                 pos.data_ptr(), nk.data_ptr(), None if outt is None else outt.data_ptr(),
                                 ws.data_ptr(), ws.numel(), _stream_ptr(stream)), "sp_score_select")
     return (imp, ids, pos, nk) if tokens is None else (imp, ids, pos, nk, outt)
+
+
+def score_chunks(Q, K, pool_k: int, chunk: int, R_valid=None, scale=None, out=None, cs=None, stream=None):
+    """The score kernel of score_select alone: (importance [B][N], chunk scores
+    [B][ceil(N / chunk)]) -- the selection's pooled chunk means computed in the
+    kernel's epilogue (same bits as the selection's own).  Raises SpError
+    (unsupported) where the plan cannot stage them."""
+    g, lay = make_geom(Q, K, R_valid, scale)
+    dev = K.device
+    n_c = (g.N + int(chunk) - 1) // int(chunk)
+    out = torch.empty((g.B, g.N), dtype=torch.float32, device=dev) if out is None else out
+    cs = torch.empty((g.B, n_c), dtype=torch.float32, device=dev) if cs is None else cs
+    nbytes = lib().sp_score_workspace_bytes(C.byref(g), ALGOS["fused"])
+    ws = workspace(("score", "fused", _geom_key(g)), nbytes, dev, stream)
+    check(lib().sp_score_chunks(Q.data_ptr(), K.data_ptr(), C.byref(g), C.byref(lay), int(pool_k), int(chunk),
+                                out.data_ptr(), cs.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
+          "sp_score_chunks")
+    return out, cs
 
 
 def gather(tokens: torch.Tensor, ids: torch.Tensor, n_kept: torch.Tensor, out=None, stream=None) -> torch.Tensor:

@@ -110,8 +110,10 @@ struct FusedParams {
                                        // (max2, sum) packed in one 64-bit word; 0 = "not yet written"
   int hier;                            // cross-rank (peer) exchange: world > 1
   unsigned* epoch;                     // [2] launch epoch (parity selects the partial buffer), CTAs done
-  float* accpart;                      // [B][n_ug][Rv][N]
-  unsigned* fin_cnt;                   // [B][n_tg]    finalize counters (self-cleaning)
+  float* accpart;                      // [B][n_ug][Rv][N] the unit groups' partial (l,h)-max maps
+  unsigned* fin_cnt;                   // [3][B][n_tg] finalize counters: [launch parity] in the full and
+                                       // statistics modes (the other parity's re-zeroed by the exchange
+                                       // warp), [2] in finish mode (self-resetting: a second count)
   float* imp;                          // [B][N]
   float* acc_out;                      // head-sharded partition: [B][Rv][N] log2-domain max instead of imp
   int* err;
@@ -129,6 +131,12 @@ struct FusedParams {
   int rank, world;
   unsigned long long* peer[kMaxPeers]; // every rank's rank-word buffer base ([2][B][U][world][NCP])
   int l2hint;                          // K tiles loaded with an L2 evict_first hint (plan; A/B: SP_FUSED_L2HINT)
+  // selection phase A in the epilogue (sp_score_select): chunk means of every
+  // token group, written into the selection workspace (null: importance only)
+  float* cs_out;                       // [B][n_c_row] chunk scores
+  unsigned* bnd_cnt;                   // [B][n_tg] token-group boundary counters (self-resetting)
+  int pool_k, chunk;
+  long long n_c_row;
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -321,6 +329,12 @@ __device__ __forceinline__ unsigned long long pack_ms(float m, float s) {
 }
 __device__ __forceinline__ float2 unpack_ms(unsigned long long w) {
   return make_float2(__uint_as_float((unsigned)w), __uint_as_float((unsigned)(w >> 32)));
+}
+
+// Shared-memory unsigned max without return (explicitly shared: the pointers
+// into the manually aligned SMEM carve are generic to the compiler).
+__device__ __forceinline__ void red_smem_max(uint32_t saddr, unsigned v) {
+  asm volatile("red.shared.max.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -692,6 +706,127 @@ __device__ __noinline__ void peer_gather_unit(const FusedParams& p, long long ub
   }
 }
 
+// Debug timeline of the epilogue (-DSP_CHUNK_TRACE builds only): per CTA,
+// [0] the job's last unit folded, [1] chunk phase entered, [2] neighbours ready,
+// [3] chunk phase done (globaltimer).
+#ifdef SP_CHUNK_TRACE
+__device__ unsigned long long g_chunk_trace[160][8];
+#define CHUNK_STAMP(k) \
+  do { if ((threadIdx.x & 127) == 0) { g_chunk_trace[blockIdx.x % 160][k] = globaltimer_ns(); } } while (0)
+#define CHUNK_STAMP0(k) \
+  do { if (threadIdx.x == 0) { g_chunk_trace[blockIdx.x % 160][k] = globaltimer_ns(); } } while (0)
+#else
+#define CHUNK_STAMP(k) do { } while (0)
+#define CHUNK_STAMP0(k) do { } while (0)
+#endif
+
+// Selection phase A in the score kernel's epilogue (sp_score_select; SURVEY
+// 8(a) rows a7-a8: "1D average pooling", then "chunk the context contiguously
+// and average").  Called by the CTA that completed a token group's
+// importance.  A chunk whose pooling windows stay inside the token group is
+// computed right here; the chunks whose windows cross the boundary with a
+// neighbouring token group are computed by whichever of the two groups
+// completes second (one self-resetting counter per boundary) -- nobody waits.
+// Same arithmetic, same order as the selection kernel's phase A
+// (select_body.cuh: centred window with shrinking edges, Z6; warp-tree sums for
+// power-of-two chunks <= 32, else a rotated fixed order; mean over the chunk's
+// true size, Z8), so the chunk scores -- and the selection -- are bit-identical
+// to sp_select's.  128 threads (the aggregation warps), named barrier 2; sm: the
+// acc region (free after the epilogue).  Out of line: once per job.
+__device__ __noinline__ void chunk_phase(const FusedParams& p, const Job& jb, float* sm, int tok) {
+  const long long n = jb.n, chunk = p.chunk, w = (p.pool_k - 1) / 2;
+  const long long n_c = (n + chunk - 1) / chunk;
+  const long long g_lo = (long long)jb.t_lo * kTileM, g_hi = min((long long)jb.t_hi * kTileM, n);
+  const bool has_l = jb.tg > 0, has_r = jb.tg + 1 < p.n_tg;
+  // chunks whose windows cross token boundary B: c*chunk - w < B <= (c+1)*chunk - 1 + w
+  auto first_x = [&](long long B) { const long long v = B - w - chunk + 1; return v <= 0 ? 0LL : (v + chunk - 1) / chunk; };
+  auto last_x = [&](long long B) { return min(n_c - 1, (B + w - 1) / chunk); };
+  long long lo_c = (g_lo + chunk - 1) / chunk, hi_c = (g_hi + chunk - 1) / chunk;   // chunks starting here
+  if (has_l) lo_c = max(lo_c, last_x(g_lo) + 1);
+  if (has_r) hi_c = min(hi_c, first_x(g_hi));
+  volatile int* flag = reinterpret_cast<volatile int*>(sm);
+  CHUNK_STAMP(1);
+  if (tok == 0) {
+    __threadfence();                                   // this token group's importance before the counts
+    unsigned* bc = p.bnd_cnt + (long long)jb.b * p.n_tg;
+    const unsigned ol = has_l ? atomicAdd(bc + jb.tg - 1, 1u) : 0u;   // boundary (tg-1 | tg)
+    const unsigned orr = has_r ? atomicAdd(bc + jb.tg, 1u) : 0u;      // boundary (tg | tg+1)
+    const bool dl = has_l && ol == 1u, dr = has_r && orr == 1u;
+    if (dl) bc[jb.tg - 1] = 0u;                        // second arrival: reset for the next launch
+    if (dr) bc[jb.tg] = 0u;
+    if (dl || dr) __threadfence();                     // the neighbour's importance
+    flag[0] = dl ? 1 : 0;
+    flag[1] = dr ? 1 : 0;
+  }
+  named_bar(2, 128);
+  const bool dl = flag[0] != 0, dr = flag[1] != 0;
+  named_bar(2, 128);
+  CHUNK_STAMP(2);
+  if (dl) lo_c = first_x(g_lo);
+  if (dr) hi_c = last_x(g_hi) + 1;
+  if (lo_c >= hi_c) return;
+  const long long a0 = lo_c * chunk, a1 = min(hi_c * chunk, n);     // pooled tokens
+  const long long lo = max(0LL, a0 - w), hi = min(n, a1 + w);        // staged importance
+  const int ns = (int)(hi - lo), np = (int)(a1 - a0);
+  float* sb = sm;                                                   // [ns] importance
+  float* pb = sm + ((ns + 3) & ~3);                                 // [np] pooled
+  const float* imp = p.imp + (long long)jb.b * p.N + lo;
+  for (int j0 = 0; j0 < ns; j0 += 16 * kTileM) {                    // all loads of a batch in flight
+    float r[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int j = j0 + k * kTileM + tok;
+      r[k] = j < ns ? __ldcg(imp + j) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int j = j0 + k * kTileM + tok;
+      if (j < ns) sb[j] = r[k];
+    }
+  }
+  named_bar(2, 128);
+  const float inv_k = 1.f / (float)p.pool_k;
+  for (int i = tok; i < np; i += kTileM) {
+    const long long t = a0 + i;
+    float ws = 0.f;
+    if (t >= w && t + w <= n - 1) {                                 // interior: full window
+      const float* q = sb + (t - w - lo);
+      for (int k = 0; k < p.pool_k; ++k) ws += q[k];
+      pb[i] = ws * inv_k;
+    } else {                                                        // sequence edges: shrink
+      const long long e0 = t - w < 0 ? 0 : t - w, e1 = t + w > n - 1 ? n - 1 : t + w;
+      for (long long j = e0; j <= e1; ++j) ws += sb[j - lo];
+      pb[i] = ws / (float)(e1 - e0 + 1);
+    }
+  }
+  named_bar(2, 128);
+  float* cs = p.cs_out + (long long)jb.b * p.n_c_row;
+  if (chunk <= 32 && (chunk & (chunk - 1)) == 0) {
+    const int lg = __ffs((int)chunk) - 1, lane = tok & 31;
+    for (int g0 = (tok >> 5) * 32; g0 < np; g0 += kTileM) {         // 32-token windows on chunk boundaries
+      float v = g0 + lane < np ? pb[g0 + lane] : 0.f;
+      for (int o = (int)chunk >> 1; o >= 1; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, (int)chunk);
+      if ((lane & ((int)chunk - 1)) == 0 && g0 + lane < np) {
+        const long long c = lo_c + ((g0 + lane) >> lg);
+        cs[c] = v / (float)(min((c + 1) * chunk, n) - c * chunk);
+      }
+    }
+  } else {
+    for (long long c = lo_c + tok; c < hi_c; c += kTileM) {
+      const long long t0 = c * chunk, t1 = min((c + 1) * chunk, n);
+      const int m = (int)(t1 - t0), ii = (int)(t0 - a0), rot = (int)(c % m);
+      float sacc = 0.f;
+      for (int j = 0; j < m; ++j) {
+        int k = j + rot;
+        if (k >= m) k -= m;
+        sacc += pb[ii + k];
+      }
+      cs[c] = sacc / (float)m;
+    }
+  }
+  CHUNK_STAMP(3);
+}
+
 // kG: compile-time GQA group size (1, 2, 4, 8) or 0 for any G.  One
 // instantiation per group size keeps the kernel's hot code small: the warp
 // roles run different code concurrently on each SMSP and share the
@@ -703,7 +838,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   // the 8B geometry): the per-tile loops become straight-line code
   const int NCP = kNCP > 0 ? kNCP : p.NCP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base as an offset into the __shared__ array, so the
+  // compiler keeps the address space: LDS/STS/ATOMS instead of generic accesses
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // warp index broadcast from lane 0: provably warp-uniform, so each role's
   // loop state (descriptors, coordinates, phases) lives in uniform registers
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -1029,6 +1166,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         const long long row = (((long long)jb.b * p.U + u) * p.n_tg + jb.tg) * NCP;
         for (int c = lane; c < NCP; c += 32) part_old[row + c] = 0ull;
       }
+      if (jb.ug == 0 && lane == 0)                                  // the token group's counter of the previous
+        p.fin_cnt[((long long)(parity ^ 1u) * p.B + jb.b) * p.n_tg + jb.tg] = 0u;   // launch parity
     }
   } else if (warp == 3 && p.mode != kModeStats) {
     // ================================================================ lse2 gather
@@ -1192,6 +1331,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         if (lane == 0) mbar_arrive(bar_lempty + 8 * par);
         if (q == 0 && lane == 0) trace_stamp(p, ui, 6);
       }
+      CHUNK_STAMP(0);
       // ---- job epilogue: importance = mean_r 2^acc (possibly across unit groups)
       //      or, head-sharded (acc_out), the log2-domain max itself for a max-reduce across ranks
       const float inv = 1.f / (float)p.Rv;
@@ -1209,6 +1349,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             p.imp[(long long)jb.b * p.N + i] = s * inv;
           }
         }
+        if (p.cs_out != nullptr) {                                  // selection phase A (sp_score_select)
+          named_bar(2, 128);
+          chunk_phase(p, jb, acc, tok);
+          named_bar(2, 128);                                        // acc is the next job's
+        }
       } else {
         for (int t = 0; t < ntile; ++t) {
           const long long i = (long long)(jb.t_lo + t) * kTileM + tok;
@@ -1216,22 +1361,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
             for (int r = 0; r < p.Rv; ++r)
               p.accpart[(((long long)jb.b * p.n_ug + jb.ug) * p.Rv + r) * p.N + i] = acc[(t * p.Rv + r) * kTileM + tok];
         }
-        __threadfence();
-        named_bar(2, 128);
-        unsigned* fc = p.fin_cnt + (long long)jb.b * p.n_tg + jb.tg;
+        named_bar(2, 128);                                          // the CTA's partial maps, then one
+        unsigned* fc = p.fin_cnt + ((long long)(p.mode == kModeFinish ? 2u : parity) * p.B + jb.b) * p.n_tg + jb.tg;
         if (threadIdx.x == kFinalWarp0 * 32) {
+          __threadfence();
           atomicAdd(fc, 1u);
           spin_geq(fc, (unsigned)p.n_ug, p.err);
           __threadfence();
         }
         named_bar(2, 128);
+        CHUNK_STAMP(4);
         // this CTA finalises slice ug of the token group's tokens: the max over
-        // the n_ug unit groups' partial maps, every (group, row, token) value
-        // loaded with many loads in flight (coalesced over tokens) and folded into
-        // SMEM with an order-preserving unsigned max (order-free, so the same bits
-        // as a sequential max); then mean_r 2^max in row order.  (A per-token loop
-        // over the groups was a chain of dependent L2 round trips: ~0.9 us per
-        // unit group at the end of every launch.)
+        // the n_ug unit groups' partial maps.  Every (group, row, token) value of
+        // the slice is loaded with 16 loads in flight per thread (coalesced over
+        // tokens) and folded into SMEM (red.shared: the generic atomic the
+        // compiler emits for this pointer costs several microseconds here) with an order-preserving unsigned max
+        // (order-free: the same bits as a sequential max); then mean_r 2^max in
+        // row order.  (A per-token loop over the groups was a chain of dependent
+        // L2 round trips: ~0.9 us per unit group at the end of every launch; fire-
+        // and-forget global atomic maxima instead of the partial maps measured no
+        // faster -- the L2 atomic rate.)
         const long long g_lo = (long long)jb.t_lo * kTileM;
         const long long g_hi = min((long long)jb.t_hi * kTileM, (long long)jb.n);
         const long long n = max(0LL, g_hi - g_lo);
@@ -1240,25 +1389,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         unsigned* mx = reinterpret_cast<unsigned*>(acc);          // [Rv][S] (acc was copied out above)
         for (int e = tok; e < RS; e += kTileM) mx[e] = 0u;        // below every ordered key
         named_bar(2, 128);
-        {
+        if (S > 0) {
           const float* src = p.accpart + (long long)jb.b * p.n_ug * p.Rv * p.N + s_lo;
           const int tot = p.n_ug * RS;
-          constexpr int kU = 8;
+          const float invS = 1.f / (float)S;
+          // e = q*S + i (q = group*Rv + row) by a float reciprocal and one correction
+          // step (exact for e < 2^22: tot <= 148 * 256 * 2048 here)
+          auto split = [&](int e, int& q, int& i) {
+            q = __float2int_rz(__int2float_rn(e) * invS);
+            i = e - q * S;
+            if (i < 0) { --q; i += S; } else if (i >= S) { ++q; i -= S; }
+          };
+          constexpr int kU = 16;                                    // two to four batches at C1-C3
           for (int e0 = tok; e0 < tot; e0 += kU * kTileM) {
             float v[kU];
-            int dst[kU];
 #pragma unroll
             for (int k = 0; k < kU; ++k) {
               const int e = e0 + k * kTileM;
-              const int gr = e / S, i = e - gr * S;                // gr = group * Rv + r
-              dst[k] = e < tot ? (gr % p.Rv) * S + i : -1;
-              v[k] = e < tot ? __ldcg(src + (long long)gr * p.N + i) : 0.f;
+              int q, i;
+              split(e, q, i);
+              v[k] = e < tot ? __ldcg(src + (long long)q * p.N + i) : 0.f;
             }
 #pragma unroll
             for (int k = 0; k < kU; ++k) {
-              if (dst[k] >= 0) {
+              const int e = e0 + k * kTileM;
+              if (e < tot) {
+                int q, i;
+                split(e, q, i);
                 const unsigned u = __float_as_uint(v[k]);
-                atomicMax(&mx[dst[k]], (u & 0x80000000u) ? ~u : (u | 0x80000000u));
+                red_smem_max(smem_u32(&mx[(q % p.Rv) * S + i]), (u & 0x80000000u) ? ~u : (u | 0x80000000u));
               }
             }
           }
@@ -1275,8 +1434,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           if (p.acc_out == nullptr) p.imp[(long long)jb.b * p.N + s_lo + i] = s * inv;
         }
         named_bar(2, 128);
-        if (threadIdx.x == kFinalWarp0 * 32) {
-          if (atomicAdd(fc, 1u) == 2u * p.n_ug - 1u) atomicExch(fc, 0u);
+        CHUNK_STAMP(5);
+        // a second count only where needed: finish mode resets its counter (the
+        // full and statistics modes' counters alternate by launch parity), and
+        // the epilogue's selection phase A goes to the token group's last slice
+        if (threadIdx.x == kFinalWarp0 * 32 && (p.mode == kModeFinish || p.cs_out != nullptr)) {
+          if (p.cs_out != nullptr) __threadfence();                 // the slices before their count
+          const bool last = atomicAdd(fc, 1u) == 2u * p.n_ug - 1u;  // every slice of the token group written
+          if (last && p.mode == kModeFinish) atomicExch(fc, 0u);
+          if (p.cs_out != nullptr) *reinterpret_cast<volatile int*>(acc) = last ? 1 : 0;
+        }
+        if (p.cs_out != nullptr) {                                  // selection phase A (sp_score_select)
+          named_bar(2, 128);
+          const bool last = *reinterpret_cast<volatile int*>(acc) != 0;
+          named_bar(2, 128);
+          if (last) chunk_phase(p, jb, acc, tok);
+          named_bar(2, 128);                                        // acc is the next job's
         }
       }
     }
@@ -1289,13 +1462,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
   }
+  CHUNK_STAMP0(6);
   if (threadIdx.x == 0 && p.mode != kModeFinish) {           // finish mode never touches the partials
-    __threadfence();
+    // (no fence: the epoch is read by the next launch only, after this grid completes)
     if (atomicAdd(p.epoch + 1, 1u) == gridDim.x - 1) {       // last CTA: next launch uses the other buffer
       atomicExch(p.epoch + 1, 0u);
       atomicAdd(p.epoch, 1u);
     }
   }
+  CHUNK_STAMP0(7);
 }
 
 // ------------------------------------------------------------------ host side
@@ -1326,8 +1501,8 @@ struct Plan {
   int nq = 2;
   int hier = 0, world = 1;                            // peer exchange (world > 1); ranks
   int l2hint = 1;                                     // K tiles loaded with an L2 evict_first hint
-  size_t ws_part = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0, ws_rank = 0;
-  size_t ws_total() const { return ws_part + ws_cnt + ws_acc + ws_fin + ws_rank; }
+  size_t ws_part = 0, ws_cnt = 0, ws_acc = 0, ws_fin = 0, ws_rank = 0, ws_tgr = 0;
+  size_t ws_total() const { return ws_part + ws_cnt + ws_acc + ws_fin + ws_rank + ws_tgr; }
   bool ok = false;
 };
 
@@ -1489,8 +1664,9 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   pl.ws_part = align256(2 * (size_t)g.B * pl.U * pl.NCP * pl.n_tg * sizeof(unsigned long long));
   pl.ws_cnt = 256;                                   // launch epoch + CTAs-done counter
   pl.ws_acc = pl.n_ug > 1 ? align256((size_t)g.B * pl.n_ug * g.Rv * g.N * sizeof(float)) : 0;
-  pl.ws_fin = align256((size_t)g.B * pl.n_tg * sizeof(unsigned));
+  pl.ws_fin = align256((size_t)3 * g.B * pl.n_tg * sizeof(unsigned));
   pl.ws_rank = 0;
+  pl.ws_tgr = align256((size_t)g.B * pl.n_tg * sizeof(unsigned));   // token-group boundary counters (sp_score_select)
   pl.ok = true;
   return pl;
 }
@@ -1539,6 +1715,18 @@ bool encode_maps(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, 
 }
 
 }  // namespace
+
+#ifdef SP_CHUNK_TRACE
+extern "C" int sp_chunk_trace_read(unsigned long long* host, int reset) {   // [160][8]
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(host, g_chunk_trace, sizeof(g_chunk_trace)) != cudaSuccess) return 1;
+  if (reset) {
+    static unsigned long long z[160][8] = {};
+    if (cudaMemcpyToSymbol(g_chunk_trace, z, sizeof(z)) != cudaSuccess) return 1;
+  }
+  return 0;
+}
+#endif
 
 static unsigned long long* g_trace = nullptr;
 static long long g_trace_records = 0;
@@ -1602,6 +1790,22 @@ struct PeerArgs {
   void* const* bufs = nullptr;                        // world partial buffers (fused_peer_buffer_bytes each)
 };
 
+// The epilogue's selection phase A needs the token group's importance plus the
+// pooling halo and its pooled values staged in the acc region (tpc * Rv * 128
+// floats), whole chunks in the selection kernel's segments (chunk <= 16384), and
+// a plain single-GPU importance launch.
+bool chunk_phase_fits(const Geom& g, const Plan& pl, int mode, const float* acc_out, int world, const PagedK* pk,
+                      int pool_k, int chunk) {
+  if (mode != kModeFull || acc_out != nullptr || world != 1 || chunk < 1 || chunk > 16384 || pool_k < 1) return false;
+  if (pk != nullptr && pk->seq_lens != nullptr) return false;
+  const long long w = (pool_k - 1) / 2;
+  // no chunk's windows may cross both boundaries of a token group
+  if (pl.n_tg >= 3 && (long long)(pl.T / pl.n_tg) * kTileM < 2 * (w + chunk)) return false;
+  const long long span = (long long)pl.tpc * kTileM + 2 * (chunk + w);   // pooled tokens, at most
+  const long long need = ((span + 2 * w + 3) & ~3LL) + span;
+  return need <= (long long)pl.tpc * g.Rv * kTileM;
+}
+
 // Row f3: the paged-cache tensor map {d, Hkv, block_size, blocks, L}, box {W, 1, min(bs, 128), 1, 1}.
 bool encode_paged_map(const PagedK& pk, const Geom& g, const Plan& pl, CUtensorMap* tmK) {
   PFN_encodeTiled_t enc = encode_fn();
@@ -1661,7 +1865,7 @@ bool encode_paged_interleaved(const PagedK& pk, const Geom& g, const Plan& pl, C
 cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay, int mode,
                          const float* lse_in, float* importance, void* ws, size_t ws_bytes, cudaStream_t st,
                          float* acc_out = nullptr, const PeerArgs& peer = PeerArgs(), const PagedK* pk = nullptr,
-                         const float2* la = nullptr) {
+                         const float2* la = nullptr, const ChunkOut* co = nullptr) {
   if (peer.world < 1 || peer.world > kMaxPeers || peer.rank < 0 || peer.rank >= peer.world) return cudaErrorInvalidValue;
   Plan pl = make_plan(g, true, peer.sm_budget, nullptr, peer.world);
   if (!pl.ok || ws_bytes < pl.ws_total()) return cudaErrorInvalidValue;
@@ -1711,6 +1915,15 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   w += pl.ws_part;
   p.accpart = pl.ws_acc ? reinterpret_cast<float*>(w) : nullptr;
   w += pl.ws_acc;
+  p.bnd_cnt = reinterpret_cast<unsigned*>(w);
+  w += pl.ws_tgr;
+  if (co != nullptr) {
+    if (!chunk_phase_fits(g, pl, mode, acc_out, peer.world, pk, co->pool_k, co->chunk)) return cudaErrorNotSupported;
+    p.cs_out = co->cs;
+    p.pool_k = co->pool_k;
+    p.chunk = co->chunk;
+    p.n_c_row = (g.N + co->chunk - 1) / co->chunk;
+  }
   p.hier = pl.hier;
   p.rank = peer.rank;
   p.world = peer.world;
@@ -1777,6 +1990,12 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
 cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                         float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
   return fused_launch(Q, K, g, lay, kModeFull, nullptr, importance, ws, ws_bytes, st);
+}
+
+cudaError_t fused_score_chunks(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                               float* importance, const ChunkOut& co, void* ws, size_t ws_bytes, cudaStream_t st) {
+  return fused_launch(Q, K, g, lay, kModeFull, nullptr, importance, ws, ws_bytes, st, nullptr, PeerArgs(), nullptr,
+                      nullptr, &co);
 }
 
 // Z2' (row f4): the look-ahead keys' (max2, sum) per (request, unit, column), one

@@ -54,11 +54,11 @@ constexpr int ST = 1024;
 #ifdef SP_SELECT_TRACE
 // [0] first CTA entry, [1] first CTA past griddepcontrol.wait, [2] phase A done
 // (last CTA), [3] B-C start, [4] B done, [5] C done
-extern "C" int sp_select_trace_read(unsigned long long* host8, int reset) {
+extern "C" int sp_select_trace_read(unsigned long long* host8, int reset) {   // 16 stamps
   cudaDeviceSynchronize();
   if (cudaMemcpyFromSymbol(host8, sel::g_sel_trace, sizeof(g_sel_trace)) != cudaSuccess) return 1;
   if (reset) {
-    unsigned long long init[8] = {~0ull, ~0ull, 0, 0, 0, 0, 0, 0};
+    unsigned long long init[16] = {~0ull, ~0ull};
     if (cudaMemcpyToSymbol(sel::g_sel_trace, init, sizeof(init)) != cudaSuccess) return 1;
   }
   return 0;
@@ -178,6 +178,32 @@ float* ws_scores(void* ws, int B) {
   return reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align256((size_t)B * sizeof(unsigned)));
 }
 }  // namespace
+
+float* select_ws_scores(void* ws, int B) { return ws_scores(ws, B); }
+
+// Phases B-C only: the chunk scores were written into the workspace by the
+// score kernel (sp_score_select).  One CTA per request, the scores staged in SMEM
+// when they fit.
+cudaError_t select_ready_launch(int B, long long N, int chunk, long long ppm, int pos0, int* ids, int* pos,
+                                int* n_kept, void* ws, cudaStream_t st, const int* tokens, int* out) {
+  cudaError_t e = configure<kPlain>();
+  if (e != cudaSuccess) return e;
+  SelArgs a{};
+  a.imp = nullptr; a.row = N; a.pool_k = 1; a.chunk = chunk; a.pos0 = pos0; a.ppm = ppm;
+  a.ids = ids; a.pos = pos; a.n_kept = n_kept; a.cs_ws = ws_scores(ws, B); a.tokens = tokens; a.out = out;
+  a.n_glob = N;
+  a.blk_cnt = ws_counters(ws);
+  a.nreq = B;
+  a.cs_ready = 1;
+  a.mode = kModeAll;
+  a.segcap = 0;
+  a.cpb = 0;
+  a.nblk = 1;
+  const long long n_c = (N + chunk - 1) / chunk;
+  const long long cs_floats = n_c <= kSmemChunks ? n_c : 0;
+  a.sh_off = (int)((cs_floats + 3) / 4 * 4);
+  return launch_pdl<kPlain>(dim3(B), (size_t)a.sh_off * sizeof(float) + sizeof(SelShared<ST>), st, a);
+}
 
 bool select_supported(int pool_k) { return pool_k <= kMaxPool; }
 

@@ -21,7 +21,7 @@ enum Variant : int { kPlain = 0, kCand = 1, kMerge = 2 };
 // Debug timeline (-DSP_SELECT_TRACE builds only, tools/sel_trace.py): globaltimer
 // stamps of the selection's phases in g_sel_trace (select.cu).
 #ifdef SP_SELECT_TRACE
-__device__ unsigned long long g_sel_trace[8];   // (select.cu is the only includer)
+__device__ unsigned long long g_sel_trace[16];   // (select.cu is the only includer)
 #define SEL_STAMP(k) \
   do { if (threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); \
        g_sel_trace[k] = t_; } } while (0)
@@ -50,6 +50,8 @@ struct SelArgs {
   const int* tokens;         // optional gather source [B][row]
   int* out;                  // optional gathered tokens [B][row]
   int mode, segcap;
+  int cs_ready;              // kPlain: the chunk scores are already in cs_ws (computed by the score
+                             // kernel's epilogue, sp_score_select): phases B-C only
   long long cpb;             // chunks per CTA in kModeA
   // sequence sharding
   long long i0;              // kCand: global index of this shard's first token
@@ -65,13 +67,15 @@ template <int NT>
 struct ScanSmem {
   int warp_tot[NT / 32];
   int total;
+  unsigned long long warp_tot64[NT / 32];
+  unsigned long long total64;
 };
 
 // The selection's shared scratch (besides the staged importance / chunk scores),
 // for NT threads: placed in dynamic shared memory by the caller.
 template <int NT>
 struct SelShared {
-  unsigned hist[256];
+  unsigned hist[4 * 256];           // one histogram per radix pass (zeroed together: one barrier per pass)
   unsigned s_digit, s_remaining;
   int s_last;
   ScanSmem<NT> scan;
@@ -109,6 +113,37 @@ __device__ __forceinline__ int block_excl_scan(int v, ScanSmem<NT>& sm, int* tot
   *total = sm.total;
   __syncthreads();                                 // sm reusable after return
   return res;
+}
+
+// The same over 64-bit values (two packed counters: kept chunks << 32 | kept tokens).
+template <int NT>
+__device__ __forceinline__ unsigned long long block_excl_scan64(unsigned long long v, ScanSmem<NT>& sm,
+                                                                unsigned long long* total) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm.warp_tot64[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long t = lane < NW ? sm.warp_tot64[lane] : 0ull;
+    unsigned long long u = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, u, o);
+      if (lane >= o) u += y;
+    }
+    if (lane < NW) sm.warp_tot64[lane] = u - t;
+    if (lane == 31) sm.total64 = u;
+  }
+  __syncthreads();
+  const unsigned long long res = sm.warp_tot64[warp] + x - v;
+  *total = sm.total64;
+  return res;                                      // (callers barrier before reusing sm)
 }
 
 // Segment length starting at chunk-aligned token `base`: whole chunks when a
@@ -154,7 +189,16 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
   const bool cs_smem = mode == kModeAll && n_c_row <= kSmemChunks;
   float* cs = cs_smem ? seg + 2 * a.segcap + 2 * w : a.cs_ws + (long long)b * n_c_row;
 
-  if (V == kMerge) {
+  if (V == kPlain && a.cs_ready) {
+    // ---- the chunk scores were computed by the score kernel (same arithmetic, same bits)
+    if (cs_smem) {
+      const float* src = a.cs_ws + (long long)b * n_c_row;
+      for (long long c = tid; c < n_c; c += NT) cs[c] = __ldcg(src + c);
+    } else {
+      cs = a.cs_ws + (long long)b * n_c_row;
+    }
+    __syncthreads();
+  } else if (V == kMerge) {
     // ---- scatter the P ranks' candidates into the dense chunk array
     unsigned* csu = reinterpret_cast<unsigned*>(cs);
     for (long long c = tid; c < n_c; c += NT) csu[c] = kInvalid;
@@ -227,6 +271,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
       }
     }
     __syncthreads();
+    SEL_STAMP(6);
     // interior tokens [i_lo, i_hi) have the full window inside the sequence
     const int i_lo = (int)(w - base > 0 ? w - base : 0);
     const int i_hi = (int)(N - 1 - w - base + 1 < len ? N - 1 - w - base + 1 : len);
@@ -245,6 +290,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
       }
     }
     __syncthreads();
+    SEL_STAMP(7);
     const long long c_first = base / chunk, c_last = (base + len - 1) / chunk;
     if (warp_chunks) {
       // a warp sums 32 consecutive pooled values in groups of `chunk` lanes (tree
@@ -275,6 +321,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
       }
     }
     __syncthreads();
+    SEL_STAMP(8);
     base += len;
   }
   for (long long c = c_lo + tid; c < c_hi; c += NT) {
@@ -303,100 +350,132 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
   }
   SEL_STAMP(3);
 
-  // ---- B. radix select: threshold bit pattern T of the K_sel-th largest score.
+  // ---- B. radix select: threshold T of the K_sel-th largest score, as a bit
+  //      prefix (T & pmask): a chunk is above the threshold iff (key & pmask) >
+  //      prefix, at it iff equal.  4 passes of 8 bits over the IEEE bits (scores
+  //      are >= 0, so bit order == value order), each pass one histogram and ONE
+  //      barrier: every warp then finds the digit itself from the 256 bins (no
+  //      second barrier round); a pass whose threshold bin holds exactly the
+  //      chunks still needed ends the search (all of them are kept).
   //      Up to kRankMax chunks the rank is counted directly instead:
   //      rank(c) = #{c' : cs[c'] > cs[c], or cs[c'] == cs[c] and c' < c} (the
-  //      (score desc, index asc) order), kept iff rank < K_sel -- one pass, no
-  //      barrier rounds (measured: 2 us faster at 128 chunks, 29 us slower at 1024).
+  //      (score desc, index asc) order), kept iff rank < K_sel, by S threads per
+  //      chunk (strided subsets, shuffle-summed).
   //      kMerge: invalid entries (bit pattern kInvalid, a NaN) never count.
   constexpr int kRankMax = 256;
-  const bool by_rank = n_c <= kRankMax;
+  const bool by_rank = n_c <= kRankMax && n_c <= NT;
   unsigned prefix = 0, pmask = 0;
   unsigned remaining = (unsigned)K_sel;
-  int rank_keep = 0;
+  unsigned eq_total = 0;                             // chunks at the threshold (its bin in the last pass)
   if (by_rank) {
-    if (tid < n_c) {
-      const float mine = cs[tid];
-      int rank = 0;
+    int lg = 0;
+    while (lg < 5 && ((long long)NT >> (lg + 1)) >= n_c) ++lg;   // S = 2^lg threads per chunk, S * n_c <= NT
+    const int S = 1 << lg;
+    const int c = tid >> lg, part = tid & (S - 1);
+    int rank = 0;
+    float mine = 0.f;
+    if (c < n_c) {
+      mine = cs[c];
 #pragma unroll 8
-      for (int c2 = 0; c2 < (int)n_c; ++c2) {
-        const float o = cs[c2];                      // same address in every lane: broadcast
-        rank += (o > mine || (o == mine && c2 < tid)) ? 1 : 0;
-      }
-      rank_keep = rank < K_sel ? 1 : 0;
-      if (V == kMerge && __float_as_uint(mine) == kInvalid) rank_keep = 0;
-    }
-  }
-  for (int shift = 24; shift >= 0 && !by_rank; shift -= 8) {
-    if (tid < 256) sh.hist[tid] = 0;
-    __syncthreads();
-    // warp-aggregated: lanes with the same digit add once (the top digits of
-    // near-equal scores collide, and SMEM atomics on one address serialise)
-    if (n_c <= 4 * NT) {
-      for (long long c0 = (long long)warp * 32; c0 < n_c; c0 += NT) {
-        const long long c = c0 + lane;
-        const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
-        const bool in = c < n_c && (V != kMerge || key != kInvalid);
-        const unsigned digit = (in && (key & pmask) == prefix) ? (key >> shift) & 255u : 256u;
-        const unsigned peers = __match_any_sync(0xffffffffu, digit);
-        if (digit < 256u && lane == __ffs(peers) - 1) atomicAdd(&sh.hist[digit], (unsigned)__popc(peers));
-      }
-    } else {
-    constexpr int U = 8;                                     // keys in flight per lane (latency-bound otherwise)
-    for (long long c0 = (long long)warp * 32; c0 < n_c; c0 += (long long)NT * U) {
-      unsigned keys[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long c = c0 + (long long)u * NT + lane;
-        keys[u] = c < n_c ? __float_as_uint(cs[c]) : kInvalid;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long c = c0 + (long long)u * NT + lane;
-        const bool in = c < n_c && (V != kMerge || keys[u] != kInvalid);
-        const unsigned digit = (in && (keys[u] & pmask) == prefix) ? (keys[u] >> shift) & 255u : 256u;
-        const unsigned peers = __match_any_sync(0xffffffffu, digit);
-        if (digit < 256u && lane == __ffs(peers) - 1) atomicAdd(&sh.hist[digit], (unsigned)__popc(peers));
+      for (int c2 = part; c2 < (int)n_c; c2 += S) {
+        const float o = cs[c2];                      // same address in every lane of a group: broadcast
+        rank += (o > mine || (o == mine && c2 < c)) ? 1 : 0;
       }
     }
+    for (int o = 1; o < S; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    if (part == 0 && c < n_c) {
+      int keep = rank < K_sel ? 1 : 0;
+      if (V == kMerge && __float_as_uint(mine) == kInvalid) keep = 0;
+      sh.kept_off[c] = keep;                         // keep flags by chunk (phase C reads them)
     }
     __syncthreads();
-    // digit D: count(digits > D) < remaining <= count(digits >= D); warps 0-7 scan 256 bins
-    if (tid < 256) {
-      // suffix sums over bins (high digit first): bin d handled by thread 255 - d
-      const int d = 255 - tid;
-      unsigned v = sh.hist[d];
-      unsigned x = v;
+  } else {
+    for (int i = tid; i < 4 * 256; i += NT) sh.hist[i] = 0u;
+    __syncthreads();
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = 24 - 8 * pass;
+      unsigned* H = sh.hist + 256 * pass;
+      // a warp whose lanes share one digit (the top digits of near-equal
+      // scores: SMEM atomics on one address serialise) adds once; otherwise
+      // every lane adds its own
+      if (n_c <= 4 * NT) {
+        for (long long c0 = (long long)warp * 32; c0 < n_c; c0 += NT) {
+          const long long c = c0 + lane;
+          const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
+          const bool in = c < n_c && (V != kMerge || key != kInvalid);
+          const unsigned digit = (in && (key & pmask) == prefix) ? (key >> shift) & 255u : 256u;
+          const unsigned d0 = __shfl_sync(0xffffffffu, digit, 0);
+          if (__all_sync(0xffffffffu, digit == d0)) {
+            if (lane == 0 && d0 < 256u) atomicAdd(&H[d0], 32u);
+          } else if (digit < 256u) {
+            atomicAdd(&H[digit], 1u);
+          }
+        }
+      } else {
+        constexpr int U = 8;                                     // keys in flight per lane (latency-bound otherwise)
+        for (long long c0 = (long long)warp * 32; c0 < n_c; c0 += (long long)NT * U) {
+          unsigned keys[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const long long c = c0 + (long long)u * NT + lane;
+            keys[u] = c < n_c ? __float_as_uint(cs[c]) : kInvalid;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const long long c = c0 + (long long)u * NT + lane;
+            const bool in = c < n_c && (V != kMerge || keys[u] != kInvalid);
+            const unsigned digit = (in && (keys[u] & pmask) == prefix) ? (keys[u] >> shift) & 255u : 256u;
+            const unsigned peers = __match_any_sync(0xffffffffu, digit);
+            if (digit < 256u && lane == __ffs(peers) - 1) atomicAdd(&H[digit], (unsigned)__popc(peers));
+          }
+        }
+      }
+      __syncthreads();
+      // digit D: count(digits > D) < remaining <= count(digits >= D).  Every warp
+      // scans the 256 bins itself: lane l holds digits 255 - 8l - k, k = 0..7.
+      const uint4 lo4 = *reinterpret_cast<const uint4*>(H + 248 - 8 * lane);
+      const uint4 hi4 = *reinterpret_cast<const uint4*>(H + 252 - 8 * lane);
+      const unsigned cnt[8] = {hi4.w, hi4.z, hi4.y, hi4.x, lo4.w, lo4.z, lo4.y, lo4.x};
+      unsigned t = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += cnt[k];
+      unsigned incl = t;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
       }
-      if (lane == 31) sh.scan.warp_tot[warp] = (int)x;
-      __syncwarp();
-      // (warps 0..7 only) combine warp totals below
-      sh.kept_off[tid] = (int)x;                      // inclusive within warp
-    }
-    __syncthreads();
-    if (tid < 256) {
-      unsigned before = 0;
-      for (int ww = 0; ww < warp; ++ww) before += (unsigned)sh.scan.warp_tot[ww];
-      const unsigned incl = before + (unsigned)sh.kept_off[tid];   // count of digits >= d
-      const unsigned excl = incl - sh.hist[255 - tid];             // count of digits > d
-      if (excl < remaining && incl >= remaining) {
-        sh.s_digit = (unsigned)(255 - tid);
-        sh.s_remaining = remaining - excl;
+      const unsigned excl = incl - t;
+      const bool here = excl < remaining && incl >= remaining;
+      const unsigned ball = __ballot_sync(0xffffffffu, here);
+      unsigned dig = 0, before = 0, bin = 0;
+      if (here) {
+        unsigned run = excl;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (bin == 0u && run + cnt[k] >= remaining) {
+            dig = 255u - 8u * lane - k;
+            before = run;
+            bin = cnt[k];
+          }
+          run += cnt[k];
+        }
       }
+      const int src = ball ? __ffs(ball) - 1 : 0;
+      dig = __shfl_sync(0xffffffffu, dig, src);
+      before = __shfl_sync(0xffffffffu, before, src);
+      bin = __shfl_sync(0xffffffffu, bin, src);
+      prefix |= dig << shift;
+      pmask |= 255u << shift;
+      remaining -= before;
+      eq_total = bin;
+      SEL_STAMP(10 + pass);
+      if (bin == remaining) break;                   // every chunk of the threshold bin is kept
     }
-    __syncthreads();
-    prefix |= sh.s_digit << shift;
-    pmask |= 255u << shift;
-    remaining = sh.s_remaining;
-    __syncthreads();
   }
   SEL_STAMP(4);
   const unsigned T = prefix;
-  const int need_eq = (int)remaining;            // chunks equal to T to keep (lowest indices first)
+  const int need_eq = (int)remaining;            // chunks at the threshold to keep (lowest indices first)
 
   // ---- C. keep flags in chunk order, compaction (+ gather) of the kept token
   //      ranges, or (kCand) the kept chunks' candidate keys
@@ -405,6 +484,56 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
   int* out = a.out ? a.out + (long long)b * Nrow : nullptr;
   int* ids = V == kCand ? nullptr : a.ids + (long long)b * Nrow;
   int* pos = V == kCand ? nullptr : a.pos + (long long)b * Nrow;
+  if (n_c <= NT) {
+    // one tile of chunks (every prompt up to NT chunks): thread c owns chunk c.
+    // The tie scan only when the threshold has more chunks than are kept; one
+    // packed scan gives each kept chunk its slot and its first output token;
+    // then a flat compaction: kept token o lies in kept chunk o / chunk (only the
+    // prompt's last chunk can be short, and it is the last kept one), so the
+    // token gather's loads are independent (no per-chunk chain).
+    const int c = tid;
+    const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
+    const bool in = c < n_c && (V != kMerge || key != kInvalid);
+    int keep;
+    if (by_rank) {
+      keep = c < n_c ? sh.kept_off[c] : 0;
+    } else {
+      const int eq = (in && (key & pmask) == T) ? 1 : 0;
+      const int gt = (in && (key & pmask) > T) ? 1 : 0;
+      if ((int)eq_total == need_eq) {
+        keep = gt | eq;
+      } else {
+        int tot;
+        const int eq_rank = block_excl_scan<NT>(eq, sh.scan, &tot);
+        keep = gt | (eq & (eq_rank < need_eq ? 1 : 0));
+      }
+    }
+    __syncthreads();                                  // (kept_off / scan scratch reused below)
+    if (V == kCand) {
+      int tot;
+      const int slot = block_excl_scan<NT>(keep, sh.scan, &tot);
+      if (keep)
+        a.cand[(long long)b * K_sel + slot] = ((unsigned long long)key << 32) | (unsigned long long)(~(unsigned)(c + c_base));
+      return;
+    }
+    const int sz = keep ? (int)(((long long)(c + 1) * chunk < N ? (long long)(c + 1) * chunk : N) - (long long)c * chunk) : 0;
+    unsigned long long tot2;
+    const unsigned long long pk = block_excl_scan64<NT>(((unsigned long long)keep << 32) | (unsigned)sz, sh.scan, &tot2);
+    if (keep) sh.kept_c[(int)(pk >> 32)] = c;
+    const int n_tok = (int)(tot2 & 0xFFFFFFFFull);
+    __syncthreads();
+#pragma unroll 4
+    for (int o = tid; o < n_tok; o += NT) {
+      const int s2 = o / chunk;
+      const int t = sh.kept_c[s2] * chunk + (o - s2 * chunk);
+      ids[o] = t;
+      pos[o] = t + a.pos0;
+      if (out) out[o] = tokens[t];
+    }
+    if (tid == 0) a.n_kept[b] = n_tok;
+    SEL_STAMP(5);
+    return;
+  }
   if (n_c > 4 * NT && !by_rank) {
     // many chunks (token-level selection of long prompts): every warp owns a
     // contiguous range of chunks and walks it in coalesced 32-chunk tiles
@@ -417,8 +546,8 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
     const unsigned lt = (1u << lane) - 1u;
     auto flags_of = [&](long long c, unsigned key, bool* eq, bool* gt) {
       const bool in = c < w1 && (V != kMerge || key != kInvalid);
-      *eq = in && key == T;
-      *gt = in && key > T;
+      *eq = in && (key & pmask) == T;
+      *gt = in && (key & pmask) > T;
     };
     constexpr int TU = 4;                                    // tiles whose keys are loaded together
     auto load4 = [&](long long c0, unsigned (&k4)[TU]) {
@@ -514,12 +643,12 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
     const long long c = base + tid;
     const unsigned key = c < n_c ? __float_as_uint(cs[c]) : 0u;
     const bool in = c < n_c && (V != kMerge || key != kInvalid);
-    const int eq = (in && key == T) ? 1 : 0;
-    const int gt = (in && key > T) ? 1 : 0;
+    const int eq = (in && (key & pmask) == T) ? 1 : 0;
+    const int gt = (in && (key & pmask) > T) ? 1 : 0;
     int tot;
     const int eq_rank = block_excl_scan<NT>(eq, sh.scan, &tot) + carry_eq;
     carry_eq += tot;
-    const int keep = by_rank ? rank_keep : (gt | (eq & (eq_rank < need_eq ? 1 : 0)));
+    const int keep = gt | (eq & (eq_rank < need_eq ? 1 : 0));
     const int slot = block_excl_scan<NT>(keep, sh.scan, &tot);          // index among kept chunks of this tile
     const int nk = tot;
     if (V == kCand) {

@@ -620,6 +620,41 @@ sp_status sp_gather(const int32_t* tokens, const int32_t* ids, const int32_t* n_
   return from_cuda(gather_launch(tokens, ids, n_kept, B, N, out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+}  // extern "C"
+
+namespace {
+// The whole device path (validated arguments; ws = score workspace, then the
+// selection's): when the fused kernel can stage them, the selection's phase A
+// (pooling + chunk means) runs in the score kernel's epilogue and the selection
+// launch -- a programmatic dependent -- does phases B-C only; otherwise the
+// score, then the full selection (+ gather).  Same bits either way.
+sp_status score_select_dev(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay,
+                           const sp_select_params* p, const int32_t* tokens, float* importance, int32_t* ids,
+                           int32_t* pos, int32_t* n_kept, int32_t* out_tokens, void* ws, size_t ws_bytes,
+                           sp_stream stream) {
+  const Geom G = to_geom(*g);
+  const Layout Lay = to_layout(*lay);
+  const size_t sb = align256(score_ws(G, SP_SCORE_AUTO));
+  void* sws = reinterpret_cast<char*>(ws) + sb;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (resolve_algo(G, SP_SCORE_AUTO) == SP_SCORE_FUSED && fused_supported(G, Lay, Q, K)) {
+    const ChunkOut co{select_ws_scores(sws, g->B), p->pool_k, p->chunk};
+    const cudaError_t e = fused_score_chunks(reinterpret_cast<const __nv_bfloat16*>(Q),
+                                             reinterpret_cast<const __nv_bfloat16*>(K), G, Lay, importance, co, ws, sb,
+                                             st);
+    if (e == cudaSuccess)
+      return from_cuda(select_ready_launch(g->B, g->N, p->chunk, keep_ppm(p->keep_rate), p->pos0, ids, pos, n_kept,
+                                           sws, st, tokens, out_tokens));
+    if (e != cudaErrorNotSupported) return from_cuda(e);
+  }
+  sp_status s = sp_score(Q, K, g, lay, importance, ws, sb, stream);
+  if (s != SP_OK) return s;
+  return sp_select_gather(importance, tokens, g->B, g->N, p, ids, pos, n_kept, out_tokens, sws, ws_bytes - sb, stream);
+}
+}  // namespace
+
+extern "C" {
+
 size_t sp_score_select_workspace_bytes(const sp_geom* g, const sp_select_params* p) {
   if (check_geom(g) != SP_OK || check_select(g->B, g->N, p) != SP_OK) return 0;
   return align256(score_ws(to_geom(*g), SP_SCORE_AUTO)) + select_ws_bytes(g->B, g->N, p->chunk);
@@ -638,11 +673,27 @@ sp_status sp_score_select(const void* Q, const void* K, const sp_geom* g, const 
   if ((s = check_device()) != SP_OK) return s;
   if (ws == nullptr || ws_bytes < sp_score_select_workspace_bytes(g, p) || (reinterpret_cast<uintptr_t>(ws) & 255u) != 0)
     return SP_EWORKSPACE;
-  // the score, then the selection (+ gather) as its programmatic dependent
-  const size_t sb = align256(score_ws(to_geom(*g), SP_SCORE_AUTO));
-  if ((s = sp_score(Q, K, g, lay, importance, ws, sb, stream)) != SP_OK) return s;
-  return sp_select_gather(importance, tokens, g->B, g->N, p, ids, pos, n_kept, out_tokens,
-                          reinterpret_cast<char*>(ws) + sb, ws_bytes - sb, stream);
+  return score_select_dev(Q, K, g, lay, p, tokens, importance, ids, pos, n_kept, out_tokens, ws, ws_bytes, stream);
+}
+
+sp_status sp_score_chunks(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay, int32_t pool_k,
+                          int32_t chunk, float* importance, float* cs, void* ws, size_t ws_bytes, sp_stream stream) {
+  sp_status s = check_geom(g);
+  if (s != SP_OK) return s;
+  if ((s = check_layout(g, lay, Q, K)) != SP_OK) return s;
+  if (importance == nullptr || cs == nullptr || pool_k < 1 || pool_k % 2 == 0 || chunk < 1) return SP_EINVAL;
+  if (!select_supported(pool_k) || chunk > 16384) return SP_EUNSUPPORTED;
+  if ((s = check_device()) != SP_OK) return s;
+  const Geom G = to_geom(*g);
+  const Layout Lay = to_layout(*lay);
+  if (!fused_supported(G, Lay, Q, K)) return SP_EUNSUPPORTED;
+  const size_t need = score_ws(G, SP_SCORE_FUSED);
+  if (ws == nullptr || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return SP_EWORKSPACE;
+  const ChunkOut co{cs, pool_k, chunk};
+  const cudaError_t e = fused_score_chunks(reinterpret_cast<const __nv_bfloat16*>(Q),
+                                           reinterpret_cast<const __nv_bfloat16*>(K), G, Lay, importance, co, ws,
+                                           ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaErrorNotSupported ? SP_EUNSUPPORTED : from_cuda(e);
 }
 
 size_t sp_run_workspace_bytes(const sp_geom* g, const sp_select_params* p) {
@@ -662,6 +713,13 @@ sp_status sp_run_host(const sp_host_io* host, const sp_device_bufs* dev, const s
   if (s != SP_OK) return s;
   if ((s = check_layout(g, lay, dev->Q, dev->K)) != SP_OK) return s;
   if ((s = check_select(g->B, g->N, p)) != SP_OK) return s;
+  if (dev->ws == nullptr || dev->ws_bytes < sp_run_workspace_bytes(g, p) ||
+      (reinterpret_cast<uintptr_t>(dev->ws) & 255u) != 0)
+    return SP_EWORKSPACE;
+  if (dev->importance == nullptr || dev->ids == nullptr || dev->pos == nullptr || dev->n_kept == nullptr ||
+      dev->tokens == nullptr || dev->out_tokens == nullptr)
+    return SP_EINVAL;
+  if ((s = check_device()) != SP_OK) return s;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const size_t tok_bytes = (size_t)g->B * g->N * sizeof(int32_t);
   if (cudaMemcpyAsync(dev->Q, host->Q, host->q_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
@@ -670,12 +728,8 @@ sp_status sp_run_host(const sp_host_io* host, const sp_device_bufs* dev, const s
     cudaGetLastError();
     return SP_ECUDA;
   }
-  if ((s = sp_score(dev->Q, dev->K, g, lay, dev->importance, dev->ws, dev->ws_bytes, stream)) != SP_OK) return s;
-  const size_t score_bytes = align256(score_ws(to_geom(*g), SP_SCORE_AUTO));
-  if (dev->ws_bytes < score_bytes) return SP_EWORKSPACE;
-  if ((s = sp_select_gather(dev->importance, dev->tokens, g->B, g->N, p, dev->ids, dev->pos, dev->n_kept,
-                            dev->out_tokens, reinterpret_cast<char*>(dev->ws) + score_bytes,
-                            dev->ws_bytes - score_bytes, stream)) != SP_OK)
+  if ((s = score_select_dev(dev->Q, dev->K, g, lay, p, dev->tokens, dev->importance, dev->ids, dev->pos, dev->n_kept,
+                            dev->out_tokens, dev->ws, dev->ws_bytes, stream)) != SP_OK)
     return s;
   if (cudaMemcpyAsync(host->n_kept, dev->n_kept, (size_t)g->B * sizeof(int32_t), cudaMemcpyDeviceToHost, st) !=
           cudaSuccess ||

@@ -62,6 +62,13 @@ struct LookaheadK {
   int shift;
 };
 
+// Selection phase A run by the score kernel's epilogue (sp_score_select): the
+// chunk scores go to cs ([B][ceil(N / chunk)], the selection workspace's).
+struct ChunkOut {
+  float* cs;
+  int pool_k, chunk;
+};
+
 // Round up to a multiple of 256 bytes (workspace carving).
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -87,6 +94,10 @@ bool fused_plan_info(const Geom& g, long long out[kPlanInfo]);
 void fused_set_trace(unsigned long long* buf, long long records);
 cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                         float* importance, void* ws, size_t ws_bytes, cudaStream_t st);
+// the importance plus the selection's chunk scores (cudaErrorNotSupported: this
+// geometry / plan cannot stage them; the caller runs the plain score + selection)
+cudaError_t fused_score_chunks(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                               float* importance, const ChunkOut& co, void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t fused_score_stats(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                               float* stats, void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t fused_score_finish(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
@@ -117,6 +128,10 @@ bool select_supported(int pool_k);
 cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int chunk, int pos0,
                           long long ppm, int* ids, int* pos, int* n_kept, void* ws, cudaStream_t st,
                           const int* tokens = nullptr, int* out = nullptr, const int* seq_lens = nullptr);
+// phases B-C over chunk scores already in the workspace (sp_score_select)
+cudaError_t select_ready_launch(int B, long long N, int chunk, long long ppm, int pos0, int* ids, int* pos,
+                                int* n_kept, void* ws, cudaStream_t st, const int* tokens, int* out);
+float* select_ws_scores(void* ws, int B);
 // sequence-sharded selection (row e)
 long long seq_candidate_count(long long N, int world, int chunk, long long ppm);
 size_t seq_select_ws_bytes(int B, long long N, int world, int chunk);

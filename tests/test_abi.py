@@ -238,3 +238,19 @@ def test_lookahead_and_ragged_validation():
     r = sp.lib().sp_select_ragged
     assert r(FAKE, None, None, 2, 100, C.byref(p), FAKE, FAKE, FAKE, None, FAKE, 1 << 20, None) == _lib.SP_EINVAL
     assert r(FAKE, FAKE, FAKE, 2, 100, C.byref(p), FAKE, FAKE, FAKE, None, FAKE, 1 << 20, None) == _lib.SP_EINVAL
+
+
+@pytest.mark.parametrize("pool,chunk,cs,code", [
+    (4, 32, FAKE, _lib.SP_EINVAL),          # even pool window
+    (0, 32, FAKE, _lib.SP_EINVAL),
+    (5, 0, FAKE, _lib.SP_EINVAL),           # empty chunk
+    (5, 32, None, _lib.SP_EINVAL),          # no chunk-score output
+    (4099, 32, FAKE, _lib.SP_EUNSUPPORTED),  # pool window above the staged halo
+    (5, 16385, FAKE, _lib.SP_EUNSUPPORTED),  # chunk longer than a selection segment
+])
+def test_score_chunks_validation(pool, chunk, cs, code):
+    """sp_score_chunks rejects bad selection parameters on the host (no device use)."""
+    g = _geom()
+    lay = _layout(g)
+    rc = sp.lib().sp_score_chunks(FAKE, FAKE, C.byref(g), C.byref(lay), pool, chunk, FAKE, cs, FAKE, 1 << 20, None)
+    assert rc == code
