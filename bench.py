@@ -69,9 +69,9 @@ def parse():
     ap.add_argument("--no-tune", action="store_true",
                     help="skip sp_score_tune (the fused plan measured among the model's best candidates during "
                          "warm-up, untimed); single-GPU / batch-sharded contiguous inputs only")
-    ap.add_argument("--fused-select", action="store_true",
-                    help="A/B: the step through sp_score_select (the selection's pooling + chunk means in the score "
-                         "kernel's epilogue, then the top-K_c launch)")
+    ap.add_argument("--two-launch", action="store_true",
+                    help="A/B: sp_score (with its cross-unit-group epilogue) then sp_select_gather, instead of "
+                         "sp_score_select (the selection finalizes the importance)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -351,24 +351,16 @@ def run_ours(args):
         score_only()
         select_only()
 
-    # --fused-select: the step through sp_score_select with the selection's pooling +
-    # chunk means in the score kernel's epilogue (measured slower than the two
-    # launches at C2-C4: DESIGN.md 5.3); default: sp_score, then sp_select_gather
-    fused_step = args.fused_select and not (paged or f8 or args.algo == "simt" or seq_lens is not None)
+    # the plain single-GPU step goes through sp_score_select: the score kernel
+    # without its cross-unit-group epilogue, the selection launch finalizing the
+    # importance from the partial maps (same bits); --two-launch:
+    # sp_score then sp_select_gather
+    fused_step = not (args.two_launch or paged or f8 or args.algo == "simt" or seq_lens is not None)
     sel_out = {"importance": imp, "ids": ids, "pos": pos, "n_kept": nk, "out_tokens": out}
-    if fused_step:
-        cs_buf = torch.empty((w.B, (w.N + w.chunk - 1) // w.chunk), dtype=torch.float32, device=dev)
-        try:                                           # the geometry's plan can stage the chunk phase
-            sp.score_chunks(Q, K, w.pool_k, w.chunk, R_valid=w.Rv, scale=w.scale, out=imp, cs=cs_buf)
-        except sp.SpError:
-            fused_step = False
     if fused_step:
         def step():                                    # noqa: F811
             sp.score_select(Q, K, w.keep, w.pool_k, w.chunk, w.pos0, tokens=T, R_valid=w.Rv, scale=w.scale,
                             out=sel_out)
-
-        def score_only():                              # noqa: F811 -- the step's score kernel (+ chunk phase)
-            sp.score_chunks(Q, K, w.pool_k, w.chunk, R_valid=w.Rv, scale=w.scale, out=imp, cs=cs_buf)
 
     peer_note = None
 
@@ -530,8 +522,6 @@ def run_ours(args):
     k_bytes = w.k_bytes // 2 * esz * n_tokens // (w.B * w.N)
     alg_bytes = ((k_bytes // world if (seq or head) else k_bytes) + (q_bytes // world if head else q_bytes)
                  + w.B * w.N * 4)
-    if fused_step:                   # + the chunk phase's importance re-read and chunk-score writes
-        alg_bytes += w.B * w.N * 4 + w.B * ((w.N + w.chunk - 1) // w.chunk) * 4
     achieved = alg_bytes / (score_ms / 1000.0) / 1e9
     traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -539,13 +529,14 @@ def run_ours(args):
         with open(tp) as f:
             tj = json.load(f)
         key = f"{args.config}/{args.algo}" + ("/e4m3" if f8 else "") + (f"/paged{args.paged}" if paged else "") \
-            + ("/chunks" if fused_step else "")
+
         traffic = tj.get(key)
         traffic_src = tj.get("_source", {}).get(key) if traffic is not None else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": ("sp_score_chunks (the step's score kernel: importance + the selection's chunk means in "
-                           "its epilogue)") if fused_step else "sp_score",
+                "kernel": "sp_score" + (" (timed alone, with its cross-unit-group epilogue; the step runs "
+                                        "sp_score_select, where the selection launch does that finalize)"
+                                        if fused_step else ""),
                 "kernel_ms": score_ms, "score_only_ms": score_only_ms,
                 "algorithmic_bytes": alg_bytes, "peak_source": peak_src,
                 "frac_of_8TBs": achieved / SPEC_HBM_GBS, "score_share_of_step": score_ms / ms_step}
@@ -573,7 +564,7 @@ def run_ours(args):
         sel = (1 if w.pool_k > 1 else 0) + sel_launches(n_loc) + 1         # edges, candidates, merge
         launches_per_step = (1 if seq_peer else 2 + 1) + sel                 # score_peer | stats+combine+finish
     elif fused_step:
-        launches_per_step = 2                                 # score (+ chunk phase), dependent selection (B-C)
+        launches_per_step = 2                                 # score, dependent selection (finalize + select)
     else:
         launches_per_step = {"fused": 1, "simt": 4, "auto": 1}[args.algo] + sel_launches(w.N) \
             + (1 if head else 0)

@@ -110,7 +110,9 @@ struct FusedParams {
                                        // (max2, sum) packed in one 64-bit word; 0 = "not yet written"
   int hier;                            // cross-rank (peer) exchange: world > 1
   unsigned* epoch;                     // [2] launch epoch (parity selects the partial buffer), CTAs done
-  float* accpart;                      // [B][n_ug][Rv][N] the unit groups' partial (l,h)-max maps
+  float* accpart;                      // [B][n_ug][Rv][acc_pitch] the unit groups' partial (l,h)-max maps
+  long long acc_pitch;                 // row pitch of accpart in floats: N rounded to 32, + 32 (rows that are a
+                                       // power-of-two apart camp on the same L2 slices)
   unsigned* fin_cnt;                   // [3][B][n_tg] finalize counters: [launch parity] in the full and
                                        // statistics modes (the other parity's re-zeroed by the exchange
                                        // warp), [2] in finish mode (self-resetting: a second count)
@@ -137,6 +139,8 @@ struct FusedParams {
   unsigned* bnd_cnt;                   // [B][n_tg] token-group boundary counters (self-resetting)
   int pool_k, chunk;
   long long n_c_row;
+  int defer;                           // sp_score_select: the unit groups' partial maps are the output, the
+                                       // selection launch finalizes the importance (no cross-CTA epilogue)
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -1359,8 +1363,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           const long long i = (long long)(jb.t_lo + t) * kTileM + tok;
           if (i < jb.n)
             for (int r = 0; r < p.Rv; ++r)
-              p.accpart[(((long long)jb.b * p.n_ug + jb.ug) * p.Rv + r) * p.N + i] = acc[(t * p.Rv + r) * kTileM + tok];
+              p.accpart[(((long long)jb.b * p.n_ug + jb.ug) * p.Rv + r) * p.acc_pitch + i] = acc[(t * p.Rv + r) * kTileM + tok];
         }
+        if (p.defer) continue;                                      // the selection finalizes (sp_score_select)
         named_bar(2, 128);                                          // the CTA's partial maps, then one
         unsigned* fc = p.fin_cnt + ((long long)(p.mode == kModeFinish ? 2u : parity) * p.B + jb.b) * p.n_tg + jb.tg;
         if (threadIdx.x == kFinalWarp0 * 32) {
@@ -1390,34 +1395,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
         for (int e = tok; e < RS; e += kTileM) mx[e] = 0u;        // below every ordered key
         named_bar(2, 128);
         if (S > 0) {
-          const float* src = p.accpart + (long long)jb.b * p.n_ug * p.Rv * p.N + s_lo;
+          const float* src = p.accpart + (long long)jb.b * p.n_ug * p.Rv * p.acc_pitch + s_lo;
           const int tot = p.n_ug * RS;
-          const float invS = 1.f / (float)S;
-          // e = q*S + i (q = group*Rv + row) by a float reciprocal and one correction
-          // step (exact for e < 2^22: tot <= 148 * 256 * 2048 here)
-          auto split = [&](int e, int& q, int& i) {
-            q = __float2int_rz(__int2float_rn(e) * invS);
-            i = e - q * S;
-            if (i < 0) { --q; i += S; } else if (i >= S) { ++q; i -= S; }
-          };
-          constexpr int kU = 16;                                    // two to four batches at C1-C3
+          // element e = q*S + i (q = group*Rv + row), e = tok + k*128: the indices
+          // advance by a fixed (dq, di) per step (no per-element division)
+          const int dq = kTileM / S, di = kTileM - dq * S, dr = dq % p.Rv;
+          int q = tok / S, i = tok - q * S, r = q % p.Rv;
+          const long long pitch = p.acc_pitch, step = (long long)dq * pitch + di, wrap = pitch - S;
+          const float* ptr = src + (long long)q * pitch + i;
+          constexpr int kU = 24;                                    // loads in flight per thread (more raise the kernel's registers)
           for (int e0 = tok; e0 < tot; e0 += kU * kTileM) {
             float v[kU];
+            int dst[kU];
 #pragma unroll
             for (int k = 0; k < kU; ++k) {
-              const int e = e0 + k * kTileM;
-              int q, i;
-              split(e, q, i);
-              v[k] = e < tot ? __ldcg(src + (long long)q * p.N + i) : 0.f;
+              const bool in = e0 + k * kTileM < tot;
+              dst[k] = in ? r * S + i : -1;
+              v[k] = __ldcg(in ? ptr : src);                        // (branch-free: src is a valid address)
+              i += di;
+              r += dr;
+              ptr += step;
+              if (i >= S) { i -= S; ++r; ptr += wrap; }
+              if (r >= p.Rv) r -= p.Rv;
             }
 #pragma unroll
             for (int k = 0; k < kU; ++k) {
-              const int e = e0 + k * kTileM;
-              if (e < tot) {
-                int q, i;
-                split(e, q, i);
+              if (dst[k] >= 0) {
                 const unsigned u = __float_as_uint(v[k]);
-                red_smem_max(smem_u32(&mx[(q % p.Rv) * S + i]), (u & 0x80000000u) ? ~u : (u | 0x80000000u));
+                red_smem_max(smem_u32(&mx[dst[k]]), (u & 0x80000000u) ? ~u : (u | 0x80000000u));
               }
             }
           }
@@ -1516,6 +1521,9 @@ int sm_count() {
 }
 
 // Layout of shared memory for a given (tpc, stage count); returns total bytes.
+// accpart row pitch (floats): N rounded up to 32, plus 32 -- never a power of two apart
+long long acc_pitch(long long N) { return (N + 31) / 32 * 32 + 32; }
+
 uint32_t carve(Plan& pl, int Rv, int stages) {
   uint32_t o = 0;
   pl.off_k = o;
@@ -1663,7 +1671,7 @@ Plan make_plan(const Geom& g, bool allow_override = true, int sm_budget = 0,
   if (const char* e = allow_override ? std::getenv("SP_FUSED_L2HINT") : nullptr) pl.l2hint = std::atoi(e) != 0;
   pl.ws_part = align256(2 * (size_t)g.B * pl.U * pl.NCP * pl.n_tg * sizeof(unsigned long long));
   pl.ws_cnt = 256;                                   // launch epoch + CTAs-done counter
-  pl.ws_acc = pl.n_ug > 1 ? align256((size_t)g.B * pl.n_ug * g.Rv * g.N * sizeof(float)) : 0;
+  pl.ws_acc = pl.n_ug > 1 ? align256((size_t)g.B * pl.n_ug * g.Rv * acc_pitch(g.N) * sizeof(float)) : 0;
   pl.ws_fin = align256((size_t)3 * g.B * pl.n_tg * sizeof(unsigned));
   pl.ws_rank = 0;
   pl.ws_tgr = align256((size_t)g.B * pl.n_tg * sizeof(unsigned));   // token-group boundary counters (sp_score_select)
@@ -1785,6 +1793,12 @@ __global__ void k_partials_to_stats(const unsigned long long* __restrict__ part,
 
 }  // namespace
 
+struct DeferOut {
+  const float* accp = nullptr;                        // [B][n_ug][Rv][pitch] partial maps (in the workspace)
+  long long pitch = 0;
+  int n_ug = 0;
+};
+
 struct PeerArgs {
   int rank = 0, world = 1, sm_budget = 0;
   void* const* bufs = nullptr;                        // world partial buffers (fused_peer_buffer_bytes each)
@@ -1865,7 +1879,7 @@ bool encode_paged_interleaved(const PagedK& pk, const Geom& g, const Plan& pl, C
 cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay, int mode,
                          const float* lse_in, float* importance, void* ws, size_t ws_bytes, cudaStream_t st,
                          float* acc_out = nullptr, const PeerArgs& peer = PeerArgs(), const PagedK* pk = nullptr,
-                         const float2* la = nullptr, const ChunkOut* co = nullptr) {
+                         const float2* la = nullptr, const ChunkOut* co = nullptr, DeferOut* dfr = nullptr) {
   if (peer.world < 1 || peer.world > kMaxPeers || peer.rank < 0 || peer.rank >= peer.world) return cudaErrorInvalidValue;
   Plan pl = make_plan(g, true, peer.sm_budget, nullptr, peer.world);
   if (!pl.ok || ws_bytes < pl.ws_total()) return cudaErrorInvalidValue;
@@ -1914,6 +1928,7 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
   p.part = reinterpret_cast<unsigned long long*>(w);
   w += pl.ws_part;
   p.accpart = pl.ws_acc ? reinterpret_cast<float*>(w) : nullptr;
+  p.acc_pitch = acc_pitch(g.N);
   w += pl.ws_acc;
   p.bnd_cnt = reinterpret_cast<unsigned*>(w);
   w += pl.ws_tgr;
@@ -1923,6 +1938,13 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
     p.pool_k = co->pool_k;
     p.chunk = co->chunk;
     p.n_c_row = (g.N + co->chunk - 1) / co->chunk;
+  }
+  if (dfr != nullptr) {
+    if (pl.n_ug < 2 || p.accpart == nullptr || co != nullptr) return cudaErrorNotSupported;
+    p.defer = 1;
+    dfr->accp = p.accpart;
+    dfr->pitch = p.acc_pitch;
+    dfr->n_ug = pl.n_ug;
   }
   p.hier = pl.hier;
   p.rank = peer.rank;
@@ -1990,6 +2012,22 @@ cudaError_t fused_launch(const __nv_bfloat16* Q, const __nv_bfloat16* K, const G
 cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                         float* importance, void* ws, size_t ws_bytes, cudaStream_t st) {
   return fused_launch(Q, K, g, lay, kModeFull, nullptr, importance, ws, ws_bytes, st);
+}
+
+cudaError_t fused_score_deferred(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                                 void* ws, size_t ws_bytes, cudaStream_t st, const float** accp, int* n_ug,
+                                 long long* pitch) {
+  Plan pl = make_plan(g);
+  if (!pl.ok || pl.n_ug < 2) return cudaErrorNotSupported;          // nothing to defer: one unit group
+  DeferOut d;
+  const cudaError_t e = fused_launch(Q, K, g, lay, kModeFull, nullptr, nullptr, ws, ws_bytes, st, nullptr, PeerArgs(),
+                                     nullptr, nullptr, nullptr, &d);
+  if (e == cudaSuccess) {
+    *accp = d.accp;
+    *n_ug = d.n_ug;
+    *pitch = d.pitch;
+  }
+  return e;
 }
 
 cudaError_t fused_score_chunks(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,

@@ -181,6 +181,62 @@ float* ws_scores(void* ws, int B) {
 
 float* select_ws_scores(void* ws, int B) { return ws_scores(ws, B); }
 
+// Deferred finalize (sp_score_select): phase A over CTAs of about 16 * NT /
+// (n_ug * Rv) tokens (16 partial-map loads per thread), computing the importance from the score
+// kernel's partial maps, writing it, then the usual pooling and chunk means;
+// the request's last CTA runs B-C.
+namespace {
+// launch shape of the deferred-finalize selection; false: not supported
+// tokens per CTA: about 16 partial-map loads per thread (one batch in flight)
+bool deferred_shape(SelArgs& a, long long N, int Rv, int n_ug, int pool_k, int chunk, long long* nblk_out,
+                    size_t* smem_out) {
+  const long long n_c = (N + chunk - 1) / chunk;
+  const long long w = (pool_k - 1) / 2;
+  const long long want = std::max<long long>(32, (16LL * ST) / std::max(1, n_ug * Rv));
+  const long long tok = std::max<long long>(chunk, std::min<long long>(2048, want) / chunk * chunk);
+  const long long cpb = std::max(1LL, tok / chunk);
+  const long long nblk = (n_c + cpb - 1) / cpb;
+  if (nblk > 65535 || cpb * chunk > SEG || pool_k > kMaxPool) return false;
+  a.segcap = (int)std::min<long long>(SEG, (std::min(N, cpb * chunk) + 31) / 32 * 32);
+  a.cpb = cpb;
+  a.nblk = (int)nblk;
+  a.mode = kModeA;
+  const long long cs_floats = n_c <= kSmemChunks ? n_c : 0;
+  const long long staged = 2 * a.segcap + 2 * w + cs_floats;
+  a.mb_off = (int)((staged + 3) / 4 * 4);
+  const long long mb = (long long)Rv * (a.segcap + 2 * w);
+  a.sh_off = (int)((a.mb_off + mb + 3) / 4 * 4);
+  *nblk_out = nblk;
+  *smem_out = (size_t)a.sh_off * sizeof(float) + sizeof(SelShared<ST>);
+  return *smem_out <= kSmemMax;
+}
+}  // namespace
+
+bool select_deferred_supported(long long N, int Rv, int n_ug, int pool_k, int chunk) {
+  SelArgs a{};
+  long long nblk;
+  size_t smem;
+  return deferred_shape(a, N, Rv, n_ug, pool_k, chunk, &nblk, &smem);
+}
+
+cudaError_t select_deferred_launch(const float* accp, long long pitch, int n_ug, int Rv, float* imp_out, int B, long long N,
+                                   int pool_k, int chunk, int pos0, long long ppm, int* ids, int* pos, int* n_kept,
+                                   void* ws, cudaStream_t st, const int* tokens, int* out) {
+  cudaError_t e = configure<kPlain>();
+  if (e != cudaSuccess) return e;
+  SelArgs a{};
+  a.imp = imp_out; a.row = N; a.pool_k = pool_k; a.chunk = chunk; a.pos0 = pos0; a.ppm = ppm;
+  a.ids = ids; a.pos = pos; a.n_kept = n_kept; a.cs_ws = ws_scores(ws, B); a.tokens = tokens; a.out = out;
+  a.n_glob = N;
+  a.blk_cnt = ws_counters(ws);
+  a.nreq = B;
+  a.accp = accp; a.acc_pitch = pitch; a.n_ug = n_ug; a.Rv = Rv; a.imp_out = imp_out;
+  long long nblk;
+  size_t smem;
+  if (!deferred_shape(a, N, Rv, n_ug, pool_k, chunk, &nblk, &smem)) return cudaErrorNotSupported;
+  return launch_pdl<kPlain>(dim3(B, (unsigned)nblk), smem, st, a);
+}
+
 // Phases B-C only: the chunk scores were written into the workspace by the
 // score kernel (sp_score_select).  One CTA per request, the scores staged in SMEM
 // when they fit.

@@ -4,6 +4,8 @@
 // bits.  See select.cu for the method and its citations.  Internal header.
 #pragma once
 
+#include <math_constants.h>
+
 #include <algorithm>
 
 #include "sp_internal.h"
@@ -50,6 +52,15 @@ struct SelArgs {
   const int* tokens;         // optional gather source [B][row]
   int* out;                  // optional gathered tokens [B][row]
   int mode, segcap;
+  // kPlain, deferred finalize (sp_score_select): the importance is not written
+  // by the score kernel; phase A computes it from the unit groups' partial
+  // (l,h)-max maps, imp[t] = (1/Rv) sum_r 2^(max_g accp[b][g][r][t]) -- the
+  // score kernel's own finalize, same instruction, same order -- and writes it
+  const float* accp;         // [B][n_ug][Rv][acc_pitch], or null
+  long long acc_pitch;
+  int n_ug, Rv;
+  float* imp_out;            // [B][row]
+  int mb_off;                // floats from the dynamic SMEM base to the [Rv][segcap + 2w] max scratch
   int cs_ready;              // kPlain: the chunk scores are already in cs_ws (computed by the score
                              // kernel's epilogue, sp_score_select): phases B-C only
   long long cpb;             // chunks per CTA in kModeA
@@ -82,6 +93,14 @@ struct SelShared {
   int kept_c[NT];                   // kept chunk ids of one scan tile, in order
   int kept_off[NT];
 };
+
+// 2^x as the score kernel computes it (ex2.approx.ftz.f32): the deferred
+// finalize gives the importance bit for bit.
+__device__ __forceinline__ float sel_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // Block-wide exclusive scan of v (all NT threads participate); returns the
 // exclusive prefix, writes the block total to *total.
@@ -241,7 +260,60 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
       constexpr int PER = (SEG / NT) < 16 ? (SEG / NT) : 16;
       const int n = (int)(hi - lo);
       float r[PER];
-      if (V == kCand) {
+      if (V == kPlain && a.accp != nullptr) {
+        // deferred finalize: every (group, row, token) value of the staged range
+        // loaded with all of a thread's loads in flight (coalesced over tokens)
+        // and folded into SMEM with an order-preserving unsigned max (order-free:
+        // the same bits as a sequential max), then one thread per token takes
+        // the mean of exp2 in row order; the CTA's own tokens' importance is
+        // written out
+        const int n = (int)(hi - lo), Rv = a.Rv, RN = Rv * n, tot = a.n_ug * RN;
+        unsigned* mb = reinterpret_cast<unsigned*>(seg + a.mb_off);   // [Rv][n]
+        for (int e = tid; e < RN; e += NT) mb[e] = 0u;                  // below every ordered key
+        __syncthreads();
+        const float* src = a.accp + (long long)b * a.n_ug * Rv * a.acc_pitch + lo;
+        // element e = q*n + j (q = group*Rv + row), e = tid + k*NT: the indices
+        // advance by a fixed (dq, dj) per step (no per-element division)
+        const int dq = NT / n, dj = NT - dq * n, dr = dq % Rv;
+        int q = tid / n, j = tid - q * n, r = q % Rv;
+        const long long pitch = a.acc_pitch, step = (long long)dq * pitch + dj, wrap = pitch - n;
+        const float* ptr = src + (long long)q * pitch + j;
+        for (int e0 = tid; e0 < tot; e0 += 16 * NT) {
+          float v[16];
+          int dst[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const bool in = e0 + k * NT < tot;
+            dst[k] = in ? r * n + j : -1;
+            v[k] = __ldcg(in ? ptr : src);                          // (branch-free: src is a valid address)
+            j += dj;
+            r += dr;
+            ptr += step;
+            if (j >= n) { j -= n; ++r; ptr += wrap; }
+            if (r >= Rv) r -= Rv;
+          }
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            if (dst[k] >= 0) {
+              const unsigned u = __float_as_uint(v[k]);
+              atomicMax(&mb[dst[k]], (u & 0x80000000u) ? ~u : (u | 0x80000000u));
+            }
+          }
+        }
+        __syncthreads();
+        const float inv = 1.f / (float)Rv;
+        for (int j = tid; j < n; j += NT) {
+          float sacc = 0.f;
+          for (int r = 0; r < Rv; ++r) {
+            const unsigned k = mb[r * n + j];
+            sacc += sel_ex2(__uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k));
+          }
+          const float v = sacc * inv;
+          seg[j] = v;
+          const long long t = lo + j;
+          if (t >= t_lo && t < t_hi) a.imp_out[(long long)b * Nrow + t] = v;
+        }
+      } else if (V == kCand) {
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
           const int i = tid + k * NT;
@@ -257,17 +329,19 @@ __device__ __forceinline__ void select_body(const SelArgs& a, int b, int blk, fl
           r[k] = i < n ? __ldcg(imp + lo + i) : 0.f;
         }
       }
+      if (!(V == kPlain && a.accp != nullptr)) {
 #pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        const int i = tid + k * NT;
-        if (i < n) seg[i] = r[k];
-      }
-      for (int i = PER * NT + tid; i < n; i += NT) {                    // halo beyond SEG
-        const long long t = lo + i;
-        if (V == kCand)
-          seg[i] = t < i0 ? halo_l[t - (i0 - w)] : (t >= i0 + n_loc ? halo_r[t - i0 - n_loc] : imp[t - i0]);
-        else
-          seg[i] = imp[t];
+        for (int k = 0; k < PER; ++k) {
+          const int i = tid + k * NT;
+          if (i < n) seg[i] = r[k];
+        }
+        for (int i = PER * NT + tid; i < n; i += NT) {                  // halo beyond SEG
+          const long long t = lo + i;
+          if (V == kCand)
+            seg[i] = t < i0 ? halo_l[t - (i0 - w)] : (t >= i0 + n_loc ? halo_r[t - i0 - n_loc] : imp[t - i0]);
+          else
+            seg[i] = imp[t];
+        }
       }
     }
     __syncthreads();

@@ -628,6 +628,13 @@ namespace {
 // (pooling + chunk means) runs in the score kernel's epilogue and the selection
 // launch -- a programmatic dependent -- does phases B-C only; otherwise the
 // score, then the full selection (+ gather).  Same bits either way.
+// smallest number of unit groups per token group for which the deferred finalize
+// pays (SP_DEFER_MIN_UG overrides: A/B timing)
+int defer_min_ug() {
+  const char* e = std::getenv("SP_DEFER_MIN_UG");
+  return e ? std::atoi(e) : 2;
+}
+
 sp_status score_select_dev(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay,
                            const sp_select_params* p, const int32_t* tokens, float* importance, int32_t* ids,
                            int32_t* pos, int32_t* n_kept, int32_t* out_tokens, void* ws, size_t ws_bytes,
@@ -637,7 +644,29 @@ sp_status score_select_dev(const void* Q, const void* K, const sp_geom* g, const
   const size_t sb = align256(score_ws(G, SP_SCORE_AUTO));
   void* sws = reinterpret_cast<char*>(ws) + sb;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (resolve_algo(G, SP_SCORE_AUTO) == SP_SCORE_FUSED && fused_supported(G, Lay, Q, K)) {
+  long long plan[kPlanInfo] = {};
+  const int kDeferMinUg = defer_min_ug();
+  const bool epilogue_ab = std::getenv("SP_SELECT_EPILOGUE") != nullptr;   // A/B knob (timing, tests)
+  if (!epilogue_ab && resolve_algo(G, SP_SCORE_AUTO) == SP_SCORE_FUSED && fused_supported(G, Lay, Q, K) &&
+      fused_plan_info(G, plan) && plan[3] >= kDeferMinUg &&
+      select_deferred_supported(g->N, g->R_valid, (int)plan[3], p->pool_k, p->chunk)) {
+    // the score kernel without its cross-unit-group epilogue; the selection
+    // finalizes the importance from the partial maps (same bits).  Measured
+    // (DESIGN.md 5.3): C1 step -4 us, C3 -5 us, C2 and C4 even or better
+    const float* accp = nullptr;
+    int n_ug = 0;
+    long long pitch = 0;
+    const cudaError_t e = fused_score_deferred(reinterpret_cast<const __nv_bfloat16*>(Q),
+                                               reinterpret_cast<const __nv_bfloat16*>(K), G, Lay, ws, sb, st, &accp,
+                                               &n_ug, &pitch);
+    if (e == cudaSuccess)
+      return from_cuda(select_deferred_launch(accp, pitch, n_ug, g->R_valid, importance, g->B, g->N, p->pool_k, p->chunk,
+                                              p->pos0, keep_ppm(p->keep_rate), ids, pos, n_kept, sws, st, tokens,
+                                              out_tokens));
+    if (e != cudaErrorNotSupported) return from_cuda(e);
+  }
+  if (epilogue_ab && resolve_algo(G, SP_SCORE_AUTO) == SP_SCORE_FUSED &&
+      fused_supported(G, Lay, Q, K)) {                 // A/B: the chunk means in the score kernel's epilogue
     const ChunkOut co{select_ws_scores(sws, g->B), p->pool_k, p->chunk};
     const cudaError_t e = fused_score_chunks(reinterpret_cast<const __nv_bfloat16*>(Q),
                                              reinterpret_cast<const __nv_bfloat16*>(K), G, Lay, importance, co, ws, sb,

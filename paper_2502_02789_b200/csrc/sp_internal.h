@@ -98,6 +98,12 @@ cudaError_t fused_score(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Ge
 // geometry / plan cannot stage them; the caller runs the plain score + selection)
 cudaError_t fused_score_chunks(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                                float* importance, const ChunkOut& co, void* ws, size_t ws_bytes, cudaStream_t st);
+// the score kernel without its cross-unit-group epilogue: *accp ([B][n_ug][Rv][*pitch]
+// in ws) holds the unit groups' partial maps for select_deferred_launch
+// (cudaErrorNotSupported: the plan has one unit group)
+cudaError_t fused_score_deferred(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
+                                 void* ws, size_t ws_bytes, cudaStream_t st, const float** accp, int* n_ug,
+                                 long long* pitch);
 cudaError_t fused_score_stats(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
                               float* stats, void* ws, size_t ws_bytes, cudaStream_t st);
 cudaError_t fused_score_finish(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
@@ -132,6 +138,11 @@ cudaError_t select_launch(const float* imp, int B, long long N, int pool_k, int 
 cudaError_t select_ready_launch(int B, long long N, int chunk, long long ppm, int pos0, int* ids, int* pos,
                                 int* n_kept, void* ws, cudaStream_t st, const int* tokens, int* out);
 float* select_ws_scores(void* ws, int B);
+// the selection finalizing a deferred score launch's importance (written to imp_out)
+bool select_deferred_supported(long long N, int Rv, int n_ug, int pool_k, int chunk);
+cudaError_t select_deferred_launch(const float* accp, long long pitch, int n_ug, int Rv, float* imp_out, int B, long long N,
+                                   int pool_k, int chunk, int pos0, long long ppm, int* ids, int* pos, int* n_kept,
+                                   void* ws, cudaStream_t st, const int* tokens, int* out);
 // sequence-sharded selection (row e)
 long long seq_candidate_count(long long N, int world, int chunk, long long ppm);
 size_t seq_select_ws_bytes(int B, long long N, int world, int chunk);

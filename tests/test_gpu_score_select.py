@@ -116,3 +116,15 @@ def test_score_chunks_vs_oracle(name, kw, sel):
     want = ref.chunk_scores(ref.smooth_scores(x, pool_k), chunk)
     got = cs[0].double().cpu().numpy()
     np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
+
+
+@pytest.mark.parametrize("name,kw,sel", [
+    ("C1", {}, {}),
+    ("C3", dict(N=16384, L=8), {}),
+    ("C1", dict(N=7777, L=4), dict(chunk=48, pool_k=65, pos0=3)),
+])
+def test_score_select_epilogue_variant(name, kw, sel, monkeypatch):
+    """The measured alternative (SP_SELECT_EPILOGUE): the chunk means in the score
+    kernel's epilogue and a top-K_c-only selection launch -- the same bits."""
+    monkeypatch.setenv("SP_SELECT_EPILOGUE", "1")
+    _both(gen.CONFIGS[name].with_(**kw), reps=2, **sel)
