@@ -2108,7 +2108,8 @@ cudaError_t fused_score_paged(const __nv_bfloat16* Q, const PagedK& K, const Geo
 constexpr int kTuneMax = SP_TUNE_MAX;        // candidates timed
 constexpr double kTuneSpan = SP_TUNE_SPAN;   // ... within this factor of the model's best cost
 cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geom& g, const Layout& lay,
-                       cudaStream_t st, int* tg_out, int* ug_out, int* hier_out, float* ms_out) {
+                       cudaStream_t user_st, int* tg_out, int* ug_out, int* hier_out, float* ms_out) {
+  constexpr int kReps = 10;
   std::vector<std::tuple<double, int, int, int>> cands;
   {
     std::lock_guard<std::mutex> lk(plan_registry_mu());
@@ -2116,6 +2117,16 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
   }
   Plan base = make_plan(g, false, 0, &cands);
   if (!base.ok) return cudaErrorInvalidValue;
+  // a private stream (capturable, unlike the legacy default stream), ordered after the caller's
+  cudaStream_t st = nullptr;
+  cudaEvent_t ready = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return cudaGetLastError();
+  if (cudaEventCreate(&ready) != cudaSuccess) {
+    cudaStreamDestroy(st);
+    return cudaGetLastError();
+  }
+  cudaEventRecord(ready, user_st);
+  cudaStreamWaitEvent(st, ready, 0);
   std::sort(cands.begin(), cands.end());
   const double best_cost = std::get<0>(cands.front());
   float best_ms = 1e30f;
@@ -2142,21 +2153,42 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
       if ((err = cudaMalloc(&ws, pl.ws_total())) != cudaSuccess) break;
       cudaMemsetAsync(ws, 0, pl.ws_total(), st);
       for (int w = 0; w < 2 && err == cudaSuccess; ++w) err = fused_score(Q, K, g, lay, imp, ws, pl.ws_total(), st);
-      cudaEventRecord(e0, st);
-      for (int r = 0; r < 5 && err == cudaSuccess; ++r) err = fused_score(Q, K, g, lay, imp, ws, pl.ws_total(), st);
-      cudaEventRecord(e1, st);
-      if (err == cudaSuccess) err = cudaEventSynchronize(e1);
-      float ms = 0.f;
-      if (err == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
+      // kReps launches replayed as a CUDA graph: the host's per-launch preparation
+      // (plan, tensor maps) must not pace short kernels (a 4K prompt runs ~60 us)
+      float ms = 1e30f;
+      cudaGraph_t graph = nullptr;
+      cudaGraphExec_t exec = nullptr;
+      if (err == cudaSuccess) err = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+      if (err == cudaSuccess) {
+        cudaError_t e2 = cudaSuccess;
+        for (int r = 0; r < kReps && e2 == cudaSuccess; ++r) e2 = fused_score(Q, K, g, lay, imp, ws, pl.ws_total(), st);
+        err = cudaStreamEndCapture(st, &graph);
+        if (err == cudaSuccess) err = e2;
+      }
+      if (err == cudaSuccess) err = cudaGraphInstantiate(&exec, graph, 0);
+      for (int it = 0; it < 3 && err == cudaSuccess; ++it) {       // first replay warms up
+        cudaEventRecord(e0, st);
+        err = cudaGraphLaunch(exec, st);
+        cudaEventRecord(e1, st);
+        if (err == cudaSuccess) err = cudaEventSynchronize(e1);
+        float t = 0.f;
+        if (err == cudaSuccess && it > 0 && cudaEventElapsedTime(&t, e0, e1) == cudaSuccess) ms = std::min(ms, t);
+      }
+      if (exec != nullptr) cudaGraphExecDestroy(exec);
+      if (graph != nullptr) cudaGraphDestroy(graph);
+      cudaStreamSynchronize(st);
       cudaFree(ws);
       if (err == cudaSuccess && ms < best_ms) {
         best_ms = ms; best_tg = tg; best_ug = ug; best_h = h; best_cap = cap; best_hint = hint;
       }
     }
   }
+  cudaStreamSynchronize(st);
   cudaFree(imp);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  cudaEventDestroy(ready);
+  cudaStreamDestroy(st);
   {
     std::lock_guard<std::mutex> lk(plan_registry_mu());
     plan_registry()[plan_key(g, 0)] = PlanChoice(best_tg, best_ug, best_h, best_cap, best_hint);
@@ -2164,7 +2196,7 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
   *tg_out = best_tg;
   *ug_out = best_ug;
   *hier_out = best_h;
-  *ms_out = best_ms / 5.f;
+  *ms_out = best_ms / kReps;
   return err;
 }
 
