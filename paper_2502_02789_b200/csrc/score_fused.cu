@@ -1403,7 +1403,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const __grid_constant__ F
           int q = tok / S, i = tok - q * S, r = q % p.Rv;
           const long long pitch = p.acc_pitch, step = (long long)dq * pitch + di, wrap = pitch - S;
           const float* ptr = src + (long long)q * pitch + i;
-          constexpr int kU = 24;                                    // loads in flight per thread (more raise the kernel's registers)
+#ifndef SP_EPI_KU
+#define SP_EPI_KU 24
+#endif
+          constexpr int kU = SP_EPI_KU;                             // loads in flight per thread (32: 163 registers)
           for (int e0 = tok; e0 < tot; e0 += kU * kTileM) {
             float v[kU];
             int dst[kU];
@@ -2166,7 +2169,7 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
         if (err == cudaSuccess) err = e2;
       }
       if (err == cudaSuccess) err = cudaGraphInstantiate(&exec, graph, 0);
-      for (int it = 0; it < 3 && err == cudaSuccess; ++it) {       // first replay warms up
+      for (int it = 0; it < 4 && err == cudaSuccess; ++it) {       // first replay warms up
         cudaEventRecord(e0, st);
         err = cudaGraphLaunch(exec, st);
         cudaEventRecord(e1, st);
@@ -2178,7 +2181,9 @@ cudaError_t fused_tune(const __nv_bfloat16* Q, const __nv_bfloat16* K, const Geo
       if (graph != nullptr) cudaGraphDestroy(graph);
       cudaStreamSynchronize(st);
       cudaFree(ws);
-      if (err == cudaSuccess && ms < best_ms) {
+      // the model's plan (timed first) is kept unless a candidate beats it by
+      // more than the timing noise (about 1 %: a graph of 10 launches)
+      if (err == cudaSuccess && ms < best_ms * (best_ms < 1e29f ? 0.99f : 1.f)) {
         best_ms = ms; best_tg = tg; best_ug = ug; best_h = h; best_cap = cap; best_hint = hint;
       }
     }
