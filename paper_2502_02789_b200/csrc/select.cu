@@ -192,7 +192,8 @@ bool deferred_shape(SelArgs& a, long long N, int Rv, int n_ug, int pool_k, int c
                     size_t* smem_out) {
   const long long n_c = (N + chunk - 1) / chunk;
   const long long w = (pool_k - 1) / 2;
-  const long long want = std::max<long long>(32, (16LL * ST) / std::max(1, n_ug * Rv));
+  static const long long loads = std::getenv("SP_DEFER_LOADS") ? std::atoll(std::getenv("SP_DEFER_LOADS")) : 16;
+  const long long want = std::max<long long>(32, (loads * ST) / std::max(1, n_ug * Rv));
   const long long tok = std::max<long long>(chunk, std::min<long long>(2048, want) / chunk * chunk);
   const long long cpb = std::max(1LL, tok / chunk);
   const long long nblk = (n_c + cpb - 1) / cpb;
