@@ -181,18 +181,19 @@ float* ws_scores(void* ws, int B) {
 
 float* select_ws_scores(void* ws, int B) { return ws_scores(ws, B); }
 
-// Deferred finalize (sp_score_select): phase A over CTAs of about 16 * NT /
-// (n_ug * Rv) tokens (16 partial-map loads per thread), computing the importance from the score
+// Deferred finalize (sp_score_select): phase A over CTAs of about 8 * NT /
+// (n_ug * Rv) tokens (8 partial-map loads per thread), computing the importance from the score
 // kernel's partial maps, writing it, then the usual pooling and chunk means;
 // the request's last CTA runs B-C.
 namespace {
 // launch shape of the deferred-finalize selection; false: not supported
-// tokens per CTA: about 16 partial-map loads per thread (one batch in flight)
+// tokens per CTA: about 8 partial-map loads per thread, one batch in flight (A/B
+// SP_DEFER_LOADS: 8 beat 16 by 0.4-0.8 us per step at C1-C3; 4 needs two waves of CTAs at C3)
 bool deferred_shape(SelArgs& a, long long N, int Rv, int n_ug, int pool_k, int chunk, long long* nblk_out,
                     size_t* smem_out) {
   const long long n_c = (N + chunk - 1) / chunk;
   const long long w = (pool_k - 1) / 2;
-  static const long long loads = std::getenv("SP_DEFER_LOADS") ? std::atoll(std::getenv("SP_DEFER_LOADS")) : 16;
+  static const long long loads = std::getenv("SP_DEFER_LOADS") ? std::atoll(std::getenv("SP_DEFER_LOADS")) : 8;
   const long long want = std::max<long long>(32, (loads * ST) / std::max(1, n_ug * Rv));
   const long long tok = std::max<long long>(chunk, std::min<long long>(2048, want) / chunk * chunk);
   const long long cpb = std::max(1LL, tok / chunk);
