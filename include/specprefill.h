@@ -365,24 +365,27 @@ sp_status sp_select_ragged(const float* importance, const int32_t* seq_lens, con
 
 /* ------------------------------------------------------------------ score + select in one call
  * sp_score followed by sp_select_gather (O1-O11, Alg.1) with the same
- * outputs, bit for bit, in one call.  On the fused kernel the selection's
- * pooling and chunk means (sec:chunk_select P:121-123, Z6, Z8) run in the score
- * kernel's epilogue -- each token group's chunks as soon as its importance and
- * its neighbours' are written, in the selection kernel's own arithmetic order --
- * and the selection launch, a programmatic dependent, runs only the top-K_c and
- * the compaction (+ gather).  Where the epilogue cannot stage a token group's
- * window (e.g. R_valid = 1, a very wide pool) it is sp_score then the whole
- * selection.  Workspace: sp_score_select_workspace_bytes(g, p) bytes, 256-byte
- * aligned, zero-filled once and reused only for this geometry and selection.
- * tokens / out_tokens may both be NULL (no gather). */
+ * outputs, bit for bit, in one call: the score kernel, then the selection
+ * launched as its programmatic dependent.  When the fused plan splits a token
+ * group over >= 2 unit groups, the score kernel leaves its cross-unit-group
+ * max (the "maximum over H and L" of sec:attn_agg) as partial maps in
+ * the workspace and the selection launch finalizes the importance from them
+ * (the same instruction, the same order: `importance` is still written, bit-
+ * identical to sp_score's) before pooling and ranking -- the epilogue's chain
+ * of cross-CTA round trips leaves the score kernel's tail.
+ * Workspace: sp_score_select_workspace_bytes(g, p) bytes, 256-byte aligned,
+ * zero-filled once and reused only for this geometry and selection.  tokens /
+ * out_tokens may both be NULL (no gather). */
 size_t sp_score_select_workspace_bytes(const sp_geom* g, const sp_select_params* p);
 sp_status sp_score_select(const void* Q, const void* K, const sp_geom* g, const sp_layout* lay,
                           const sp_select_params* p, const int32_t* tokens, float* importance, int32_t* ids,
                           int32_t* pos, int32_t* n_kept, int32_t* out_tokens, void* ws, size_t ws_bytes,
                           sp_stream stream);
 
-/* The score kernel of sp_score_select on its own: the importance (as sp_score)
- * plus the selection's chunk scores cs[b][c] = mean over chunk c of the pooled
+/* The score kernel with the selection's pooling and chunk means in its
+ * epilogue (each token group's chunks once its importance and its neighbours'
+ * are written; the measured alternative to the deferred finalize, DESIGN.md
+ * 5.3): the importance (as sp_score) plus the chunk scores cs[b][c] = mean over chunk c of the pooled
  * importance (O5-O6: centred window of pool_k with shrinking edges, Z6; the
  * partial last chunk over its true size, Z8), c < ceil(N / chunk), the same bits
  * as the selection computes -- for callers that rank the chunks themselves.
