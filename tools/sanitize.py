@@ -1,5 +1,6 @@
 """Small invocations of every kernel family for compute-sanitizer runs (dev tool):
-fused + SIMT score (C0, a C1-shaped 2K prompt), select / select_gather /
+fused + SIMT score (C0, a C1-shaped 2K prompt), score_select (deferred finalize and
+the epilogue chunk phase), select / select_gather /
 ragged select, the sequence-sharded select (2 virtual ranks), paged and e4m3
 score, the split API and the head-sharded accumulate."""
 import os
@@ -27,6 +28,12 @@ for w in (gen.CONFIGS["C0"], gen.CONFIGS["C1"].with_(N=2048, L=4)):
         e = torch.stack([sp.seq_edges(x, 2, w.N, w.keep, w.pool_k, w.chunk) for x in sh]).contiguous()
         c = torch.stack([sp.seq_candidates(sh[p], e, p, 2, w.N, w.keep, w.pool_k, w.chunk) for p in range(2)])
         sp.seq_merge(c.contiguous(), 2, w.N, w.keep, w.pool_k, w.chunk, tokens=T)
+    # sp_score_select: the deferred finalize (selection computes the importance) and
+    # the epilogue chunk-phase variant (score kernel computes the chunk means)
+    sp.score_select(Q, K, w.keep, w.pool_k, w.chunk, tokens=T, R_valid=w.Rv, scale=w.scale)
+    os.environ["SP_SELECT_EPILOGUE"] = "1"
+    sp.score_select(Q, K, w.keep, w.pool_k, w.chunk, tokens=T, R_valid=w.Rv, scale=w.scale)
+    del os.environ["SP_SELECT_EPILOGUE"]
     st = sp.score_stats(Q, K, w.Rv, w.scale)
     lse2 = sp.stats_combine(st[None].contiguous())
     sp.score_finish(Q, K, lse2, w.Rv, w.scale)
